@@ -1,0 +1,157 @@
+/*
+ * sa.h -- C ABI of the B200-native retrieval library (libsa.so).
+ *
+ * The operation is the retrieval step SearchAgent-X interleaves with LLM
+ * reasoning (§3.1: "the system checks for special tags
+ * that trigger the Retriever"; Alg. 1 LaunchAsyncRetrievalTask):
+ * top-k search of query embeddings against a dense passage-embedding
+ * knowledge base (§2.1: queries "encoded into dense vector
+ * representations"; top-k documents concatenated into the context, P:44,
+ * P:216).  Similarity is the inner product (maximum inner-product
+ * search, BASELINE.json north_star; reading R1).  Two modes:
+ *   - exact flat scan ("exact nearest neighbor (ENN) search");
+ *   - IVF approximate search whose nprobe knob plays the role of the HNSW
+ *     "search range": more effort, higher recall.
+ *
+ * Conventions (all entry points):
+ *   - Every call returns sa_status; nothing else crosses the boundary.  On
+ *     error, sa_last_error() returns a thread-local message.
+ *   - Argument validation is synchronous and side-effect free: an invalid
+ *     call returns SA_ERR_INVALID_ARG (or SA_ERR_STATE) and leaves every
+ *     output untouched.
+ *   - "DEVICE" pointers are CUDA global-memory pointers on the index's
+ *     device; "HOST" pointers are ordinary (pinned or pageable) host memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Result order (R5): fp32 score descending, then global id
+ *     ascending; -0.0 ranks as +0.0.  If fewer than k candidates exist the
+ *     tail is padded with id -1 and score -INFINITY (R6).
+ *   - Limits: 1 <= k <= 256; d <= 768 (d is zero-padded to a multiple of 64
+ *     internally); global ids < 2^32; n_local < 2^31.
+ *   - Requires an sm_100 device (B200); other devices -> SA_ERR_UNSUPPORTED.
+ */
+#ifndef SA_H_
+#define SA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SA_OK = 0,
+  SA_ERR_INVALID_ARG = 1, /* bad argument; nothing was done */
+  SA_ERR_STATE = 2,       /* call not valid for this object (e.g. nprobe>0 on a flat index) */
+  SA_ERR_OOM = 3,         /* device allocation failed */
+  SA_ERR_CUDA = 4,        /* CUDA runtime / launch error */
+  SA_ERR_NCCL = 5,        /* NCCL error (sharded indexes) */
+  SA_ERR_UNSUPPORTED = 6  /* not an sm_100 device, or a size beyond the limits above */
+} sa_status;
+
+typedef enum { SA_BF16 = 0, SA_F32 = 1 } sa_dtype;
+
+typedef struct sa_index sa_index; /* opaque; owns all device memory of one rank's shard */
+typedef struct sa_comm sa_comm;   /* opaque; wraps an NCCL communicator */
+
+typedef struct {
+  sa_dtype dtype;          /* dtype of `corpus` (default SA_BF16) */
+  int32_t kmeans_iters;    /* Lloyd iterations for the IVF quantiser (default 20) */
+  int32_t train_per_list;  /* training rows per list: n_train = min(n_total, this*nlist) (256) */
+  uint64_t seed;           /* k-means initialisation seed (default 0x5A2505) */
+  int64_t row_offset;      /* global id of local row 0 (default 0) */
+  int64_t n_total;         /* total rows over all shards (default: n) */
+  const sa_comm* comm;     /* NULL = unsharded; else the communicator this shard belongs to */
+  void* stream;            /* stream used for the build (default NULL) */
+} sa_build_opts;
+
+/* Fill *o with the defaults listed above. */
+void sa_build_opts_default(sa_build_opts* o);
+
+/*
+ * Build an index over `corpus` (DEVICE, [n, d] row-major contiguous, bf16).
+ * nlist = 0 -> flat-only index (exact search); nlist >= 1 -> also trains an
+ * IVF coarse quantiser with nlist lists (requires nlist <= n_total) and
+ * permutes the rows list-major.  Synchronous: returns after the index is
+ * complete; the caller may free `corpus` afterwards.  The index copies the
+ * rows into its own bf16 [n, d_pad] buffer (fp32 inputs are rounded to
+ * nearest-even, R3).
+ */
+sa_status sa_index_build(const void* corpus, int64_t n, int32_t d, int32_t nlist, sa_index** out);
+sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nlist,
+                            const sa_build_opts* opts, sa_index** out);
+
+/*
+ * Top-k search.  queries: DEVICE bf16 [nq, d]; out_ids: DEVICE int64 [nq, k];
+ * out_scores: DEVICE fp32 [nq, k].  nprobe = 0 -> exact flat scan;
+ * 1 <= nprobe <= nlist -> IVF search over the nprobe best lists.
+ * Stream-ordered and asynchronous: returns after enqueue; inputs must stay
+ * valid and outputs must not be read until `stream` reaches this point.
+ * For a sharded index every rank must call with identical (nq, k, nprobe) in
+ * the same order; every rank receives the global result.
+ */
+sa_status sa_search(const sa_index* idx, const void* queries, int64_t nq, int32_t k, int32_t nprobe,
+                    int64_t* out_ids, float* out_scores, void* stream);
+sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                       int32_t k, int32_t nprobe, int64_t* out_ids, float* out_scores,
+                       void* stream);
+/*
+ * Same search with HOST buffers (queries HOST [nq, d] of qdtype, out_ids HOST
+ * int64 [nq, k], out_scores HOST fp32 [nq, k]).  The host->device copy of the
+ * queries, the search and the device->host copy of the results are enqueued
+ * on `stream`; the call returns after the results are in host memory.
+ */
+sa_status sa_search_host(const sa_index* idx, const void* queries_host, sa_dtype qdtype,
+                         int64_t nq, int32_t k, int32_t nprobe, int64_t* out_ids_host,
+                         float* out_scores_host, void* stream);
+
+sa_status sa_index_free(sa_index* idx);
+
+/* NCCL plumbing for row-sharded indexes.  The 128-byte unique
+ * id is created on rank 0 with sa_comm_unique_id and broadcast by the caller
+ * (e.g. torch.distributed).  libnccl is resolved at run time (the copy the
+ * process already loaded, else libnccl.so.2). */
+sa_status sa_comm_unique_id(void* out_128_bytes);
+sa_status sa_comm_init(const void* nccl_unique_id, int32_t rank, int32_t world, int32_t cuda_device,
+                       sa_comm** out);
+sa_status sa_comm_free(sa_comm* c);
+
+const char* sa_status_string(sa_status s);
+const char* sa_last_error(void);
+
+/* ---- introspection (tests); HOST outputs, synchronous ---- */
+sa_status sa_index_info(const sa_index* idx, int64_t* n_local, int32_t* d, int32_t* nlist,
+                        int64_t* row_offset);
+/* IVF centroids as fp32 [nlist, d] (HOST). */
+sa_status sa_index_export_centroids(const sa_index* idx, float* host_out);
+/* IVF layout: offsets int64 [nlist+1] and the global id of every stored row,
+ * int64 [n_local], list-major (HOST). */
+sa_status sa_index_export_lists(const sa_index* idx, int64_t* host_offsets, int64_t* host_ids);
+/* The probe step alone: out_lists DEVICE int32 [nq, nprobe], best list first. */
+sa_status sa_search_probes(const sa_index* idx, const void* queries, int64_t nq, int32_t nprobe,
+                           int32_t* out_lists, void* stream);
+/* Debug: the raw fp32 score matrix S = Q . X^T of the flat kernel, DEVICE
+ * [nq, n_local], columns in stored-row order (tests of the tensor-core path only). */
+sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, float* out_scores,
+                          void* stream);
+
+/* ---- kernel accounting (bench.py) ----
+ * When enabled, every kernel launch is counted per kind and the dominant
+ * kernels are bracketed by CUDA events on the stream they run on. */
+typedef enum {
+  SA_KERNEL_FLAT_SCAN = 0, /* fused tcgen05 scan + top-k */
+  SA_KERNEL_MERGE = 1,     /* partial-list merge / final merge */
+  SA_KERNEL_STAGE = 2,     /* query/corpus cast + pad */
+  SA_KERNEL_IVF_PROBE = 3, /* centroid scoring + top-nprobe */
+  SA_KERNEL_IVF_SCAN = 4,  /* inverted-list scan + partial top-k */
+  SA_KERNEL_OTHER = 5,
+  SA_KERNEL_KINDS = 6
+} sa_kernel_kind;
+sa_status sa_profile_enable(int32_t on); /* also resets the counters */
+/* Synchronises the recorded events; ms_total = summed event time of that kind,
+ * launches = kernels launched of that kind since the last reset. */
+sa_status sa_profile_read(int32_t kind, double* ms_total, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SA_H_ */

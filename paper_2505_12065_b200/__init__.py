@@ -1,0 +1,304 @@
+"""paper_2505_12065_b200 -- B200-native top-k inner-product retrieval (SearchAgent-X's
+retrieval step, arXiv 2505.12065) behind the C ABI in include/sa.h.
+
+This module is a thin ctypes binding: argument marshalling only.  Every step
+of the search runs in libsa.so's sm_100a kernels; torch is used for device
+memory, streams and process groups.  There is no CPU fallback: importing the
+binding without the built library raises.
+
+Function names mirror the C ABI (sa_index_build, sa_search, ...); the `Index`
+class is the same calls with RAII.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_PKG, "libsa.so")
+
+SA_OK, SA_ERR_INVALID_ARG, SA_ERR_STATE, SA_ERR_OOM, SA_ERR_CUDA, SA_ERR_NCCL, SA_ERR_UNSUPPORTED = range(7)
+SA_BF16, SA_F32 = 0, 1
+KERNEL_KINDS = ("flat_scan", "merge", "stage", "ivf_probe", "ivf_scan", "other")
+
+
+class SAError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{status_string(status)}: {msg}")
+        self.status = status
+
+
+class _BuildOpts(ctypes.Structure):
+    _fields_ = [
+        ("dtype", ctypes.c_int),
+        ("kmeans_iters", ctypes.c_int32),
+        ("train_per_list", ctypes.c_int32),
+        ("seed", ctypes.c_uint64),
+        ("row_offset", ctypes.c_int64),
+        ("n_total", ctypes.c_int64),
+        ("comm", ctypes.c_void_p),
+        ("stream", ctypes.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libsa.so (built in-tree by build.py / __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_SO):
+        raise ImportError(f"{_SO} is missing: run `python -m paper_2505_12065_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(_SO)
+    P, i64, i32, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
+    st = ctypes.c_int
+    sigs = {
+        "sa_build_opts_default": (None, [ctypes.POINTER(_BuildOpts)]),
+        "sa_index_build": (st, [P, i64, i32, i32, ctypes.POINTER(P)]),
+        "sa_index_build_ex": (st, [P, i64, i32, i32, ctypes.POINTER(_BuildOpts), ctypes.POINTER(P)]),
+        "sa_search": (st, [P, P, i64, i32, i32, P, P, P]),
+        "sa_search_ex": (st, [P, P, ctypes.c_int, i64, i32, i32, P, P, P]),
+        "sa_search_host": (st, [P, P, ctypes.c_int, i64, i32, i32, P, P, P]),
+        "sa_index_free": (st, [P]),
+        "sa_comm_unique_id": (st, [P]),
+        "sa_comm_init": (st, [P, i32, i32, i32, ctypes.POINTER(P)]),
+        "sa_comm_free": (st, [P]),
+        "sa_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+        "sa_last_error": (ctypes.c_char_p, []),
+        "sa_index_info": (st, [P, ctypes.POINTER(i64), ctypes.POINTER(i32), ctypes.POINTER(i32),
+                               ctypes.POINTER(i64)]),
+        "sa_index_export_centroids": (st, [P, P]),
+        "sa_index_export_lists": (st, [P, P, P]),
+        "sa_search_probes": (st, [P, P, i64, i32, P, P]),
+        "sa_debug_scores": (st, [P, P, i64, P, P]),
+        "sa_profile_enable": (st, [i32]),
+        "sa_profile_read": (st, [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    import re
+    hdr = open(os.path.join(os.path.dirname(_PKG), "include", "sa.h")).read()
+    return sorted(set(re.findall(r"\b(sa_[a-z_0-9]+)\s*\(", hdr)))
+
+
+def status_string(s: int) -> str:
+    try:
+        return lib().sa_status_string(int(s)).decode()
+    except ImportError:
+        return str(s)
+
+
+def last_error() -> str:
+    return lib().sa_last_error().decode()
+
+
+def _check(status: int):
+    if status != SA_OK:
+        raise SAError(status, last_error())
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t: torch.Tensor):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return SA_BF16
+    if t.dtype == torch.float32:
+        return SA_F32
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or f32)")
+
+
+# ----------------------------------------------------------------- comm
+class Comm:
+    """NCCL communicator for a row-sharded index; unique id exchanged via torch.distributed."""
+
+    def __init__(self, handle, rank, world):
+        self.handle, self.rank, self.world = handle, rank, world
+
+    @classmethod
+    def from_torch_distributed(cls, device: int | None = None):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = (ctypes.c_uint8 * 128)()
+            _check(lib().sa_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+            uid = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if dist.get_backend() == "nccl":
+            uid = uid.cuda()
+        dist.broadcast(uid, 0)
+        raw = bytes(uid.cpu().tolist())
+        h = ctypes.c_void_p()
+        dev = torch.cuda.current_device() if device is None else device
+        _check(lib().sa_comm_init(ctypes.c_char_p(raw), rank, world, dev, ctypes.byref(h)))
+        return cls(h, rank, world)
+
+    def free(self):
+        if self.handle:
+            lib().sa_comm_free(self.handle)
+            self.handle = None
+
+
+def shard_range(n_total: int, rank: int, world: int):
+    """Balanced contiguous split: off_r = r*floor(n/w) + min(r, n mod w)."""
+    base, rem = divmod(int(n_total), int(world))
+    off = rank * base + min(rank, rem)
+    return off, base + (1 if rank < rem else 0)
+
+
+# ----------------------------------------------------------------- index
+class Index:
+    def __init__(self, handle, d):
+        self.handle = handle
+        self.d = d
+
+    # sa_index_build / sa_index_build_ex
+    @classmethod
+    def build(cls, corpus: torch.Tensor, nlist: int = 0, *, kmeans_iters: int = 20,
+              train_per_list: int = 256, seed: int = 0x5A2505, row_offset: int = 0,
+              n_total: int | None = None, comm: Comm | None = None, stream=None) -> "Index":
+        if not corpus.is_cuda or corpus.dim() != 2 or not corpus.is_contiguous():
+            raise ValueError("corpus must be a contiguous 2-D CUDA tensor")
+        o = _BuildOpts()
+        lib().sa_build_opts_default(ctypes.byref(o))
+        o.dtype = _dtype_code(corpus)
+        o.kmeans_iters = kmeans_iters
+        o.train_per_list = train_per_list
+        o.seed = seed
+        o.row_offset = row_offset
+        o.n_total = n_total if n_total is not None else 0
+        o.comm = comm.handle if comm is not None else None
+        o.stream = _stream_ptr(stream)
+        h = ctypes.c_void_p()
+        _check(lib().sa_index_build_ex(_ptr(corpus), corpus.shape[0], corpus.shape[1], nlist,
+                                       ctypes.byref(o), ctypes.byref(h)))
+        return cls(h, corpus.shape[1])
+
+    # sa_search / sa_search_ex
+    def search(self, queries: torch.Tensor, k: int, nprobe: int = 0, out=None, stream=None):
+        if not queries.is_cuda or queries.dim() != 2 or not queries.is_contiguous():
+            raise ValueError("queries must be a contiguous 2-D CUDA tensor")
+        if queries.shape[1] != self.d:
+            raise SAError(SA_ERR_INVALID_ARG, f"queries have d={queries.shape[1]}, index d={self.d}")
+        nq = queries.shape[0]
+        if out is None:
+            ids = torch.empty(nq, k, dtype=torch.int64, device=queries.device)
+            scores = torch.empty(nq, k, dtype=torch.float32, device=queries.device)
+        else:
+            ids, scores = out
+        _check(lib().sa_search_ex(self.handle, _ptr(queries), _dtype_code(queries), nq, k, nprobe,
+                                  _ptr(ids), _ptr(scores), _stream_ptr(stream)))
+        return ids, scores
+
+    # sa_search_host: host buffers in and out, copies inside the call
+    def search_host(self, queries: torch.Tensor, k: int, nprobe: int = 0, out=None, stream=None):
+        if queries.is_cuda or queries.dim() != 2 or not queries.is_contiguous():
+            raise ValueError("queries must be a contiguous 2-D host tensor")
+        if queries.shape[1] != self.d:
+            raise SAError(SA_ERR_INVALID_ARG, f"queries have d={queries.shape[1]}, index d={self.d}")
+        nq = queries.shape[0]
+        if out is None:
+            ids = torch.empty(nq, k, dtype=torch.int64).pin_memory()
+            scores = torch.empty(nq, k, dtype=torch.float32).pin_memory()
+        else:
+            ids, scores = out
+        _check(lib().sa_search_host(self.handle, _ptr(queries), _dtype_code(queries), nq, k, nprobe,
+                                    _ptr(ids), _ptr(scores), _stream_ptr(stream)))
+        return ids, scores
+
+    def info(self):
+        n = ctypes.c_int64()
+        d = ctypes.c_int32()
+        nl = ctypes.c_int32()
+        off = ctypes.c_int64()
+        _check(lib().sa_index_info(self.handle, ctypes.byref(n), ctypes.byref(d), ctypes.byref(nl),
+                                   ctypes.byref(off)))
+        return dict(n_local=n.value, d=d.value, nlist=nl.value, row_offset=off.value)
+
+    def export_centroids(self) -> np.ndarray:
+        inf = self.info()
+        out = np.empty((inf["nlist"], inf["d"]), dtype=np.float32)
+        _check(lib().sa_index_export_centroids(self.handle, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
+    def export_lists(self):
+        inf = self.info()
+        off = np.empty(inf["nlist"] + 1, dtype=np.int64)
+        ids = np.empty(inf["n_local"], dtype=np.int64)
+        _check(lib().sa_index_export_lists(self.handle, off.ctypes.data_as(ctypes.c_void_p),
+                                           ids.ctypes.data_as(ctypes.c_void_p)))
+        return off, ids
+
+    def probes(self, queries: torch.Tensor, nprobe: int, stream=None) -> torch.Tensor:
+        out = torch.empty(queries.shape[0], nprobe, dtype=torch.int32, device=queries.device)
+        _check(lib().sa_search_probes(self.handle, _ptr(queries), queries.shape[0], nprobe,
+                                      _ptr(out), _stream_ptr(stream)))
+        return out
+
+    def debug_scores(self, queries: torch.Tensor, stream=None) -> torch.Tensor:
+        n = self.info()["n_local"]
+        out = torch.empty(queries.shape[0], n, dtype=torch.float32, device=queries.device)
+        _check(lib().sa_debug_scores(self.handle, _ptr(queries), queries.shape[0], _ptr(out),
+                                     _stream_ptr(stream)))
+        return out
+
+    def free(self):
+        if self.handle:
+            lib().sa_index_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+# C-ABI-named aliases
+def sa_index_build(corpus, nlist=0, **kw) -> Index:
+    return Index.build(corpus, nlist, **kw)
+
+
+def sa_search(index: Index, queries, k, nprobe=0, out=None, stream=None):
+    return index.search(queries, k, nprobe, out, stream)
+
+
+def sa_search_host(index: Index, queries, k, nprobe=0, out=None, stream=None):
+    return index.search_host(queries, k, nprobe, out, stream)
+
+
+def sa_index_free(index: Index):
+    index.free()
+
+
+# ----------------------------------------------------------------- accounting
+def profile_enable(on: bool = True):
+    _check(lib().sa_profile_enable(1 if on else 0))
+
+
+def profile_read(kind: str | int):
+    kid = KERNEL_KINDS.index(kind) if isinstance(kind, str) else int(kind)
+    ms = ctypes.c_double()
+    n = ctypes.c_int64()
+    _check(lib().sa_profile_read(kid, ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value

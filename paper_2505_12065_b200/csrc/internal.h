@@ -1,0 +1,71 @@
+// internal.h -- library-private declarations shared by the C-ABI translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/sa.h"
+
+struct sa_comm {
+  void* nccl = nullptr;  // ncclComm_t
+  int32_t rank = 0, world = 1, device = 0;
+};
+
+struct sa_index {
+  int device = 0;
+  int num_sms = 148;
+  int64_t n_local = 0;
+  int32_t d = 0, d_pad = 0;
+  int32_t nlist = 0;
+  int64_t row_offset = 0, n_total = 0;
+  __nv_bfloat16* X = nullptr;  // [n_local, d_pad] (list-major when nlist > 0)
+  CUtensorMap tmap_x;
+  int32_t* row_ids = nullptr;  // nlist > 0: stored row -> global id (fits 32 bits)
+  // IVF coarse quantiser
+  float* centroids = nullptr;                // [nlist, d_pad] fp32 (unit norm)
+  __nv_bfloat16* centroids_bf16 = nullptr;   // [nlist, d_pad]
+  CUtensorMap tmap_c;
+  int64_t* list_off = nullptr;               // device [nlist + 1]
+  std::vector<int64_t> h_list_off;           // host copy
+  int32_t max_list = 0;
+  const sa_comm* comm = nullptr;
+};
+
+namespace sa {
+
+sa_status set_error(sa_status s, const std::string& msg);
+sa_status cuda_status(cudaError_t e, const char* what);
+
+// TMA descriptor for a row-major bf16 [rows, cols] matrix with box [box_rows, 64 cols], SW128.
+sa_status make_tmap_bf16(CUtensorMap* m, const void* base, int64_t rows, int32_t cols,
+                         int32_t box_rows);
+
+// profiler hooks
+void prof_count(int kind);
+void prof_begin(int kind, cudaStream_t s);
+void prof_end(int kind, cudaStream_t s);
+
+// Where a search writes its [nq, k] result: packed keys (for a cross-rank
+// merge) or unpacked (id, score) pairs.
+struct SearchOut {
+  uint64_t* keys = nullptr;
+  int64_t* ids = nullptr;
+  float* scores = nullptr;
+};
+
+// exact flat scan + intra-GPU merge (flat.cu / sa_api.cu)
+sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
+                      int32_t k, const SearchOut& out, cudaStream_t s);
+
+// IVF (ivf.cu)
+sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s);
+sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
+                     int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s);
+sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
+                    int32_t nprobe, int32_t* out_lists, cudaStream_t s);
+
+}  // namespace sa

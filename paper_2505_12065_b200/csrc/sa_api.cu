@@ -1,0 +1,588 @@
+// sa_api.cu -- the C ABI (include/sa.h): validation, index object, search planner,
+// NCCL plumbing and kernel accounting.  Every step of the path runs in this
+// library's kernels; there is no host or library fallback.
+#include <cudaTypedefs.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels/flat_scan.cuh"
+#include "kernels/merge.cuh"
+
+// ====================================================================== errors
+static thread_local std::string g_last_error;
+
+namespace sa {
+
+sa_status set_error(sa_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+sa_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return SA_OK;
+  if (e == cudaErrorMemoryAllocation)
+    return set_error(SA_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+  return set_error(SA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ====================================================================== TMA
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+sa_status make_tmap_bf16(CUtensorMap* m, const void* base, int64_t rows, int32_t cols,
+                         int32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return set_error(SA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(SA_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return SA_OK;
+}
+
+// ====================================================================== profiler
+namespace {
+struct Prof {
+  std::mutex mu;
+  bool on = false;
+  int64_t launches[SA_KERNEL_KINDS] = {};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[SA_KERNEL_KINDS];
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+Prof g_prof;
+thread_local cudaEvent_t t_open[SA_KERNEL_KINDS];
+}  // namespace
+
+void prof_count(int kind) {
+  std::lock_guard<std::mutex> l(g_prof.mu);
+  g_prof.launches[kind]++;
+}
+void prof_begin(int kind, cudaStream_t s) {
+  std::lock_guard<std::mutex> l(g_prof.mu);
+  if (!g_prof.on) return;
+  t_open[kind] = g_prof.get();
+  cudaEventRecord(t_open[kind], s);
+}
+void prof_end(int kind, cudaStream_t s) {
+  std::lock_guard<std::mutex> l(g_prof.mu);
+  if (!g_prof.on || !t_open[kind]) return;
+  cudaEvent_t e = g_prof.get();
+  cudaEventRecord(e, s);
+  g_prof.ev[kind].push_back({t_open[kind], e});
+  t_open[kind] = nullptr;
+}
+
+// ====================================================================== helpers
+static sa_status check_device(int* dev_out, int* sms_out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  int major = 0, minor = 0, sms = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (major != 10 || minor != 0)
+    return set_error(SA_ERR_UNSUPPORTED, "libsa is built for sm_100a (B200); device is sm_" +
+                                             std::to_string(major) + std::to_string(minor));
+  if (dev_out) *dev_out = dev;
+  if (sms_out) *sms_out = sms;
+  return SA_OK;
+}
+
+template <typename T>
+static sa_status dalloc(T** p, size_t count, cudaStream_t s, const char* what) {
+  *p = nullptr;
+  if (count == 0) return SA_OK;
+  return cuda_status(cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), s), what);
+}
+
+// ====================================================================== flat search
+sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
+                      int32_t k, const SearchOut& out, cudaStream_t s) {
+  const int64_t T = (idx->n_local + FS_BN - 1) / FS_BN;
+  const int32_t QB = (int32_t)(nq_pad / FS_BM);
+  int64_t S = std::max<int64_t>(1, idx->num_sms / QB);
+  S = std::min<int64_t>(S, T);
+  const int grid = (int)std::min<int64_t>(idx->num_sms, (int64_t)QB * S);
+
+  uint64_t *part = nullptr, *heap = nullptr;
+  sa_status st = dalloc(&part, (size_t)nq_pad * S * k, s, "alloc partials");
+  if (st != SA_OK) return st;
+  if (k > FS_KSMEM) {
+    st = dalloc(&heap, (size_t)grid * k * FS_BM, s, "alloc heaps");
+    if (st != SA_OK) { cudaFreeAsync(part, s); return st; }
+  }
+  FlatScanArgs a{};
+  a.Q = Qs;
+  a.nq_pad = nq_pad;
+  a.d_pad = idx->d_pad;
+  a.n_rows = idx->n_local;
+  a.QB = QB;
+  a.S = (int32_t)S;
+  a.k = k;
+  a.row_ids = idx->row_ids;
+  a.id_base = idx->row_ids ? 0u : (uint32_t)idx->row_offset;
+  a.part = part;
+  a.heap_g = heap;
+  a.mode = 0;
+  prof_begin(SA_KERNEL_FLAT_SCAN, s);
+  cudaError_t e = launch_flat_scan(idx->tmap_x, a, grid, s);
+  prof_end(SA_KERNEL_FLAT_SCAN, s);
+  prof_count(SA_KERNEL_FLAT_SCAN);
+  if (e == cudaSuccess) {
+    MergeArgs m{};
+    m.cand = part;
+    m.groups = (int32_t)S;
+    m.k = k;
+    m.qstride = S * k;
+    m.gstride = k;
+    m.out_keys = out.keys;
+    m.out_ids = out.ids;
+    m.out_scores = out.scores;
+    m.id_offset = 0;
+    prof_begin(SA_KERNEL_MERGE, s);
+    e = launch_merge(m, nq, s);
+    prof_end(SA_KERNEL_MERGE, s);
+    prof_count(SA_KERNEL_MERGE);
+  }
+  if (heap) cudaFreeAsync(heap, s);
+  cudaFreeAsync(part, s);
+  return cuda_status(e, "flat search launch");
+}
+
+}  // namespace sa
+
+using namespace sa;
+
+// ====================================================================== NCCL (dlopen)
+namespace {
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+    api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather;
+  });
+  return api;
+}
+sa_status nccl_status(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return SA_OK;
+  const char* m = nccl().GetErrorString ? nccl().GetErrorString(r) : "?";
+  return set_error(SA_ERR_NCCL, std::string(what) + ": " + m);
+}
+}  // namespace
+
+extern "C" {
+
+const char* sa_status_string(sa_status s) {
+  switch (s) {
+    case SA_OK: return "SA_OK";
+    case SA_ERR_INVALID_ARG: return "SA_ERR_INVALID_ARG";
+    case SA_ERR_STATE: return "SA_ERR_STATE";
+    case SA_ERR_OOM: return "SA_ERR_OOM";
+    case SA_ERR_CUDA: return "SA_ERR_CUDA";
+    case SA_ERR_NCCL: return "SA_ERR_NCCL";
+    case SA_ERR_UNSUPPORTED: return "SA_ERR_UNSUPPORTED";
+  }
+  return "SA_ERR_UNKNOWN";
+}
+
+const char* sa_last_error(void) { return g_last_error.c_str(); }
+
+void sa_build_opts_default(sa_build_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->dtype = SA_BF16;
+  o->kmeans_iters = 20;
+  o->train_per_list = 256;
+  o->seed = 0x5A2505ull;
+  o->row_offset = 0;
+  o->n_total = 0;
+  o->comm = nullptr;
+  o->stream = nullptr;
+}
+
+sa_status sa_comm_unique_id(void* out) {
+  if (!out) return set_error(SA_ERR_INVALID_ARG, "out is NULL");
+  if (!nccl().ok) return set_error(SA_ERR_NCCL, "libnccl.so.2 not found");
+  ncclUniqueId id;
+  sa_status st = nccl_status(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+  if (st != SA_OK) return st;
+  std::memcpy(out, &id, sizeof(id));
+  return SA_OK;
+}
+
+sa_status sa_comm_init(const void* uid, int32_t rank, int32_t world, int32_t device,
+                       sa_comm** out) {
+  if (!uid || !out) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (world < 1 || rank < 0 || rank >= world) return set_error(SA_ERR_INVALID_ARG, "bad rank/world");
+  if (!nccl().ok) return set_error(SA_ERR_NCCL, "libnccl.so.2 not found");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  ncclComm_t c;
+  sa_status st = nccl_status(nccl().CommInitRank(&c, world, id, rank), "ncclCommInitRank");
+  if (st != SA_OK) return st;
+  sa_comm* sc = new sa_comm;
+  sc->nccl = c;
+  sc->rank = rank;
+  sc->world = world;
+  sc->device = device;
+  *out = sc;
+  return SA_OK;
+}
+
+sa_status sa_comm_free(sa_comm* c) {
+  if (!c) return SA_OK;
+  if (c->nccl && nccl().ok) nccl().CommDestroy((ncclComm_t)c->nccl);
+  delete c;
+  return SA_OK;
+}
+
+sa_status sa_index_build(const void* corpus, int64_t n, int32_t d, int32_t nlist, sa_index** out) {
+  sa_build_opts o;
+  sa_build_opts_default(&o);
+  return sa_index_build_ex(corpus, n, d, nlist, &o, out);
+}
+
+sa_status sa_index_free(sa_index* idx) {
+  if (!idx) return SA_OK;
+  cudaDeviceSynchronize();
+  cudaFree(idx->X);
+  cudaFree(idx->row_ids);
+  cudaFree(idx->centroids);
+  cudaFree(idx->centroids_bf16);
+  cudaFree(idx->list_off);
+  delete idx;
+  return SA_OK;
+}
+
+sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nlist,
+                            const sa_build_opts* opts, sa_index** out) {
+  if (!corpus || !out || !opts) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (n < 1) return set_error(SA_ERR_INVALID_ARG, "n must be >= 1");
+  if (d < 1) return set_error(SA_ERR_INVALID_ARG, "d must be >= 1");
+  if (nlist < 0) return set_error(SA_ERR_INVALID_ARG, "nlist must be >= 0");
+  if (opts->dtype != SA_BF16 && opts->dtype != SA_F32)
+    return set_error(SA_ERR_INVALID_ARG, "bad dtype");
+  const int64_t n_total = opts->n_total > 0 ? opts->n_total : n;
+  if (opts->row_offset < 0 || opts->row_offset + n > n_total)
+    return set_error(SA_ERR_INVALID_ARG, "row_offset + n exceeds n_total");
+  if (nlist > n_total) return set_error(SA_ERR_INVALID_ARG, "nlist exceeds n_total");
+  if (nlist > 0 && (opts->kmeans_iters < 0 || opts->train_per_list < 1))
+    return set_error(SA_ERR_INVALID_ARG, "bad k-means options");
+  const int32_t d_pad = (d + 63) / 64 * 64;
+  if (d_pad > FS_MAX_DPAD) return set_error(SA_ERR_UNSUPPORTED, "d > 768 not supported");
+  if (n >= (1ll << 31)) return set_error(SA_ERR_UNSUPPORTED, "n_local >= 2^31");
+  if (n_total >= (1ll << 32) - 1) return set_error(SA_ERR_UNSUPPORTED, "n_total >= 2^32");
+  if (opts->comm && opts->comm->world > 1 && nlist > 0 && opts->n_total <= 0)
+    return set_error(SA_ERR_INVALID_ARG, "sharded IVF build needs n_total");
+  int dev = 0, sms = 0;
+  sa_status st = check_device(&dev, &sms);
+  if (st != SA_OK) return st;
+
+  cudaStream_t s = (cudaStream_t)opts->stream;
+  sa_index* idx = new sa_index;
+  idx->device = dev;
+  idx->num_sms = sms;
+  idx->n_local = n;
+  idx->d = d;
+  idx->d_pad = d_pad;
+  idx->nlist = nlist;
+  idx->row_offset = opts->row_offset;
+  idx->n_total = n_total;
+  idx->comm = opts->comm;
+  st = cuda_status(cudaMalloc(&idx->X, (size_t)n * d_pad * sizeof(__nv_bfloat16)), "alloc corpus");
+  if (st == SA_OK) {
+    st = cuda_status(launch_cast_pad(corpus, opts->dtype == SA_F32, n, d, idx->X, n, d_pad, sms, s),
+                     "cast/pad corpus");
+    prof_count(SA_KERNEL_STAGE);
+  }
+  if (st == SA_OK && nlist > 0) st = ivf_build(idx, *opts, s);
+  if (st == SA_OK) st = make_tmap_bf16(&idx->tmap_x, idx->X, n, d_pad, FS_BN);
+  if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "build sync");
+  if (st != SA_OK) {
+    sa_index_free(idx);
+    return st;
+  }
+  *out = idx;
+  return SA_OK;
+}
+
+static sa_status validate_search(const sa_index* idx, const void* q, int64_t nq, int32_t k,
+                                 int32_t nprobe, const void* ids, const void* scores) {
+  if (!idx || !q || !ids || !scores) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (nq < 1) return set_error(SA_ERR_INVALID_ARG, "nq must be >= 1");
+  if (k < 1 || k > 256) return set_error(SA_ERR_INVALID_ARG, "k must be in [1, 256]");
+  if (nprobe < 0) return set_error(SA_ERR_INVALID_ARG, "nprobe must be >= 0");
+  if (nprobe > 0 && idx->nlist == 0)
+    return set_error(SA_ERR_STATE, "nprobe > 0 on a flat-only index (nlist = 0)");
+  if (nprobe > idx->nlist) return set_error(SA_ERR_INVALID_ARG, "nprobe > nlist");
+  if (nq > (1ll << 31) / 2) return set_error(SA_ERR_UNSUPPORTED, "nq too large");
+  return SA_OK;
+}
+
+sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                       int32_t k, int32_t nprobe, int64_t* out_ids, float* out_scores,
+                       void* stream) {
+  sa_status st = validate_search(idx, queries, nq, k, nprobe, out_ids, out_scores);
+  if (st != SA_OK) return st;
+  if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nq_pad = (nq + FS_BM - 1) / FS_BM * FS_BM;
+  __nv_bfloat16* Qs = nullptr;
+  st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "alloc staged queries");
+  if (st != SA_OK) return st;
+  prof_begin(SA_KERNEL_STAGE, s);
+  cudaError_t e = launch_cast_pad(queries, qdtype == SA_F32, nq, idx->d, Qs, nq_pad, idx->d_pad,
+                                  idx->num_sms, s);
+  prof_end(SA_KERNEL_STAGE, s);
+  prof_count(SA_KERNEL_STAGE);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(Qs, s);
+    return cuda_status(e, "stage queries");
+  }
+  const bool sharded = idx->comm && idx->comm->world > 1;
+  uint64_t *keys_local = nullptr, *keys_all = nullptr;
+  SearchOut out;
+  if (sharded) {
+    const int w = idx->comm->world;
+    st = dalloc(&keys_local, (size_t)nq * k, s, "alloc local keys");
+    if (st == SA_OK) st = dalloc(&keys_all, (size_t)nq * k * w, s, "alloc gathered keys");
+    out.keys = keys_local;
+  } else {
+    out.ids = out_ids;
+    out.scores = out_scores;
+  }
+  if (st == SA_OK) {
+    st = nprobe == 0 ? flat_search(idx, Qs, nq, nq_pad, k, out, s)
+                     : ivf_search(idx, Qs, nq, nq_pad, k, nprobe, out, s);
+  }
+  if (st == SA_OK && sharded) {
+    // a9: all-gather the per-rank sorted [nq, k] key lists, then a k-way merge.
+    st = nccl_status(nccl().AllGather(keys_local, keys_all, (size_t)nq * k, ncclUint64,
+                                      (ncclComm_t)idx->comm->nccl, s),
+                     "ncclAllGather");
+    if (st == SA_OK) {
+      MergeArgs m{};
+      m.cand = keys_all;
+      m.groups = idx->comm->world;
+      m.k = k;
+      m.qstride = k;
+      m.gstride = nq * k;
+      m.out_ids = out_ids;
+      m.out_scores = out_scores;
+      prof_begin(SA_KERNEL_MERGE, s);
+      st = cuda_status(launch_merge(m, nq, s), "final merge");
+      prof_end(SA_KERNEL_MERGE, s);
+      prof_count(SA_KERNEL_MERGE);
+    }
+  }
+  if (keys_local) cudaFreeAsync(keys_local, s);
+  if (keys_all) cudaFreeAsync(keys_all, s);
+  cudaFreeAsync(Qs, s);
+  return st;
+}
+
+sa_status sa_search(const sa_index* idx, const void* queries, int64_t nq, int32_t k, int32_t nprobe,
+                    int64_t* out_ids, float* out_scores, void* stream) {
+  return sa_search_ex(idx, queries, SA_BF16, nq, k, nprobe, out_ids, out_scores, stream);
+}
+
+sa_status sa_search_host(const sa_index* idx, const void* queries_host, sa_dtype qdtype,
+                         int64_t nq, int32_t k, int32_t nprobe, int64_t* out_ids_host,
+                         float* out_scores_host, void* stream) {
+  sa_status st = validate_search(idx, queries_host, nq, k, nprobe, out_ids_host, out_scores_host);
+  if (st != SA_OK) return st;
+  if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t qbytes = (size_t)nq * idx->d * (qdtype == SA_F32 ? 4 : 2);
+  void* dq = nullptr;
+  int64_t* dids = nullptr;
+  float* dsc = nullptr;
+  st = cuda_status(cudaMallocAsync(&dq, qbytes, s), "alloc queries");
+  if (st == SA_OK) st = dalloc(&dids, (size_t)nq * k, s, "alloc ids");
+  if (st == SA_OK) st = dalloc(&dsc, (size_t)nq * k, s, "alloc scores");
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(dq, queries_host, qbytes, cudaMemcpyHostToDevice, s), "H2D");
+  if (st == SA_OK) st = sa_search_ex(idx, dq, qdtype, nq, k, nprobe, dids, dsc, stream);
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(out_ids_host, dids, (size_t)nq * k * 8,
+                                     cudaMemcpyDeviceToHost, s), "D2H ids");
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(out_scores_host, dsc, (size_t)nq * k * 4,
+                                     cudaMemcpyDeviceToHost, s), "D2H scores");
+  if (dq) cudaFreeAsync(dq, s);
+  if (dids) cudaFreeAsync(dids, s);
+  if (dsc) cudaFreeAsync(dsc, s);
+  sa_status st2 = cuda_status(cudaStreamSynchronize(s), "search sync");
+  return st != SA_OK ? st : st2;
+}
+
+sa_status sa_index_info(const sa_index* idx, int64_t* n_local, int32_t* d, int32_t* nlist,
+                        int64_t* row_offset) {
+  if (!idx) return set_error(SA_ERR_INVALID_ARG, "null index");
+  if (n_local) *n_local = idx->n_local;
+  if (d) *d = idx->d;
+  if (nlist) *nlist = idx->nlist;
+  if (row_offset) *row_offset = idx->row_offset;
+  return SA_OK;
+}
+
+sa_status sa_index_export_centroids(const sa_index* idx, float* host_out) {
+  if (!idx || !host_out) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (idx->nlist == 0) return set_error(SA_ERR_STATE, "flat-only index has no centroids");
+  cudaError_t e = cudaMemcpy2D(host_out, (size_t)idx->d * 4, idx->centroids, (size_t)idx->d_pad * 4,
+                               (size_t)idx->d * 4, idx->nlist, cudaMemcpyDeviceToHost);
+  return cuda_status(e, "export centroids");
+}
+
+sa_status sa_index_export_lists(const sa_index* idx, int64_t* host_offsets, int64_t* host_ids) {
+  if (!idx || !host_offsets || !host_ids) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (idx->nlist == 0) return set_error(SA_ERR_STATE, "flat-only index has no lists");
+  std::memcpy(host_offsets, idx->h_list_off.data(), (idx->nlist + 1) * sizeof(int64_t));
+  std::vector<int32_t> tmp(idx->n_local);
+  cudaError_t e = cudaMemcpy(tmp.data(), idx->row_ids, idx->n_local * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_status(e, "export lists");
+  for (int64_t i = 0; i < idx->n_local; ++i) host_ids[i] = (int64_t)(uint32_t)tmp[i];
+  return SA_OK;
+}
+
+sa_status sa_search_probes(const sa_index* idx, const void* queries, int64_t nq, int32_t nprobe,
+                           int32_t* out_lists, void* stream) {
+  if (!idx || !queries || !out_lists) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (nq < 1) return set_error(SA_ERR_INVALID_ARG, "nq must be >= 1");
+  if (idx->nlist == 0) return set_error(SA_ERR_STATE, "flat-only index");
+  if (nprobe < 1 || nprobe > idx->nlist) return set_error(SA_ERR_INVALID_ARG, "bad nprobe");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nq_pad = (nq + FS_BM - 1) / FS_BM * FS_BM;
+  __nv_bfloat16* Qs = nullptr;
+  sa_status st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "alloc staged queries");
+  if (st != SA_OK) return st;
+  st = cuda_status(launch_cast_pad(queries, false, nq, idx->d, Qs, nq_pad, idx->d_pad,
+                                   idx->num_sms, s), "stage queries");
+  if (st == SA_OK) st = ivf_probe(idx, Qs, nq, nq_pad, nprobe, out_lists, s);
+  cudaFreeAsync(Qs, s);
+  return st;
+}
+
+sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, float* out_scores,
+                          void* stream) {
+  if (!idx || !queries || !out_scores) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (nq < 1) return set_error(SA_ERR_INVALID_ARG, "nq must be >= 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nq_pad = (nq + FS_BM - 1) / FS_BM * FS_BM;
+  __nv_bfloat16* Qs = nullptr;
+  float* dbg = nullptr;
+  sa_status st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "alloc staged queries");
+  if (st == SA_OK) st = dalloc(&dbg, (size_t)nq_pad * idx->n_local, s, "alloc debug scores");
+  if (st == SA_OK)
+    st = cuda_status(launch_cast_pad(queries, false, nq, idx->d, Qs, nq_pad, idx->d_pad,
+                                     idx->num_sms, s), "stage queries");
+  if (st == SA_OK) {
+    const int64_t T = (idx->n_local + FS_BN - 1) / FS_BN;
+    const int32_t QB = (int32_t)(nq_pad / FS_BM);
+    int64_t S = std::min<int64_t>(std::max<int64_t>(1, idx->num_sms / QB), T);
+    FlatScanArgs a{};
+    a.Q = Qs;
+    a.nq_pad = nq_pad;
+    a.d_pad = idx->d_pad;
+    a.n_rows = idx->n_local;
+    a.QB = QB;
+    a.S = (int32_t)S;
+    a.k = 1;
+    a.dbg = dbg;
+    a.mode = 1;
+    st = cuda_status(launch_flat_scan(idx->tmap_x, a,
+                                      (int)std::min<int64_t>(idx->num_sms, QB * S), s),
+                     "debug scan");
+  }
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(out_scores, dbg, (size_t)nq * idx->n_local * 4,
+                                     cudaMemcpyDeviceToDevice, s), "copy scores");
+  if (Qs) cudaFreeAsync(Qs, s);
+  if (dbg) cudaFreeAsync(dbg, s);
+  return st;
+}
+
+sa_status sa_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> l(g_prof.mu);
+  for (int k = 0; k < SA_KERNEL_KINDS; ++k) {
+    for (auto& p : g_prof.ev[k]) {
+      g_prof.pool.push_back(p.first);
+      g_prof.pool.push_back(p.second);
+    }
+    g_prof.ev[k].clear();
+    g_prof.launches[k] = 0;
+  }
+  g_prof.on = on != 0;
+  return SA_OK;
+}
+
+sa_status sa_profile_read(int32_t kind, double* ms_total, int64_t* launches) {
+  if (kind < 0 || kind >= SA_KERNEL_KINDS) return set_error(SA_ERR_INVALID_ARG, "bad kind");
+  std::lock_guard<std::mutex> l(g_prof.mu);
+  double tot = 0.0;
+  for (auto& p : g_prof.ev[kind]) {
+    cudaError_t e = cudaEventSynchronize(p.second);
+    if (e != cudaSuccess) return cuda_status(e, "profile sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.first, p.second);
+    tot += ms;
+  }
+  if (ms_total) *ms_total = tot;
+  if (launches) *launches = g_prof.launches[kind];
+  return SA_OK;
+}
+
+}  // extern "C"
