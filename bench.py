@@ -1,0 +1,346 @@
+"""bench.py -- throughput of the retrieval hot path (BASELINE.json metric) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--nprobe P]
+                  [--impl reference]
+
+A step = one search batch through the whole search path (stage queries ->
+fused tcgen05 scan + top-k -> merge -> [NCCL all-gather -> final merge] ->
+output) over the workload of --config (default c3: exact top-10 over
+21,015,324 x 768 bf16, batch 512; the largest BASELINE config that fits one
+GPU).  The index build (§8(a) a1-a3) happens once before timing and is
+reported as build_s.  Inputs are larger than L2 (the corpus is 32 GB), so no
+L2 flush is needed between steps.
+
+--impl reference times the CPU oracle (oracle/oracle.c, as it stands) on the
+host cores on a bounded sample of the same workload and reports the same
+metric extrapolated to the full corpus.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from datagen import CONFIGS, CORPUS_SEED, QUERY_SEED, make_mixture, draw_rows_into  # noqa: E402
+
+METRIC = "queries/sec at recall@10>=0.95 on 21Mx768 corpus (1/2/4/8 B200); p50 batch latency"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return dict(hbm=j["hbm_gbs"], bf16=j["bf16_tflops"], bf16_sus=j.get("bf16_tflops_sustained"),
+                    src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+def workload_name(cfg, name, nprobe):
+    mode = "exact flat" if nprobe == 0 else f"IVF nlist={cfg.get('nlist')} nprobe={nprobe}"
+    return f"{name}: {mode} top-{cfg['k']}, {cfg['n']}x{cfg['d']} bf16 corpus, batch {cfg['nq']}"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm (CPU oracle)
+def cpu_oracle_sample(X_host_bits: np.ndarray, Q_bits: np.ndarray, k: int, n_total: int):
+    """Time the oracle on Q_bits x X_host_bits; returns (extrapolated q/s, seconds, cores)."""
+    import oracle
+    cores = oracle.num_threads()
+    t0 = time.perf_counter()
+    oracle.flat_topk(X_host_bits, Q_bits, k)
+    dt = time.perf_counter() - t0
+    nq, ns = Q_bits.shape[0], X_host_bits.shape[0]
+    # full-corpus q/s = queries / (time * n_total / n_sample)
+    return nq / (dt * n_total / ns), dt, cores
+
+
+def sample_bits(cfg, rows, nq, device):
+    mix = make_mixture(cfg["d"], cfg["C"], cfg["r"], cfg["s_sub"], cfg["s_n"], CORPUS_SEED, device)
+    X = torch.empty(rows, cfg["d"], dtype=torch.bfloat16, device=device)
+    draw_rows_into(mix, X, CORPUS_SEED, 0)
+    Q = torch.empty(nq, cfg["d"], dtype=torch.bfloat16, device=device)
+    draw_rows_into(mix, Q, QUERY_SEED, 0)
+    tob = lambda t: t.cpu().view(torch.int16).numpy().view(np.uint16)  # noqa: E731
+    return tob(X), tob(Q)
+
+
+def run_reference(args, cfg, name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    cores = oracle.num_threads()
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    rows = min(1 << 18, cfg["n"])
+    Xb, Qb = sample_bits(cfg, rows, cores, dev)
+    for _ in range(args.warmup):
+        cpu_oracle_sample(Xb, Qb, cfg["k"], cfg["n"])
+    vals, times = [], []
+    for _ in range(args.steps):
+        v, dt, _ = cpu_oracle_sample(Xb, Qb, cfg["k"], cfg["n"])
+        vals.append(v)
+        times.append(dt)
+    value = len(vals) * Qb.shape[0] / (sum(times) * cfg["n"] / rows)
+    sample = (f"{Qb.shape[0]} queries x first {rows} corpus rows per step, exact top-{cfg['k']} "
+              f"in fp64; q/s extrapolated x{rows}/{cfg['n']} to the full corpus")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times) * cfg["n"] / rows,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": workload_name(cfg, name, args.nprobe),
+                                        "n": cfg["n"], "d": cfg["d"], "nq": cfg["nq"], "k": cfg["k"]},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--nprobe", type=int, default=0)
+    ap.add_argument("--nq", type=int, default=None, help="override batch size")
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = dict(CONFIGS[args.config])
+    if args.nq:
+        cfg["nq"] = args.nq
+    if args.k:
+        cfg["k"] = args.k
+    if args.impl == "reference":
+        return run_reference(args, cfg, args.config)
+
+    import paper_2505_12065_b200 as sa
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = sa.Comm.from_torch_distributed(local)
+
+    n, d, nq, k = cfg["n"], cfg["d"], cfg["nq"], cfg["k"]
+    off, n_local = sa.shard_range(n, rank, world)
+    mix = make_mixture(d, cfg["C"], cfg["r"], cfg["s_sub"], cfg["s_n"], CORPUS_SEED, "cuda")
+    X = torch.empty(n_local, d, dtype=torch.bfloat16, device="cuda")
+    t0 = time.perf_counter()
+    draw_rows_into(mix, X, CORPUS_SEED, off)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    nlist = cfg.get("nlist", 0) if args.nprobe > 0 else 0
+    idx = sa.Index.build(X, nlist, row_offset=off, n_total=n, comm=comm)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    del X
+    torch.cuda.empty_cache()
+
+    nb = args.warmup + args.steps
+    Qall = torch.empty(nb * nq, d, dtype=torch.bfloat16, device="cuda")
+    draw_rows_into(mix, Qall, QUERY_SEED, 0)
+    batches = [Qall[i * nq:(i + 1) * nq] for i in range(nb)]
+    ids = torch.empty(nq, k, dtype=torch.int64, device="cuda")
+    scores = torch.empty(nq, k, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        idx.search(batches[i], k, args.nprobe, out=(ids, scores))
+    barrier()
+    sa.profile_enable(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lat = []
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for i in range(args.steps):
+            idx.search(batches[args.warmup + i], k, args.nprobe, out=(ids, scores))
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    kern = {kind: sa.profile_read(kind) for kind in sa.KERNEL_KINDS}
+    sa.profile_enable(False)
+    launches = sum(v[1] for v in kern.values())
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = args.steps * nq / (ms / 1e3)
+
+    # ---- end to end through the host-buffer C-ABI call (H2D + search + D2H per step)
+    qh = [batches[i].float().cpu().pin_memory() for i in range(nb)]
+    ids_h = torch.empty(nq, k, dtype=torch.int64).pin_memory()
+    sc_h = torch.empty(nq, k, dtype=torch.float32).pin_memory()
+    for i in range(args.warmup):
+        idx.search_host(qh[i], k, args.nprobe, out=(ids_h, sc_h))
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(args.steps):
+        t_s = time.perf_counter()
+        if i == 0:
+            e0.record(stream)
+        idx.search_host(qh[args.warmup + i], k, args.nprobe, out=(ids_h, sc_h))
+        lat.append(time.perf_counter() - t_s)
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = args.steps * nq / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel
+    pk = peaks()
+    if args.nprobe == 0:
+        fs_ms, fs_n = kern["flat_scan"]
+        per_launch = fs_ms / max(fs_n, 1)
+        flops = 2.0 * nq * n_local * d
+        achieved = flops / (per_launch / 1e3) / 1e12
+        roof = {"kernel": "flat_scan_topk_kernel", "bound": "tensor", "achieved": achieved,
+                "peak": pk["bf16"], "unit": "TFLOP/s", "frac": achieved / pk["bf16"],
+                "peak_kind": f"bf16 dense, {pk['src']} burst (MEASURED_PEAKS.json)",
+                "frac_of_sustained": achieved / pk["bf16_sus"] if pk["bf16_sus"] else None,
+                "kernel_ms": per_launch, "kernel_share_of_step": fs_ms / ms,
+                "traffic": traffic_from_profiles("flat_scan", args.config, nq)}
+    else:
+        sc_ms, sc_n = kern["ivf_scan"]
+        roof = {"kernel": "ivf_scan", "bound": "hbm", "achieved": None, "peak": pk["hbm"],
+                "unit": "GB/s", "frac": None, "traffic": None}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded low-rank Gaussian mixture, unit-norm; DESIGN.md §3)",
+        "config": {"workload": workload_name(cfg, args.config, args.nprobe), "n": n, "d": d,
+                   "nq": nq, "k": k, "nprobe": args.nprobe, "n_local": n_local,
+                   "parallelism": f"row-shard x{world}",
+                   "l2": "inputs larger than L2 (corpus 32 GB >> 126 MB); no flush"},
+        "roofline": roof,
+        "e2e": {"value": e2e_value, "unit": "queries/s",
+                "h2d_bytes_per_step": nq * d * 4, "d2h_bytes_per_step": nq * k * (8 + 4),
+                "p50_batch_ms": 1e3 * statistics.median(lat) if lat else None},
+        "gpu_launches": launches,
+        "kernel_ms": {kk: v[0] for kk, v in kern.items()},
+        "kernel_launches": {kk: v[1] for kk, v in kern.items()},
+        "clocks": clk.summary(),
+        "build_s": build_s, "gen_s": gen_s,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle  # cpu_baseline leg: the oracle as it stands, bounded sample
+        cores = oracle.num_threads()
+        rows = min(1 << 22, n)
+        Xb, Qb = sample_bits(cfg, rows, cores, "cuda")
+        v, dt, cores = cpu_oracle_sample(Xb, Qb, k, n)
+        line["cpu_baseline"] = {
+            "value": v, "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "sample": f"{cores} queries x first {rows} corpus rows ({dt:.1f} s), exact top-{k} "
+                      f"fp64; q/s scaled by {rows}/{n} to the full corpus"}
+    if rank == 0:
+        print(json.dumps(line))
+    idx.free()
+    if comm is not None:
+        comm.free()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def traffic_from_profiles(kernel, config, nq):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        j = json.load(open(p))
+        return j.get(f"{kernel}:{config}:nq{nq}")
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -8,6 +8,8 @@ App. B.3, "approximately 21 million text chunks ... embedded into a
 """
 from .synth import (  # noqa: F401
     CONFIGS,
+    CORPUS_SEED,
+    QUERY_SEED,
     Mixture,
     make_mixture,
     draw_rows,
