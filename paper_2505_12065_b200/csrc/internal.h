@@ -23,7 +23,8 @@ struct sa_index {
   int32_t nlist = 0;
   int64_t row_offset = 0, n_total = 0;
   __nv_bfloat16* X = nullptr;  // [n_local, d_pad] (list-major when nlist > 0)
-  CUtensorMap tmap_x;
+  CUtensorMap tmap_x;   // box 128 rows (cta_group 1)
+  CUtensorMap tmap_x2;  // box 64 rows (cta_group 2: each CTA of a pair stages half a tile)
   int32_t* row_ids = nullptr;  // nlist > 0: stored row -> global id (fits 32 bits)
   // IVF coarse quantiser
   float* centroids = nullptr;                // [nlist, d_pad] fp32 (unit norm)
@@ -48,6 +49,14 @@ sa_status make_tmap_bf16(CUtensorMap* m, const void* base, int64_t rows, int32_t
 void prof_count(int kind);
 void prof_begin(int kind, cudaStream_t s);
 void prof_end(int kind, cudaStream_t s);
+
+// Query padding / kernel variant: cta_group 2 (M=256 pairs) when more than one
+// 128-query block is searched, else cta_group 1.
+inline int flat_cta_group(int64_t nq) { return nq > 128 ? 2 : 1; }
+inline int64_t padded_nq(int64_t nq) {
+  const int64_t m = 128 * flat_cta_group(nq);
+  return (nq + m - 1) / m * m;
+}
 
 // Where a search writes its [nq, k] result: packed keys (for a cross-rank
 // merge) or unpacked (id, score) pairs.

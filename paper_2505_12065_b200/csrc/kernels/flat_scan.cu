@@ -8,19 +8,23 @@
 // so the score matrix never reaches HBM (BASELINE.json north_star).
 //
 // Mapping:
-//   * MMA M side = 128 queries of one query block.  The block's bf16 rows live
+//   * MMA M side = queries.  Each CTA keeps its block of 128 bf16 query rows
 //     in TMEM for the whole scan (A operand from TMEM, "TS" form): lane m =
-//     query m, columns [A_COL, A_COL + d_pad/2) hold its 2-packed bf16.
-//   * MMA N side = 64 corpus rows per tile, TMA-staged from HBM into a
-//     FS_STAGES-deep smem ring (128-byte swizzle, one 64x64 box per K-step).
-//   * fp32 accumulators: two 64-column TMEM buffers (cols 0 and 64) so the
-//     epilogue drains tile t while the tensor core computes tile t+1.
-//   * warp 0: TMA producer, warp 1: TMEM alloc + single-thread MMA issuer,
-//     warps 2..5: epilogue, thread = query (TMEM lane quadrant = warp % 4).
-//     Each epilogue thread keeps a size-k min-heap of packed keys; the
-//     per-tile fast path is a 64-way max + one compare against the heap root.
-//   * persistent grid: work item w = (query block qb, corpus slice s); slices
-//     partition the corpus tiles; partial top-k lists go to part[q][s][k].
+//     query m, 2-packed bf16 in columns [a_col, a_col + d_pad/2).
+//   * MMA N side = 128 corpus rows per tile, TMA-staged from HBM into an smem
+//     ring (128-byte swizzle, one box per 64-wide K step).
+//   * CG = 2: a cluster of two CTAs is one cta_group::2 MMA of M = 256 (two
+//     query blocks); each CTA stages half of the tile (64 rows) and the
+//     leader issues the MMAs, so every SM receives half the corpus bytes per
+//     FLOP of the CG = 1 layout (L2->SM traffic is the limiter).
+//   * fp32 accumulators: 128 TMEM columns per buffer; double-buffered when
+//     d_pad <= 512, single-buffered at d = 768 (A fills the other 384).
+//   * warp 0: TMA producer; warp 1: TMEM alloc + single-thread MMA issuer
+//     (leader CTA); warps 2..9: epilogue -- thread = (query, column half),
+//     each with a size-k min-heap of packed keys; per tile the fast path is
+//     a 64-way max and one compare against the heap root.
+//   * persistent grid: work item = (query group, corpus slice); partial
+//     lists go to part[q][slice][half][k] and are merged by merge.cu.
 #include <cuda_bf16.h>
 
 #include "flat_scan.cuh"
@@ -34,15 +38,21 @@ namespace {
 constexpr int kBM = FS_BM;
 constexpr int kBN = FS_BN;
 constexpr int kBK = FS_BK;
-constexpr int kStages = FS_STAGES;
-constexpr int kStageBytes = kBN * kBK * 2;  // 8 KB
-constexpr int kAccCols = kBN;               // fp32 columns per accumulator
-constexpr int kACol = 2 * kAccCols;         // A (queries) starts after two accumulators
+constexpr int kEpiT = FS_EPI_THREADS;
 constexpr uint32_t kTmemCols = 512;
 
+template <int CG>
+struct Cfg {
+  static constexpr int kRowsPerCta = kBN / CG;             // corpus rows staged per CTA per K step
+  static constexpr int kStageBytes = kRowsPerCta * kBK * 2;
+  static constexpr int kStages = CG == 1 ? 10 : 16;
+  static constexpr uint32_t kIdesc = ptx::umma_idesc_bf16(kBM * CG, kBN);
+};
+
+template <int CG>
 struct __align__(8) SmemTail {
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+  uint64_t full[Cfg<CG>::kStages];
+  uint64_t empty[Cfg<CG>::kStages];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
   uint64_t a_full;
@@ -53,7 +63,7 @@ __device__ __forceinline__ float heap_threshold(uint64_t root) {
   return root == 0ull ? -__int_as_float(0x7f800000) : key_score(root);
 }
 
-// Offer `key` to a size-k min-heap whose element i lives at h[i * kBM].
+// Offer `key` to a size-k min-heap whose element i lives at h[i * kEpiT].
 // Returns the new threshold score (score of the root).
 __device__ __noinline__ float heap_offer(uint64_t* h, int k, uint64_t key) {
   if (key <= h[0]) return heap_threshold(h[0]);
@@ -62,29 +72,29 @@ __device__ __noinline__ float heap_offer(uint64_t* h, int k, uint64_t key) {
     int l = 2 * i + 1;
     if (l >= k) break;
     int r = l + 1;
-    uint64_t hl = h[(size_t)l * kBM];
+    uint64_t hl = h[(size_t)l * kEpiT];
     int c = l;
     uint64_t hc = hl;
     if (r < k) {
-      uint64_t hr = h[(size_t)r * kBM];
+      uint64_t hr = h[(size_t)r * kEpiT];
       if (hr < hl) { c = r; hc = hr; }
     }
     if (hc >= key) break;
-    h[(size_t)i * kBM] = hc;
+    h[(size_t)i * kEpiT] = hc;
     i = c;
   }
-  h[(size_t)i * kBM] = key;
+  h[(size_t)i * kEpiT] = key;
   return heap_threshold(h[0]);
 }
 
 struct WorkItem {
-  int qb, s;
+  int qp, s;
   int64_t t0, t1;
 };
 
 __device__ __forceinline__ WorkItem work_item(int w, int S, int64_t T) {
   WorkItem wi;
-  wi.qb = w / S;
+  wi.qp = w / S;
   wi.s = w % S;
   wi.t0 = (int64_t)wi.s * T / S;
   wi.t1 = (int64_t)(wi.s + 1) * T / S;
@@ -93,174 +103,223 @@ __device__ __forceinline__ WorkItem work_item(int w, int S, int64_t T) {
 
 }  // namespace
 
+template <int CG>
 __global__ void __launch_bounds__(FS_THREADS, 1)
 flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScanArgs a) {
+  using C = Cfg<CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* stage_base = smem;
-  uint64_t* heap_s = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
-  SmemTail* tail =
-      reinterpret_cast<SmemTail*>(smem + kStages * kStageBytes + FS_KSMEM * kBM * sizeof(uint64_t));
+  uint64_t* heap_s = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  SmemTail<CG>* tail = reinterpret_cast<SmemTail<CG>*>(smem + C::kStages * C::kStageBytes +
+                                                       FS_KSMEM * kEpiT * sizeof(uint64_t));
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int unit = blockIdx.x / CG;        // CTA (CG=1) or CTA pair (CG=2)
+  const int n_units = gridDim.x / CG;
   const int S = a.S;
-  const int n_work = a.QB * S;
+  const int n_work = a.QP * S;
   const int64_t T = (a.n_rows + kBN - 1) / kBN;
   const int num_kb = a.d_pad / kBK;
+  const int nacc = (2 * kBN + a.d_pad / 2 <= (int)kTmemCols) ? 2 : 1;
+  const uint32_t a_col = (uint32_t)(nacc * kBN);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < C::kStages; ++i) {
       ptx::mbar_init(ptx::smem_u32(&tail->full[i]), 1);
       ptx::mbar_init(ptx::smem_u32(&tail->empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(ptx::smem_u32(&tail->tmem_full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&tail->tmem_empty[i]), 4);
+      ptx::mbar_init(ptx::smem_u32(&tail->tmem_empty[i]), FS_EPI_WARPS * CG);
     }
-    ptx::mbar_init(ptx::smem_u32(&tail->a_full), 4);
+    ptx::mbar_init(ptx::smem_u32(&tail->a_full), FS_EPI_WARPS * CG);
     ptx::fence_mbar_init();
     ptx::fence_proxy_async_smem();
   }
   if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
   if (warp == 1) {
-    ptx::tmem_alloc(ptx::smem_u32(&tail->tmem_base), kTmemCols);
-    ptx::tmem_relinquish();
+    if (CG == 2) {
+      ptx::tmem_alloc_2sm(ptx::smem_u32(&tail->tmem_base), kTmemCols);
+      ptx::tmem_relinquish_2sm();
+    } else {
+      ptx::tmem_alloc(ptx::smem_u32(&tail->tmem_base), kTmemCols);
+      ptx::tmem_relinquish();
+    }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = tail->tmem_base;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        WorkItem wi = work_item(w, S, T);
+      const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
+      for (int w = unit; w < n_work; w += n_units) {
+        const WorkItem wi = work_item(w, S, T);
         for (int64_t t = wi.t0; t < wi.t1; ++t) {
+          const int32_t row = (int32_t)(t * kBN) + (int32_t)rank * C::kRowsPerCta;
           for (int kb = 0; kb < num_kb; ++kb) {
             ptx::mbar_wait(ptx::smem_u32(&tail->empty[stage]), phase ^ 1);
-            const uint32_t fb = ptx::smem_u32(&tail->full[stage]);
-            ptx::mbar_arrive_expect_tx(fb, kStageBytes);
-            ptx::tma_load_2d(ptx::smem_u32(stage_base + stage * kStageBytes), &tmap_x, fb,
-                             kb * kBK, (int32_t)(t * kBN));
-            if (++stage == kStages) { stage = 0; phase ^= 1; }
+            const uint32_t dst = ptx::smem_u32(stage_base + stage * C::kStageBytes);
+            const uint32_t fb = full0 + stage * 8;
+            if (CG == 1) {
+              ptx::mbar_arrive_expect_tx(fb, C::kStageBytes);
+              ptx::tma_load_2d(dst, &tmap_x, fb, kb * kBK, row);
+            } else {
+              if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * C::kStageBytes);
+              ptx::tma_load_2d_2sm(dst, &tmap_x, ptx::mapa(fb, 0), kb * kBK, row);
+            }
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
           }
         }
+      }
+      // Drain: wait until every stage has been released by its final MMA commit, so no
+      // tcgen05.commit arrival can target this CTA's smem after it exits.
+      for (int i = 0; i < C::kStages; ++i) {
+        ptx::mbar_wait(ptx::smem_u32(&tail->empty[stage]), phase ^ 1);
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
-      const uint32_t idesc = ptx::umma_idesc_bf16(kBM, kBN);
+    // ===================== MMA issuer (leader CTA, one thread) =====================
+    if (leader && lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      int cur_qb = -1;
+      int cur_qp = -1;
       uint32_t a_phase = 0;
-      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-        WorkItem wi = work_item(w, S, T);
-        if (wi.qb != cur_qb) {
+      const uint32_t stage0 = ptx::smem_u32(stage_base);
+      const uint64_t desc0 = ptx::umma_desc_sw128(stage0);
+      const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
+      const uint32_t empty0 = ptx::smem_u32(&tail->empty[0]);
+      for (int w = unit; w < n_work; w += n_units) {
+        const WorkItem wi = work_item(w, S, T);
+        if (wi.qp != cur_qp) {
           ptx::mbar_wait(ptx::smem_u32(&tail->a_full), a_phase);
           a_phase ^= 1;
-          cur_qb = wi.qb;
+          cur_qp = wi.qp;
           ptx::tc_fence_after();
         }
         for (int64_t t = wi.t0; t < wi.t1; ++t) {
           ptx::mbar_wait(ptx::smem_u32(&tail->tmem_empty[acc]), acc_phase ^ 1);
           ptx::tc_fence_after();
-          const uint32_t d_tmem = tmem + acc * kAccCols;
+          const uint32_t d_tmem = tmem + (uint32_t)(acc * kBN);
+          uint32_t a_tmem = tmem + a_col;
           for (int kb = 0; kb < num_kb; ++kb) {
-            ptx::mbar_wait(ptx::smem_u32(&tail->full[stage]), phase);
+            ptx::mbar_wait(full0 + stage * 8, phase);
             ptx::tc_fence_after();
-            const uint64_t bdesc = ptx::umma_desc_sw128(ptx::smem_u32(stage_base + stage * kStageBytes));
+            const uint64_t bdesc = desc0 + (uint64_t)((stage * C::kStageBytes) >> 4);
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk) {
-              const uint32_t a_tmem = tmem + kACol + kb * (kBK / 2) + kk * 8;
-              ptx::mma_bf16_ts(d_tmem, a_tmem, bdesc + (uint64_t)(kk * 2), idesc,
-                               (kb | kk) != 0 ? 1u : 0u);
+              if (CG == 2)
+                ptx::mma_bf16_ts_2sm(d_tmem, a_tmem + kk * 8, bdesc + kk * 2, C::kIdesc,
+                                     (kb | kk) ? 1u : 0u);
+              else
+                ptx::mma_bf16_ts(d_tmem, a_tmem + kk * 8, bdesc + kk * 2, C::kIdesc,
+                                 (kb | kk) ? 1u : 0u);
             }
-            ptx::tc_commit(ptx::smem_u32(&tail->empty[stage]));
-            if (++stage == kStages) { stage = 0; phase ^= 1; }
+            if (CG == 2) ptx::tc_commit_2sm_mc(empty0 + stage * 8);
+            else ptx::tc_commit(empty0 + stage * 8);
+            a_tmem += kBK / 2;
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
           }
-          ptx::tc_commit(ptx::smem_u32(&tail->tmem_full[acc]));
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          if (CG == 2) ptx::tc_commit_2sm_mc(ptx::smem_u32(&tail->tmem_full[acc]));
+          else ptx::tc_commit(ptx::smem_u32(&tail->tmem_full[acc]));
+          if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
         }
       }
     }
     __syncwarp();
   } else {
-    // ===================== epilogue: 4 warps, thread = query =====================
-    const int quad = warp & 3;                 // TMEM lane quadrant this warp may access
-    const int rib = quad * 32 + lane;          // row in query block
+    // ===================== epilogue: 8 warps, thread = (query, column half) =====================
+    const int ew = warp - 2;
+    const int quad = warp & 3;               // TMEM lane quadrant this warp may access
+    const int half = ew >> 2;                // accumulator columns [half*64, half*64+64)
+    const int rib = quad * 32 + lane;        // query row within this CTA's block
+    const int et = ew * 32 + lane;           // epilogue thread index 0..255
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const int k = a.k;
-    uint64_t* heap = (k <= FS_KSMEM) ? (heap_s + rib)
-                                     : (a.heap_g + (size_t)blockIdx.x * k * kBM + rib);
-    for (int i = 0; i < k; ++i) heap[(size_t)i * kBM] = 0ull;
+    uint64_t* heap = (k <= FS_KSMEM) ? (heap_s + et)
+                                     : (a.heap_g + (size_t)blockIdx.x * k * kEpiT + et);
+    for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
     float thr = heap_threshold(0ull);
     int acc = 0;
     uint32_t acc_phase = 0;
-    int cur_qb = -1;
-    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
-      WorkItem wi = work_item(w, S, T);
-      const int64_t q = (int64_t)wi.qb * kBM + rib;
-      if (wi.qb != cur_qb) {
-        // Stage this query block into TMEM columns [kACol, kACol + d_pad/2).
-        // All MMAs reading the previous block completed before the previous
-        // item's last tmem_full commit, which this thread already consumed.
-        const uint4* src = reinterpret_cast<const uint4*>(a.Q + (size_t)q * a.d_pad);
-        for (int c = 0; c < num_kb; ++c) {
-          uint32_t r[32];
+    int cur_qp = -1;
+    const uint32_t a_full_leader = CG == 2 ? ptx::mapa(ptx::smem_u32(&tail->a_full), 0)
+                                           : ptx::smem_u32(&tail->a_full);
+    const uint32_t tmem_empty0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&tail->tmem_empty[0]), 0)
+                                         : ptx::smem_u32(&tail->tmem_empty[0]);
+    for (int w = unit; w < n_work; w += n_units) {
+      const WorkItem wi = work_item(w, S, T);
+      const int64_t q = ((int64_t)wi.qp * CG + rank) * kBM + rib;
+      if (wi.qp != cur_qp) {
+        // Stage this query block into TMEM.  All MMAs that read the previous
+        // block completed before the last tmem_full this thread consumed.
+        if (half == 0) {
+          const uint4* src = reinterpret_cast<const uint4*>(a.Q + (size_t)q * a.d_pad);
+          for (int c = 0; c < num_kb; ++c) {
+            uint32_t r[32];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            uint4 v = __ldg(src + c * 8 + i);
-            r[4 * i + 0] = v.x; r[4 * i + 1] = v.y; r[4 * i + 2] = v.z; r[4 * i + 3] = v.w;
+            for (int i = 0; i < 8; ++i) {
+              uint4 v = __ldg(src + c * 8 + i);
+              r[4 * i + 0] = v.x; r[4 * i + 1] = v.y; r[4 * i + 2] = v.z; r[4 * i + 3] = v.w;
+            }
+            ptx::tmem_st32(tmem + lane_addr + a_col + c * 32, r);
           }
-          ptx::tmem_st32(tmem + lane_addr + kACol + c * 32, r);
+          ptx::tmem_wait_st();
         }
-        ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&tail->a_full));
-        cur_qb = wi.qb;
+        if (lane == 0) {
+          if (CG == 2) ptx::mbar_arrive_cluster(a_full_leader);
+          else ptx::mbar_arrive(a_full_leader);
+        }
+        cur_qp = wi.qp;
       }
       for (int64_t t = wi.t0; t < wi.t1; ++t) {
         ptx::mbar_wait(ptx::smem_u32(&tail->tmem_full[acc]), acc_phase);
         ptx::tc_fence_after();
         uint32_t r0[32], r1[32];
-        ptx::tmem_ld32(tmem + lane_addr + acc * kAccCols, r0);
-        ptx::tmem_ld32(tmem + lane_addr + acc * kAccCols + 32, r1);
+        const uint32_t col = (uint32_t)(acc * kBN + half * 64);
+        ptx::tmem_ld32(tmem + lane_addr + col, r0);
+        ptx::tmem_ld32(tmem + lane_addr + col + 32, r1);
         ptx::tmem_wait_ld();
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&tail->tmem_empty[acc]));
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (lane == 0) {
+          if (CG == 2) ptx::mbar_arrive_cluster(tmem_empty0 + acc * 8);
+          else ptx::mbar_arrive(tmem_empty0 + acc * 8);
+        }
+        if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
 
-        const int64_t row0 = t * kBN;
+        const int64_t row0 = t * kBN + half * 64;
         if (a.mode == 1) {
           // debug: materialise the score tile (tests only)
-          if (q < a.nq_pad) {
-            float* dst = a.dbg + (size_t)q * a.n_rows;
+          float* dst = a.dbg + (size_t)q * a.n_rows;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (row0 + j < a.n_rows) dst[row0 + j] = __uint_as_float(r0[j]);
-              if (row0 + 32 + j < a.n_rows) dst[row0 + 32 + j] = __uint_as_float(r1[j]);
-            }
+          for (int j = 0; j < 32; ++j) {
+            if (row0 + j < a.n_rows) dst[row0 + j] = __uint_as_float(r0[j]);
+            if (row0 + 32 + j < a.n_rows) dst[row0 + 32 + j] = __uint_as_float(r1[j]);
           }
           continue;
         }
-        float m0 = __uint_as_float(r0[0]);
-        float m1 = __uint_as_float(r1[0]);
+        float m0 = fmaxf(__uint_as_float(r0[0]), __uint_as_float(r0[1]));
+        float m1 = fmaxf(__uint_as_float(r1[0]), __uint_as_float(r1[1]));
 #pragma unroll
-        for (int j = 1; j < 32; ++j) {
-          m0 = fmaxf(m0, __uint_as_float(r0[j]));
-          m1 = fmaxf(m1, __uint_as_float(r1[j]));
+        for (int j = 2; j < 32; j += 2) {
+          m0 = fmaxf(m0, fmaxf(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1])));
+          m1 = fmaxf(m1, fmaxf(__uint_as_float(r1[j]), __uint_as_float(r1[j + 1])));
         }
         if (fmaxf(m0, m1) >= thr) {
 #pragma unroll
@@ -269,7 +328,8 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
             if (s >= thr) {
               const int64_t row = row0 + j;
               if (row < a.n_rows) {
-                const uint32_t id = a.id_base + (a.row_ids ? (uint32_t)a.row_ids[row] : (uint32_t)row);
+                const uint32_t id =
+                    a.id_base + (a.row_ids ? (uint32_t)a.row_ids[row] : (uint32_t)row);
                 thr = heap_offer(heap, k, make_key(s, id));
               }
             }
@@ -278,10 +338,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
       }
       if (a.mode == 0) {
         // flush this work item's partial list and reset the heap
-        uint64_t* dst = a.part + ((size_t)q * S + wi.s) * k;
+        uint64_t* dst = a.part + (((size_t)q * S + wi.s) * FS_LISTS_PER_ITEM + half) * k;
         for (int i = 0; i < k; ++i) {
-          dst[i] = heap[(size_t)i * kBM];
-          heap[(size_t)i * kBM] = 0ull;
+          dst[i] = heap[(size_t)i * kEpiT];
+          heap[(size_t)i * kEpiT] = 0ull;
         }
         thr = heap_threshold(0ull);
       }
@@ -289,30 +349,55 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) ptx::cluster_sync(); else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, kTmemCols);
+    if (CG == 2) ptx::tmem_dealloc_2sm(tmem, kTmemCols);
+    else ptx::tmem_dealloc(tmem, kTmemCols);
   }
 }
 
-size_t flat_scan_smem_bytes() {
-  return 1024 + (size_t)kStages * kStageBytes + (size_t)FS_KSMEM * kBM * sizeof(uint64_t) +
-         sizeof(SmemTail);
+size_t flat_scan_smem_bytes(int cta_group) {
+  if (cta_group == 2)
+    return 1024 + (size_t)Cfg<2>::kStages * Cfg<2>::kStageBytes +
+           (size_t)FS_KSMEM * kEpiT * sizeof(uint64_t) + sizeof(SmemTail<2>);
+  return 1024 + (size_t)Cfg<1>::kStages * Cfg<1>::kStageBytes +
+         (size_t)FS_KSMEM * kEpiT * sizeof(uint64_t) + sizeof(SmemTail<1>);
 }
 
-cudaError_t launch_flat_scan(const CUtensorMap& tmap, const FlatScanArgs& a, int grid,
-                             cudaStream_t stream) {
-  static bool attr_set = false;
-  const size_t smem = flat_scan_smem_bytes();
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(flat_scan_topk_kernel,
+cudaError_t launch_flat_scan(const CUtensorMap& tmap, const FlatScanArgs& a, int cta_group,
+                             int grid, cudaStream_t stream) {
+  const size_t smem = flat_scan_smem_bytes(cta_group);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(FS_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cta_group;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cta_group == 2) {
+    static bool set2 = false;
+    if (!set2) {
+      cudaError_t e = cudaFuncSetAttribute(flat_scan_topk_kernel<2>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      set2 = true;
+    }
+    return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<2>, tmap, a);
+  }
+  static bool set1 = false;
+  if (!set1) {
+    cudaError_t e = cudaFuncSetAttribute(flat_scan_topk_kernel<1>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    set1 = true;
   }
-  flat_scan_topk_kernel<<<grid, FS_THREADS, smem, stream>>>(tmap, a);
-  return cudaGetLastError();
+  return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<1>, tmap, a);
 }
 
 }  // namespace sa

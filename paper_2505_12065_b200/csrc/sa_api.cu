@@ -129,19 +129,31 @@ static sa_status dalloc(T** p, size_t count, cudaStream_t s, const char* what) {
 }
 
 // ====================================================================== flat search
+// Plan of one flat scan: units (CTAs or CTA pairs), corpus slices and grid.
+struct FlatPlan {
+  int cg, QP, S, grid;
+};
+static FlatPlan plan_flat(const sa_index* idx, int64_t nq_pad) {
+  FlatPlan p;
+  p.cg = nq_pad > 128 ? 2 : 1;
+  const int64_t T = (idx->n_local + FS_BN - 1) / FS_BN;
+  p.QP = (int)(nq_pad / (FS_BM * p.cg));
+  const int units = idx->num_sms / p.cg;
+  int64_t S = std::max<int64_t>(1, units / p.QP);
+  S = std::min<int64_t>(S, T);
+  p.S = (int)S;
+  p.grid = (int)std::min<int64_t>(units, (int64_t)p.QP * S) * p.cg;
+  return p;
+}
+
 sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
                       int32_t k, const SearchOut& out, cudaStream_t s) {
-  const int64_t T = (idx->n_local + FS_BN - 1) / FS_BN;
-  const int32_t QB = (int32_t)(nq_pad / FS_BM);
-  int64_t S = std::max<int64_t>(1, idx->num_sms / QB);
-  S = std::min<int64_t>(S, T);
-  const int grid = (int)std::min<int64_t>(idx->num_sms, (int64_t)QB * S);
-
+  const FlatPlan p = plan_flat(idx, nq_pad);
   uint64_t *part = nullptr, *heap = nullptr;
-  sa_status st = dalloc(&part, (size_t)nq_pad * S * k, s, "alloc partials");
+  sa_status st = dalloc(&part, (size_t)nq_pad * p.S * FS_LISTS_PER_ITEM * k, s, "alloc partials");
   if (st != SA_OK) return st;
   if (k > FS_KSMEM) {
-    st = dalloc(&heap, (size_t)grid * k * FS_BM, s, "alloc heaps");
+    st = dalloc(&heap, (size_t)p.grid * k * FS_EPI_THREADS, s, "alloc heaps");
     if (st != SA_OK) { cudaFreeAsync(part, s); return st; }
   }
   FlatScanArgs a{};
@@ -149,8 +161,8 @@ sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, 
   a.nq_pad = nq_pad;
   a.d_pad = idx->d_pad;
   a.n_rows = idx->n_local;
-  a.QB = QB;
-  a.S = (int32_t)S;
+  a.QP = p.QP;
+  a.S = p.S;
   a.k = k;
   a.row_ids = idx->row_ids;
   a.id_base = idx->row_ids ? 0u : (uint32_t)idx->row_offset;
@@ -158,15 +170,15 @@ sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, 
   a.heap_g = heap;
   a.mode = 0;
   prof_begin(SA_KERNEL_FLAT_SCAN, s);
-  cudaError_t e = launch_flat_scan(idx->tmap_x, a, grid, s);
+  cudaError_t e = launch_flat_scan(p.cg == 2 ? idx->tmap_x2 : idx->tmap_x, a, p.cg, p.grid, s);
   prof_end(SA_KERNEL_FLAT_SCAN, s);
   prof_count(SA_KERNEL_FLAT_SCAN);
   if (e == cudaSuccess) {
     MergeArgs m{};
     m.cand = part;
-    m.groups = (int32_t)S;
+    m.groups = p.S * FS_LISTS_PER_ITEM;
     m.k = k;
-    m.qstride = S * k;
+    m.qstride = (int64_t)p.S * FS_LISTS_PER_ITEM * k;
     m.gstride = k;
     m.out_keys = out.keys;
     m.out_ids = out.ids;
@@ -350,6 +362,7 @@ sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nl
   }
   if (st == SA_OK && nlist > 0) st = ivf_build(idx, *opts, s);
   if (st == SA_OK) st = make_tmap_bf16(&idx->tmap_x, idx->X, n, d_pad, FS_BN);
+  if (st == SA_OK) st = make_tmap_bf16(&idx->tmap_x2, idx->X, n, d_pad, FS_BN / 2);
   if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "build sync");
   if (st != SA_OK) {
     sa_index_free(idx);
@@ -379,7 +392,7 @@ sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype
   if (st != SA_OK) return st;
   if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t nq_pad = (nq + FS_BM - 1) / FS_BM * FS_BM;
+  const int64_t nq_pad = padded_nq(nq);
   __nv_bfloat16* Qs = nullptr;
   st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "alloc staged queries");
   if (st != SA_OK) return st;
@@ -505,7 +518,7 @@ sa_status sa_search_probes(const sa_index* idx, const void* queries, int64_t nq,
   if (idx->nlist == 0) return set_error(SA_ERR_STATE, "flat-only index");
   if (nprobe < 1 || nprobe > idx->nlist) return set_error(SA_ERR_INVALID_ARG, "bad nprobe");
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t nq_pad = (nq + FS_BM - 1) / FS_BM * FS_BM;
+  const int64_t nq_pad = padded_nq(nq);
   __nv_bfloat16* Qs = nullptr;
   sa_status st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "alloc staged queries");
   if (st != SA_OK) return st;
@@ -521,7 +534,7 @@ sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, 
   if (!idx || !queries || !out_scores) return set_error(SA_ERR_INVALID_ARG, "null pointer");
   if (nq < 1) return set_error(SA_ERR_INVALID_ARG, "nq must be >= 1");
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t nq_pad = (nq + FS_BM - 1) / FS_BM * FS_BM;
+  const int64_t nq_pad = padded_nq(nq);
   __nv_bfloat16* Qs = nullptr;
   float* dbg = nullptr;
   sa_status st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "alloc staged queries");
@@ -530,21 +543,18 @@ sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, 
     st = cuda_status(launch_cast_pad(queries, false, nq, idx->d, Qs, nq_pad, idx->d_pad,
                                      idx->num_sms, s), "stage queries");
   if (st == SA_OK) {
-    const int64_t T = (idx->n_local + FS_BN - 1) / FS_BN;
-    const int32_t QB = (int32_t)(nq_pad / FS_BM);
-    int64_t S = std::min<int64_t>(std::max<int64_t>(1, idx->num_sms / QB), T);
+    const FlatPlan p = plan_flat(idx, nq_pad);
     FlatScanArgs a{};
     a.Q = Qs;
     a.nq_pad = nq_pad;
     a.d_pad = idx->d_pad;
     a.n_rows = idx->n_local;
-    a.QB = QB;
-    a.S = (int32_t)S;
+    a.QP = p.QP;
+    a.S = p.S;
     a.k = 1;
     a.dbg = dbg;
     a.mode = 1;
-    st = cuda_status(launch_flat_scan(idx->tmap_x, a,
-                                      (int)std::min<int64_t>(idx->num_sms, QB * S), s),
+    st = cuda_status(launch_flat_scan(p.cg == 2 ? idx->tmap_x2 : idx->tmap_x, a, p.cg, p.grid, s),
                      "debug scan");
   }
   if (st == SA_OK)
