@@ -9,16 +9,19 @@
 //
 // Mapping:
 //   * MMA M side = queries.  Each CTA keeps its block of 128 bf16 query rows
-//     in TMEM for the whole scan (A operand from TMEM, "TS" form): lane m =
-//     query m, 2-packed bf16 in columns [a_col, a_col + d_pad/2).
+//     resident for the whole scan: the first FS_KB_TMEM K-blocks in TMEM (A
+//     operand from TMEM, "TS" form: lane m = query m, 2-packed bf16 columns),
+//     any remaining K-blocks (d = 768: 4 of 12) in a 64 KB smem region read
+//     with the SS form.  That keeps 256 TMEM columns free for two fp32
+//     accumulator buffers at every d <= 768.
 //   * MMA N side = 128 corpus rows per tile, TMA-staged from HBM into an smem
 //     ring (128-byte swizzle, one box per 64-wide K step).
 //   * CG = 2: a cluster of two CTAs is one cta_group::2 MMA of M = 256 (two
 //     query blocks); each CTA stages half of the tile (64 rows) and the
 //     leader issues the MMAs, so every SM receives half the corpus bytes per
 //     FLOP of the CG = 1 layout (L2->SM traffic is the limiter).
-//   * fp32 accumulators: 128 TMEM columns per buffer; double-buffered when
-//     d_pad <= 512, single-buffered at d = 768 (A fills the other 384).
+//   * fp32 accumulators: two 128-column TMEM buffers, so the epilogue drains
+//     tile t while the tensor core computes tile t+1.
 //   * warp 0: TMA producer; warp 1: TMEM alloc + single-thread MMA issuer
 //     (leader CTA); warps 2..9: epilogue -- thread = (query, column half),
 //     each with a size-k min-heap of packed keys; per tile the fast path is
@@ -40,12 +43,13 @@ constexpr int kBN = FS_BN;
 constexpr int kBK = FS_BK;
 constexpr int kEpiT = FS_EPI_THREADS;
 constexpr uint32_t kTmemCols = 512;
+constexpr int kASmemKb = FS_BM * FS_BK * 2;  // one 128-row x 64-col K-block of A in smem: 16 KB
 
 template <int CG>
 struct Cfg {
   static constexpr int kRowsPerCta = kBN / CG;             // corpus rows staged per CTA per K step
   static constexpr int kStageBytes = kRowsPerCta * kBK * 2;
-  static constexpr int kStages = CG == 1 ? 10 : 16;
+  static constexpr int kStages = CG == 1 ? 7 : 14;
   static constexpr uint32_t kIdesc = ptx::umma_idesc_bf16(kBM * CG, kBN);
 };
 
@@ -56,6 +60,7 @@ struct __align__(8) SmemTail {
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
   uint64_t a_full;
+  uint64_t a_tma;
   uint32_t tmem_base;
 };
 
@@ -105,14 +110,16 @@ __device__ __forceinline__ WorkItem work_item(int w, int S, int64_t T) {
 
 template <int CG>
 __global__ void __launch_bounds__(FS_THREADS, 1)
-flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScanArgs a) {
+flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                      const __grid_constant__ CUtensorMap tmap_q, const FlatScanArgs a) {
   using C = Cfg<CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* stage_base = smem;
-  uint64_t* heap_s = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
-  SmemTail<CG>* tail = reinterpret_cast<SmemTail<CG>*>(smem + C::kStages * C::kStageBytes +
+  uint8_t* a_smem = smem + C::kStages * C::kStageBytes;  // [FS_KB_SMEM][128 rows][128 B], SW128
+  uint64_t* heap_s = reinterpret_cast<uint64_t*>(a_smem + FS_KB_SMEM * kASmemKb);
+  SmemTail<CG>* tail = reinterpret_cast<SmemTail<CG>*>(reinterpret_cast<uint8_t*>(heap_s) +
                                                        FS_KSMEM * kEpiT * sizeof(uint64_t));
 
   const int warp = threadIdx.x / 32;
@@ -125,8 +132,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
   const int n_work = a.QP * S;
   const int64_t T = (a.n_rows + kBN - 1) / kBN;
   const int num_kb = a.d_pad / kBK;
-  const int nacc = (2 * kBN + a.d_pad / 2 <= (int)kTmemCols) ? 2 : 1;
-  const uint32_t a_col = (uint32_t)(nacc * kBN);
+  const int nacc = 2;
+  const uint32_t a_col = (uint32_t)(nacc * kBN);          // A (TMEM part) after the accumulators
+  const int kb_t = num_kb < FS_KB_TMEM ? num_kb : FS_KB_TMEM;  // K-blocks of A held in TMEM
+  const int kb_s = num_kb - kb_t;                         // K-blocks of A held in smem
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::kStages; ++i) {
@@ -138,10 +147,14 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
       ptx::mbar_init(ptx::smem_u32(&tail->tmem_empty[i]), FS_EPI_WARPS * CG);
     }
     ptx::mbar_init(ptx::smem_u32(&tail->a_full), FS_EPI_WARPS * CG);
+    ptx::mbar_init(ptx::smem_u32(&tail->a_tma), 1);
     ptx::fence_mbar_init();
     ptx::fence_proxy_async_smem();
   }
-  if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmap_x);
+    if (kb_s > 0) ptx::prefetch_tmap(&tmap_q);
+  }
   if (warp == 1) {
     if (CG == 2) {
       ptx::tmem_alloc_2sm(ptx::smem_u32(&tail->tmem_base), kTmemCols);
@@ -200,6 +213,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
       uint32_t a_phase = 0;
       const uint32_t stage0 = ptx::smem_u32(stage_base);
       const uint64_t desc0 = ptx::umma_desc_sw128(stage0);
+      const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(a_smem));
       const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
       const uint32_t empty0 = ptx::smem_u32(&tail->empty[0]);
       for (int w = unit; w < n_work; w += n_units) {
@@ -219,14 +233,25 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
             ptx::mbar_wait(full0 + stage * 8, phase);
             ptx::tc_fence_after();
             const uint64_t bdesc = desc0 + (uint64_t)((stage * C::kStageBytes) >> 4);
+            if (kb < kb_t) {
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-              if (CG == 2)
-                ptx::mma_bf16_ts_2sm(d_tmem, a_tmem + kk * 8, bdesc + kk * 2, C::kIdesc,
-                                     (kb | kk) ? 1u : 0u);
-              else
-                ptx::mma_bf16_ts(d_tmem, a_tmem + kk * 8, bdesc + kk * 2, C::kIdesc,
-                                 (kb | kk) ? 1u : 0u);
+              for (int kk = 0; kk < kBK / 16; ++kk) {
+                if (CG == 2)
+                  ptx::mma_bf16_ts_2sm(d_tmem, a_tmem + kk * 8, bdesc + kk * 2, C::kIdesc,
+                                       (kb | kk) ? 1u : 0u);
+                else
+                  ptx::mma_bf16_ts(d_tmem, a_tmem + kk * 8, bdesc + kk * 2, C::kIdesc,
+                                   (kb | kk) ? 1u : 0u);
+              }
+            } else {
+              const uint64_t adesc = adesc0 + (uint64_t)(((kb - kb_t) * kASmemKb) >> 4);
+#pragma unroll
+              for (int kk = 0; kk < kBK / 16; ++kk) {
+                if (CG == 2)
+                  ptx::mma_bf16_ss_2sm(d_tmem, adesc + kk * 2, bdesc + kk * 2, C::kIdesc, 1u);
+                else
+                  ptx::mma_bf16_ss(d_tmem, adesc + kk * 2, bdesc + kk * 2, C::kIdesc, 1u);
+              }
             }
             if (CG == 2) ptx::tc_commit_2sm_mc(empty0 + stage * 8);
             else ptx::tc_commit(empty0 + stage * 8);
@@ -256,6 +281,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
     int acc = 0;
     uint32_t acc_phase = 0;
     int cur_qp = -1;
+    uint32_t a_tma_phase = 0;
     const uint32_t a_full_leader = CG == 2 ? ptx::mapa(ptx::smem_u32(&tail->a_full), 0)
                                            : ptx::smem_u32(&tail->a_full);
     const uint32_t tmem_empty0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&tail->tmem_empty[0]), 0)
@@ -266,9 +292,19 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
       if (wi.qp != cur_qp) {
         // Stage this query block into TMEM.  All MMAs that read the previous
         // block completed before the last tmem_full this thread consumed.
+        const bool tma_thread = (ew == 0 && lane == 0 && kb_s > 0);
+        if (tma_thread) {
+          // K-blocks [kb_t, num_kb) of this CTA's 128 query rows -> smem (SS operand)
+          const uint32_t bar = ptx::smem_u32(&tail->a_tma);
+          ptx::mbar_arrive_expect_tx(bar, (uint32_t)(kb_s * kASmemKb));
+          const int32_t qrow0 = (int32_t)(((int64_t)wi.qp * CG + rank) * kBM);
+          for (int j = 0; j < kb_s; ++j)
+            ptx::tma_load_2d(ptx::smem_u32(a_smem + j * kASmemKb), &tmap_q, bar,
+                             (kb_t + j) * kBK, qrow0);
+        }
         if (half == 0) {
           const uint4* src = reinterpret_cast<const uint4*>(a.Q + (size_t)q * a.d_pad);
-          for (int c = 0; c < num_kb; ++c) {
+          for (int c = 0; c < kb_t; ++c) {
             uint32_t r[32];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -279,11 +315,15 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
           }
           ptx::tmem_wait_st();
         }
+        if (tma_thread) {
+          ptx::mbar_wait(ptx::smem_u32(&tail->a_tma), a_tma_phase);
+          a_tma_phase ^= 1;
+        }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if (CG == 2) ptx::mbar_arrive_cluster(a_full_leader);
-          else ptx::mbar_arrive(a_full_leader);
+          if (CG == 2 && !leader) ptx::mbar_arrive_cluster(a_full_leader);
+          else ptx::mbar_arrive(ptx::smem_u32(&tail->a_full));
         }
         cur_qp = wi.qp;
       }
@@ -298,8 +338,8 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if (CG == 2) ptx::mbar_arrive_cluster(tmem_empty0 + acc * 8);
-          else ptx::mbar_arrive(tmem_empty0 + acc * 8);
+          if (CG == 2 && !leader) ptx::mbar_arrive_cluster(tmem_empty0 + acc * 8);
+          else ptx::mbar_arrive(ptx::smem_u32(&tail->tmem_empty[acc]));
         }
         if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
 
@@ -358,15 +398,14 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x, const FlatScan
 }
 
 size_t flat_scan_smem_bytes(int cta_group) {
+  const size_t fixed = (size_t)FS_KB_SMEM * kASmemKb + (size_t)FS_KSMEM * kEpiT * sizeof(uint64_t);
   if (cta_group == 2)
-    return 1024 + (size_t)Cfg<2>::kStages * Cfg<2>::kStageBytes +
-           (size_t)FS_KSMEM * kEpiT * sizeof(uint64_t) + sizeof(SmemTail<2>);
-  return 1024 + (size_t)Cfg<1>::kStages * Cfg<1>::kStageBytes +
-         (size_t)FS_KSMEM * kEpiT * sizeof(uint64_t) + sizeof(SmemTail<1>);
+    return 1024 + (size_t)Cfg<2>::kStages * Cfg<2>::kStageBytes + fixed + sizeof(SmemTail<2>);
+  return 1024 + (size_t)Cfg<1>::kStages * Cfg<1>::kStageBytes + fixed + sizeof(SmemTail<1>);
 }
 
-cudaError_t launch_flat_scan(const CUtensorMap& tmap, const FlatScanArgs& a, int cta_group,
-                             int grid, cudaStream_t stream) {
+cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_q,
+                             const FlatScanArgs& a, int cta_group, int grid, cudaStream_t stream) {
   const size_t smem = flat_scan_smem_bytes(cta_group);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
@@ -388,7 +427,7 @@ cudaError_t launch_flat_scan(const CUtensorMap& tmap, const FlatScanArgs& a, int
       if (e != cudaSuccess) return e;
       set2 = true;
     }
-    return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<2>, tmap, a);
+    return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<2>, tmap, tmap_q, a);
   }
   static bool set1 = false;
   if (!set1) {
@@ -397,7 +436,7 @@ cudaError_t launch_flat_scan(const CUtensorMap& tmap, const FlatScanArgs& a, int
     if (e != cudaSuccess) return e;
     set1 = true;
   }
-  return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<1>, tmap, a);
+  return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<1>, tmap, tmap_q, a);
 }
 
 }  // namespace sa

@@ -15,7 +15,9 @@ constexpr int FS_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, 64 columns
 constexpr int FS_THREADS = 64 + 32 * FS_EPI_WARPS;  // warp 0 TMA, warp 1 MMA, 8 epilogue warps
 constexpr int FS_EPI_THREADS = 32 * FS_EPI_WARPS;
 constexpr int FS_KSMEM = 16;     // heaps live in smem for k <= 16, else in global scratch
-constexpr int FS_MAX_DPAD = 768; // A operand in TMEM: FS_BN + d_pad/2 <= 512 columns
+constexpr int FS_MAX_DPAD = 768; // queries: up to 8 K-blocks in TMEM + 4 in smem
+constexpr int FS_KB_TMEM = 8;    // K-blocks of the A operand held in TMEM (256 columns)
+constexpr int FS_KB_SMEM = 4;    // K-blocks of the A operand held in smem (64 KB)
 constexpr int FS_LISTS_PER_ITEM = 2;  // partial lists per (query, work item): one per column half
 
 struct FlatScanArgs {
@@ -37,7 +39,9 @@ struct FlatScanArgs {
 // cta_group = 1: one CTA per query block of 128 (M=128, box 128 rows).
 // cta_group = 2: CTA pairs (cluster of 2) share each corpus tile, M=256 (box 64 rows per CTA).
 size_t flat_scan_smem_bytes(int cta_group);
-cudaError_t launch_flat_scan(const CUtensorMap& tmap, const FlatScanArgs& a, int cta_group,
-                             int grid, cudaStream_t stream);
+// tmap: corpus rows (box 128 rows for cta_group 1, 64 for 2); tmap_q: the staged queries
+// (box 128 rows), used for the K-blocks of the A operand that live in smem.
+cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_q,
+                             const FlatScanArgs& a, int cta_group, int grid, cudaStream_t stream);
 
 }  // namespace sa

@@ -169,8 +169,16 @@ sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, 
   a.part = part;
   a.heap_g = heap;
   a.mode = 0;
+  CUtensorMap tmap_q;
+  st = make_tmap_bf16(&tmap_q, Qs, nq_pad, idx->d_pad, FS_BM);
+  if (st != SA_OK) {
+    if (heap) cudaFreeAsync(heap, s);
+    cudaFreeAsync(part, s);
+    return st;
+  }
   prof_begin(SA_KERNEL_FLAT_SCAN, s);
-  cudaError_t e = launch_flat_scan(p.cg == 2 ? idx->tmap_x2 : idx->tmap_x, a, p.cg, p.grid, s);
+  cudaError_t e =
+      launch_flat_scan(p.cg == 2 ? idx->tmap_x2 : idx->tmap_x, tmap_q, a, p.cg, p.grid, s);
   prof_end(SA_KERNEL_FLAT_SCAN, s);
   prof_count(SA_KERNEL_FLAT_SCAN);
   if (e == cudaSuccess) {
@@ -554,8 +562,12 @@ sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, 
     a.k = 1;
     a.dbg = dbg;
     a.mode = 1;
-    st = cuda_status(launch_flat_scan(p.cg == 2 ? idx->tmap_x2 : idx->tmap_x, a, p.cg, p.grid, s),
-                     "debug scan");
+    CUtensorMap tmap_q;
+    st = make_tmap_bf16(&tmap_q, Qs, nq_pad, idx->d_pad, FS_BM);
+    if (st == SA_OK)
+      st = cuda_status(
+          launch_flat_scan(p.cg == 2 ? idx->tmap_x2 : idx->tmap_x, tmap_q, a, p.cg, p.grid, s),
+          "debug scan");
   }
   if (st == SA_OK)
     st = cuda_status(cudaMemcpyAsync(out_scores, dbg, (size_t)nq * idx->n_local * 4,
