@@ -45,11 +45,14 @@ constexpr int kEpiT = FS_EPI_THREADS;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kASmemKb = FS_BM * FS_BK * 2;  // one 128-row x 64-col K-block of A in smem: 16 KB
 
+constexpr int kKbPerStage = 2;  // K-blocks (64 wide) per ring stage: 8 MMAs per barrier round trip
+
 template <int CG>
 struct Cfg {
-  static constexpr int kRowsPerCta = kBN / CG;             // corpus rows staged per CTA per K step
-  static constexpr int kStageBytes = kRowsPerCta * kBK * 2;
-  static constexpr int kStages = CG == 1 ? 7 : 14;
+  static constexpr int kRowsPerCta = kBN / CG;              // corpus rows staged per CTA per tile
+  static constexpr int kBoxBytes = kRowsPerCta * kBK * 2;  // one TMA box: rows x 64 bf16
+  static constexpr int kStageBytes = kBoxBytes * kKbPerStage;
+  static constexpr int kStages = CG == 1 ? 4 : 9;          // 128 / 144 KB of corpus in flight
   static constexpr uint32_t kIdesc = ptx::umma_idesc_bf16(kBM * CG, kBN);
 };
 
@@ -118,9 +121,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                              ~uintptr_t(1023));
   uint8_t* stage_base = smem;
   uint8_t* a_smem = smem + C::kStages * C::kStageBytes;  // [FS_KB_SMEM][128 rows][128 B], SW128
-  uint64_t* heap_s = reinterpret_cast<uint64_t*>(a_smem + FS_KB_SMEM * kASmemKb);
-  SmemTail<CG>* tail = reinterpret_cast<SmemTail<CG>*>(reinterpret_cast<uint8_t*>(heap_s) +
-                                                       FS_KSMEM * kEpiT * sizeof(uint64_t));
+  SmemTail<CG>* tail = reinterpret_cast<SmemTail<CG>*>(a_smem + FS_KB_SMEM * kASmemKb);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -169,6 +170,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
   ptx::tc_fence_after();
   const uint32_t tmem = tail->tmem_base;
 
+  const int n_sl = (num_kb + kKbPerStage - 1) / kKbPerStage;  // ring stages per tile
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
@@ -179,16 +181,21 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         const WorkItem wi = work_item(w, S, T);
         for (int64_t t = wi.t0; t < wi.t1; ++t) {
           const int32_t row = (int32_t)(t * kBN) + (int32_t)rank * C::kRowsPerCta;
-          for (int kb = 0; kb < num_kb; ++kb) {
+          for (int sl = 0; sl < n_sl; ++sl) {
+            const int kb0 = sl * kKbPerStage;
+            const int nkb = num_kb - kb0 < kKbPerStage ? num_kb - kb0 : kKbPerStage;
             ptx::mbar_wait(ptx::smem_u32(&tail->empty[stage]), phase ^ 1);
             const uint32_t dst = ptx::smem_u32(stage_base + stage * C::kStageBytes);
             const uint32_t fb = full0 + stage * 8;
             if (CG == 1) {
-              ptx::mbar_arrive_expect_tx(fb, C::kStageBytes);
-              ptx::tma_load_2d(dst, &tmap_x, fb, kb * kBK, row);
+              ptx::mbar_arrive_expect_tx(fb, nkb * C::kBoxBytes);
+              for (int j = 0; j < nkb; ++j)
+                ptx::tma_load_2d(dst + j * C::kBoxBytes, &tmap_x, fb, (kb0 + j) * kBK, row);
             } else {
-              if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * C::kStageBytes);
-              ptx::tma_load_2d_2sm(dst, &tmap_x, ptx::mapa(fb, 0), kb * kBK, row);
+              if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * nkb * C::kBoxBytes);
+              const uint32_t fbl = ptx::mapa(fb, 0);
+              for (int j = 0; j < nkb; ++j)
+                ptx::tma_load_2d_2sm(dst + j * C::kBoxBytes, &tmap_x, fbl, (kb0 + j) * kBK, row);
             }
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
           }
@@ -203,16 +210,15 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ===================== MMA issuer (leader CTA, one thread) =====================
-    if (leader && lane == 0) {
+    // ===================== MMA issuer (leader CTA; warp-convergent, elect.sync issues) ======
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       int cur_qp = -1;
       uint32_t a_phase = 0;
-      const uint32_t stage0 = ptx::smem_u32(stage_base);
-      const uint64_t desc0 = ptx::umma_desc_sw128(stage0);
+      const uint64_t desc0 = ptx::umma_desc_sw128(ptx::smem_u32(stage_base));
       const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(a_smem));
       const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
       const uint32_t empty0 = ptx::smem_u32(&tail->empty[0]);
@@ -228,38 +234,34 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           ptx::mbar_wait(ptx::smem_u32(&tail->tmem_empty[acc]), acc_phase ^ 1);
           ptx::tc_fence_after();
           const uint32_t d_tmem = tmem + (uint32_t)(acc * kBN);
-          uint32_t a_tmem = tmem + a_col;
-          for (int kb = 0; kb < num_kb; ++kb) {
+          for (int sl = 0; sl < n_sl; ++sl) {
             ptx::mbar_wait(full0 + stage * 8, phase);
             ptx::tc_fence_after();
-            const uint64_t bdesc = desc0 + (uint64_t)((stage * C::kStageBytes) >> 4);
-            if (kb < kb_t) {
+            const uint64_t sdesc = desc0 + (uint64_t)((stage * C::kStageBytes) >> 4);
 #pragma unroll
-              for (int kk = 0; kk < kBK / 16; ++kk) {
-                if (CG == 2)
-                  ptx::mma_bf16_ts_2sm(d_tmem, a_tmem + kk * 8, bdesc + kk * 2, C::kIdesc,
-                                       (kb | kk) ? 1u : 0u);
-                else
-                  ptx::mma_bf16_ts(d_tmem, a_tmem + kk * 8, bdesc + kk * 2, C::kIdesc,
-                                   (kb | kk) ? 1u : 0u);
-              }
-            } else {
-              const uint64_t adesc = adesc0 + (uint64_t)(((kb - kb_t) * kASmemKb) >> 4);
+            for (int j = 0; j < kKbPerStage; ++j) {
+              const int kb = sl * kKbPerStage + j;
+              if (kb < num_kb) {
+                const uint64_t bdesc = sdesc + (uint64_t)((j * C::kBoxBytes) >> 4);
+                if (kb < kb_t) {
+                  const uint32_t a_tmem = tmem + a_col + (uint32_t)(kb * (kBK / 2));
 #pragma unroll
-              for (int kk = 0; kk < kBK / 16; ++kk) {
-                if (CG == 2)
-                  ptx::mma_bf16_ss_2sm(d_tmem, adesc + kk * 2, bdesc + kk * 2, C::kIdesc, 1u);
-                else
-                  ptx::mma_bf16_ss(d_tmem, adesc + kk * 2, bdesc + kk * 2, C::kIdesc, 1u);
+                  for (int kk = 0; kk < kBK / 16; ++kk)
+                    ptx::mma_bf16_elect<CG, true>(d_tmem, a_tmem + kk * 8, bdesc + kk * 2,
+                                                  C::kIdesc, (kb | kk) ? 1u : 0u);
+                } else {
+                  const uint64_t adesc = adesc0 + (uint64_t)(((kb - kb_t) * kASmemKb) >> 4);
+#pragma unroll
+                  for (int kk = 0; kk < kBK / 16; ++kk)
+                    ptx::mma_bf16_elect<CG, false>(d_tmem, adesc + kk * 2, bdesc + kk * 2,
+                                                   C::kIdesc, 1u);
+                }
               }
             }
-            if (CG == 2) ptx::tc_commit_2sm_mc(empty0 + stage * 8);
-            else ptx::tc_commit(empty0 + stage * 8);
-            a_tmem += kBK / 2;
+            ptx::tc_commit_elect<CG>(empty0 + stage * 8);
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
           }
-          if (CG == 2) ptx::tc_commit_2sm_mc(ptx::smem_u32(&tail->tmem_full[acc]));
-          else ptx::tc_commit(ptx::smem_u32(&tail->tmem_full[acc]));
+          ptx::tc_commit_elect<CG>(ptx::smem_u32(&tail->tmem_full[acc]));
           if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
         }
       }
@@ -274,9 +276,11 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     const int et = ew * 32 + lane;           // epilogue thread index 0..255
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const int k = a.k;
-    uint64_t* heap = (k <= FS_KSMEM) ? (heap_s + et)
-                                     : (a.heap_g + (size_t)blockIdx.x * k * kEpiT + et);
-    for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
+    // Heaps live in global scratch (L1/L2 resident; touched only on insertions), which
+    // leaves the smem to the TMA ring.
+    uint64_t* heap = a.heap_g + (size_t)blockIdx.x * k * kEpiT + et;
+    if (a.mode == 0)
+      for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
     float thr = heap_threshold(0ull);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -398,7 +402,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
 }
 
 size_t flat_scan_smem_bytes(int cta_group) {
-  const size_t fixed = (size_t)FS_KB_SMEM * kASmemKb + (size_t)FS_KSMEM * kEpiT * sizeof(uint64_t);
+  const size_t fixed = (size_t)FS_KB_SMEM * kASmemKb;
   if (cta_group == 2)
     return 1024 + (size_t)Cfg<2>::kStages * Cfg<2>::kStageBytes + fixed + sizeof(SmemTail<2>);
   return 1024 + (size_t)Cfg<1>::kStages * Cfg<1>::kStageBytes + fixed + sizeof(SmemTail<1>);

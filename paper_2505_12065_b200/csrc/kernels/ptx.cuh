@@ -228,6 +228,58 @@ __device__ __forceinline__ void mma_bf16_ts_2sm(uint32_t d_tmem, uint32_t a_tmem
       : "memory");
 }
 
+
+// ---------------------------------------------------------------- warp-convergent MMA issue
+// The whole warp executes these with identical operands; elect.sync picks one lane to
+// issue, so ptxas can keep the operands in uniform registers (no per-MMA waterfall).
+template <int CG, bool A_TMEM>
+__device__ __forceinline__ void mma_bf16_elect(uint32_t d_tmem, uint64_t a, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  if constexpr (A_TMEM) {
+    if constexpr (CG == 2)
+      asm volatile(
+          "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+          "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "r"((uint32_t)a), "l"(b_desc), "r"(idesc), "r"(accumulate)
+          : "memory");
+    else
+      asm volatile(
+          "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+          "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "r"((uint32_t)a), "l"(b_desc), "r"(idesc), "r"(accumulate)
+          : "memory");
+  } else {
+    if constexpr (CG == 2)
+      asm volatile(
+          "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+          "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "l"(a), "l"(b_desc), "r"(idesc), "r"(accumulate)
+          : "memory");
+    else
+      asm volatile(
+          "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+          "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "l"(a), "l"(b_desc), "r"(idesc), "r"(accumulate)
+          : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
+  if constexpr (CG == 2)
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+        "[%0], %1;\n}\n" ::"r"(bar),
+        "h"((uint16_t)3)
+        : "memory");
+  else
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+            bar)
+        : "memory");
+}
+
 // ---------------------------------------------------------------- descriptors
 // UMMA shared-memory descriptor, K-major operand staged by TMA with 128-byte swizzle:
 // rows of 64 bf16 (128 B), 8-row core groups 1024 B apart (SBO), LBO unused (=1),
