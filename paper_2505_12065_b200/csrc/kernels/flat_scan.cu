@@ -52,7 +52,7 @@ struct Cfg {
   static constexpr int kRowsPerCta = kBN / CG;              // corpus rows staged per CTA per tile
   static constexpr int kBoxBytes = kRowsPerCta * kBK * 2;  // one TMA box: rows x 64 bf16
   static constexpr int kStageBytes = kBoxBytes * kKbPerStage;
-  static constexpr int kStages = CG == 1 ? 4 : 9;          // 128 / 144 KB of corpus in flight
+  static constexpr int kStages = CG == 1 ? 3 : 7;          // 96 / 112 KB of corpus in flight
   static constexpr uint32_t kIdesc = ptx::umma_idesc_bf16(kBM * CG, kBN);
 };
 
@@ -121,7 +121,9 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                              ~uintptr_t(1023));
   uint8_t* stage_base = smem;
   uint8_t* a_smem = smem + C::kStages * C::kStageBytes;  // [FS_KB_SMEM][128 rows][128 B], SW128
-  SmemTail<CG>* tail = reinterpret_cast<SmemTail<CG>*>(a_smem + FS_KB_SMEM * kASmemKb);
+  uint64_t* heap_s = reinterpret_cast<uint64_t*>(a_smem + FS_KB_SMEM * kASmemKb);
+  SmemTail<CG>* tail = reinterpret_cast<SmemTail<CG>*>(reinterpret_cast<uint8_t*>(heap_s) +
+                                                       FS_KSMEM * kEpiT * sizeof(uint64_t));
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -276,9 +278,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     const int et = ew * 32 + lane;           // epilogue thread index 0..255
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const int k = a.k;
-    // Heaps live in global scratch (L1/L2 resident; touched only on insertions), which
-    // leaves the smem to the TMA ring.
-    uint64_t* heap = a.heap_g + (size_t)blockIdx.x * k * kEpiT + et;
+    // Heaps live in smem for k <= FS_KSMEM (insertions are latency-critical: the epilogue
+    // must finish a tile within one MMA tile time), else in global scratch.
+    uint64_t* heap = (k <= FS_KSMEM) ? (heap_s + et)
+                                     : (a.heap_g + (size_t)blockIdx.x * k * kEpiT + et);
     if (a.mode == 0)
       for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
     float thr = heap_threshold(0ull);
@@ -402,7 +405,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
 }
 
 size_t flat_scan_smem_bytes(int cta_group) {
-  const size_t fixed = (size_t)FS_KB_SMEM * kASmemKb;
+  const size_t fixed = (size_t)FS_KB_SMEM * kASmemKb + (size_t)FS_KSMEM * kEpiT * sizeof(uint64_t);
   if (cta_group == 2)
     return 1024 + (size_t)Cfg<2>::kStages * Cfg<2>::kStageBytes + fixed + sizeof(SmemTail<2>);
   return 1024 + (size_t)Cfg<1>::kStages * Cfg<1>::kStageBytes + fixed + sizeof(SmemTail<1>);

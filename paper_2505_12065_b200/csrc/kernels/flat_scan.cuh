@@ -17,6 +17,7 @@ constexpr int FS_EPI_THREADS = 32 * FS_EPI_WARPS;
 constexpr int FS_MAX_DPAD = 768; // queries: up to 8 K-blocks in TMEM + 4 in smem
 constexpr int FS_KB_TMEM = 8;    // K-blocks of the A operand held in TMEM (256 columns)
 constexpr int FS_KB_SMEM = 4;    // K-blocks of the A operand held in smem (64 KB)
+constexpr int FS_KSMEM = 16;     // running heaps in smem for k <= 16, else in global scratch
 constexpr int FS_LISTS_PER_ITEM = 2;  // partial lists per (query, work item): one per column half
 
 struct FlatScanArgs {
@@ -30,7 +31,7 @@ struct FlatScanArgs {
   const int32_t* row_ids;  // optional row -> id map (nullptr: id = row)
   uint32_t id_base;        // added to the id stored in each key
   uint64_t* part;          // out: [nq_pad][S][FS_LISTS_PER_ITEM][k] packed keys (unordered)
-  uint64_t* heap_g;        // scratch [grid][k][FS_EPI_THREADS]: per-thread running heaps
+  uint64_t* heap_g;        // scratch [grid][k][FS_EPI_THREADS] when k > FS_KSMEM
   float* dbg;              // mode 1: [nq_pad][n_rows] raw scores
   int32_t mode;            // 0 = top-k, 1 = debug score dump
 };

@@ -152,8 +152,10 @@ sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, 
   uint64_t *part = nullptr, *heap = nullptr;
   sa_status st = dalloc(&part, (size_t)nq_pad * p.S * FS_LISTS_PER_ITEM * k, s, "alloc partials");
   if (st != SA_OK) return st;
-  st = dalloc(&heap, (size_t)p.grid * k * FS_EPI_THREADS, s, "alloc heaps");
-  if (st != SA_OK) { cudaFreeAsync(part, s); return st; }
+  if (k > FS_KSMEM) {
+    st = dalloc(&heap, (size_t)p.grid * k * FS_EPI_THREADS, s, "alloc heaps");
+    if (st != SA_OK) { cudaFreeAsync(part, s); return st; }
+  }
   FlatScanArgs a{};
   a.Q = Qs;
   a.nq_pad = nq_pad;
