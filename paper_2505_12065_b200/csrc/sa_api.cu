@@ -352,6 +352,16 @@ sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nl
   if (st != SA_OK) return st;
 
   cudaStream_t s = (cudaStream_t)opts->stream;
+  {
+    // Search scratch comes from the stream-ordered pool; keep freed blocks cached instead
+    // of returning them to the driver at every synchronisation (which would make the next
+    // cudaMallocAsync map fresh pages inside the timed search path).
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   sa_index* idx = new sa_index;
   idx->device = dev;
   idx->num_sms = sms;
