@@ -28,6 +28,12 @@
 //     a 64-way max and one compare against the heap root.
 //   * persistent grid: work item = (query group, corpus slice); partial
 //     lists go to part[q][slice][half][k] and are merged by merge.cu.
+//   * FS_MODE_IVF (list-major IVF scan, §8(a) a8): work item = (inverted
+//     list, block of <= 128 queries that probe it, row chunk).  The query
+//     rows are gathered into the A operand per item, the list's rows stream
+//     through the same TMA ring, and each (query, item) writes its partial
+//     list to the query's own output slot -- one read of a list serves every
+//     query that probes it.
 #include <cuda_bf16.h>
 
 #include "flat_scan.cuh"
@@ -95,17 +101,45 @@ __device__ __noinline__ float heap_offer(uint64_t* h, int k, uint64_t key) {
   return heap_threshold(h[0]);
 }
 
+// One unit of work for all three roles (producer, MMA, epilogue decode it identically).
 struct WorkItem {
-  int qp, s;
-  int64_t t0, t1;
+  int qkey;          // query-block identity (flat: query group); -1 = always reload (ivf)
+  int s;             // flat: corpus slice
+  int64_t t0, t1;    // tile range
+  int64_t row_base;  // first corpus row of tile 0
+  int64_t row_end;   // rows >= row_end are masked (list end / corpus end)
+  int chunk;         // ivf: chunk index within the list
+  int e0, cnt;       // ivf: probing queries lq_ent[e0, e0 + cnt)
 };
 
-__device__ __forceinline__ WorkItem work_item(int w, int S, int64_t T) {
+__device__ __forceinline__ WorkItem work_item(int w, const FlatScanArgs& a, int64_t T) {
   WorkItem wi;
-  wi.qp = w / S;
-  wi.s = w % S;
-  wi.t0 = (int64_t)wi.s * T / S;
-  wi.t1 = (int64_t)(wi.s + 1) * T / S;
+  if (a.mode == FS_MODE_IVF) {
+    const int4 it = a.items[w];
+    const int64_t lo = a.list_off[it.x], hi = a.list_off[it.x + 1];
+    const int64_t r0 = lo + (int64_t)it.z * a.chunk_rows;
+    const int64_t r1 = hi < r0 + a.chunk_rows ? hi : r0 + a.chunk_rows;
+    wi.qkey = -1;
+    wi.s = 0;
+    wi.t0 = 0;
+    wi.t1 = (r1 - r0 + FS_BN - 1) / FS_BN;
+    wi.row_base = r0;
+    wi.row_end = r1;
+    wi.chunk = it.z;
+    wi.e0 = a.lq_off[it.x] + it.y * FS_BM;
+    const int rem = a.lq_off[it.x + 1] - wi.e0;
+    wi.cnt = rem < FS_BM ? rem : FS_BM;
+  } else {
+    wi.qkey = w / a.S;
+    wi.s = w % a.S;
+    wi.t0 = (int64_t)wi.s * T / a.S;
+    wi.t1 = (int64_t)(wi.s + 1) * T / a.S;
+    wi.row_base = 0;
+    wi.row_end = a.n_rows;
+    wi.chunk = 0;
+    wi.e0 = 0;
+    wi.cnt = 0;
+  }
   return wi;
 }
 
@@ -132,7 +166,8 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
   const int unit = blockIdx.x / CG;        // CTA (CG=1) or CTA pair (CG=2)
   const int n_units = gridDim.x / CG;
   const int S = a.S;
-  const int n_work = a.QP * S;
+  const bool ivf = a.mode == FS_MODE_IVF;
+  const int n_work = ivf ? *a.n_items : a.QP * S;
   const int64_t T = (a.n_rows + kBN - 1) / kBN;
   const int num_kb = a.d_pad / kBK;
   const int nacc = 2;
@@ -180,9 +215,9 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       uint32_t phase = 0;
       const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
       for (int w = unit; w < n_work; w += n_units) {
-        const WorkItem wi = work_item(w, S, T);
+        const WorkItem wi = work_item(w, a, T);
         for (int64_t t = wi.t0; t < wi.t1; ++t) {
-          const int32_t row = (int32_t)(t * kBN) + (int32_t)rank * C::kRowsPerCta;
+          const int32_t row = (int32_t)(wi.row_base + t * kBN) + (int32_t)rank * C::kRowsPerCta;
           for (int sl = 0; sl < n_sl; ++sl) {
             const int kb0 = sl * kKbPerStage;
             const int nkb = num_kb - kb0 < kKbPerStage ? num_kb - kb0 : kKbPerStage;
@@ -225,11 +260,11 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
       const uint32_t empty0 = ptx::smem_u32(&tail->empty[0]);
       for (int w = unit; w < n_work; w += n_units) {
-        const WorkItem wi = work_item(w, S, T);
-        if (wi.qp != cur_qp) {
+        const WorkItem wi = work_item(w, a, T);
+        if (wi.qkey < 0 || wi.qkey != cur_qp) {
           ptx::mbar_wait(ptx::smem_u32(&tail->a_full), a_phase);
           a_phase ^= 1;
-          cur_qp = wi.qp;
+          cur_qp = wi.qkey;
           ptx::tc_fence_after();
         }
         for (int64_t t = wi.t0; t < wi.t1; ++t) {
@@ -282,7 +317,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // must finish a tile within one MMA tile time), else in global scratch.
     uint64_t* heap = (k <= FS_KSMEM) ? (heap_s + et)
                                      : (a.heap_g + (size_t)blockIdx.x * k * kEpiT + et);
-    if (a.mode == 0)
+    if (a.mode != FS_MODE_DEBUG)
       for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
     float thr = heap_threshold(0ull);
     int acc = 0;
@@ -294,33 +329,63 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     const uint32_t tmem_empty0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&tail->tmem_empty[0]), 0)
                                          : ptx::smem_u32(&tail->tmem_empty[0]);
     for (int w = unit; w < n_work; w += n_units) {
-      const WorkItem wi = work_item(w, S, T);
-      const int64_t q = ((int64_t)wi.qp * CG + rank) * kBM + rib;
-      if (wi.qp != cur_qp) {
-        // Stage this query block into TMEM.  All MMAs that read the previous
+      const WorkItem wi = work_item(w, a, T);
+      // This thread's query: flat -> row of the staged batch; ivf -> gathered prober.
+      int64_t q;
+      int probe_j = 0;
+      bool valid;
+      if (ivf) {
+        valid = rib < wi.cnt;
+        if (valid) {
+          const int2 e = a.lq_ent[wi.e0 + rib];
+          q = e.x;
+          probe_j = e.y;
+        } else {
+          q = 0;
+        }
+      } else {
+        q = ((int64_t)wi.qkey * CG + rank) * kBM + rib;
+        valid = q < a.nq;
+      }
+      if (wi.qkey < 0 || wi.qkey != cur_qp) {
+        // Stage this query block into the A operand.  All MMAs that read the previous
         // block completed before the last tmem_full this thread consumed.
-        const bool tma_thread = (ew == 0 && lane == 0 && kb_s > 0);
+        const bool tma_thread = (!ivf && ew == 0 && lane == 0 && kb_s > 0);
         if (tma_thread) {
           // K-blocks [kb_t, num_kb) of this CTA's 128 query rows -> smem (SS operand)
           const uint32_t bar = ptx::smem_u32(&tail->a_tma);
           ptx::mbar_arrive_expect_tx(bar, (uint32_t)(kb_s * kASmemKb));
-          const int32_t qrow0 = (int32_t)(((int64_t)wi.qp * CG + rank) * kBM);
+          const int32_t qrow0 = (int32_t)(((int64_t)wi.qkey * CG + rank) * kBM);
           for (int j = 0; j < kb_s; ++j)
             ptx::tma_load_2d(ptx::smem_u32(a_smem + j * kASmemKb), &tmap_q, bar,
                              (kb_t + j) * kBK, qrow0);
         }
         if (half == 0) {
+          // Rows of absent queries are left as they are: MMA output rows are independent
+          // and the epilogue never reads the rows of invalid lanes.
           const uint4* src = reinterpret_cast<const uint4*>(a.Q + (size_t)q * a.d_pad);
           for (int c = 0; c < kb_t; ++c) {
             uint32_t r[32];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              uint4 v = __ldg(src + c * 8 + i);
+              uint4 v = valid ? __ldg(src + c * 8 + i) : make_uint4(0, 0, 0, 0);
               r[4 * i + 0] = v.x; r[4 * i + 1] = v.y; r[4 * i + 2] = v.z; r[4 * i + 3] = v.w;
             }
             ptx::tmem_st32(tmem + lane_addr + a_col + c * 32, r);
           }
           ptx::tmem_wait_st();
+          if (ivf && valid) {
+            // smem K-blocks of a gathered row, written in the 128-byte-swizzled K-major
+            // layout the UMMA descriptor expects (16-byte chunk c of row r at c ^ (r & 7)).
+            for (int j = 0; j < kb_s; ++j) {
+              uint8_t* blk = a_smem + j * kASmemKb + (rib >> 3) * 1024 + (rib & 7) * 128;
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                *reinterpret_cast<uint4*>(blk + ((c ^ (rib & 7)) << 4)) =
+                    __ldg(src + (kb_t + j) * 8 + c);
+            }
+            ptx::fence_proxy_async_smem();
+          }
         }
         if (tma_thread) {
           ptx::mbar_wait(ptx::smem_u32(&tail->a_tma), a_tma_phase);
@@ -332,7 +397,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           if (CG == 2 && !leader) ptx::mbar_arrive_cluster(a_full_leader);
           else ptx::mbar_arrive(ptx::smem_u32(&tail->a_full));
         }
-        cur_qp = wi.qp;
+        cur_qp = wi.qkey;
       }
       for (int64_t t = wi.t0; t < wi.t1; ++t) {
         ptx::mbar_wait(ptx::smem_u32(&tail->tmem_full[acc]), acc_phase);
@@ -349,9 +414,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           else ptx::mbar_arrive(ptx::smem_u32(&tail->tmem_empty[acc]));
         }
         if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
+        if (!valid) continue;
 
-        const int64_t row0 = t * kBN + half * 64;
-        if (a.mode == 1) {
+        const int64_t row0 = wi.row_base + t * kBN + half * 64;
+        if (a.mode == FS_MODE_DEBUG) {
           // debug: materialise the score tile (tests only)
           float* dst = a.dbg + (size_t)q * a.n_rows;
 #pragma unroll
@@ -374,7 +440,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const float s = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
             if (s >= thr) {
               const int64_t row = row0 + j;
-              if (row < a.n_rows) {
+              if (row < wi.row_end) {
                 const uint32_t id =
                     a.id_base + (a.row_ids ? (uint32_t)a.row_ids[row] : (uint32_t)row);
                 thr = heap_offer(heap, k, make_key(s, id));
@@ -383,13 +449,15 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           }
         }
       }
-      if (a.mode == 0) {
+      if (a.mode != FS_MODE_DEBUG) {
         // flush this work item's partial list and reset the heap
-        uint64_t* dst = a.part + (((size_t)q * S + wi.s) * FS_LISTS_PER_ITEM + half) * k;
-        for (int i = 0; i < k; ++i) {
-          dst[i] = heap[(size_t)i * kEpiT];
-          heap[(size_t)i * kEpiT] = 0ull;
+        if (valid) {
+          const size_t slot = ivf ? (size_t)(a.q_slot[(size_t)q * a.nprobe + probe_j] + wi.chunk)
+                                  : (size_t)q * S + wi.s;
+          uint64_t* dst = a.part + (slot * FS_LISTS_PER_ITEM + half) * k;
+          for (int i = 0; i < k; ++i) dst[i] = heap[(size_t)i * kEpiT];
         }
+        for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
         thr = heap_threshold(0ull);
       }
     }

@@ -20,27 +20,44 @@ constexpr int FS_KB_SMEM = 4;    // K-blocks of the A operand held in smem (64 K
 constexpr int FS_KSMEM = 16;     // running heaps in smem for k <= 16, else in global scratch
 constexpr int FS_LISTS_PER_ITEM = 2;  // partial lists per (query, work item): one per column half
 
+enum FlatScanMode : int32_t {
+  FS_MODE_TOPK = 0,   // flat: work item = (query group, corpus slice)
+  FS_MODE_DEBUG = 1,  // flat, raw score dump (tests)
+  FS_MODE_IVF = 2,    // grouped: work item = (inverted list, block of <=128 probing queries, chunk)
+};
+
 struct FlatScanArgs {
-  const __nv_bfloat16* Q;  // staged queries [nq_pad, d_pad] bf16, zero padded
-  int64_t nq_pad;          // multiple of FS_BM * cta_group
+  const __nv_bfloat16* Q;  // staged queries [>= nq rows, d_pad] bf16, zero padded columns
+  int64_t nq;              // real query rows (rows >= nq are never read)
+  int64_t nq_pad;          // multiple of FS_BM * cta_group (flat modes)
   int32_t d_pad;           // multiple of 64, <= FS_MAX_DPAD
-  int64_t n_rows;          // corpus rows scanned (the tensor map covers exactly these)
-  int32_t QP;              // query groups = nq_pad / (FS_BM * cta_group)
-  int32_t S;               // corpus slices per query group
+  int64_t n_rows;          // corpus rows (the tensor map covers exactly these)
+  int32_t QP;              // flat: query groups = nq_pad / (FS_BM * cta_group)
+  int32_t S;               // flat: corpus slices per query group
   int32_t k;               // 1..256
   const int32_t* row_ids;  // optional row -> id map (nullptr: id = row)
   uint32_t id_base;        // added to the id stored in each key
-  uint64_t* part;          // out: [nq_pad][S][FS_LISTS_PER_ITEM][k] packed keys (unordered)
+  uint64_t* part;          // flat out: [nq_pad][S][FS_LISTS_PER_ITEM][k] packed keys (unordered)
+                           // ivf out:  [slot][FS_LISTS_PER_ITEM][k]
   uint64_t* heap_g;        // scratch [grid][k][FS_EPI_THREADS] when k > FS_KSMEM
-  float* dbg;              // mode 1: [nq_pad][n_rows] raw scores
-  int32_t mode;            // 0 = top-k, 1 = debug score dump
+  float* dbg;              // debug: [nq_pad][n_rows] raw scores
+  int32_t mode;            // FlatScanMode
+  // ---- FS_MODE_IVF (cta_group 1 only)
+  const int4* items;       // [*n_items] {list, query block, chunk, 0}
+  const int32_t* n_items;  // device scalar
+  const int64_t* list_off; // [nlist + 1] stored-row range of each list
+  const int32_t* lq_off;   // [nlist + 1] range of each list in lq_ent
+  const int2* lq_ent;      // (query, probe rank) pairs grouped by list
+  const int64_t* q_slot;   // [nq * nprobe] first output slot of (query, probe rank)
+  int32_t nprobe;
+  int32_t chunk_rows;      // rows per IVF work item (multiple of FS_BN)
 };
 
 // cta_group = 1: one CTA per query block of 128 (M=128, box 128 rows).
 // cta_group = 2: CTA pairs (cluster of 2) share each corpus tile, M=256 (box 64 rows per CTA).
 size_t flat_scan_smem_bytes(int cta_group);
 // tmap: corpus rows (box 128 rows for cta_group 1, 64 for 2); tmap_q: the staged queries
-// (box 128 rows), used for the K-blocks of the A operand that live in smem.
+// (box 128 rows, rows = nq), used for the K-blocks of the A operand that live in smem.
 cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_q,
                              const FlatScanArgs& a, int cta_group, int grid, cudaStream_t stream);
 

@@ -158,6 +158,7 @@ sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, 
   }
   FlatScanArgs a{};
   a.Q = Qs;
+  a.nq = nq;
   a.nq_pad = nq_pad;
   a.d_pad = idx->d_pad;
   a.n_rows = idx->n_local;
@@ -564,6 +565,7 @@ sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, 
     const FlatPlan p = plan_flat(idx, nq_pad);
     FlatScanArgs a{};
     a.Q = Qs;
+    a.nq = nq;
     a.nq_pad = nq_pad;
     a.d_pad = idx->d_pad;
     a.n_rows = idx->n_local;
