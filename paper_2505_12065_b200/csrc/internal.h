@@ -29,10 +29,11 @@ struct sa_index {
   // IVF coarse quantiser
   float* centroids = nullptr;                // [nlist, d_pad] fp32 (unit norm)
   __nv_bfloat16* centroids_bf16 = nullptr;   // [nlist, d_pad]
-  CUtensorMap tmap_c;
+  CUtensorMap tmap_c;    // centroids, box 128 rows (cta_group 1)
+  CUtensorMap tmap_c2;   // centroids, box 64 rows (cta_group 2)
   int64_t* list_off = nullptr;               // device [nlist + 1]
   std::vector<int64_t> h_list_off;           // host copy
-  int32_t max_list = 0;
+  int64_t max_list = 0;
   const sa_comm* comm = nullptr;
 };
 
@@ -66,9 +67,28 @@ struct SearchOut {
   float* scores = nullptr;
 };
 
-// exact flat scan + intra-GPU merge (flat.cu / sa_api.cu)
+// A matrix scanned by the flat kernel: the index corpus, or the IVF centroids.
+struct CorpusView {
+  const CUtensorMap* tmap1;  // box 128 rows (cta_group 1)
+  const CUtensorMap* tmap2;  // box 64 rows (cta_group 2)
+  int64_t n_rows;
+  int32_t d_pad;
+  const int32_t* row_ids;    // stored row -> global id, or nullptr (id = id_base + row)
+  uint32_t id_base;
+};
+
+// exact scan of `cv` for nq staged queries (bf16 [>= nq, d_pad]) + intra-GPU merge (sa_api.cu)
+sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
+                           int32_t k, const SearchOut& out, cudaStream_t s);
 sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
                       int32_t k, const SearchOut& out, cudaStream_t s);
+
+template <typename T>
+sa_status dalloc(T** p, size_t count, cudaStream_t s, const char* what) {
+  *p = nullptr;
+  if (count == 0) return SA_OK;
+  return cuda_status(cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), s), what);
+}
 
 // IVF (ivf.cu)
 sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s);

@@ -1,16 +1,342 @@
-// ivf.cu -- IVF coarse quantiser build and search (placeholder until the IVF kernels land).
+// ivf.cu -- IVF coarse quantiser build and IVF search (§8(a) a2, a3, a7, a8).
+//
+// The paper's retriever is an HNSW graph whose "search range" trades recall for
+// effort (§2.2.1; App. B.3 efSearch).  BJ
+// replaces it with an inverted-file index whose nprobe knob plays that role.
+// Everything that is a dense contraction runs on the tcgen05 flat kernel:
+//   * k-means assignment (a2) and the full assignment (a3): queries = rows,
+//     corpus = the bf16 centroids, k = 1 (ties -> lowest list id, R8);
+//   * the probe (a7): queries x centroids, k = nprobe (ties -> lowest id, R11);
+//   * the list scan (a8): the flat kernel's list-major IVF mode.
+// The rest (sample gather, stable sort by list, deterministic centroid update,
+// empty-list repair, probe inversion) is SIMT glue in ivf_kernels.cu.
+#include <algorithm>
+#include <vector>
+
 #include "internal.h"
+#include "kernels/flat_scan.cuh"
+#include "kernels/ivf_kernels.cuh"
+#include "kernels/merge.cuh"
 
 namespace sa {
-sa_status ivf_build(sa_index*, const sa_build_opts&, cudaStream_t) {
-  return set_error(SA_ERR_UNSUPPORTED, "IVF build not available in this build");
+
+namespace {
+constexpr int kChunkRows = 4096;  // rows per IVF work item (multiple of FS_BN)
+
+struct Freer {
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  ~Freer() {
+    for (void* p : ptrs)
+      if (p) cudaFreeAsync(p, s);
+  }
+  template <typename T>
+  T* add(T* p) {
+    ptrs.push_back(p);
+    return p;
+  }
+};
+
+#define SA_TRY(expr)                   \
+  do {                                 \
+    sa_status _st = (expr);            \
+    if (_st != SA_OK) return _st;      \
+  } while (0)
+#define SA_CUDA(expr, what) SA_TRY(cuda_status((expr), (what)))
+
+// Stable sort of rows by list id + CSR offsets: perm = rows in list-major order (ascending row
+// inside a list), off[nlist + 1].
+sa_status sort_by_list(const int64_t* ids, int64_t n, int nlist, int num_sms, int32_t* perm,
+                       int64_t* off, cudaStream_t s) {
+  Freer f{s};
+  int32_t *keys, *ktmp, *vtmp, *kout;
+  int64_t *counts, *offs, *scratch, *hist;
+  const int64_t cs = sort_counts_size(n);
+  SA_TRY(dalloc(&keys, n, s, "sort keys"));
+  f.add(keys);
+  SA_TRY(dalloc(&ktmp, n, s, "sort tmp"));
+  f.add(ktmp);
+  SA_TRY(dalloc(&vtmp, n, s, "sort tmp"));
+  f.add(vtmp);
+  SA_TRY(dalloc(&kout, n, s, "sort out"));
+  f.add(kout);
+  SA_TRY(dalloc(&counts, cs, s, "sort counts"));
+  f.add(counts);
+  SA_TRY(dalloc(&offs, cs + 1, s, "sort offs"));
+  f.add(offs);
+  const int64_t sc = std::max<int64_t>(cs, nlist) / 1024 + 4;
+  SA_TRY(dalloc(&scratch, sc, s, "scan scratch"));
+  f.add(scratch);
+  SA_TRY(dalloc(&hist, nlist, s, "hist"));
+  f.add(hist);
+  SA_CUDA(launch_i64_to_i32(ids, n, keys, num_sms, s), "ids->keys");
+  SA_CUDA(stable_sort_by_key16(keys, n, ktmp, vtmp, kout, perm, counts, offs, scratch, s), "sort");
+  SA_CUDA(cudaMemsetAsync(hist, 0, sizeof(int64_t) * nlist, s), "memset");
+  SA_CUDA(launch_histogram(keys, n, hist, num_sms, s), "histogram");
+  SA_CUDA(exclusive_scan_i64(hist, nlist, off, scratch, s), "scan");
+  for (int i = 0; i < 9; ++i) prof_count(SA_KERNEL_OTHER);
+  return SA_OK;
 }
-sa_status ivf_search(const sa_index*, const __nv_bfloat16*, int64_t, int64_t, int32_t, int32_t,
-                     const SearchOut&, cudaStream_t) {
-  return set_error(SA_ERR_UNSUPPORTED, "IVF search not available in this build");
+
+}  // namespace
+
+sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
+  const int nlist = idx->nlist;
+  const int dp = idx->d_pad;
+  const int sms = idx->num_sms;
+  const int64_t n = idx->n_local;
+  if (nlist > 65536) return set_error(SA_ERR_UNSUPPORTED, "nlist > 65536");
+  if (idx->comm && idx->comm->world > 1)
+    return set_error(SA_ERR_UNSUPPORTED, "sharded IVF build is not available yet");
+  const int64_t n_total = idx->n_total;
+  const int64_t n_train = std::min<int64_t>(n_total, (int64_t)o.train_per_list * nlist);
+  Freer f{s};
+
+  // ---- a2: training sample by global id (R9), centroids
+  __nv_bfloat16* sample;
+  SA_TRY(dalloc(&sample, (size_t)n_train * dp, s, "alloc sample"));
+  f.add(sample);
+  SA_CUDA(launch_gather_rows(idx->X, dp, nullptr, n_total, idx->row_offset, n_train, sample, sms, s),
+          "gather sample");
+  prof_count(SA_KERNEL_OTHER);
+  SA_CUDA(cudaMalloc(&idx->centroids, (size_t)nlist * dp * sizeof(float)), "alloc centroids");
+  SA_CUDA(cudaMalloc(&idx->centroids_bf16, (size_t)nlist * dp * sizeof(__nv_bfloat16)),
+          "alloc centroids bf16");
+  SA_CUDA(launch_init_centroids(sample, dp, nlist, n_train, o.seed, idx->centroids, s), "init");
+  prof_count(SA_KERNEL_OTHER);
+  SA_TRY(make_tmap_bf16(&idx->tmap_c, idx->centroids_bf16, nlist, dp, FS_BN));
+  SA_TRY(make_tmap_bf16(&idx->tmap_c2, idx->centroids_bf16, nlist, dp, FS_BN / 2));
+  const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, nlist, dp, nullptr, 0u};
+
+  int64_t* ids;
+  float* scores;
+  int32_t* perm;
+  int64_t* off;
+  int32_t *empty_flag, *n_empty;
+  uint64_t *rkeys, *rsel;
+  SA_TRY(dalloc(&ids, n_train, s, "alloc ids"));
+  f.add(ids);
+  SA_TRY(dalloc(&scores, n_train, s, "alloc scores"));
+  f.add(scores);
+  SA_TRY(dalloc(&perm, n_train, s, "alloc perm"));
+  f.add(perm);
+  SA_TRY(dalloc(&off, nlist + 1, s, "alloc off"));
+  f.add(off);
+  SA_TRY(dalloc(&empty_flag, nlist, s, "alloc flags"));
+  f.add(empty_flag);
+  SA_TRY(dalloc(&n_empty, 1, s, "alloc n_empty"));
+  f.add(n_empty);
+  SA_TRY(dalloc(&rkeys, n_train, s, "alloc repair keys"));
+  f.add(rkeys);
+  SA_TRY(dalloc(&rsel, 256, s, "alloc repair sel"));
+  f.add(rsel);
+
+  for (int it = 0; it < o.kmeans_iters; ++it) {
+    SA_CUDA(launch_f32_to_bf16(idx->centroids, (int64_t)nlist * dp, idx->centroids_bf16, sms, s),
+            "centroids->bf16");
+    prof_count(SA_KERNEL_OTHER);
+    SearchOut so;
+    so.ids = ids;
+    so.scores = scores;
+    SA_TRY(flat_search_view(cvc, sms, sample, n_train, 1, so, s));   // assignment (GEMM + top-1)
+    SA_TRY(sort_by_list(ids, n_train, nlist, sms, perm, off, s));
+    SA_CUDA(cudaMemsetAsync(n_empty, 0, sizeof(int32_t), s), "memset");
+    SA_CUDA(launch_centroid_update(sample, dp, perm, off, nlist, idx->centroids, empty_flag, n_empty,
+                                   s),
+            "centroid update");
+    prof_count(SA_KERNEL_OTHER);
+    int32_t h_empty = 0;
+    SA_CUDA(cudaMemcpyAsync(&h_empty, n_empty, sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H");
+    SA_CUDA(cudaStreamSynchronize(s), "sync");
+    if (h_empty > 0) {
+      // R10: empty lists take the sample rows with the lowest assigned score
+      int left = h_empty;
+      if (left > 256) return set_error(SA_ERR_UNSUPPORTED, "more than 256 empty IVF lists");
+      SA_CUDA(launch_repair_keys(scores, n_train, rkeys, sms, s), "repair keys");
+      MergeArgs m{};
+      m.cand = rkeys;
+      m.k = left;
+      m.qstride = 0;
+      m.m_flat = n_train;
+      m.out_keys = rsel;
+      SA_CUDA(launch_merge(m, 1, s), "repair select");
+      SA_CUDA(launch_repair_apply(sample, dp, nlist, empty_flag, rsel, idx->centroids, s),
+              "repair apply");
+      for (int i = 0; i < 3; ++i) prof_count(SA_KERNEL_OTHER);
+    }
+  }
+  SA_CUDA(launch_f32_to_bf16(idx->centroids, (int64_t)nlist * dp, idx->centroids_bf16, sms, s),
+          "centroids->bf16");
+  prof_count(SA_KERNEL_OTHER);
+
+  // ---- a3: assign every local row, sort list-major, permute
+  int64_t* ids_all;
+  float* sc_all;
+  int32_t* perm_all;
+  SA_TRY(dalloc(&ids_all, n, s, "alloc ids"));
+  f.add(ids_all);
+  SA_TRY(dalloc(&sc_all, n, s, "alloc scores"));
+  f.add(sc_all);
+  SA_TRY(dalloc(&perm_all, n, s, "alloc perm"));
+  f.add(perm_all);
+  {
+    SearchOut so;
+    so.ids = ids_all;
+    so.scores = sc_all;
+    SA_TRY(flat_search_view(cvc, sms, idx->X, n, 1, so, s));
+  }
+  SA_CUDA(cudaMalloc(&idx->list_off, (nlist + 1) * sizeof(int64_t)), "alloc list offsets");
+  SA_TRY(sort_by_list(ids_all, n, nlist, sms, perm_all, idx->list_off, s));
+  __nv_bfloat16* Xp = nullptr;
+  SA_CUDA(cudaMalloc(&Xp, (size_t)n * dp * sizeof(__nv_bfloat16)), "alloc list-major corpus");
+  cudaError_t e = launch_gather_rows(idx->X, dp, perm_all, 0, 0, n, Xp, sms, s);
+  if (e == cudaSuccess) e = cudaMalloc(&idx->row_ids, (size_t)n * sizeof(int32_t));
+  if (e == cudaSuccess) e = launch_perm_ids(perm_all, n, idx->row_offset, idx->row_ids, sms, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    cudaFree(Xp);
+    return cuda_status(e, "permute corpus");
+  }
+  prof_count(SA_KERNEL_OTHER);
+  prof_count(SA_KERNEL_OTHER);
+  cudaFree(idx->X);
+  idx->X = Xp;
+  SA_TRY(make_tmap_bf16(&idx->tmap_x, idx->X, n, dp, FS_BN));
+  SA_TRY(make_tmap_bf16(&idx->tmap_x2, idx->X, n, dp, FS_BN / 2));
+  idx->h_list_off.resize(nlist + 1);
+  SA_CUDA(cudaMemcpy(idx->h_list_off.data(), idx->list_off, (nlist + 1) * sizeof(int64_t),
+                     cudaMemcpyDeviceToHost),
+          "list offsets D2H");
+  idx->max_list = 0;
+  for (int l = 0; l < nlist; ++l)
+    idx->max_list = std::max<int64_t>(idx->max_list, idx->h_list_off[l + 1] - idx->h_list_off[l]);
+  return SA_OK;
 }
-sa_status ivf_probe(const sa_index*, const __nv_bfloat16*, int64_t, int64_t, int32_t, int32_t*,
-                    cudaStream_t) {
-  return set_error(SA_ERR_UNSUPPORTED, "IVF probe not available in this build");
+
+sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
+                    int32_t nprobe, int32_t* out_lists, cudaStream_t s) {
+  (void)nq_pad;
+  Freer f{s};
+  uint64_t* pkeys;
+  SA_TRY(dalloc(&pkeys, (size_t)nq * nprobe, s, "alloc probe keys"));
+  f.add(pkeys);
+  const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, idx->nlist, idx->d_pad, nullptr, 0u};
+  SearchOut so;
+  so.keys = pkeys;
+  SA_TRY(flat_search_view(cvc, idx->num_sms, Qs, nq, nprobe, so, s));
+  SA_CUDA(launch_keys_to_lists(pkeys, nq * nprobe, nullptr, out_lists, idx->num_sms, s), "lists");
+  prof_count(SA_KERNEL_OTHER);
+  return SA_OK;
 }
+
+sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
+                     int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s) {
+  (void)nq_pad;
+  const int nlist = idx->nlist;
+  const int sms = idx->num_sms;
+  const int64_t np = nq * nprobe;
+  Freer f{s};
+  // ---- a7: probe = top-nprobe centroids per query on the tensor cores
+  uint64_t* pkeys;
+  int64_t* probes;
+  SA_TRY(dalloc(&pkeys, np, s, "alloc probe keys"));
+  f.add(pkeys);
+  SA_TRY(dalloc(&probes, np, s, "alloc probes"));
+  f.add(probes);
+  {
+    const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, nlist, idx->d_pad, nullptr, 0u};
+    SearchOut so;
+    so.keys = pkeys;
+    prof_begin(SA_KERNEL_IVF_PROBE, s);
+    sa_status st = flat_search_view(cvc, sms, Qs, nq, nprobe, so, s);
+    prof_end(SA_KERNEL_IVF_PROBE, s);
+    if (st != SA_OK) return st;
+  }
+  SA_CUDA(launch_keys_to_lists(pkeys, np, probes, nullptr, sms, s), "probe lists");
+  prof_count(SA_KERNEL_OTHER);
+
+  // ---- invert: lists -> probing queries, output slots, work items
+  const int64_t max_chunks = std::max<int64_t>(1, (idx->max_list + kChunkRows - 1) / kChunkRows);
+  IvfSearchScratch w{};
+  SA_TRY(dalloc(&w.cnt, nlist, s, "ivf scratch"));
+  f.add(w.cnt);
+  SA_TRY(dalloc(&w.cursor, nlist, s, "ivf scratch"));
+  f.add(w.cursor);
+  SA_TRY(dalloc(&w.tmp64, nlist + 1, s, "ivf scratch"));
+  f.add(w.tmp64);
+  SA_TRY(dalloc(&w.tmp64b, np, s, "ivf scratch"));
+  f.add(w.tmp64b);
+  SA_TRY(dalloc(&w.lq_off64, nlist + 1, s, "ivf scratch"));
+  f.add(w.lq_off64);
+  SA_TRY(dalloc(&w.lq_off, nlist + 1, s, "ivf scratch"));
+  f.add(w.lq_off);
+  SA_TRY(dalloc(&w.lq_ent, np, s, "ivf scratch"));
+  f.add(w.lq_ent);
+  SA_TRY(dalloc(&w.q_slot, np + 1, s, "ivf scratch"));
+  f.add(w.q_slot);
+  SA_TRY(dalloc(&w.item_off, nlist + 1, s, "ivf scratch"));
+  f.add(w.item_off);
+  SA_TRY(dalloc(&w.items, (size_t)np * max_chunks, s, "ivf items"));
+  f.add(w.items);
+  SA_TRY(dalloc(&w.n_items, 1, s, "ivf scratch"));
+  f.add(w.n_items);
+  SA_TRY(dalloc(&w.scratch, std::max<int64_t>(nlist, np) / 1024 + 4, s, "ivf scratch"));
+  f.add(w.scratch);
+  SA_CUDA(launch_probe_invert(probes, nq, nprobe, nlist, idx->list_off, kChunkRows, w, sms, s),
+          "probe inversion");
+  for (int i = 0; i < 11; ++i) prof_count(SA_KERNEL_OTHER);
+
+  // ---- a8: list-major scan on the tensor cores
+  const size_t max_slots = (size_t)np * max_chunks;
+  uint64_t *part, *heap = nullptr;
+  SA_TRY(dalloc(&part, max_slots * FS_LISTS_PER_ITEM * k, s, "ivf partials"));
+  f.add(part);
+  if (k > FS_KSMEM) {
+    SA_TRY(dalloc(&heap, (size_t)sms * k * FS_EPI_THREADS, s, "ivf heaps"));
+    f.add(heap);
+  }
+  CUtensorMap tmap_q;
+  SA_TRY(make_tmap_bf16(&tmap_q, Qs, nq, idx->d_pad, FS_BM));
+  FlatScanArgs a{};
+  a.Q = Qs;
+  a.nq = nq;
+  a.nq_pad = nq;
+  a.d_pad = idx->d_pad;
+  a.n_rows = idx->n_local;
+  a.k = k;
+  a.row_ids = idx->row_ids;
+  a.id_base = 0;
+  a.part = part;
+  a.heap_g = heap;
+  a.mode = FS_MODE_IVF;
+  a.items = w.items;
+  a.n_items = w.n_items;
+  a.list_off = idx->list_off;
+  a.lq_off = w.lq_off;
+  a.lq_ent = w.lq_ent;
+  a.q_slot = w.q_slot;
+  a.nprobe = nprobe;
+  a.chunk_rows = kChunkRows;
+  prof_begin(SA_KERNEL_IVF_SCAN, s);
+  cudaError_t e = launch_flat_scan(idx->tmap_x, tmap_q, a, 1, sms, s);
+  prof_end(SA_KERNEL_IVF_SCAN, s);
+  prof_count(SA_KERNEL_IVF_SCAN);
+  SA_CUDA(e, "ivf scan");
+
+  MergeArgs m{};
+  m.cand = part;
+  m.k = k;
+  m.slot_off = w.q_slot;
+  m.slot_stride = nprobe;
+  m.slot_keys = FS_LISTS_PER_ITEM * k;
+  m.out_keys = out.keys;
+  m.out_ids = out.ids;
+  m.out_scores = out.scores;
+  prof_begin(SA_KERNEL_MERGE, s);
+  e = launch_merge(m, nq, s);
+  prof_end(SA_KERNEL_MERGE, s);
+  prof_count(SA_KERNEL_MERGE);
+  return cuda_status(e, "ivf merge");
+}
+
 }  // namespace sa

@@ -27,19 +27,31 @@ merge_topk_kernel(const MergeArgs a) {
 
   const int64_t q = blockIdx.x;
   const int k = a.k;
-  const int M = a.groups * k;
+  int64_t base = 0;
+  int64_t M;
+  if (a.slot_off) {
+    base = a.slot_off[q * a.slot_stride] * a.slot_keys;
+    M = a.slot_off[(q + 1) * a.slot_stride] * a.slot_keys - base;
+  } else if (a.m_flat > 0) {
+    base = q * a.qstride;
+    M = a.m_flat;
+  } else {
+    M = (int64_t)a.groups * k;
+  }
+  const bool grouped = !a.slot_off && a.m_flat <= 0;
   const int tid = threadIdx.x;
   const bool cached = M <= kSmemCand;
 
-  auto cand_g = [&](int i) -> uint64_t {
-    const int g = i / k, j = i % k;
+  auto cand_g = [&](int64_t i) -> uint64_t {
+    if (!grouped) return a.cand[base + i];
+    const int64_t g = i / k, j = i % k;
     return a.cand[(size_t)g * a.gstride + (size_t)q * a.qstride + j];
   };
   if (cached) {
     for (int i = tid; i < M; i += kThreads) cache[i] = cand_g(i);
     __syncthreads();
   }
-  auto cand = [&](int i) -> uint64_t { return cached ? cache[i] : cand_g(i); };
+  auto cand = [&](int64_t i) -> uint64_t { return cached ? cache[i] : cand_g(i); };
 
   uint64_t prefix = 0, pmask = 0;
   int kr = k;
@@ -47,7 +59,7 @@ merge_topk_kernel(const MergeArgs a) {
     const int shift = 56 - 8 * pass;
     for (int i = tid; i < 256; i += kThreads) hist[i] = 0;
     __syncthreads();
-    for (int i = tid; i < M; i += kThreads) {
+    for (int64_t i = tid; i < M; i += kThreads) {
       const uint64_t c = cand(i);
       if ((c & pmask) == prefix) atomicAdd(&hist[(c >> shift) & 255u], 1u);
     }
@@ -72,7 +84,7 @@ merge_topk_kernel(const MergeArgs a) {
   if (tid == 0) s_pos = 0;
   for (int i = tid; i < kMaxK; i += kThreads) sel[i] = 0ull;
   __syncthreads();
-  for (int i = tid; i < M; i += kThreads) {
+  for (int64_t i = tid; i < M; i += kThreads) {
     const uint64_t c = cand(i);
     if (c > T) sel[atomicAdd(&s_pos, 1)] = c;
   }
@@ -109,8 +121,36 @@ merge_topk_kernel(const MergeArgs a) {
   }
 }
 
+// k = 1 with few grouped candidates (k-means / full assignment: millions of queries):
+// one thread per query, max over its candidate keys.
+__global__ void merge_top1_kernel(const MergeArgs a, int64_t nq) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t best = 0ull;
+    for (int g = 0; g < a.groups; ++g) {
+      const uint64_t c = a.cand[(size_t)g * a.gstride + (size_t)q * a.qstride];
+      best = c > best ? c : best;
+    }
+    if (a.out_keys) {
+      a.out_keys[q] = best;
+    } else if (best == 0ull) {
+      a.out_ids[q] = -1;
+      a.out_scores[q] = -__int_as_float(0x7f800000);
+    } else {
+      a.out_ids[q] = (int64_t)key_id(best) + a.id_offset;
+      a.out_scores[q] = key_score(best);
+    }
+  }
+}
+
 cudaError_t launch_merge(const MergeArgs& a, int64_t nq, cudaStream_t stream) {
   if (nq <= 0) return cudaSuccess;
+  if (a.k == 1 && !a.slot_off && a.m_flat <= 0 && a.groups <= 64) {
+    int64_t blocks = (nq + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    merge_top1_kernel<<<(unsigned)blocks, 256, 0, stream>>>(a, nq);
+    return cudaGetLastError();
+  }
   merge_topk_kernel<<<(unsigned)nq, kThreads, 0, stream>>>(a);
   return cudaGetLastError();
 }

@@ -8,12 +8,20 @@
 namespace sa {
 
 // Candidate j of group g for query q is cand[g*gstride + q*qstride + j], j < k.
+// Alternative candidate layouts (checked in this order):
+//   slot_off != nullptr: query q's candidates are cand[slot_off[q*slot_stride]*slot_keys,
+//                        slot_off[(q+1)*slot_stride]*slot_keys)   (IVF: variable per query)
+//   m_flat > 0:          cand[q*qstride + i], i < m_flat
 struct MergeArgs {
   const uint64_t* cand;
   int32_t groups;
   int32_t k;
   int64_t qstride;
   int64_t gstride;
+  const int64_t* slot_off = nullptr;
+  int32_t slot_stride = 0;
+  int32_t slot_keys = 0;
+  int64_t m_flat = 0;
   int64_t* out_ids;     // [nq, k] (when out_keys == nullptr)
   float* out_scores;    // [nq, k]
   uint64_t* out_keys;   // [nq, k] packed keys, sorted (for another merge level)

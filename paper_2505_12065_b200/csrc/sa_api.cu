@@ -121,24 +121,17 @@ static sa_status check_device(int* dev_out, int* sms_out) {
   return SA_OK;
 }
 
-template <typename T>
-static sa_status dalloc(T** p, size_t count, cudaStream_t s, const char* what) {
-  *p = nullptr;
-  if (count == 0) return SA_OK;
-  return cuda_status(cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), s), what);
-}
-
 // ====================================================================== flat search
 // Plan of one flat scan: units (CTAs or CTA pairs), corpus slices and grid.
 struct FlatPlan {
   int cg, QP, S, grid;
 };
-static FlatPlan plan_flat(const sa_index* idx, int64_t nq_pad) {
+static FlatPlan plan_flat(int64_t n_rows, int num_sms, int64_t nq_pad) {
   FlatPlan p;
   p.cg = nq_pad > 128 ? 2 : 1;
-  const int64_t T = (idx->n_local + FS_BN - 1) / FS_BN;
+  const int64_t T = (n_rows + FS_BN - 1) / FS_BN;
   p.QP = (int)(nq_pad / (FS_BM * p.cg));
-  const int units = idx->num_sms / p.cg;
+  const int units = num_sms / p.cg;
   int64_t S = std::max<int64_t>(1, units / p.QP);
   S = std::min<int64_t>(S, T);
   p.S = (int)S;
@@ -146,9 +139,10 @@ static FlatPlan plan_flat(const sa_index* idx, int64_t nq_pad) {
   return p;
 }
 
-sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
-                      int32_t k, const SearchOut& out, cudaStream_t s) {
-  const FlatPlan p = plan_flat(idx, nq_pad);
+sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
+                           int32_t k, const SearchOut& out, cudaStream_t s) {
+  const int64_t nq_pad = padded_nq(nq);
+  const FlatPlan p = plan_flat(cv.n_rows, num_sms, nq_pad);
   uint64_t *part = nullptr, *heap = nullptr;
   sa_status st = dalloc(&part, (size_t)nq_pad * p.S * FS_LISTS_PER_ITEM * k, s, "alloc partials");
   if (st != SA_OK) return st;
@@ -160,26 +154,25 @@ sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, 
   a.Q = Qs;
   a.nq = nq;
   a.nq_pad = nq_pad;
-  a.d_pad = idx->d_pad;
-  a.n_rows = idx->n_local;
+  a.d_pad = cv.d_pad;
+  a.n_rows = cv.n_rows;
   a.QP = p.QP;
   a.S = p.S;
   a.k = k;
-  a.row_ids = idx->row_ids;
-  a.id_base = idx->row_ids ? 0u : (uint32_t)idx->row_offset;
+  a.row_ids = cv.row_ids;
+  a.id_base = cv.id_base;
   a.part = part;
   a.heap_g = heap;
-  a.mode = 0;
+  a.mode = FS_MODE_TOPK;
   CUtensorMap tmap_q;
-  st = make_tmap_bf16(&tmap_q, Qs, nq_pad, idx->d_pad, FS_BM);
+  st = make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM);
   if (st != SA_OK) {
     if (heap) cudaFreeAsync(heap, s);
     cudaFreeAsync(part, s);
     return st;
   }
   prof_begin(SA_KERNEL_FLAT_SCAN, s);
-  cudaError_t e =
-      launch_flat_scan(p.cg == 2 ? idx->tmap_x2 : idx->tmap_x, tmap_q, a, p.cg, p.grid, s);
+  cudaError_t e = launch_flat_scan(p.cg == 2 ? *cv.tmap2 : *cv.tmap1, tmap_q, a, p.cg, p.grid, s);
   prof_end(SA_KERNEL_FLAT_SCAN, s);
   prof_count(SA_KERNEL_FLAT_SCAN);
   if (e == cudaSuccess) {
@@ -201,6 +194,14 @@ sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, 
   if (heap) cudaFreeAsync(heap, s);
   cudaFreeAsync(part, s);
   return cuda_status(e, "flat search launch");
+}
+
+sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
+                      int32_t k, const SearchOut& out, cudaStream_t s) {
+  (void)nq_pad;
+  CorpusView cv{&idx->tmap_x, &idx->tmap_x2, idx->n_local, idx->d_pad, idx->row_ids,
+                idx->row_ids ? 0u : (uint32_t)idx->row_offset};
+  return flat_search_view(cv, idx->num_sms, Qs, nq, k, out, s);
 }
 
 }  // namespace sa
@@ -379,9 +380,10 @@ sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nl
                      "cast/pad corpus");
     prof_count(SA_KERNEL_STAGE);
   }
-  if (st == SA_OK && nlist > 0) st = ivf_build(idx, *opts, s);
   if (st == SA_OK) st = make_tmap_bf16(&idx->tmap_x, idx->X, n, d_pad, FS_BN);
   if (st == SA_OK) st = make_tmap_bf16(&idx->tmap_x2, idx->X, n, d_pad, FS_BN / 2);
+  // ivf_build permutes X list-major and re-encodes the tensor maps
+  if (st == SA_OK && nlist > 0) st = ivf_build(idx, *opts, s);
   if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "build sync");
   if (st != SA_OK) {
     sa_index_free(idx);
@@ -562,7 +564,7 @@ sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, 
     st = cuda_status(launch_cast_pad(queries, false, nq, idx->d, Qs, nq_pad, idx->d_pad,
                                      idx->num_sms, s), "stage queries");
   if (st == SA_OK) {
-    const FlatPlan p = plan_flat(idx, nq_pad);
+    const FlatPlan p = plan_flat(idx->n_local, idx->num_sms, nq_pad);
     FlatScanArgs a{};
     a.Q = Qs;
     a.nq = nq;
