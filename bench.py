@@ -168,13 +168,26 @@ def run_reference(args, cfg, name):
 
 
 # ------------------------------------------------------------------ GPU arm
+NPROBE_LADDER = (8, 16, 24, 32, 40, 48, 64, 96, 128, 192, 256)
+RECALL_TARGET = 0.95
+
+
+def recall_at_k(got: torch.Tensor, gt: torch.Tensor) -> float:
+    g, t = got.cpu().numpy(), gt.cpu().numpy()
+    return float(np.mean([len(set(g[i]) & set(t[i])) / t.shape[1] for i in range(t.shape[0])]))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="auto", choices=["auto", "exact", "ivf"],
+                    help="auto: IVF at the smallest nprobe with recall@10 >= 0.95 (headline), "
+                         "plus the exact mode; exact: flat scan only; ivf: fixed --nprobe")
     ap.add_argument("--nprobe", type=int, default=0)
+    ap.add_argument("--nlist", type=int, default=16384)
     ap.add_argument("--nq", type=int, default=None, help="override batch size")
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -201,6 +214,11 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = sa.Comm.from_torch_distributed(local)
+    mode = args.mode
+    if mode == "auto" and world > 1:
+        mode = "exact"          # sharded IVF build lands later
+    use_ivf = mode in ("auto", "ivf")
+    nlist = args.nlist if use_ivf else 0
 
     n, d, nq, k = cfg["n"], cfg["d"], cfg["nq"], cfg["k"]
     off, n_local = sa.shard_range(n, rank, world)
@@ -211,7 +229,6 @@ def main():
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    nlist = cfg.get("nlist", 0) if args.nprobe > 0 else 0
     idx = sa.Index.build(X, nlist, row_offset=off, n_total=n, comm=comm)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
@@ -231,87 +248,158 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    for i in range(args.warmup):
-        idx.search(batches[i], k, args.nprobe, out=(ids, scores))
-    barrier()
-    sa.profile_enable(True)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    lat = []
-    with ClockSampler(local) as clk:
-        barrier()
-        ev0.record(stream)
-        for i in range(args.steps):
-            idx.search(batches[args.warmup + i], k, args.nprobe, out=(ids, scores))
-        ev1.record(stream)
-        barrier()
-    ms = ev0.elapsed_time(ev1)
-    kern = {kind: sa.profile_read(kind) for kind in sa.KERNEL_KINDS}
-    sa.profile_enable(False)
-    launches = sum(v[1] for v in kern.values())
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda")
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = args.steps * nq / (ms / 1e3)
+        return float(t.item())
+
+    def timed(nprobe):
+        """W warm-up + K timed search steps; returns (ms, per-kind kernel (ms, launches), clocks)."""
+        for i in range(args.warmup):
+            idx.search(batches[i], k, nprobe, out=(ids, scores))
+        barrier()
+        sa.profile_enable(True)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            barrier()
+            ev0.record(stream)
+            for i in range(args.steps):
+                idx.search(batches[args.warmup + i], k, nprobe, out=(ids, scores))
+            ev1.record(stream)
+            barrier()
+        ms = max_over_ranks(ev0.elapsed_time(ev1))
+        kern = {kind: sa.profile_read(kind) for kind in sa.KERNEL_KINDS}
+        sa.profile_enable(False)
+        return ms, kern, clk.summary()
+
+    # ---- ground truth (exact mode, parity-tested) for every timed batch, untimed
+    gt = {}
+    if use_ivf:
+        for i in range(args.warmup, nb):
+            gi, _ = idx.search(batches[i], k, 0)
+            gt[i] = gi.clone()
+
+    # ---- pick nprobe: smallest on the ladder with recall@k >= target on the first batch
+    sweep = []
+    nprobe = 0
+    if mode == "auto":
+        for p in NPROBE_LADDER:
+            if p > nlist:
+                break
+            gi, _ = idx.search(batches[args.warmup], k, p)
+            r = recall_at_k(gi, gt[args.warmup])
+            sweep.append({"nprobe": p, "recall": r})
+            if r >= RECALL_TARGET:
+                nprobe = p
+                break
+        if nprobe == 0:
+            nprobe = sweep[-1]["nprobe"]
+    elif mode == "ivf":
+        nprobe = args.nprobe
+
+    pk = peaks()
+    result_exact = None
+    if mode in ("auto", "exact"):
+        ms_e, kern_e, clk_e = timed(0)
+        fs_ms, fs_n = kern_e["flat_scan"]
+        per_launch = fs_ms / max(fs_n, 1)
+        achieved = 2.0 * nq * n_local * d / (per_launch / 1e3) / 1e12
+        result_exact = {
+            "value": args.steps * nq / (ms_e / 1e3), "unit": "queries/s", "recall": 1.0,
+            "ms_per_step": ms_e / args.steps, "clocks": clk_e,
+            "kernel_ms": {kk: v[0] for kk, v in kern_e.items()},
+            "kernel_launches": {kk: v[1] for kk, v in kern_e.items()},
+            "roofline": {"kernel": "flat_scan_topk_kernel", "bound": "tensor",
+                         "achieved": achieved, "peak": pk["bf16"], "unit": "TFLOP/s",
+                         "frac": achieved / pk["bf16"],
+                         "peak_kind": f"bf16 dense, {pk['src']} burst (MEASURED_PEAKS.json)",
+                         "frac_of_sustained": achieved / pk["bf16_sus"] if pk["bf16_sus"] else None,
+                         "kernel_ms": per_launch, "kernel_share_of_step": fs_ms / ms_e,
+                         "traffic": traffic_from_profiles("flat_scan", args.config, nq)},
+        }
+    result_ivf = None
+    if use_ivf:
+        ms_i, kern_i, clk_i = timed(nprobe)
+        rec = []
+        for i in range(args.warmup, nb):
+            gi, _ = idx.search(batches[i], k, nprobe)
+            rec.append(recall_at_k(gi, gt[i]))
+        # algorithmic bytes per batch: rows of the distinct probed lists (+ the centroids)
+        loff, _ = idx.export_lists()
+        sizes = np.diff(loff)
+        byts = []
+        for i in range(args.warmup, nb):
+            P = idx.probes(batches[i], nprobe).cpu().numpy()
+            u = np.unique(P)
+            byts.append(float(sizes[u].sum()) * d * 2)
+        alg_bytes = float(np.mean(byts)) + nlist * d * 2
+        sc_ms, sc_n = kern_i["ivf_scan"]
+        per_launch = sc_ms / max(sc_n, 1)
+        achieved = float(np.mean(byts)) / (per_launch / 1e3) / 1e9
+        result_ivf = {
+            "value": args.steps * nq / (ms_i / 1e3), "unit": "queries/s",
+            "recall": float(np.mean(rec)), "nprobe": nprobe, "nlist": nlist, "sweep": sweep,
+            "ms_per_step": ms_i / args.steps, "clocks": clk_i,
+            "kernel_ms": {kk: v[0] for kk, v in kern_i.items()},
+            "kernel_launches": {kk: v[1] for kk, v in kern_i.items()},
+            "algorithmic_bytes_per_step": alg_bytes,
+            "roofline": {"kernel": "flat_scan_topk_kernel (FS_MODE_IVF list scan)", "bound": "hbm",
+                         "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
+                         "frac": achieved / pk["hbm"],
+                         "peak_kind": f"HBM copy, {pk['src']} (MEASURED_PEAKS.json)",
+                         "frac_of_8TBs": achieved / 8000.0,
+                         "kernel_ms": per_launch, "kernel_share_of_step": sc_ms / ms_i,
+                         "traffic": traffic_from_profiles("ivf_scan", args.config, nq)},
+        }
+
+    # headline: the faster of the modes that meet recall@10 >= 0.95
+    cands = [r for r in (result_ivf, result_exact) if r is not None and r["recall"] >= RECALL_TARGET]
+    head = max(cands, key=lambda r: r["value"]) if cands else (result_ivf or result_exact)
+    head_nprobe = head.get("nprobe", 0)
 
     # ---- end to end through the host-buffer C-ABI call (H2D + search + D2H per step)
     qh = [batches[i].float().cpu().pin_memory() for i in range(nb)]
     ids_h = torch.empty(nq, k, dtype=torch.int64).pin_memory()
     sc_h = torch.empty(nq, k, dtype=torch.float32).pin_memory()
     for i in range(args.warmup):
-        idx.search_host(qh[i], k, args.nprobe, out=(ids_h, sc_h))
+        idx.search_host(qh[i], k, head_nprobe, out=(ids_h, sc_h))
     barrier()
+    lat = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for i in range(args.steps):
         t_s = time.perf_counter()
         if i == 0:
             e0.record(stream)
-        idx.search_host(qh[args.warmup + i], k, args.nprobe, out=(ids_h, sc_h))
+        idx.search_host(qh[args.warmup + i], k, head_nprobe, out=(ids_h, sc_h))
         lat.append(time.perf_counter() - t_s)
     e1.record(stream)
     barrier()
-    e2e_ms = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     e2e_value = args.steps * nq / (e2e_ms / 1e3)
 
-    # ---- roofline of the dominant kernel
-    pk = peaks()
-    if args.nprobe == 0:
-        fs_ms, fs_n = kern["flat_scan"]
-        per_launch = fs_ms / max(fs_n, 1)
-        flops = 2.0 * nq * n_local * d
-        achieved = flops / (per_launch / 1e3) / 1e12
-        roof = {"kernel": "flat_scan_topk_kernel", "bound": "tensor", "achieved": achieved,
-                "peak": pk["bf16"], "unit": "TFLOP/s", "frac": achieved / pk["bf16"],
-                "peak_kind": f"bf16 dense, {pk['src']} burst (MEASURED_PEAKS.json)",
-                "frac_of_sustained": achieved / pk["bf16_sus"] if pk["bf16_sus"] else None,
-                "kernel_ms": per_launch, "kernel_share_of_step": fs_ms / ms,
-                "traffic": traffic_from_profiles("flat_scan", args.config, nq)}
-    else:
-        sc_ms, sc_n = kern["ivf_scan"]
-        roof = {"kernel": "ivf_scan", "bound": "hbm", "achieved": None, "peak": pk["hbm"],
-                "unit": "GB/s", "frac": None, "traffic": None}
-
+    mode_name = "exact flat" if head_nprobe == 0 else f"IVF nlist={nlist} nprobe={head_nprobe}"
     line = {
-        "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "metric": METRIC, "value": head["value"], "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded low-rank Gaussian mixture, unit-norm; DESIGN.md §3)",
-        "config": {"workload": workload_name(cfg, args.config, args.nprobe), "n": n, "d": d,
-                   "nq": nq, "k": k, "nprobe": args.nprobe, "n_local": n_local,
+        "config": {"workload": f"{args.config}: {mode_name} top-{k}, {n}x{d} bf16 corpus, "
+                               f"batch {nq}",
+                   "n": n, "d": d, "nq": nq, "k": k, "nprobe": head_nprobe, "nlist": nlist,
+                   "recall_at_k": head["recall"], "n_local": n_local,
                    "parallelism": f"row-shard x{world}",
                    "l2": "inputs larger than L2 (corpus 32 GB >> 126 MB); no flush"},
-        "roofline": roof,
+        "roofline": head["roofline"],
         "e2e": {"value": e2e_value, "unit": "queries/s",
                 "h2d_bytes_per_step": nq * d * 4, "d2h_bytes_per_step": nq * k * (8 + 4),
-                "p50_batch_ms": 1e3 * statistics.median(lat) if lat else None},
-        "gpu_launches": launches,
-        "kernel_ms": {kk: v[0] for kk, v in kern.items()},
-        "kernel_launches": {kk: v[1] for kk, v in kern.items()},
-        "clocks": clk.summary(),
+                "p50_batch_ms": 1e3 * statistics.median(lat) if lat else None,
+                "p99_batch_ms": 1e3 * float(np.percentile(lat, 99)) if lat else None},
+        "gpu_launches": int(sum(v for v in head["kernel_launches"].values())),
+        "kernel_ms": head["kernel_ms"], "kernel_launches": head["kernel_launches"],
+        "clocks": head["clocks"],
+        "exact": result_exact, "ivf": result_ivf,
         "build_s": build_s, "gen_s": gen_s,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
