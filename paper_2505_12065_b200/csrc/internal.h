@@ -80,6 +80,9 @@ struct CorpusView {
 // exact scan of `cv` for nq staged queries (bf16 [>= nq, d_pad]) + intra-GPU merge (sa_api.cu)
 sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
                            int32_t k, const SearchOut& out, cudaStream_t s);
+// raw fp32 score matrix out[q, row] = <Q_q, X_row> for q < nq (tensor cores, no selection)
+sa_status flat_scores_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
+                           float* out, cudaStream_t s);
 sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
                       int32_t k, const SearchOut& out, cudaStream_t s);
 

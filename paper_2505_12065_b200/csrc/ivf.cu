@@ -213,6 +213,28 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   return SA_OK;
 }
 
+// a7: centroid scores on the tensor cores (dumped, nq x nlist fp32 -- 32 MB at nq=512,
+// L2-resident), then an exact per-query top-nprobe radix select (ties -> lowest id, R11).
+// Sorted packed keys [nq, nprobe] (list id in the key).
+static sa_status probe_keys(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq,
+                            int32_t nprobe, uint64_t* pkeys, cudaStream_t s) {
+  Freer f{s};
+  float* sc;
+  SA_TRY(dalloc(&sc, (size_t)nq * idx->nlist, s, "alloc probe scores"));
+  f.add(sc);
+  const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, idx->nlist, idx->d_pad, nullptr, 0u};
+  SA_TRY(flat_scores_view(cvc, idx->num_sms, Qs, nq, sc, s));
+  MergeArgs m{};
+  m.cand_scores = sc;
+  m.m_flat = idx->nlist;
+  m.qstride = idx->nlist;
+  m.k = nprobe;
+  m.out_keys = pkeys;
+  SA_CUDA(launch_merge(m, nq, s), "probe select");
+  prof_count(SA_KERNEL_MERGE);
+  return SA_OK;
+}
+
 sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
                     int32_t nprobe, int32_t* out_lists, cudaStream_t s) {
   (void)nq_pad;
@@ -220,10 +242,7 @@ sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, in
   uint64_t* pkeys;
   SA_TRY(dalloc(&pkeys, (size_t)nq * nprobe, s, "alloc probe keys"));
   f.add(pkeys);
-  const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, idx->nlist, idx->d_pad, nullptr, 0u};
-  SearchOut so;
-  so.keys = pkeys;
-  SA_TRY(flat_search_view(cvc, idx->num_sms, Qs, nq, nprobe, so, s));
+  SA_TRY(probe_keys(idx, Qs, nq, nprobe, pkeys, s));
   SA_CUDA(launch_keys_to_lists(pkeys, nq * nprobe, nullptr, out_lists, idx->num_sms, s), "lists");
   prof_count(SA_KERNEL_OTHER);
   return SA_OK;
@@ -244,11 +263,8 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   SA_TRY(dalloc(&probes, np, s, "alloc probes"));
   f.add(probes);
   {
-    const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, nlist, idx->d_pad, nullptr, 0u};
-    SearchOut so;
-    so.keys = pkeys;
     prof_begin(SA_KERNEL_IVF_PROBE, s);
-    sa_status st = flat_search_view(cvc, sms, Qs, nq, nprobe, so, s);
+    sa_status st = probe_keys(idx, Qs, nq, nprobe, pkeys, s);
     prof_end(SA_KERNEL_IVF_PROBE, s);
     if (st != SA_OK) return st;
   }

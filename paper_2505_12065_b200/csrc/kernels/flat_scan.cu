@@ -328,77 +328,108 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                            : ptx::smem_u32(&tail->a_full);
     const uint32_t tmem_empty0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&tail->tmem_empty[0]), 0)
                                          : ptx::smem_u32(&tail->tmem_empty[0]);
-    for (int w = unit; w < n_work; w += n_units) {
-      const WorkItem wi = work_item(w, a, T);
-      // This thread's query: flat -> row of the staged batch; ivf -> gathered prober.
+    // This thread's query in a work item: flat -> row of the staged batch; ivf -> gathered
+    // prober (query id, probe rank).
+    struct QSel {
       int64_t q;
-      int probe_j = 0;
+      int j;
       bool valid;
+    };
+    auto qsel = [&](const WorkItem& wi) -> QSel {
+      QSel r{0, 0, false};
       if (ivf) {
-        valid = rib < wi.cnt;
-        if (valid) {
+        r.valid = rib < wi.cnt;
+        if (r.valid) {
           const int2 e = a.lq_ent[wi.e0 + rib];
-          q = e.x;
-          probe_j = e.y;
-        } else {
-          q = 0;
+          r.q = e.x;
+          r.j = e.y;
         }
       } else {
-        q = ((int64_t)wi.qkey * CG + rank) * kBM + rib;
-        valid = q < a.nq;
+        r.q = ((int64_t)wi.qkey * CG + rank) * kBM + rib;
+        r.valid = r.q < a.nq;
       }
-      if (wi.qkey < 0 || wi.qkey != cur_qp) {
-        // Stage this query block into the A operand.  All MMAs that read the previous
-        // block completed before the last tmem_full this thread consumed.
-        const bool tma_thread = (!ivf && ew == 0 && lane == 0 && kb_s > 0);
-        if (tma_thread) {
-          // K-blocks [kb_t, num_kb) of this CTA's 128 query rows -> smem (SS operand)
-          const uint32_t bar = ptx::smem_u32(&tail->a_tma);
-          ptx::mbar_arrive_expect_tx(bar, (uint32_t)(kb_s * kASmemKb));
-          const int32_t qrow0 = (int32_t)(((int64_t)wi.qkey * CG + rank) * kBM);
-          for (int j = 0; j < kb_s; ++j)
-            ptx::tma_load_2d(ptx::smem_u32(a_smem + j * kASmemKb), &tmap_q, bar,
-                             (kb_t + j) * kBK, qrow0);
-        }
-        if (half == 0) {
-          // Rows of absent queries are left as they are: MMA output rows are independent
-          // and the epilogue never reads the rows of invalid lanes.
-          const uint4* src = reinterpret_cast<const uint4*>(a.Q + (size_t)q * a.d_pad);
-          for (int c = 0; c < kb_t; ++c) {
-            uint32_t r[32];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              uint4 v = valid ? __ldg(src + c * 8 + i) : make_uint4(0, 0, 0, 0);
-              r[4 * i + 0] = v.x; r[4 * i + 1] = v.y; r[4 * i + 2] = v.z; r[4 * i + 3] = v.w;
-            }
-            ptx::tmem_st32(tmem + lane_addr + a_col + c * 32, r);
-          }
-          ptx::tmem_wait_st();
-          if (ivf && valid) {
-            // smem K-blocks of a gathered row, written in the 128-byte-swizzled K-major
-            // layout the UMMA descriptor expects (16-byte chunk c of row r at c ^ (r & 7)).
-            for (int j = 0; j < kb_s; ++j) {
-              uint8_t* blk = a_smem + j * kASmemKb + (rib >> 3) * 1024 + (rib & 7) * 128;
-#pragma unroll
-              for (int c = 0; c < 8; ++c)
-                *reinterpret_cast<uint4*>(blk + ((c ^ (rib & 7)) << 4)) =
-                    __ldg(src + (kb_t + j) * 8 + c);
-            }
-            ptx::fence_proxy_async_smem();
-          }
-        }
-        if (tma_thread) {
-          ptx::mbar_wait(ptx::smem_u32(&tail->a_tma), a_tma_phase);
-          a_tma_phase ^= 1;
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (CG == 2 && !leader) ptx::mbar_arrive_cluster(a_full_leader);
-          else ptx::mbar_arrive(ptx::smem_u32(&tail->a_full));
-        }
-        cur_qp = wi.qkey;
+      return r;
+    };
+    // Stage item wi's query block into the A operand (TMEM K-blocks + smem K-blocks) and
+    // arrive on a_full.  Callers guarantee every MMA that read the previous block has
+    // completed (they consumed that block's last tmem_full).
+    auto stage_a = [&](const WorkItem& wi, const QSel& qs) {
+      const bool tma_thread = (!ivf && ew == 0 && lane == 0 && kb_s > 0);
+      if (tma_thread) {
+        // K-blocks [kb_t, num_kb) of this CTA's 128 query rows -> smem (SS operand)
+        const uint32_t bar = ptx::smem_u32(&tail->a_tma);
+        ptx::mbar_arrive_expect_tx(bar, (uint32_t)(kb_s * kASmemKb));
+        const int32_t qrow0 = (int32_t)(((int64_t)wi.qkey * CG + rank) * kBM);
+        for (int j = 0; j < kb_s; ++j)
+          ptx::tma_load_2d(ptx::smem_u32(a_smem + j * kASmemKb), &tmap_q, bar,
+                           (kb_t + j) * kBK, qrow0);
       }
+      if (half == 0) {
+        // Rows of absent queries are left as they are: MMA output rows are independent
+        // and the epilogue never reads the rows of invalid lanes.
+        const uint4* src = reinterpret_cast<const uint4*>(a.Q + (size_t)qs.q * a.d_pad);
+        for (int c = 0; c < kb_t; ++c) {
+          uint32_t r[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            uint4 v = qs.valid ? __ldg(src + c * 8 + i) : make_uint4(0, 0, 0, 0);
+            r[4 * i + 0] = v.x; r[4 * i + 1] = v.y; r[4 * i + 2] = v.z; r[4 * i + 3] = v.w;
+          }
+          ptx::tmem_st32(tmem + lane_addr + a_col + c * 32, r);
+        }
+        ptx::tmem_wait_st();
+        if (ivf && qs.valid) {
+          // smem K-blocks of a gathered row, written in the 128-byte-swizzled K-major
+          // layout the UMMA descriptor expects (16-byte chunk c of row r at c ^ (r & 7)).
+          for (int j = 0; j < kb_s; ++j) {
+            uint8_t* blk = a_smem + j * kASmemKb + (rib >> 3) * 1024 + (rib & 7) * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<uint4*>(blk + ((c ^ (rib & 7)) << 4)) =
+                  __ldg(src + (kb_t + j) * 8 + c);
+          }
+          ptx::fence_proxy_async_smem();
+        }
+      }
+      if (tma_thread) {
+        ptx::mbar_wait(ptx::smem_u32(&tail->a_tma), a_tma_phase);
+        a_tma_phase ^= 1;
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2 && !leader) ptx::mbar_arrive_cluster(a_full_leader);
+        else ptx::mbar_arrive(ptx::smem_u32(&tail->a_full));
+      }
+      cur_qp = wi.qkey;
+    };
+
+    int w = unit;
+    WorkItem wi{};
+    QSel cs{};
+    if (w < n_work) {
+      wi = work_item(w, a, T);
+      cs = qsel(wi);
+      stage_a(wi, cs);
+    }
+    while (w < n_work) {
+      const int wn = w + n_units;
+      const bool has_next = wn < n_work;
+      WorkItem nx{};
+      QSel ns{};
+      bool next_staged = false;
+      if (has_next) {
+        nx = work_item(wn, a, T);
+        ns = qsel(nx);
+      }
+      const bool next_needs_a = has_next && (nx.qkey < 0 || nx.qkey != wi.qkey);
+      if (wi.t1 <= wi.t0 && next_needs_a) {
+        stage_a(nx, ns);
+        next_staged = true;
+      }
+      const int64_t q = cs.q;
+      const int probe_j = cs.j;
+      const bool valid = cs.valid;
       for (int64_t t = wi.t0; t < wi.t1; ++t) {
         ptx::mbar_wait(ptx::smem_u32(&tail->tmem_full[acc]), acc_phase);
         ptx::tc_fence_after();
@@ -414,6 +445,13 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           else ptx::mbar_arrive(ptx::smem_u32(&tail->tmem_empty[acc]));
         }
         if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
+        // The last accumulator of this item is in registers, so every MMA that read this
+        // item's A operand has completed: stage the next item's queries now, before the
+        // score processing, so the tensor core restarts as early as possible.
+        if (t == wi.t1 - 1 && next_needs_a && !next_staged) {
+          stage_a(nx, ns);
+          next_staged = true;
+        }
         if (!valid) continue;
 
         const int64_t row0 = wi.row_base + t * kBN + half * 64;
@@ -460,6 +498,9 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
         thr = heap_threshold(0ull);
       }
+      w = wn;
+      wi = nx;
+      cs = ns;
     }
   }
 

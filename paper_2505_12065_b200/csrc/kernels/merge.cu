@@ -43,6 +43,7 @@ merge_topk_kernel(const MergeArgs a) {
   const bool cached = M <= kSmemCand;
 
   auto cand_g = [&](int64_t i) -> uint64_t {
+    if (a.cand_scores) return make_key(a.cand_scores[base + i], (uint32_t)i);
     if (!grouped) return a.cand[base + i];
     const int64_t g = i / k, j = i % k;
     return a.cand[(size_t)g * a.gstride + (size_t)q * a.qstride + j];

@@ -22,6 +22,7 @@ struct MergeArgs {
   int32_t slot_stride = 0;
   int32_t slot_keys = 0;
   int64_t m_flat = 0;
+  const float* cand_scores = nullptr;  // with m_flat: candidate i = key(cand_scores[q*qstride+i], i)
   int64_t* out_ids;     // [nq, k] (when out_keys == nullptr)
   float* out_scores;    // [nq, k]
   uint64_t* out_keys;   // [nq, k] packed keys, sorted (for another merge level)

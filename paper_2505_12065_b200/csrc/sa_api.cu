@@ -196,6 +196,29 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   return cuda_status(e, "flat search launch");
 }
 
+sa_status flat_scores_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
+                           float* out, cudaStream_t s) {
+  const int64_t nq_pad = padded_nq(nq);
+  const FlatPlan p = plan_flat(cv.n_rows, num_sms, nq_pad);
+  FlatScanArgs a{};
+  a.Q = Qs;
+  a.nq = nq;
+  a.nq_pad = nq_pad;
+  a.d_pad = cv.d_pad;
+  a.n_rows = cv.n_rows;
+  a.QP = p.QP;
+  a.S = p.S;
+  a.k = 1;
+  a.dbg = out;
+  a.mode = FS_MODE_DEBUG;
+  CUtensorMap tmap_q;
+  sa_status st = make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM);
+  if (st != SA_OK) return st;
+  cudaError_t e = launch_flat_scan(p.cg == 2 ? *cv.tmap2 : *cv.tmap1, tmap_q, a, p.cg, p.grid, s);
+  prof_count(SA_KERNEL_FLAT_SCAN);
+  return cuda_status(e, "score scan");
+}
+
 sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
                       int32_t k, const SearchOut& out, cudaStream_t s) {
   (void)nq_pad;
@@ -564,24 +587,8 @@ sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, 
     st = cuda_status(launch_cast_pad(queries, false, nq, idx->d, Qs, nq_pad, idx->d_pad,
                                      idx->num_sms, s), "stage queries");
   if (st == SA_OK) {
-    const FlatPlan p = plan_flat(idx->n_local, idx->num_sms, nq_pad);
-    FlatScanArgs a{};
-    a.Q = Qs;
-    a.nq = nq;
-    a.nq_pad = nq_pad;
-    a.d_pad = idx->d_pad;
-    a.n_rows = idx->n_local;
-    a.QP = p.QP;
-    a.S = p.S;
-    a.k = 1;
-    a.dbg = dbg;
-    a.mode = 1;
-    CUtensorMap tmap_q;
-    st = make_tmap_bf16(&tmap_q, Qs, nq_pad, idx->d_pad, FS_BM);
-    if (st == SA_OK)
-      st = cuda_status(
-          launch_flat_scan(p.cg == 2 ? idx->tmap_x2 : idx->tmap_x, tmap_q, a, p.cg, p.grid, s),
-          "debug scan");
+    CorpusView cv{&idx->tmap_x, &idx->tmap_x2, idx->n_local, idx->d_pad, nullptr, 0u};
+    st = flat_scores_view(cv, idx->num_sms, Qs, nq, dbg, s);
   }
   if (st == SA_OK)
     st = cuda_status(cudaMemcpyAsync(out_scores, dbg, (size_t)nq * idx->n_local * 4,
