@@ -311,6 +311,10 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
     SA_TRY(dalloc(&heap, (size_t)sms * k * FS_EPI_THREADS, s, "ivf heaps"));
     f.add(heap);
   }
+  uint32_t* hint;
+  SA_TRY(dalloc(&hint, nq, s, "ivf hints"));
+  f.add(hint);
+  SA_CUDA(cudaMemsetAsync(hint, 0, sizeof(uint32_t) * nq, s), "memset hints");
   CUtensorMap tmap_q;
   SA_TRY(make_tmap_bf16(&tmap_q, Qs, nq, idx->d_pad, FS_BM));
   FlatScanArgs a{};
@@ -333,6 +337,7 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   a.q_slot = w.q_slot;
   a.nprobe = nprobe;
   a.chunk_rows = kChunkRows;
+  a.q_hint = hint;
   prof_begin(SA_KERNEL_IVF_SCAN, s);
   cudaError_t e = launch_flat_scan(idx->tmap_x, tmap_q, a, 1, sms, s);
   prof_end(SA_KERNEL_IVF_SCAN, s);

@@ -338,9 +338,13 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     auto qsel = [&](const WorkItem& wi) -> QSel {
       QSel r{0, 0, false};
       if (ivf) {
-        r.valid = rib < wi.cnt;
+        // Prober i of the item sits on TMEM lane (i % 4) * 32 + i / 4: an item usually has
+        // only a few probers, and this spreads them over the four lane quadrants, i.e. over
+        // four different warps / SM sub-partitions, instead of piling them onto one warp.
+        const int i = lane * 4 + quad;
+        r.valid = i < wi.cnt;
         if (r.valid) {
-          const int2 e = a.lq_ent[wi.e0 + rib];
+          const int2 e = a.lq_ent[wi.e0 + i];
           r.q = e.x;
           r.j = e.y;
         }
@@ -430,6 +434,16 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       const int64_t q = cs.q;
       const int probe_j = cs.j;
       const bool valid = cs.valid;
+      // Exact pruning bound (IVF): q_hint[q] holds the best k-th score any finished item of
+      // query q has seen; the query's final k-th score can only be >= it, so smaller scores
+      // can never be returned.  Ties pass (s >= thr).  Cuts the insertion burst that every
+      // freshly reset per-item heap would otherwise take.
+      float hint = heap_threshold(0ull);
+      if (valid && a.q_hint) {
+        const uint32_t h = *reinterpret_cast<volatile const uint32_t*>(a.q_hint + q);
+        if (h != 0u) hint = float_from_ordered(h);
+      }
+      thr = fmaxf(thr, hint);
       for (int64_t t = wi.t0; t < wi.t1; ++t) {
         ptx::mbar_wait(ptx::smem_u32(&tail->tmem_full[acc]), acc_phase);
         ptx::tc_fence_after();
@@ -481,7 +495,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
               if (row < wi.row_end) {
                 const uint32_t id =
                     a.id_base + (a.row_ids ? (uint32_t)a.row_ids[row] : (uint32_t)row);
-                thr = heap_offer(heap, k, make_key(s, id));
+                thr = fmaxf(heap_offer(heap, k, make_key(s, id)), hint);
               }
             }
           }
@@ -494,6 +508,8 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                   : (size_t)q * S + wi.s;
           uint64_t* dst = a.part + (slot * FS_LISTS_PER_ITEM + half) * k;
           for (int i = 0; i < k; ++i) dst[i] = heap[(size_t)i * kEpiT];
+          const uint64_t root = heap[0];
+          if (a.q_hint && root != 0ull) atomicMax(a.q_hint + q, (uint32_t)(root >> 32));
         }
         for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
         thr = heap_threshold(0ull);

@@ -51,6 +51,8 @@ struct FlatScanArgs {
   const int64_t* q_slot;   // [nq * nprobe] first output slot of (query, probe rank)
   int32_t nprobe;
   int32_t chunk_rows;      // rows per IVF work item (multiple of FS_BN)
+  uint32_t* q_hint;        // optional [nq] ordered-fp32 lower bound of each query's k-th score
+                           // (zero-initialised by the caller; 0 = none)
 };
 
 // cta_group = 1: one CTA per query block of 128 (M=128, box 128 rows).
