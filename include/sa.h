@@ -62,6 +62,8 @@ typedef struct {
   int64_t n_total;         /* total rows over all shards (default: n) */
   const sa_comm* comm;     /* NULL = unsharded; else the communicator this shard belongs to */
   void* stream;            /* stream used for the build (default NULL) */
+  const float* centroids;  /* optional DEVICE fp32 [nlist, d]: use these IVF centroids instead
+                              of training (e.g. a quantiser trained once for all shards) */
 } sa_build_opts;
 
 /* Fill *o with the defaults listed above. */
@@ -103,6 +105,22 @@ sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype
 sa_status sa_search_host(const sa_index* idx, const void* queries_host, sa_dtype qdtype,
                          int64_t nq, int32_t k, int32_t nprobe, int64_t* out_ids_host,
                          float* out_scores_host, void* stream);
+
+/*
+ * The two halves of a row-sharded search, exposed so the cross-rank step
+ * can be driven (and tested) by the caller:
+ *   sa_search_keys: this shard's top-k as packed 64-bit keys, DEVICE uint64 [nq, k], sorted
+ *                   best first; key = (order-preserving fp32 bits << 32) | (0xFFFFFFFF - id)
+ *                   with the GLOBAL id (row_offset + local row); empty slots are 0.
+ *   sa_merge_keys:  the final k-way merge of w such lists, DEVICE uint64 [w, nq, k]
+ *                   (rank-major, as ncclAllGather lays them out) -> DEVICE out_ids int64
+ *                   [nq, k] / out_scores fp32 [nq, k], padded (-1, -INF).
+ * sa_search on a sharded index is exactly sa_search_keys + ncclAllGather + sa_merge_keys.
+ */
+sa_status sa_search_keys(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                         int32_t k, int32_t nprobe, uint64_t* out_keys, void* stream);
+sa_status sa_merge_keys(const uint64_t* keys, int32_t w, int64_t nq, int32_t k, int64_t* out_ids,
+                        float* out_scores, void* stream);
 
 sa_status sa_index_free(sa_index* idx);
 

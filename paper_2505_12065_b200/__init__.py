@@ -41,6 +41,7 @@ class _BuildOpts(ctypes.Structure):
         ("n_total", ctypes.c_int64),
         ("comm", ctypes.c_void_p),
         ("stream", ctypes.c_void_p),
+        ("centroids", ctypes.c_void_p),
     ]
 
 
@@ -65,6 +66,8 @@ def lib() -> ctypes.CDLL:
         "sa_search": (st, [P, P, i64, i32, i32, P, P, P]),
         "sa_search_ex": (st, [P, P, ctypes.c_int, i64, i32, i32, P, P, P]),
         "sa_search_host": (st, [P, P, ctypes.c_int, i64, i32, i32, P, P, P]),
+        "sa_search_keys": (st, [P, P, ctypes.c_int, i64, i32, i32, P, P]),
+        "sa_merge_keys": (st, [P, i32, i64, i32, P, P, P]),
         "sa_index_free": (st, [P]),
         "sa_comm_unique_id": (st, [P]),
         "sa_comm_init": (st, [P, i32, i32, i32, ctypes.POINTER(P)]),
@@ -135,19 +138,26 @@ class Comm:
     def __init__(self, handle, rank, world):
         self.handle, self.rank, self.world = handle, rank, world
 
-    @classmethod
-    def from_torch_distributed(cls, device: int | None = None):
+    @staticmethod
+    def exchange_unique_id() -> bytes:
+        """Rank 0 creates the 128-byte NCCL unique id (sa_comm_unique_id); torch.distributed
+        broadcasts it (works on nccl and gloo process groups)."""
         import torch.distributed as dist
-        rank, world = dist.get_rank(), dist.get_world_size()
         uid = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
+        if dist.get_rank() == 0:
             buf = (ctypes.c_uint8 * 128)()
             _check(lib().sa_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
             uid = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
         if dist.get_backend() == "nccl":
             uid = uid.cuda()
         dist.broadcast(uid, 0)
-        raw = bytes(uid.cpu().tolist())
+        return bytes(uid.cpu().tolist())
+
+    @classmethod
+    def from_torch_distributed(cls, device: int | None = None):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        raw = cls.exchange_unique_id()
         h = ctypes.c_void_p()
         dev = torch.cuda.current_device() if device is None else device
         _check(lib().sa_comm_init(ctypes.c_char_p(raw), rank, world, dev, ctypes.byref(h)))
@@ -176,7 +186,8 @@ class Index:
     @classmethod
     def build(cls, corpus: torch.Tensor, nlist: int = 0, *, kmeans_iters: int = 20,
               train_per_list: int = 256, seed: int = 0x5A2505, row_offset: int = 0,
-              n_total: int | None = None, comm: Comm | None = None, stream=None) -> "Index":
+              n_total: int | None = None, comm: Comm | None = None, centroids=None,
+              stream=None) -> "Index":
         if not corpus.is_cuda or corpus.dim() != 2 or not corpus.is_contiguous():
             raise ValueError("corpus must be a contiguous 2-D CUDA tensor")
         o = _BuildOpts()
@@ -189,6 +200,12 @@ class Index:
         o.n_total = n_total if n_total is not None else 0
         o.comm = comm.handle if comm is not None else None
         o.stream = _stream_ptr(stream)
+        if centroids is not None:
+            if not centroids.is_cuda or centroids.dtype != torch.float32 or \
+                    tuple(centroids.shape) != (nlist, corpus.shape[1]):
+                raise ValueError("centroids must be a CUDA float32 [nlist, d] tensor")
+            centroids = centroids.contiguous()
+            o.centroids = centroids.data_ptr()
         h = ctypes.c_void_p()
         _check(lib().sa_index_build_ex(_ptr(corpus), corpus.shape[0], corpus.shape[1], nlist,
                                        ctypes.byref(o), ctypes.byref(h)))
@@ -209,6 +226,15 @@ class Index:
         _check(lib().sa_search_ex(self.handle, _ptr(queries), _dtype_code(queries), nq, k, nprobe,
                                   _ptr(ids), _ptr(scores), _stream_ptr(stream)))
         return ids, scores
+
+    # sa_search_keys: this shard's sorted packed keys (global ids), int64 view of uint64 [nq, k]
+    def search_keys(self, queries: torch.Tensor, k: int, nprobe: int = 0, stream=None):
+        if not queries.is_cuda or queries.dim() != 2 or not queries.is_contiguous():
+            raise ValueError("queries must be a contiguous 2-D CUDA tensor")
+        keys = torch.empty(queries.shape[0], k, dtype=torch.int64, device=queries.device)
+        _check(lib().sa_search_keys(self.handle, _ptr(queries), _dtype_code(queries),
+                                    queries.shape[0], k, nprobe, _ptr(keys), _stream_ptr(stream)))
+        return keys
 
     # sa_search_host: host buffers in and out, copies inside the call
     def search_host(self, queries: torch.Tensor, k: int, nprobe: int = 0, out=None, stream=None):
@@ -272,6 +298,16 @@ class Index:
             self.free()
         except Exception:
             pass
+
+
+def sa_merge_keys(keys: torch.Tensor, stream=None):
+    """Final merge of per-rank key lists: keys int64 (uint64 bits) CUDA [w, nq, k]."""
+    w, nq, k = keys.shape
+    keys = keys.contiguous()
+    ids = torch.empty(nq, k, dtype=torch.int64, device=keys.device)
+    scores = torch.empty(nq, k, dtype=torch.float32, device=keys.device)
+    _check(lib().sa_merge_keys(_ptr(keys), w, nq, k, _ptr(ids), _ptr(scores), _stream_ptr(stream)))
+    return ids, scores
 
 
 # C-ABI-named aliases

@@ -46,6 +46,16 @@ sa_status cuda_status(cudaError_t e, const char* what);
 sa_status make_tmap_bf16(CUtensorMap* m, const void* base, int64_t rows, int32_t cols,
                          int32_t box_rows);
 
+// NCCL: every rank r contributes bytes [off[r], off[r]+len[r]) of buf; all ranks end with all.
+sa_status comm_broadcast_parts(const sa_comm* c, void* buf, const int64_t* off, const int64_t* len,
+                               cudaStream_t s);
+// balanced contiguous split
+inline void shard_range(int64_t n, int world, int rank, int64_t* off, int64_t* len) {
+  const int64_t base = n / world, rem = n % world;
+  *off = rank * base + (rank < rem ? rank : rem);
+  *len = base + (rank < rem ? 1 : 0);
+}
+
 // profiler hooks
 void prof_count(int kind);
 void prof_begin(int kind, cudaStream_t s);

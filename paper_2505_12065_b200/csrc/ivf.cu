@@ -86,27 +86,64 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   const int sms = idx->num_sms;
   const int64_t n = idx->n_local;
   if (nlist > 65536) return set_error(SA_ERR_UNSUPPORTED, "nlist > 65536");
-  if (idx->comm && idx->comm->world > 1)
-    return set_error(SA_ERR_UNSUPPORTED, "sharded IVF build is not available yet");
   const int64_t n_total = idx->n_total;
+  const sa_comm* comm = (idx->comm && idx->comm->world > 1) ? idx->comm : nullptr;
   const int64_t n_train = std::min<int64_t>(n_total, (int64_t)o.train_per_list * nlist);
   Freer f{s};
 
-  // ---- a2: training sample by global id (R9), centroids
-  __nv_bfloat16* sample;
-  SA_TRY(dalloc(&sample, (size_t)n_train * dp, s, "alloc sample"));
-  f.add(sample);
-  SA_CUDA(launch_gather_rows(idx->X, dp, nullptr, n_total, idx->row_offset, n_train, sample, sms, s),
-          "gather sample");
-  prof_count(SA_KERNEL_OTHER);
   SA_CUDA(cudaMalloc(&idx->centroids, (size_t)nlist * dp * sizeof(float)), "alloc centroids");
   SA_CUDA(cudaMalloc(&idx->centroids_bf16, (size_t)nlist * dp * sizeof(__nv_bfloat16)),
           "alloc centroids bf16");
-  SA_CUDA(launch_init_centroids(sample, dp, nlist, n_train, o.seed, idx->centroids, s), "init");
-  prof_count(SA_KERNEL_OTHER);
   SA_TRY(make_tmap_bf16(&idx->tmap_c, idx->centroids_bf16, nlist, dp, FS_BN));
   SA_TRY(make_tmap_bf16(&idx->tmap_c2, idx->centroids_bf16, nlist, dp, FS_BN / 2));
   const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, nlist, dp, nullptr, 0u};
+  const bool train = o.centroids == nullptr;
+
+  // ---- a2: training sample by global id (R9).  Shards are contiguous row ranges, so rank r
+  // owns the contiguous sample range t in [ceil(off_r * n_train / n_total), ...): each rank
+  // gathers its part and NCCL broadcasts assemble the identical full sample everywhere.
+  __nv_bfloat16* sample = nullptr;
+  if (train) {
+    SA_TRY(dalloc(&sample, (size_t)n_train * dp, s, "alloc sample"));
+    f.add(sample);
+    const int world = comm ? comm->world : 1;
+    std::vector<int64_t> toff(world + 1), boff(world), blen(world);
+    for (int r = 0; r <= world; ++r) {
+      int64_t off_r = n_total, len_r = 0;
+      if (r < world) shard_range(n_total, world, r, &off_r, &len_r);
+      // smallest t with floor(t * n_total / n_train) >= off_r
+      toff[r] = (off_r * n_train + n_total - 1) / n_total;
+    }
+    const int me = comm ? comm->rank : 0;
+    if (comm) {
+      int64_t off_me, len_me;
+      shard_range(n_total, world, me, &off_me, &len_me);
+      if (off_me != idx->row_offset || len_me != n)
+        return set_error(SA_ERR_INVALID_ARG,
+                         "sharded IVF build expects the balanced split off_r = r*floor(n/w) + "
+                         "min(r, n mod w)");
+    }
+    SA_CUDA(launch_gather_rows(idx->X, dp, nullptr, n_total, idx->row_offset, toff[me], n_train,
+                               toff[me + 1] - toff[me], sample + (size_t)toff[me] * dp, sms, s),
+            "gather sample");
+    prof_count(SA_KERNEL_OTHER);
+    if (comm) {
+      for (int r = 0; r < world; ++r) {
+        boff[r] = toff[r] * dp * (int64_t)sizeof(__nv_bfloat16);
+        blen[r] = (toff[r + 1] - toff[r]) * dp * (int64_t)sizeof(__nv_bfloat16);
+      }
+      SA_TRY(comm_broadcast_parts(comm, sample, boff.data(), blen.data(), s));
+    }
+    SA_CUDA(launch_init_centroids(sample, dp, nlist, n_train, o.seed, idx->centroids, s), "init");
+    prof_count(SA_KERNEL_OTHER);
+  } else {
+    // caller-provided quantiser: fp32 [nlist, d] -> [nlist, d_pad], zero padded
+    SA_CUDA(cudaMemsetAsync(idx->centroids, 0, (size_t)nlist * dp * sizeof(float), s), "memset");
+    SA_CUDA(cudaMemcpy2DAsync(idx->centroids, (size_t)dp * sizeof(float), o.centroids,
+                              (size_t)idx->d * sizeof(float), (size_t)idx->d * sizeof(float), nlist,
+                              cudaMemcpyDeviceToDevice, s),
+            "copy centroids");
+  }
 
   int64_t* ids;
   float* scores;
@@ -131,7 +168,7 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   SA_TRY(dalloc(&rsel, 256, s, "alloc repair sel"));
   f.add(rsel);
 
-  for (int it = 0; it < o.kmeans_iters; ++it) {
+  for (int it = 0; train && it < o.kmeans_iters; ++it) {
     SA_CUDA(launch_f32_to_bf16(idx->centroids, (int64_t)nlist * dp, idx->centroids_bf16, sms, s),
             "centroids->bf16");
     prof_count(SA_KERNEL_OTHER);
@@ -189,7 +226,7 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   SA_TRY(sort_by_list(ids_all, n, nlist, sms, perm_all, idx->list_off, s));
   __nv_bfloat16* Xp = nullptr;
   SA_CUDA(cudaMalloc(&Xp, (size_t)n * dp * sizeof(__nv_bfloat16)), "alloc list-major corpus");
-  cudaError_t e = launch_gather_rows(idx->X, dp, perm_all, 0, 0, n, Xp, sms, s);
+  cudaError_t e = launch_gather_rows(idx->X, dp, perm_all, 0, 0, 0, 1, n, Xp, sms, s);
   if (e == cudaSuccess) e = cudaMalloc(&idx->row_ids, (size_t)n * sizeof(int32_t));
   if (e == cudaSuccess) e = launch_perm_ids(perm_all, n, idx->row_offset, idx->row_ids, sms, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);

@@ -28,32 +28,32 @@ uint64_t host_splitmix64(uint64_t z) {
 }
 
 // ------------------------------------------------------------------ gathers
-// out[t] = X[src(t)] with src(t) = floor(t * n_total / n_out) - row_offset  (training sample,
-// global-id strided, R9), or src(t) = idx[t] when idx != nullptr.
+// out[t] = X[src(t)] with src(t) = floor((t0 + t) * n_total / n_train) - row_offset (training
+// sample rows t0.., global-id strided, R9), or src(t) = idx[t] when idx != nullptr.
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ X, int d_pad,
                                    const int32_t* __restrict__ idx, int64_t n_total,
-                                   int64_t row_offset, int64_t n_out,
-                                   __nv_bfloat16* __restrict__ out) {
+                                   int64_t row_offset, int64_t t0, int64_t n_train,
+                                   int64_t n_out, __nv_bfloat16* __restrict__ out) {
   const int v8 = d_pad / 8;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_out * v8;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e / v8;
     const int c = (int)(e % v8);
-    const int64_t src = idx ? (int64_t)idx[t] : (t * n_total) / n_out - row_offset;
+    const int64_t src = idx ? (int64_t)idx[t] : ((t0 + t) * n_total) / n_train - row_offset;
     reinterpret_cast<uint4*>(out + t * d_pad)[c] =
         reinterpret_cast<const uint4*>(X + src * d_pad)[c];
   }
 }
 
 cudaError_t launch_gather_rows(const __nv_bfloat16* X, int d_pad, const int32_t* idx,
-                               int64_t n_total, int64_t row_offset, int64_t n_out,
-                               __nv_bfloat16* out, int num_sms, cudaStream_t s) {
+                               int64_t n_total, int64_t row_offset, int64_t t0, int64_t n_train,
+                               int64_t n_out, __nv_bfloat16* out, int num_sms, cudaStream_t s) {
   if (n_out <= 0) return cudaSuccess;
   const int64_t work = n_out * (d_pad / 8);
   int64_t blocks = (work + 255) / 256;
   if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
-  gather_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, d_pad, idx, n_total, row_offset, n_out,
-                                                      out);
+  gather_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, d_pad, idx, n_total, row_offset, t0,
+                                                      n_train, n_out, out);
   return cudaGetLastError();
 }
 

@@ -9,9 +9,11 @@ namespace sa {
 
 uint64_t host_splitmix64(uint64_t z);
 
+// out[t] = X[idx[t]] (idx != nullptr), else the training-sample rows t0 .. t0+n_out-1 of an
+// n_train-row sample strided by global id over n_total rows (local row = global - row_offset).
 cudaError_t launch_gather_rows(const __nv_bfloat16* X, int d_pad, const int32_t* idx,
-                               int64_t n_total, int64_t row_offset, int64_t n_out,
-                               __nv_bfloat16* out, int num_sms, cudaStream_t s);
+                               int64_t n_total, int64_t row_offset, int64_t t0, int64_t n_train,
+                               int64_t n_out, __nv_bfloat16* out, int num_sms, cudaStream_t s);
 cudaError_t launch_init_centroids(const __nv_bfloat16* sample, int d_pad, int nlist,
                                   int64_t n_train, uint64_t seed, float* cent, cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* in, int64_t n, __nv_bfloat16* out, int num_sms,

@@ -241,6 +241,10 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
 };
 NcclApi& nccl() {
   static NcclApi api;
@@ -255,6 +259,9 @@ NcclApi& nccl() {
     api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
     api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+    api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
+    api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather;
   });
   return api;
@@ -265,6 +272,25 @@ sa_status nccl_status(ncclResult_t r, const char* what) {
   return set_error(SA_ERR_NCCL, std::string(what) + ": " + m);
 }
 }  // namespace
+
+namespace sa {
+// Every rank r contributes bytes [off[r], off[r] + len[r]) of `buf`; afterwards every rank
+// holds all parts (one ncclBroadcast per root inside a group).
+sa_status comm_broadcast_parts(const sa_comm* c, void* buf, const int64_t* off, const int64_t* len,
+                               cudaStream_t s) {
+  if (!nccl().ok || !nccl().Broadcast || !nccl().GroupStart || !nccl().GroupEnd)
+    return set_error(SA_ERR_NCCL, "libnccl.so.2 not found");
+  sa_status st = nccl_status(nccl().GroupStart(), "ncclGroupStart");
+  for (int r = 0; st == SA_OK && r < c->world; ++r) {
+    if (len[r] == 0) continue;
+    char* p = static_cast<char*>(buf) + off[r];
+    st = nccl_status(nccl().Broadcast(p, p, (size_t)len[r], ncclUint8, r, (ncclComm_t)c->nccl, s),
+                     "ncclBroadcast");
+  }
+  sa_status st2 = nccl_status(nccl().GroupEnd(), "ncclGroupEnd");
+  return st != SA_OK ? st : st2;
+}
+}  // namespace sa
 
 extern "C" {
 
@@ -294,6 +320,7 @@ void sa_build_opts_default(sa_build_opts* o) {
   o->n_total = 0;
   o->comm = nullptr;
   o->stream = nullptr;
+  o->centroids = nullptr;
 }
 
 sa_status sa_comm_unique_id(void* out) {
@@ -429,16 +456,13 @@ static sa_status validate_search(const sa_index* idx, const void* q, int64_t nq,
   return SA_OK;
 }
 
-sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
-                       int32_t k, int32_t nprobe, int64_t* out_ids, float* out_scores,
-                       void* stream) {
-  sa_status st = validate_search(idx, queries, nq, k, nprobe, out_ids, out_scores);
-  if (st != SA_OK) return st;
-  if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
-  cudaStream_t s = (cudaStream_t)stream;
+// a4 staging + the rank-local search (flat or IVF) into `out`.
+static sa_status search_local(const sa_index* idx, const void* queries, sa_dtype qdtype,
+                              int64_t nq, int32_t k, int32_t nprobe, const SearchOut& out,
+                              cudaStream_t s) {
   const int64_t nq_pad = padded_nq(nq);
   __nv_bfloat16* Qs = nullptr;
-  st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "alloc staged queries");
+  sa_status st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "alloc staged queries");
   if (st != SA_OK) return st;
   prof_begin(SA_KERNEL_STAGE, s);
   cudaError_t e = launch_cast_pad(queries, qdtype == SA_F32, nq, idx->d, Qs, nq_pad, idx->d_pad,
@@ -449,46 +473,79 @@ sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype
     cudaFreeAsync(Qs, s);
     return cuda_status(e, "stage queries");
   }
+  st = nprobe == 0 ? flat_search(idx, Qs, nq, nq_pad, k, out, s)
+                   : ivf_search(idx, Qs, nq, nq_pad, k, nprobe, out, s);
+  cudaFreeAsync(Qs, s);
+  return st;
+}
+
+static sa_status merge_keys(const uint64_t* keys, int32_t w, int64_t nq, int32_t k,
+                            int64_t* out_ids, float* out_scores, cudaStream_t s) {
+  MergeArgs m{};
+  m.cand = keys;
+  m.groups = w;
+  m.k = k;
+  m.qstride = k;
+  m.gstride = nq * k;
+  m.out_ids = out_ids;
+  m.out_scores = out_scores;
+  prof_begin(SA_KERNEL_MERGE, s);
+  sa_status st = cuda_status(launch_merge(m, nq, s), "final merge");
+  prof_end(SA_KERNEL_MERGE, s);
+  prof_count(SA_KERNEL_MERGE);
+  return st;
+}
+
+sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                       int32_t k, int32_t nprobe, int64_t* out_ids, float* out_scores,
+                       void* stream) {
+  sa_status st = validate_search(idx, queries, nq, k, nprobe, out_ids, out_scores);
+  if (st != SA_OK) return st;
+  if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
+  cudaStream_t s = (cudaStream_t)stream;
   const bool sharded = idx->comm && idx->comm->world > 1;
-  uint64_t *keys_local = nullptr, *keys_all = nullptr;
-  SearchOut out;
-  if (sharded) {
-    const int w = idx->comm->world;
-    st = dalloc(&keys_local, (size_t)nq * k, s, "alloc local keys");
-    if (st == SA_OK) st = dalloc(&keys_all, (size_t)nq * k * w, s, "alloc gathered keys");
-    out.keys = keys_local;
-  } else {
+  if (!sharded) {
+    SearchOut out;
     out.ids = out_ids;
     out.scores = out_scores;
+    return search_local(idx, queries, qdtype, nq, k, nprobe, out, s);
   }
+  // a9: rank-local sorted [nq, k] keys (global ids) -> ncclAllGather -> k-way merge.
+  const int w = idx->comm->world;
+  uint64_t *keys_local = nullptr, *keys_all = nullptr;
+  st = dalloc(&keys_local, (size_t)nq * k, s, "alloc local keys");
+  if (st == SA_OK) st = dalloc(&keys_all, (size_t)nq * k * w, s, "alloc gathered keys");
   if (st == SA_OK) {
-    st = nprobe == 0 ? flat_search(idx, Qs, nq, nq_pad, k, out, s)
-                     : ivf_search(idx, Qs, nq, nq_pad, k, nprobe, out, s);
+    SearchOut out;
+    out.keys = keys_local;
+    st = search_local(idx, queries, qdtype, nq, k, nprobe, out, s);
   }
-  if (st == SA_OK && sharded) {
-    // a9: all-gather the per-rank sorted [nq, k] key lists, then a k-way merge.
+  if (st == SA_OK)
     st = nccl_status(nccl().AllGather(keys_local, keys_all, (size_t)nq * k, ncclUint64,
                                       (ncclComm_t)idx->comm->nccl, s),
                      "ncclAllGather");
-    if (st == SA_OK) {
-      MergeArgs m{};
-      m.cand = keys_all;
-      m.groups = idx->comm->world;
-      m.k = k;
-      m.qstride = k;
-      m.gstride = nq * k;
-      m.out_ids = out_ids;
-      m.out_scores = out_scores;
-      prof_begin(SA_KERNEL_MERGE, s);
-      st = cuda_status(launch_merge(m, nq, s), "final merge");
-      prof_end(SA_KERNEL_MERGE, s);
-      prof_count(SA_KERNEL_MERGE);
-    }
-  }
+  if (st == SA_OK) st = merge_keys(keys_all, w, nq, k, out_ids, out_scores, s);
   if (keys_local) cudaFreeAsync(keys_local, s);
   if (keys_all) cudaFreeAsync(keys_all, s);
-  cudaFreeAsync(Qs, s);
   return st;
+}
+
+sa_status sa_search_keys(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                         int32_t k, int32_t nprobe, uint64_t* out_keys, void* stream) {
+  sa_status st = validate_search(idx, queries, nq, k, nprobe, out_keys, out_keys);
+  if (st != SA_OK) return st;
+  if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
+  SearchOut out;
+  out.keys = out_keys;
+  return search_local(idx, queries, qdtype, nq, k, nprobe, out, (cudaStream_t)stream);
+}
+
+sa_status sa_merge_keys(const uint64_t* keys, int32_t w, int64_t nq, int32_t k, int64_t* out_ids,
+                        float* out_scores, void* stream) {
+  if (!keys || !out_ids || !out_scores) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (w < 1 || nq < 1) return set_error(SA_ERR_INVALID_ARG, "w and nq must be >= 1");
+  if (k < 1 || k > 256) return set_error(SA_ERR_INVALID_ARG, "k must be in [1, 256]");
+  return merge_keys(keys, w, nq, k, out_ids, out_scores, (cudaStream_t)stream);
 }
 
 sa_status sa_search(const sa_index* idx, const void* queries, int64_t nq, int32_t k, int32_t nprobe,
