@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--nlist", type=int, default=16384)
     ap.add_argument("--nq", type=int, default=None, help="override batch size")
     ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--d", type=int, default=None, help="override dimension (experiments)")
+    ap.add_argument("--n", type=int, default=None, help="override corpus rows (experiments)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -199,6 +201,10 @@ def main():
         cfg["nq"] = args.nq
     if args.k:
         cfg["k"] = args.k
+    if args.d:
+        cfg["d"] = args.d
+    if args.n:
+        cfg["n"] = args.n
     if args.impl == "reference":
         return run_reference(args, cfg, args.config)
 

@@ -143,6 +143,22 @@ __device__ __forceinline__ WorkItem work_item(int w, const FlatScanArgs& a, int6
   return wi;
 }
 
+// Warp-uniform copy of a work item (whole warp must call): values loaded from memory
+// (IVF items) are broadcast from lane 0 so the MMA loop stays provably uniform.
+__device__ __forceinline__ WorkItem uniform_item(const WorkItem& w) {
+  WorkItem u;
+  u.qkey = __shfl_sync(0xffffffffu, w.qkey, 0);
+  u.s = __shfl_sync(0xffffffffu, w.s, 0);
+  u.t0 = __shfl_sync(0xffffffffu, w.t0, 0);
+  u.t1 = __shfl_sync(0xffffffffu, w.t1, 0);
+  u.row_base = __shfl_sync(0xffffffffu, w.row_base, 0);
+  u.row_end = __shfl_sync(0xffffffffu, w.row_end, 0);
+  u.chunk = __shfl_sync(0xffffffffu, w.chunk, 0);
+  u.e0 = __shfl_sync(0xffffffffu, w.e0, 0);
+  u.cnt = __shfl_sync(0xffffffffu, w.cnt, 0);
+  return u;
+}
+
 }  // namespace
 
 template <int CG>
@@ -159,7 +175,9 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
   SmemTail<CG>* tail = reinterpret_cast<SmemTail<CG>*>(reinterpret_cast<uint8_t*>(heap_s) +
                                                        FS_KSMEM * kEpiT * sizeof(uint64_t));
 
-  const int warp = threadIdx.x / 32;
+  // Broadcast from lane 0 so the compiler knows role branches are warp-uniform (lets ptxas
+  // keep the MMA operands in uniform registers instead of a per-MMA R2UR waterfall).
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0);
   const int lane = threadIdx.x % 32;
   const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
   const bool leader = rank == 0;
@@ -249,6 +267,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA; warp-convergent, elect.sync issues) ======
     if (leader) {
+      const int n_work_u = __shfl_sync(0xffffffffu, n_work, 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -259,8 +278,8 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(a_smem));
       const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
       const uint32_t empty0 = ptx::smem_u32(&tail->empty[0]);
-      for (int w = unit; w < n_work; w += n_units) {
-        const WorkItem wi = work_item(w, a, T);
+      for (int w = unit; w < n_work_u; w += n_units) {
+        const WorkItem wi = uniform_item(work_item(w, a, T));
         if (wi.qkey < 0 || wi.qkey != cur_qp) {
           ptx::mbar_wait(ptx::smem_u32(&tail->a_full), a_phase);
           a_phase ^= 1;
