@@ -12,7 +12,7 @@ constexpr int FS_BM = 128;       // query rows per CTA (TMEM lanes)
 constexpr int FS_BN = 128;       // corpus rows per tile (MMA N, accumulator columns)
 constexpr int FS_BK = 64;        // bf16 per 128-byte swizzle row (one TMA box column extent)
 constexpr int FS_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, 64 columns each
-constexpr int FS_THREADS = 64 + 32 * FS_EPI_WARPS;  // warp 0 TMA, warp 1 MMA, 8 epilogue warps
+constexpr int FS_THREADS = 64 + 32 * FS_EPI_WARPS;  // 8 epilogue warps, TMA warp, MMA warp
 constexpr int FS_EPI_THREADS = 32 * FS_EPI_WARPS;
 constexpr int FS_MAX_DPAD = 768; // queries: up to 8 K-blocks in TMEM + 4 in smem
 constexpr int FS_KB_TMEM = 8;    // K-blocks of the A operand held in TMEM (256 columns)
@@ -53,6 +53,8 @@ struct FlatScanArgs {
   int32_t chunk_rows;      // rows per IVF work item (multiple of FS_BN)
   uint32_t* q_hint;        // optional [nq] ordered-fp32 lower bound of each query's k-th score
                            // (zero-initialised by the caller; 0 = none)
+  int32_t experiment;      // timing experiments only (env SA_EXPERIMENT): 1 = skip score
+                           // processing, 2 = also skip the TMEM loads.  0 in production.
 };
 
 // cta_group = 1: one CTA per query block of 128 (M=128, box 128 rows).

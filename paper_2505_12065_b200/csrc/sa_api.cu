@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -150,7 +151,19 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
     st = dalloc(&heap, (size_t)p.grid * k * FS_EPI_THREADS, s, "alloc heaps");
     if (st != SA_OK) { cudaFreeAsync(part, s); return st; }
   }
+  // shared per-query pruning bound, useful when a query's rows are split over slices
+  uint32_t* hint = nullptr;
+  if (p.S > 1) {
+    st = dalloc(&hint, (size_t)nq, s, "alloc hints");
+    if (st == SA_OK) st = cuda_status(cudaMemsetAsync(hint, 0, nq * sizeof(uint32_t), s), "memset");
+    if (st != SA_OK) {
+      if (heap) cudaFreeAsync(heap, s);
+      cudaFreeAsync(part, s);
+      return st;
+    }
+  }
   FlatScanArgs a{};
+  a.q_hint = hint;
   a.Q = Qs;
   a.nq = nq;
   a.nq_pad = nq_pad;
@@ -164,6 +177,13 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   a.part = part;
   a.heap_g = heap;
   a.mode = FS_MODE_TOPK;
+  {
+    static const int experiment = [] {
+      const char* e = getenv("SA_EXPERIMENT");
+      return e ? atoi(e) : 0;
+    }();
+    a.experiment = experiment;
+  }
   CUtensorMap tmap_q;
   st = make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM);
   if (st != SA_OK) {
@@ -192,6 +212,7 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
     prof_count(SA_KERNEL_MERGE);
   }
   if (heap) cudaFreeAsync(heap, s);
+  if (hint) cudaFreeAsync(hint, s);
   cudaFreeAsync(part, s);
   return cuda_status(e, "flat search launch");
 }
