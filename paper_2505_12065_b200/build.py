@@ -19,6 +19,11 @@ NVCC_FLAGS = [
 ]
 
 
+# flat_scan_topk_kernel runs 320 threads at 1 CTA/SM: 65536 / 320 = 204 registers are
+# available; let ptxas use them instead of spilling the epilogue's state.
+PER_FILE_FLAGS = {"flat_scan.cu": ["-maxrregcount=200"]}
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "kernels", "*.cu")))
 
@@ -46,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     logs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.relpath(src, CSRC).replace(os.sep, "_") + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        extra = PER_FILE_FLAGS.get(os.path.basename(src), [])
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stdout + r.stderr)
         if r.returncode != 0:

@@ -105,20 +105,20 @@ __device__ __noinline__ float heap_offer(uint64_t* h, int k, uint64_t key) {
 struct WorkItem {
   int qkey;          // query-block identity (flat: query group); -1 = always reload (ivf)
   int s;             // flat: corpus slice
-  int64_t t0, t1;    // tile range
-  int64_t row_base;  // first corpus row of tile 0
-  int64_t row_end;   // rows >= row_end are masked (list end / corpus end)
+  int32_t t0, t1;    // tile range
+  int32_t row_base;  // first corpus row of tile 0 (rows < 2^31: n_local limit)
+  int32_t row_end;   // rows >= row_end are masked (list end / corpus end)
   int chunk;         // ivf: chunk index within the list
   int e0, cnt;       // ivf: probing queries lq_ent[e0, e0 + cnt)
 };
 
-__device__ __forceinline__ WorkItem work_item(int w, const FlatScanArgs& a, int64_t T) {
+__device__ __forceinline__ WorkItem work_item(int w, const FlatScanArgs& a, int32_t T) {
   WorkItem wi;
   if (a.mode == FS_MODE_IVF) {
     const int4 it = a.items[w];
-    const int64_t lo = a.list_off[it.x], hi = a.list_off[it.x + 1];
-    const int64_t r0 = lo + (int64_t)it.z * a.chunk_rows;
-    const int64_t r1 = hi < r0 + a.chunk_rows ? hi : r0 + a.chunk_rows;
+    const int32_t lo = (int32_t)a.list_off[it.x], hi = (int32_t)a.list_off[it.x + 1];
+    const int32_t r0 = lo + it.z * a.chunk_rows;
+    const int32_t r1 = hi < r0 + a.chunk_rows ? hi : r0 + a.chunk_rows;
     wi.qkey = -1;
     wi.s = 0;
     wi.t0 = 0;
@@ -132,10 +132,10 @@ __device__ __forceinline__ WorkItem work_item(int w, const FlatScanArgs& a, int6
   } else {
     wi.qkey = w / a.S;
     wi.s = w % a.S;
-    wi.t0 = (int64_t)wi.s * T / a.S;
-    wi.t1 = (int64_t)(wi.s + 1) * T / a.S;
+    wi.t0 = (int32_t)((int64_t)wi.s * T / a.S);
+    wi.t1 = (int32_t)((int64_t)(wi.s + 1) * T / a.S);
     wi.row_base = 0;
-    wi.row_end = a.n_rows;
+    wi.row_end = (int32_t)a.n_rows;
     wi.chunk = 0;
     wi.e0 = 0;
     wi.cnt = 0;
@@ -192,7 +192,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
   const int S = a.S;
   const bool ivf = a.mode == FS_MODE_IVF;
   const int n_work = ivf ? *a.n_items : a.QP * S;
-  const int64_t T = (a.n_rows + kBN - 1) / kBN;
+  const int32_t T = (int32_t)((a.n_rows + kBN - 1) / kBN);
   const int num_kb = a.d_pad / kBK;
   const int nacc = 2;
   const uint32_t a_col = (uint32_t)(nacc * kBN);          // A (TMEM part) after the accumulators
@@ -240,8 +240,8 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
       for (int w = unit; w < n_work; w += n_units) {
         const WorkItem wi = work_item(w, a, T);
-        for (int64_t t = wi.t0; t < wi.t1; ++t) {
-          const int32_t row = (int32_t)(wi.row_base + t * kBN) + (int32_t)rank * C::kRowsPerCta;
+        for (int32_t t = wi.t0; t < wi.t1; ++t) {
+          const int32_t row = wi.row_base + t * kBN + (int32_t)rank * C::kRowsPerCta;
           for (int sl = 0; sl < n_sl; ++sl) {
             const int kb0 = sl * kKbPerStage;
             const int nkb = num_kb - kb0 < kKbPerStage ? num_kb - kb0 : kKbPerStage;
@@ -292,7 +292,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           cur_qp = wi.qkey;
           ptx::tc_fence_after();
         }
-        for (int64_t t = wi.t0; t < wi.t1; ++t) {
+        for (int32_t t = wi.t0; t < wi.t1; ++t) {
           ptx::mbar_wait(ptx::smem_u32(&tail->tmem_empty[acc]), acc_phase ^ 1);
           ptx::tc_fence_after();
           const uint32_t d_tmem = tmem + (uint32_t)(acc * kBN);
@@ -360,7 +360,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       int j;
       bool valid;
     };
-    auto qsel = [&](const WorkItem& wi) -> QSel {
+    auto qsel = [&](const WorkItem& wi) __attribute__((always_inline)) -> QSel {
       QSel r{0, 0, false};
       if (ivf) {
         // Prober i of the item sits on TMEM lane (i % 4) * 32 + i / 4: an item usually has
@@ -382,7 +382,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // Stage item wi's query block into the A operand (TMEM K-blocks + smem K-blocks) and
     // arrive on a_full.  Callers guarantee every MMA that read the previous block has
     // completed (they consumed that block's last tmem_full).
-    auto stage_a = [&](const WorkItem& wi, const QSel& qs) {
+    auto stage_a = [&](const WorkItem& wi, const QSel& qs) __attribute__((always_inline)) {
       const bool tma_thread = (!ivf && ew == 0 && lane == 0 && kb_s > 0);
       if (tma_thread) {
         // K-blocks [kb_t, num_kb) of this CTA's 128 query rows -> smem (SS operand)
@@ -444,25 +444,20 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     while (w < n_work) {
       const int wn = w + n_units;
       const bool has_next = wn < n_work;
+      // The next item is decoded only when needed (at this item's last tile) to keep its
+      // state out of the registers of the tile loop.
       WorkItem nx{};
       QSel ns{};
-      bool next_staged = false;
-      if (has_next) {
+      bool nx_ready = false;
+      if (wi.t1 <= wi.t0 && has_next) {
         nx = work_item(wn, a, T);
         ns = qsel(nx);
-      }
-      const bool next_needs_a = has_next && (nx.qkey < 0 || nx.qkey != wi.qkey);
-      if (wi.t1 <= wi.t0 && next_needs_a) {
-        stage_a(nx, ns);
-        next_staged = true;
+        nx_ready = true;
+        if (nx.qkey < 0 || nx.qkey != wi.qkey) stage_a(nx, ns);
       }
       const int64_t q = cs.q;
       const int probe_j = cs.j;
       const bool valid = cs.valid;
-      // Exact pruning bound (IVF): q_hint[q] holds the best k-th score any finished item of
-      // query q has seen; the query's final k-th score can only be >= it, so smaller scores
-      // can never be returned.  Ties pass (s >= thr).  Cuts the insertion burst that every
-      // freshly reset per-item heap would otherwise take.
       // Exact pruning bound shared by all heaps of a query (all corpus slices / IVF items /
       // column halves): q_hint[q] = max over published heap roots.  Each root is the k-th
       // best score of a subset of q's candidates, so q's final k-th score is >= q_hint[q]
@@ -472,13 +467,13 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       float hint = heap_threshold(0ull);
       uint32_t published = 0u;
       if (valid && a.q_hint) {
-        const uint32_t h = *reinterpret_cast<volatile const uint32_t*>(a.q_hint + q);
+        const uint32_t h = __ldcg(a.q_hint + q);
         if (h != 0u) hint = float_from_ordered(h);
       }
       thr = fmaxf(thr, hint);
-      for (int64_t t = wi.t0; t < wi.t1; ++t) {
+      for (int32_t t = wi.t0; t < wi.t1; ++t) {
         if (valid && a.q_hint && ((t - wi.t0) & 3) == 3) {
-          const uint32_t h = *reinterpret_cast<volatile const uint32_t*>(a.q_hint + q);
+          const uint32_t h = __ldcg(a.q_hint + q);
           if (h != 0u) {
             hint = fmaxf(hint, float_from_ordered(h));
             thr = fmaxf(thr, hint);
@@ -503,13 +498,15 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         // The last accumulator of this item is in registers, so every MMA that read this
         // item's A operand has completed: stage the next item's queries now, before the
         // score processing, so the tensor core restarts as early as possible.
-        if (t == wi.t1 - 1 && next_needs_a && !next_staged) {
-          stage_a(nx, ns);
-          next_staged = true;
+        if (t == wi.t1 - 1 && has_next) {
+          nx = work_item(wn, a, T);
+          ns = qsel(nx);
+          nx_ready = true;
+          if (nx.qkey < 0 || nx.qkey != wi.qkey) stage_a(nx, ns);
         }
         if (!valid || a.experiment != 0) continue;
 
-        const int64_t row0 = wi.row_base + t * kBN + half * 64;
+        const int32_t row0 = wi.row_base + t * kBN + half * 64;
         if (a.mode == FS_MODE_DEBUG) {
           // debug: materialise the score tile (tests only)
           float* dst = a.dbg + (size_t)q * a.n_rows;
@@ -532,7 +529,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           for (int j = 0; j < 64; ++j) {
             const float s = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
             if (s >= thr) {
-              const int64_t row = row0 + j;
+              const int32_t row = row0 + j;
               if (row < wi.row_end) {
                 const uint32_t id =
                     a.id_base + (a.row_ids ? (uint32_t)a.row_ids[row] : (uint32_t)row);
@@ -562,6 +559,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         }
         for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
         thr = heap_threshold(0ull);
+      }
+      if (has_next && !nx_ready) {
+        nx = work_item(wn, a, T);
+        ns = qsel(nx);
       }
       w = wn;
       wi = nx;
