@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -13,6 +15,21 @@
 struct sa_comm {
   void* nccl = nullptr;  // ncclComm_t
   int32_t rank = 0, world = 1, device = 0;
+};
+
+// One captured search (sa_search_host fast path): H2D from a pinned staging buffer, the whole
+// search, D2H into pinned staging -- replayed with a single cudaGraphLaunch.
+struct sa_graph_entry {
+  int64_t nq = 0;
+  int32_t k = 0, nprobe = 0, qdtype = 0;
+  cudaGraphExec_t exec = nullptr;
+  void* h_q = nullptr;
+  int64_t* h_ids = nullptr;
+  float* h_sc = nullptr;
+  void* d_q = nullptr;
+  int64_t* d_ids = nullptr;
+  float* d_sc = nullptr;
+  int64_t kernels = 0;
 };
 
 struct sa_index {
@@ -35,6 +52,9 @@ struct sa_index {
   std::vector<int64_t> h_list_off;           // host copy
   int64_t max_list = 0;
   const sa_comm* comm = nullptr;
+  // captured small-batch searches (host-buffer path), guarded by graph_mu
+  std::mutex graph_mu;
+  std::vector<sa_graph_entry> graphs;
 };
 
 namespace sa {

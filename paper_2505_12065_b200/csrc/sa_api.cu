@@ -84,19 +84,27 @@ struct Prof {
 };
 Prof g_prof;
 thread_local cudaEvent_t t_open[SA_KERNEL_KINDS];
+thread_local bool t_capturing = false;  // inside a graph capture: no events, no counting
 }  // namespace
 
 void prof_count(int kind) {
+  if (t_capturing) return;
   std::lock_guard<std::mutex> l(g_prof.mu);
   g_prof.launches[kind]++;
 }
+static void prof_count_n(int kind, int64_t n) {
+  std::lock_guard<std::mutex> l(g_prof.mu);
+  g_prof.launches[kind] += n;
+}
 void prof_begin(int kind, cudaStream_t s) {
+  if (t_capturing) return;
   std::lock_guard<std::mutex> l(g_prof.mu);
   if (!g_prof.on) return;
   t_open[kind] = g_prof.get();
   cudaEventRecord(t_open[kind], s);
 }
 void prof_end(int kind, cudaStream_t s) {
+  if (t_capturing) return;
   std::lock_guard<std::mutex> l(g_prof.mu);
   if (!g_prof.on || !t_open[kind]) return;
   cudaEvent_t e = g_prof.get();
@@ -388,9 +396,13 @@ sa_status sa_index_build(const void* corpus, int64_t n, int32_t d, int32_t nlist
   return sa_index_build_ex(corpus, n, d, nlist, &o, out);
 }
 
+static void free_graph_entry(sa_graph_entry& g);
+
 sa_status sa_index_free(sa_index* idx) {
   if (!idx) return SA_OK;
   cudaDeviceSynchronize();
+  for (auto& g : idx->graphs) free_graph_entry(g);
+  idx->graphs.clear();
   cudaFree(idx->X);
   cudaFree(idx->row_ids);
   cudaFree(idx->centroids);
@@ -574,6 +586,74 @@ sa_status sa_search(const sa_index* idx, const void* queries, int64_t nq, int32_
   return sa_search_ex(idx, queries, SA_BF16, nq, k, nprobe, out_ids, out_scores, stream);
 }
 
+static void free_graph_entry(sa_graph_entry& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  cudaFreeHost(g.h_q);
+  cudaFreeHost(g.h_ids);
+  cudaFreeHost(g.h_sc);
+  cudaFree(g.d_q);
+  cudaFree(g.d_ids);
+  cudaFree(g.d_sc);
+  g = sa_graph_entry{};
+}
+
+// Capture H2D + search + D2H for one (nq, k, nprobe, qdtype) into a graph.
+static sa_status capture_search(const sa_index* idx, sa_graph_entry& g) {
+  const size_t qbytes = (size_t)g.nq * idx->d * (g.qdtype == SA_F32 ? 4 : 2);
+  const size_t nk = (size_t)g.nq * g.k;
+  sa_status st = cuda_status(cudaMallocHost(&g.h_q, qbytes), "pinned staging");
+  if (st == SA_OK) st = cuda_status(cudaMallocHost(&g.h_ids, nk * 8), "pinned staging");
+  if (st == SA_OK) st = cuda_status(cudaMallocHost(&g.h_sc, nk * 4), "pinned staging");
+  if (st == SA_OK) st = cuda_status(cudaMalloc(&g.d_q, qbytes), "graph buffers");
+  if (st == SA_OK) st = cuda_status(cudaMalloc(&g.d_ids, nk * 8), "graph buffers");
+  if (st == SA_OK) st = cuda_status(cudaMalloc(&g.d_sc, nk * 4), "graph buffers");
+  if (st != SA_OK) return st;
+  cudaStream_t cs;
+  st = cuda_status(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
+  if (st != SA_OK) return st;
+  cudaGraph_t graph = nullptr;
+  st = cuda_status(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
+  if (st == SA_OK) {
+    t_capturing = true;
+    sa_status s1 = cuda_status(cudaMemcpyAsync(g.d_q, g.h_q, qbytes, cudaMemcpyHostToDevice, cs),
+                               "H2D");
+    SearchOut out;
+    out.ids = g.d_ids;
+    out.scores = g.d_sc;
+    if (s1 == SA_OK)
+      s1 = search_local(idx, g.d_q, (sa_dtype)g.qdtype, g.nq, g.k, g.nprobe, out, cs);
+    if (s1 == SA_OK)
+      s1 = cuda_status(cudaMemcpyAsync(g.h_ids, g.d_ids, nk * 8, cudaMemcpyDeviceToHost, cs), "D2H");
+    if (s1 == SA_OK)
+      s1 = cuda_status(cudaMemcpyAsync(g.h_sc, g.d_sc, nk * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+    t_capturing = false;
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    st = s1 != SA_OK ? s1 : cuda_status(e, "end capture");
+  }
+  if (st == SA_OK) st = cuda_status(cudaGraphInstantiate(&g.exec, graph, 0), "instantiate");
+  if (st == SA_OK) {
+    size_t nn = 0;
+    cudaGraphGetNodes(graph, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(graph, nodes.data(), &nn);
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++g.kernels;
+    }
+  }
+  if (graph) cudaGraphDestroy(graph);
+  cudaStreamDestroy(cs);
+  return st;
+}
+
+static bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SA_NO_GRAPH");
+    return !(e && atoi(e) != 0);
+  }();
+  return on;
+}
+
 sa_status sa_search_host(const sa_index* idx, const void* queries_host, sa_dtype qdtype,
                          int64_t nq, int32_t k, int32_t nprobe, int64_t* out_ids_host,
                          float* out_scores_host, void* stream) {
@@ -582,6 +662,37 @@ sa_status sa_search_host(const sa_index* idx, const void* queries_host, sa_dtype
   if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t qbytes = (size_t)nq * idx->d * (qdtype == SA_F32 ? 4 : 2);
+  const bool sharded = idx->comm && idx->comm->world > 1;
+  if (!sharded && nq <= 1024 && graphs_enabled()) {
+    // Small batches (agent-step retrieval) are launch-bound: replay a captured graph.
+    sa_index* mi = const_cast<sa_index*>(idx);
+    std::lock_guard<std::mutex> lock(mi->graph_mu);
+    sa_graph_entry* g = nullptr;
+    for (auto& e : mi->graphs)
+      if (e.nq == nq && e.k == k && e.nprobe == nprobe && e.qdtype == (int32_t)qdtype) g = &e;
+    if (!g) {
+      sa_graph_entry e;
+      e.nq = nq;
+      e.k = k;
+      e.nprobe = nprobe;
+      e.qdtype = (int32_t)qdtype;
+      st = capture_search(idx, e);
+      if (st != SA_OK) {
+        free_graph_entry(e);
+        return st;
+      }
+      mi->graphs.push_back(e);
+      g = &mi->graphs.back();
+    }
+    std::memcpy(g->h_q, queries_host, qbytes);
+    st = cuda_status(cudaGraphLaunch(g->exec, s), "graph launch");
+    if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "search sync");
+    if (st != SA_OK) return st;
+    std::memcpy(out_ids_host, g->h_ids, (size_t)nq * k * 8);
+    std::memcpy(out_scores_host, g->h_sc, (size_t)nq * k * 4);
+    prof_count_n(SA_KERNEL_OTHER, g->kernels);
+    return SA_OK;
+  }
   void* dq = nullptr;
   int64_t* dids = nullptr;
   float* dsc = nullptr;

@@ -171,3 +171,18 @@ def test_c2_parity(sa):
     rep = check_against_rows(ids.cpu().numpy()[sub], sc.cpu().numpy()[sub], Xb, Qb[sub], 10)
     idx.free()
     assert rep["ok"], rep
+
+
+def test_search_host_graph_replay_matches_device(sa):
+    """The small-batch host path replays a captured CUDA graph; results must equal the
+    device path for repeated calls with new data and for several shapes (exact + IVF)."""
+    g = torch.Generator().manual_seed(19)
+    X = torch.randn(20_000, 128, generator=g)
+    idx = sa.Index.build(X.cuda(), 16, kmeans_iters=4)
+    for nq, k, nprobe in [(1, 5, 0), (7, 5, 4), (64, 10, 16), (7, 5, 4)]:
+        for rep in range(3):
+            Q = torch.randn(nq, 128, generator=g)
+            i_d, s_d = idx.search(Q.cuda(), k, nprobe)
+            i_h, s_h = idx.search_host(Q.contiguous(), k, nprobe)
+            assert torch.equal(i_d.cpu(), i_h) and torch.equal(s_d.cpu(), s_h), (nq, k, nprobe, rep)
+    idx.free()
