@@ -26,7 +26,7 @@
  *     ascending; -0.0 ranks as +0.0.  If fewer than k candidates exist the
  *     tail is padded with id -1 and score -INFINITY (R6).
  *   - Limits: 1 <= k <= 256; d <= 768 (d is zero-padded to a multiple of 64
- *     internally); global ids < 2^32; n_local < 2^31.
+ *     internally); nlist <= 32768; global ids < 2^32; n_local < 2^31.
  *   - Requires an sm_100 device (B200); other devices -> SA_ERR_UNSUPPORTED.
  */
 #ifndef SA_H_

@@ -21,7 +21,11 @@
 namespace sa {
 
 namespace {
-constexpr int kChunkRows = 4096;  // rows per IVF work item (multiple of FS_BN)
+// Rows per IVF work item (multiple of FS_BN).  Big batches have many lists to spread over the
+// SMs; small (agent-step) batches probe only a few dozen lists, so lists are cut into short
+// chunks to put every SM on the few lists there are.
+constexpr int kChunkRows = 4096;
+constexpr int kChunkRowsSmall = 256;
 
 struct Freer {
   cudaStream_t s;
@@ -309,7 +313,8 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   prof_count(SA_KERNEL_OTHER);
 
   // ---- invert: lists -> probing queries, output slots, work items
-  const int64_t max_chunks = std::max<int64_t>(1, (idx->max_list + kChunkRows - 1) / kChunkRows);
+  const int chunk_rows = np < 4 * (int64_t)sms ? kChunkRowsSmall : kChunkRows;
+  const int64_t max_chunks = std::max<int64_t>(1, (idx->max_list + chunk_rows - 1) / chunk_rows);
   IvfSearchScratch w{};
   SA_TRY(dalloc(&w.cnt, nlist, s, "ivf scratch"));
   f.add(w.cnt);
@@ -321,8 +326,6 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   f.add(w.tmp64b);
   SA_TRY(dalloc(&w.lq_off64, nlist + 1, s, "ivf scratch"));
   f.add(w.lq_off64);
-  SA_TRY(dalloc(&w.lq_off, nlist + 1, s, "ivf scratch"));
-  f.add(w.lq_off);
   SA_TRY(dalloc(&w.lq_ent, np, s, "ivf scratch"));
   f.add(w.lq_ent);
   SA_TRY(dalloc(&w.q_slot, np + 1, s, "ivf scratch"));
@@ -335,9 +338,15 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   f.add(w.n_items);
   SA_TRY(dalloc(&w.scratch, std::max<int64_t>(nlist, np) / 1024 + 4, s, "ivf scratch"));
   f.add(w.scratch);
-  SA_CUDA(launch_probe_invert(probes, nq, nprobe, nlist, idx->list_off, kChunkRows, w, sms, s),
-          "probe inversion");
-  for (int i = 0; i < 11; ++i) prof_count(SA_KERNEL_OTHER);
+  if (np <= kInvertSmallMax) {
+    SA_CUDA(launch_invert_small(probes, (int)nq, nprobe, idx->list_off, chunk_rows, w, s),
+            "probe inversion");
+    prof_count(SA_KERNEL_OTHER);
+  } else {
+    SA_CUDA(launch_probe_invert(probes, nq, nprobe, nlist, idx->list_off, chunk_rows, w, sms, s),
+            "probe inversion");
+    for (int i = 0; i < 10; ++i) prof_count(SA_KERNEL_OTHER);
+  }
 
   // ---- a8: list-major scan on the tensor cores
   const size_t max_slots = (size_t)np * max_chunks;
@@ -369,11 +378,10 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   a.items = w.items;
   a.n_items = w.n_items;
   a.list_off = idx->list_off;
-  a.lq_off = w.lq_off;
   a.lq_ent = w.lq_ent;
   a.q_slot = w.q_slot;
   a.nprobe = nprobe;
-  a.chunk_rows = kChunkRows;
+  a.chunk_rows = chunk_rows;
   a.q_hint = hint;
   prof_begin(SA_KERNEL_IVF_SCAN, s);
   cudaError_t e = launch_flat_scan(idx->tmap_x, tmap_q, a, 1, sms, s);

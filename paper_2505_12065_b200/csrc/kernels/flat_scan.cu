@@ -126,9 +126,8 @@ __device__ __forceinline__ WorkItem work_item(int w, const FlatScanArgs& a, int3
     wi.row_base = r0;
     wi.row_end = r1;
     wi.chunk = it.z;
-    wi.e0 = a.lq_off[it.x] + it.y * FS_BM;
-    const int rem = a.lq_off[it.x + 1] - wi.e0;
-    wi.cnt = rem < FS_BM ? rem : FS_BM;
+    wi.e0 = it.y;   // probers of this item: lq_ent[e0, e0 + cnt), cnt <= FS_BM
+    wi.cnt = it.w;
   } else {
     wi.qkey = w / a.S;
     wi.s = w % a.S;

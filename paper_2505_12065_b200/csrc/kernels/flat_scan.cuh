@@ -43,10 +43,9 @@ struct FlatScanArgs {
   float* dbg;              // debug: [nq_pad][n_rows] raw scores
   int32_t mode;            // FlatScanMode
   // ---- FS_MODE_IVF (cta_group 1 only)
-  const int4* items;       // [*n_items] {list, query block, chunk, 0}
+  const int4* items;       // [*n_items] {list, first prober in lq_ent, chunk, prober count}
   const int32_t* n_items;  // device scalar
   const int64_t* list_off; // [nlist + 1] stored-row range of each list
-  const int32_t* lq_off;   // [nlist + 1] range of each list in lq_ent
   const int2* lq_ent;      // (query, probe rank) pairs grouped by list
   const int64_t* q_slot;   // [nq * nprobe] first output slot of (query, probe rank)
   int32_t nprobe;

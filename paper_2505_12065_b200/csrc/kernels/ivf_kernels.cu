@@ -389,6 +389,7 @@ __global__ void probe_fill_kernel(const int64_t* __restrict__ probes, int64_t nq
 }
 __global__ void items_fill_kernel(const int32_t* __restrict__ cnt, int nlist,
                                   const int64_t* __restrict__ list_off, int chunk_rows,
+                                  const int64_t* __restrict__ lq_off64,
                                   const int64_t* __restrict__ item_off, int4* __restrict__ items,
                                   int32_t* __restrict__ n_items) {
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlist; l += gridDim.x * blockDim.x) {
@@ -396,10 +397,132 @@ __global__ void items_fill_kernel(const int32_t* __restrict__ cnt, int nlist,
     const int nch = (int)((len + chunk_rows - 1) / chunk_rows);
     const int nqb = (cnt[l] + 127) / 128;
     int64_t o = item_off[l];
-    for (int b = 0; b < nqb; ++b)
-      for (int c = 0; c < nch; ++c) items[o++] = make_int4(l, b, c, 0);
+    for (int b = 0; b < nqb; ++b) {
+      const int e0 = (int)lq_off64[l] + b * 128;
+      const int c_b = cnt[l] - b * 128 < 128 ? cnt[l] - b * 128 : 128;
+      for (int c = 0; c < nch; ++c) items[o++] = make_int4(l, e0, c, c_b);
+    }
     if (l == nlist - 1) *n_items = (int32_t)item_off[nlist];
   }
+}
+
+// Whole inversion in one CTA for small batches (nq * nprobe <= kInvertSmallMax): sort the
+// (list, query, probe rank) entries by list in smem, emit probers grouped by list, the
+// per-(query, probe) output slots and the work items -- one launch instead of ~13.
+__global__ void __launch_bounds__(1024)
+invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
+                    const int64_t* __restrict__ list_off, int chunk_rows,
+                    int2* __restrict__ lq_ent, int64_t* __restrict__ q_slot,
+                    int4* __restrict__ items, int32_t* __restrict__ n_items) {
+  extern __shared__ uint64_t ent[];  // [P2] (list << 32 | entry index)
+  __shared__ int wtot[32];
+  __shared__ int s_total;
+  const int n = nq * nprobe;
+  int P2 = 1;
+  while (P2 < n) P2 <<= 1;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int i = tid; i < P2; i += nt)
+    ent[i] = i < n ? (((uint64_t)(uint32_t)probes[i] << 32) | (uint32_t)i) : ~0ull;
+  __syncthreads();
+  for (int sz = 2; sz <= P2; sz <<= 1)
+    for (int st = sz >> 1; st > 0; st >>= 1) {
+      for (int i = tid; i < P2; i += nt) {
+        const int j = i ^ st;
+        if (j > i) {
+          const bool up = (i & sz) == 0;
+          const uint64_t x = ent[i], y = ent[j];
+          if (up ? x > y : x < y) { ent[i] = y; ent[j] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  // block exclusive scan helper over one int per thread
+  auto block_scan = [&](int v, int* total) -> int {
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wtot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int w = lane < (nt >> 5) ? wtot[lane] : 0;
+      int wi = w;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += t;
+      }
+      if (lane < (nt >> 5)) wtot[lane] = wi - w;
+      if (lane == 31) s_total = wi;
+    }
+    __syncthreads();
+    const int base = wtot[wid];
+    const int tot = s_total;
+    __syncthreads();
+    *total = tot;
+    return base + incl - v;
+  };
+  // contiguous chunk per thread
+  const int per = (n + nt - 1) / nt;
+  const int lo = tid * per, hi = min(n, lo + per);
+  // probers grouped by list (sorted order) and item counts of the runs that start here
+  int my_items = 0;
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t e = (uint32_t)ent[i];
+    lq_ent[i] = make_int2((int)(e / nprobe), (int)(e % nprobe));
+    const uint32_t l = (uint32_t)(ent[i] >> 32);
+    if (i == 0 || (uint32_t)(ent[i - 1] >> 32) != l) {
+      int c = 1;
+      while (i + c < n && (uint32_t)(ent[i + c] >> 32) == l) ++c;
+      const int64_t len = list_off[l + 1] - list_off[l];
+      const int nch = (int)((len + chunk_rows - 1) / chunk_rows);
+      my_items += ((c + 127) / 128) * nch;
+    }
+  }
+  int total_items;
+  int o = block_scan(my_items, &total_items);
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t l = (uint32_t)(ent[i] >> 32);
+    if (i == 0 || (uint32_t)(ent[i - 1] >> 32) != l) {
+      int c = 1;
+      while (i + c < n && (uint32_t)(ent[i + c] >> 32) == l) ++c;
+      const int64_t len = list_off[l + 1] - list_off[l];
+      const int nch = (int)((len + chunk_rows - 1) / chunk_rows);
+      for (int b = 0; b * 128 < c; ++b)
+        for (int ch = 0; ch < nch; ++ch)
+          items[o++] = make_int4((int)l, i + b * 128, ch, c - b * 128 < 128 ? c - b * 128 : 128);
+    }
+  }
+  // output slots per (q, j), original order: chunks of the probed list
+  int my_slots = 0;
+  for (int i = lo; i < hi; ++i) {
+    const int64_t l = probes[i];
+    const int64_t len = list_off[l + 1] - list_off[l];
+    my_slots += (int)((len + chunk_rows - 1) / chunk_rows);
+  }
+  int total_slots;
+  int so = block_scan(my_slots, &total_slots);
+  for (int i = lo; i < hi; ++i) {
+    q_slot[i] = so;
+    const int64_t l = probes[i];
+    const int64_t len = list_off[l + 1] - list_off[l];
+    so += (int)((len + chunk_rows - 1) / chunk_rows);
+  }
+  if (tid == 0) {
+    q_slot[n] = total_slots;
+    *n_items = total_items;
+  }
+}
+
+cudaError_t launch_invert_small(const int64_t* probes, int nq, int nprobe, const int64_t* list_off,
+                                int chunk_rows, IvfSearchScratch& w, cudaStream_t s) {
+  int P2 = 1;
+  while (P2 < nq * nprobe) P2 <<= 1;
+  invert_small_kernel<<<1, 1024, P2 * sizeof(uint64_t), s>>>(probes, nq, nprobe, list_off,
+                                                              chunk_rows, w.lq_ent, w.q_slot,
+                                                              w.items, w.n_items);
+  return cudaGetLastError();
 }
 __global__ void i32_to_i64_kernel(const int32_t* __restrict__ in, int64_t n,
                                   int64_t* __restrict__ out) {
@@ -422,14 +545,12 @@ cudaError_t launch_probe_invert(const int64_t* probes, int64_t nq, int nprobe, i
   i32_to_i64_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, w.tmp64);
   exclusive_scan_i64(w.tmp64, nlist, w.lq_off64, w.scratch, s);
   probe_fill_kernel<<<b, 256, 0, s>>>(probes, nq, nprobe, w.lq_off64, w.cursor, w.lq_ent);
-  // int32 view of lq_off for the scan kernel (entries < 2^31)
-  i64_to_i32_kernel<<<bl + 1, 256, 0, s>>>(w.lq_off64, nlist + 1, w.lq_off);
   probe_slots_kernel<<<b, 256, 0, s>>>(probes, n, list_off, chunk_rows, w.tmp64b);
   exclusive_scan_i64(w.tmp64b, n, w.q_slot, w.scratch, s);
   list_items_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, list_off, chunk_rows, w.tmp64);
   exclusive_scan_i64(w.tmp64, nlist, w.item_off, w.scratch, s);
-  items_fill_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, list_off, chunk_rows, w.item_off, w.items,
-                                       w.n_items);
+  items_fill_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, list_off, chunk_rows, w.lq_off64, w.item_off,
+                                       w.items, w.n_items);
   return cudaGetLastError();
 }
 

@@ -50,7 +50,6 @@ struct IvfSearchScratch {
   int64_t* tmp64;      // [nlist + 1]
   int64_t* tmp64b;     // [nq * nprobe]
   int64_t* lq_off64;   // [nlist + 1]
-  int32_t* lq_off;     // [nlist + 1]
   int2* lq_ent;        // [nq * nprobe] (query, probe rank) grouped by list
   int64_t* q_slot;     // [nq * nprobe + 1] first output slot of (q, j)
   int64_t* item_off;   // [nlist + 1]
@@ -58,6 +57,9 @@ struct IvfSearchScratch {
   int32_t* n_items;    // [1]
   int64_t* scratch;    // [ceil(max(nlist, nq*nprobe) / 1024) + 2]
 };
+constexpr int kInvertSmallMax = 4096;  // nq * nprobe handled by one-CTA inversion
+cudaError_t launch_invert_small(const int64_t* probes, int nq, int nprobe, const int64_t* list_off,
+                                int chunk_rows, IvfSearchScratch& w, cudaStream_t s);
 cudaError_t launch_probe_invert(const int64_t* probes, int64_t nq, int nprobe, int nlist,
                                 const int64_t* list_off, int chunk_rows, IvfSearchScratch& w,
                                 int num_sms, cudaStream_t s);

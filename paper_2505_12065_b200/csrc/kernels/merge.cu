@@ -15,8 +15,78 @@ namespace sa {
 namespace {
 constexpr int kThreads = 256;
 constexpr int kMaxK = 256;
-constexpr int kSmemCand = 4096;  // candidates cached in smem when G*k fits
+constexpr int kSmemCand = 4096;  // u64 candidates cached in smem when they fit (32 KB)
+
+// Warp 0 finds the radix bucket holding the kr-th largest element: buckets are scanned from
+// the top, 8 per lane, with one warp prefix sum (instead of a 256-step serial loop).
+__device__ __forceinline__ void pick_bucket(const uint32_t* hist, int kr, int* s_bucket,
+                                            int* s_above) {
+  const int lane = threadIdx.x & 31;
+  uint32_t c[8];
+  uint32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    c[i] = hist[255 - (lane * 8 + i)];
+    sum += c[i];
+  }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const uint32_t excl = incl - sum;
+  const unsigned hit = __ballot_sync(0xffffffffu, incl >= (uint32_t)kr);
+  // hit != 0 whenever at least kr candidates remain; otherwise take the lowest bucket (0)
+  const int owner = hit ? __ffs(hit) - 1 : 31;
+  if (lane == owner) {
+    uint32_t acc = excl;
+    int b = 255 - lane * 8;
+    for (int i = 0; i < 8; ++i, --b) {
+      if (b == 0 || acc + c[i] >= (uint32_t)kr) break;
+      acc += c[i];
+    }
+    *s_bucket = b;
+    *s_above = (int)acc;
+  }
 }
+
+// Bitonic sort of sel[0..size) descending; size = power of two >= k.
+__device__ __forceinline__ void sort_desc(uint64_t* sel, int size) {
+  for (int sz = 2; sz <= size; sz <<= 1) {
+    for (int stride = sz >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < size; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool desc = ((i & sz) == 0);
+          const uint64_t x = sel[i], y = sel[j];
+          if (desc ? (x < y) : (x > y)) { sel[i] = y; sel[j] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ int pow2_at_least(int k) {
+  int s = 1;
+  while (s < k) s <<= 1;
+  return s < 2 ? 2 : s;
+}
+
+__device__ __forceinline__ void write_out(const MergeArgs& a, int64_t q, int i, uint64_t key) {
+  const int k = a.k;
+  if (a.out_keys) {
+    a.out_keys[(size_t)q * k + i] = key;
+  } else if (key == 0ull) {
+    a.out_ids[(size_t)q * k + i] = -1;
+    a.out_scores[(size_t)q * k + i] = -__int_as_float(0x7f800000);
+  } else {
+    a.out_ids[(size_t)q * k + i] = (int64_t)key_id(key) + a.id_offset;
+    a.out_scores[(size_t)q * k + i] = key_score(key);
+  }
+}
+}  // namespace
 
 __global__ void __launch_bounds__(kThreads)
 merge_topk_kernel(const MergeArgs a) {
@@ -43,7 +113,6 @@ merge_topk_kernel(const MergeArgs a) {
   const bool cached = M <= kSmemCand;
 
   auto cand_g = [&](int64_t i) -> uint64_t {
-    if (a.cand_scores) return make_key(a.cand_scores[base + i], (uint32_t)i);
     if (!grouped) return a.cand[base + i];
     const int64_t g = i / k, j = i % k;
     return a.cand[(size_t)g * a.gstride + (size_t)q * a.qstride + j];
@@ -65,25 +134,17 @@ merge_topk_kernel(const MergeArgs a) {
       if ((c & pmask) == prefix) atomicAdd(&hist[(c >> shift) & 255u], 1u);
     }
     __syncthreads();
-    if (tid == 0) {
-      int acc = 0, b = 255;
-      for (; b > 0; --b) {
-        if (acc + (int)hist[b] >= kr) break;
-        acc += hist[b];
-      }
-      s_bucket = b;
-      s_above = acc;
-    }
+    if (tid < 32) pick_bucket(hist, kr, &s_bucket, &s_above);
     __syncthreads();
     prefix |= (uint64_t)s_bucket << shift;
     pmask |= 255ull << shift;
     kr -= s_above;
-    __syncthreads();
   }
   // prefix = T, the k-th largest key; (k - kr) keys are strictly larger.
   const uint64_t T = prefix;
+  const int size = pow2_at_least(k);
   if (tid == 0) s_pos = 0;
-  for (int i = tid; i < kMaxK; i += kThreads) sel[i] = 0ull;
+  for (int i = tid; i < size; i += kThreads) sel[i] = 0ull;
   __syncthreads();
   for (int64_t i = tid; i < M; i += kThreads) {
     const uint64_t c = cand(i);
@@ -92,34 +153,82 @@ merge_topk_kernel(const MergeArgs a) {
   __syncthreads();
   for (int i = (k - kr) + tid; i < k; i += kThreads) sel[i] = T;
   __syncthreads();
-  // bitonic sort of sel[0..256) descending (zeros = empty sink to the end)
-  for (int size = 2; size <= kMaxK; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < kMaxK; i += kThreads) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const bool desc = ((i & size) == 0);
-          const uint64_t x = sel[i], y = sel[j];
-          if (desc ? (x < y) : (x > y)) { sel[i] = y; sel[j] = x; }
-        }
-      }
-      __syncthreads();
+  sort_desc(sel, size);   // zeros (empty) sink to the end
+  for (int i = tid; i < k; i += kThreads) write_out(a, q, i, sel[i]);
+}
+
+// Top-k of a dense score row (probe: one row of nq x nlist centroid scores): keys
+// (score desc, index asc).  Scores are cached in dynamic smem as order-preserving uint32,
+// a 4-pass radix select finds the k-th value T, and the values equal to T are taken in
+// index order (contiguous per-thread chunks + a block prefix sum), which reproduces the
+// 64-bit key order exactly.
+__global__ void __launch_bounds__(kThreads)
+select_dense_kernel(const MergeArgs a) {
+  extern __shared__ uint32_t vals[];
+  __shared__ uint32_t hist[256];
+  __shared__ uint64_t sel[kMaxK];
+  __shared__ int s_bucket, s_above, s_pos;
+  __shared__ int wsum[kThreads / 32];
+
+  const int64_t q = blockIdx.x;
+  const int k = a.k;
+  const int M = (int)a.m_flat;
+  const float* row = a.cand_scores + (size_t)q * a.qstride;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < M; i += kThreads) vals[i] = ordered_from_float(row[i]);
+  __syncthreads();
+
+  uint32_t prefix = 0, pmask = 0;
+  int kr = k;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int i = tid; i < 256; i += kThreads) hist[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < M; i += kThreads) {
+      const uint32_t v = vals[i];
+      if ((v & pmask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
     }
+    __syncthreads();
+    if (tid < 32) pick_bucket(hist, kr, &s_bucket, &s_above);
+    __syncthreads();
+    prefix |= (uint32_t)s_bucket << shift;
+    pmask |= 255u << shift;
+    kr -= s_above;
   }
-  for (int i = tid; i < k; i += kThreads) {
-    const uint64_t key = sel[i];
-    if (a.out_keys) {
-      a.out_keys[(size_t)q * k + i] = key;
-    } else {
-      if (key == 0ull) {
-        a.out_ids[(size_t)q * k + i] = -1;
-        a.out_scores[(size_t)q * k + i] = -__int_as_float(0x7f800000);
-      } else {
-        a.out_ids[(size_t)q * k + i] = (int64_t)key_id(key) + a.id_offset;
-        a.out_scores[(size_t)q * k + i] = key_score(key);
-      }
+  const uint32_t T = prefix;            // k-th largest value; k - kr values are larger
+  const int size = pow2_at_least(k);
+  if (tid == 0) s_pos = 0;
+  for (int i = tid; i < size; i += kThreads) sel[i] = 0ull;
+  __syncthreads();
+  // values > T: any order (the sort fixes it)
+  for (int i = tid; i < M; i += kThreads)
+    if (vals[i] > T) sel[atomicAdd(&s_pos, 1)] = ((uint64_t)vals[i] << 32) | (0xFFFFFFFFu - (uint32_t)i);
+  // values == T: the kr smallest indices -- contiguous chunks, block prefix count
+  const int chunk = (M + kThreads - 1) / kThreads;
+  const int lo = tid * chunk, hi = min(M, lo + chunk);
+  int my = 0;
+  for (int i = lo; i < hi; ++i) my += vals[i] == T;
+  int incl = my;
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  int wbase = 0;
+  for (int w = 0; w < wid; ++w) wbase += wsum[w];
+  int r = wbase + incl - my;           // rank among equal values of my first equal element
+  const int first = k - kr;
+  for (int i = lo; i < hi && r < kr; ++i)
+    if (vals[i] == T) {
+      sel[first + r] = ((uint64_t)T << 32) | (0xFFFFFFFFu - (uint32_t)i);
+      ++r;
     }
-  }
+  __syncthreads();
+  sort_desc(sel, size);
+  for (int i = tid; i < k; i += kThreads) write_out(a, q, i, sel[i]);
 }
 
 // k = 1 with few grouped candidates (k-means / full assignment: millions of queries):
@@ -132,20 +241,24 @@ __global__ void merge_top1_kernel(const MergeArgs a, int64_t nq) {
       const uint64_t c = a.cand[(size_t)g * a.gstride + (size_t)q * a.qstride];
       best = c > best ? c : best;
     }
-    if (a.out_keys) {
-      a.out_keys[q] = best;
-    } else if (best == 0ull) {
-      a.out_ids[q] = -1;
-      a.out_scores[q] = -__int_as_float(0x7f800000);
-    } else {
-      a.out_ids[q] = (int64_t)key_id(best) + a.id_offset;
-      a.out_scores[q] = key_score(best);
-    }
+    write_out(a, q, 0, best);
   }
 }
 
 cudaError_t launch_merge(const MergeArgs& a, int64_t nq, cudaStream_t stream) {
   if (nq <= 0) return cudaSuccess;
+  if (a.cand_scores) {
+    const size_t smem = (size_t)a.m_flat * sizeof(uint32_t);
+    static int cur = 0;
+    if ((int)smem > cur) {
+      cudaError_t e = cudaFuncSetAttribute(select_dense_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      cur = (int)smem;
+    }
+    select_dense_kernel<<<(unsigned)nq, kThreads, smem, stream>>>(a);
+    return cudaGetLastError();
+  }
   if (a.k == 1 && !a.slot_off && a.m_flat <= 0 && a.groups <= 64) {
     int64_t blocks = (nq + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;

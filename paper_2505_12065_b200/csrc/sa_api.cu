@@ -424,6 +424,7 @@ sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nl
   if (opts->row_offset < 0 || opts->row_offset + n > n_total)
     return set_error(SA_ERR_INVALID_ARG, "row_offset + n exceeds n_total");
   if (nlist > n_total) return set_error(SA_ERR_INVALID_ARG, "nlist exceeds n_total");
+  if (nlist > 32768) return set_error(SA_ERR_UNSUPPORTED, "nlist > 32768 not supported");
   if (nlist > 0 && (opts->kmeans_iters < 0 || opts->train_per_list < 1))
     return set_error(SA_ERR_INVALID_ARG, "bad k-means options");
   const int32_t d_pad = (d + 63) / 64 * 64;
