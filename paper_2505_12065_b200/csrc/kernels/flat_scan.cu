@@ -392,9 +392,9 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           ptx::tma_load_2d(ptx::smem_u32(a_smem + j * kASmemKb), &tmap_q, bar,
                            (kb_t + j) * kBK, qrow0);
       }
-      if (half == 0) {
-        // Rows of absent queries are left as they are: MMA output rows are independent
-        // and the epilogue never reads the rows of invalid lanes.
+      // Rows of absent queries are left as they are: MMA output rows are independent and the
+      // epilogue never reads the rows of invalid lanes, so a warp with no valid lane skips.
+      if (half == 0 && __any_sync(0xffffffffu, qs.valid)) {
         const uint4* src = reinterpret_cast<const uint4*>(a.Q + (size_t)qs.q * a.d_pad);
         for (int c = 0; c < kb_t; ++c) {
           uint32_t r[32];

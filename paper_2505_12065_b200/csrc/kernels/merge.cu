@@ -16,6 +16,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMaxK = 256;
 constexpr int kSmemCand = 4096;  // u64 candidates cached in smem when they fit (32 KB)
+constexpr int kPrefilterCap = 2048;  // dense select: candidates surviving the prefilter
 
 // Warp 0 finds the radix bucket holding the kr-th largest element: buckets are scanned from
 // the top, 8 per lane, with one warp prefix sum (instead of a 256-step serial loop).
@@ -123,6 +124,55 @@ merge_topk_kernel(const MergeArgs a) {
   }
   auto cand = [&](int64_t i) -> uint64_t { return cached ? cache[i] : cand_g(i); };
 
+  // Prefilter (as in select_dense_kernel): T0 = k-th largest per-thread maximum is a lower
+  // bound of the k-th largest key; sort the keys >= T0 directly when they are few.
+  {
+    __shared__ uint64_t tmax[kThreads];
+    uint64_t mx = 0ull;
+    for (int64_t i = tid; i < M; i += kThreads) {
+      const uint64_t c = cand(i);
+      mx = c > mx ? c : mx;
+    }
+    tmax[tid] = mx;
+    if (tid == 0) s_pos = 0;
+    __syncthreads();
+    for (int sz = 2; sz <= kThreads; sz <<= 1)
+      for (int st = sz >> 1; st > 0; st >>= 1) {
+        const int j = tid ^ st;
+        if (j > tid) {
+          const bool desc = (tid & sz) == 0;
+          const uint64_t x = tmax[tid], y = tmax[j];
+          if (desc ? x < y : x > y) { tmax[tid] = y; tmax[j] = x; }
+        }
+        __syncthreads();
+      }
+    const uint64_t T0 = tmax[k - 1];
+    uint64_t* buf = cached ? nullptr : cache;   // reuse the smem cache when it is not in use
+    __shared__ uint64_t small[512];
+    const int cap = cached ? 512 : kSmemCand;
+    if (cached) buf = small;
+    for (int64_t i = tid; i < M; i += kThreads) {
+      const uint64_t c = cand(i);
+      if (c >= T0 && c != 0ull) {
+        const int p = atomicAdd(&s_pos, 1);
+        if (p < cap) buf[p] = c;
+      }
+    }
+    __syncthreads();
+    const int nc = s_pos;
+    if (nc <= cap) {
+      const int size = pow2_at_least(nc < k ? k : nc);
+      if (size <= cap) {
+        for (int i = nc + tid; i < size; i += kThreads) buf[i] = 0ull;
+        __syncthreads();
+        sort_desc(buf, size);
+        for (int i = tid; i < k; i += kThreads) write_out(a, q, i, i < nc ? buf[i] : 0ull);
+        return;
+      }
+    }
+    __syncthreads();
+  }
+
   uint64_t prefix = 0, pmask = 0;
   int kr = k;
   for (int pass = 0; pass < 8; ++pass) {
@@ -169,14 +219,81 @@ select_dense_kernel(const MergeArgs a) {
   __shared__ uint64_t sel[kMaxK];
   __shared__ int s_bucket, s_above, s_pos;
   __shared__ int wsum[kThreads / 32];
+  __shared__ uint32_t tmax[kThreads];
+  __shared__ uint64_t cand[kPrefilterCap];
 
   const int64_t q = blockIdx.x;
   const int k = a.k;
   const int M = (int)a.m_flat;
   const float* row = a.cand_scores + (size_t)q * a.qstride;
   const int tid = threadIdx.x;
-  for (int i = tid; i < M; i += kThreads) vals[i] = ordered_from_float(row[i]);
+  uint32_t mx = 0u;
+  if ((M & 3) == 0 && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+    // 16-byte loads, 4 in flight per thread: this load is the latency-critical part for
+    // small batches (one CTA per query streams the whole score row)
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const int M4 = M >> 2;
+    for (int i0 = tid; i0 < M4; i0 += 4 * kThreads) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = (i0 + u * kThreads < M4) ? __ldg(r4 + i0 + u * kThreads)
+                                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kThreads;
+        if (i < M4) {
+          const uint32_t o0 = ordered_from_float(v[u].x), o1 = ordered_from_float(v[u].y);
+          const uint32_t o2 = ordered_from_float(v[u].z), o3 = ordered_from_float(v[u].w);
+          *reinterpret_cast<uint4*>(vals + 4 * i) = make_uint4(o0, o1, o2, o3);
+          mx = max(mx, max(max(o0, o1), max(o2, o3)));
+        }
+      }
+    }
+  } else {
+    for (int i = tid; i < M; i += kThreads) {
+      const uint32_t v = ordered_from_float(row[i]);
+      vals[i] = v;
+      mx = v > mx ? v : mx;
+    }
+  }
+  tmax[tid] = mx;
+  if (tid == 0) s_pos = 0;
   __syncthreads();
+  // Prefilter: the k-th largest of the per-thread maxima (k <= kThreads) is a lower bound
+  // T0 of the k-th largest value (k threads each hold a value >= it).  Usually only a few
+  // hundred values reach T0; they are sorted directly.  Too many (heavy ties) -> radix path.
+  {
+    // bitonic sort of the 256 maxima, descending
+    for (int sz = 2; sz <= kThreads; sz <<= 1)
+      for (int st = sz >> 1; st > 0; st >>= 1) {
+        const int j = tid ^ st;
+        if (j > tid) {
+          const bool desc = (tid & sz) == 0;
+          const uint32_t x = tmax[tid], y = tmax[j];
+          if (desc ? x < y : x > y) { tmax[tid] = y; tmax[j] = x; }
+        }
+        __syncthreads();
+      }
+    const uint32_t T0 = k <= kThreads ? tmax[k - 1] : 0u;
+    for (int i = tid; i < M; i += kThreads) {
+      const uint32_t v = vals[i];
+      if (v >= T0) {
+        const int p = atomicAdd(&s_pos, 1);
+        if (p < kPrefilterCap) cand[p] = ((uint64_t)v << 32) | (0xFFFFFFFFu - (uint32_t)i);
+      }
+    }
+    __syncthreads();
+    const int nc = s_pos;
+    if (k <= kThreads && nc <= kPrefilterCap) {
+      const int size = pow2_at_least(nc < k ? k : nc);
+      for (int i = nc + tid; i < size; i += kThreads) cand[i] = 0ull;
+      __syncthreads();
+      sort_desc(cand, size);
+      for (int i = tid; i < k; i += kThreads) write_out(a, q, i, i < nc ? cand[i] : 0ull);
+      return;
+    }
+    __syncthreads();
+  }
 
   uint32_t prefix = 0, pmask = 0;
   int kr = k;
