@@ -51,7 +51,8 @@ constexpr int kEpiT = FS_EPI_THREADS;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kASmemKb = FS_BM * FS_BK * 2;  // one 128-row x 64-col K-block of A in smem: 16 KB
 
-constexpr int kKbPerStage = 2;  // K-blocks (64 wide) per ring stage: 8 MMAs per barrier round trip
+constexpr int kKbPerStage = 2;
+constexpr int kLockstepLag = 8;  // tiles a unit may run ahead of units sharing its slice  // K-blocks (64 wide) per ring stage: 8 MMAs per barrier round trip
 
 template <int CG>
 struct Cfg {
@@ -237,9 +238,26 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
+      // Soft lockstep (flat mode, one work item per unit, several query groups): the units
+      // that scan the same corpus slice for different query groups publish their progress
+      // and none runs more than kLockstepLag tiles ahead of another, so the slice is read
+      // from HBM once and served from L2 to the other groups (37 slices x lag x 192 KB
+      // stays well inside the 126 MB L2).  Only the pair leader's producer paces.
+      const bool lockstep = a.progress != nullptr && leader;
       for (int w = unit; w < n_work; w += n_units) {
         const WorkItem wi = work_item(w, a, T);
         for (int32_t t = wi.t0; t < wi.t1; ++t) {
+          if (lockstep) {
+            const int32_t done = t - wi.t0;
+            if ((done & 3) == 0) {
+              ptx::st_release_gpu(a.progress + unit, done);
+              for (int g = 0; g < a.QP; ++g) {
+                const int p = g * S + wi.s;
+                if (p == unit) continue;
+                while (ptx::ld_acquire_gpu(a.progress + p) < done - kLockstepLag) __nanosleep(256);
+              }
+            }
+          }
           const int32_t row = wi.row_base + t * kBN + (int32_t)rank * C::kRowsPerCta;
           for (int sl = 0; sl < n_sl; ++sl) {
             const int kb0 = sl * kKbPerStage;

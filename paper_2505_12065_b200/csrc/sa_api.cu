@@ -170,7 +170,17 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
       return st;
     }
   }
+  // soft lockstep of units sharing a corpus slice (see flat_scan.cu)
+  int32_t* progress = nullptr;
+  const int units = p.grid / p.cg;
+  if (p.QP > 1 && p.S > 1 && (int64_t)p.QP * p.S <= units) {
+    st = dalloc(&progress, (size_t)units, s, "alloc progress");
+    if (st == SA_OK)
+      st = cuda_status(cudaMemsetAsync(progress, 0, units * sizeof(int32_t), s), "memset");
+    if (st != SA_OK) return st;
+  }
   FlatScanArgs a{};
+  a.progress = progress;
   a.q_hint = hint;
   a.Q = Qs;
   a.nq = nq;
@@ -221,6 +231,7 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   }
   if (heap) cudaFreeAsync(heap, s);
   if (hint) cudaFreeAsync(hint, s);
+  if (progress) cudaFreeAsync(progress, s);
   cudaFreeAsync(part, s);
   return cuda_status(e, "flat search launch");
 }
