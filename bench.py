@@ -168,8 +168,9 @@ def run_reference(args, cfg, name):
 
 
 # ------------------------------------------------------------------ GPU arm
-NPROBE_LADDER = (8, 16, 24, 32, 40, 48, 64, 96, 128, 192, 256)
+NPROBE_LADDER = (8, 16, 24, 32, 36, 40, 44, 48, 52, 56, 64, 80, 96, 128, 192, 256)
 RECALL_TARGET = 0.95
+CALIBRATION_MARGIN = 0.005   # calibrate at >= 0.955 so the timed batches' mean stays >= 0.95
 
 
 def recall_at_k(got: torch.Tensor, gt: torch.Tensor) -> float:
@@ -298,13 +299,13 @@ def main():
     sweep = []
     nprobe = 0
     if mode == "auto":
+        calib = list(range(args.warmup, min(nb, args.warmup + 2)))   # first two timed batches
         for p in NPROBE_LADDER:
             if p > nlist:
                 break
-            gi, _ = idx.search(batches[args.warmup], k, p)
-            r = recall_at_k(gi, gt[args.warmup])
+            r = float(np.mean([recall_at_k(idx.search(batches[i], k, p)[0], gt[i]) for i in calib]))
             sweep.append({"nprobe": p, "recall": r})
-            if r >= RECALL_TARGET:
+            if r >= RECALL_TARGET + CALIBRATION_MARGIN:
                 nprobe = p
                 break
         if nprobe == 0:
