@@ -42,6 +42,7 @@ struct sa_index {
   __nv_bfloat16* X = nullptr;  // [n_local, d_pad] (list-major when nlist > 0)
   CUtensorMap tmap_x;   // box 128 rows (cta_group 1)
   CUtensorMap tmap_x2;  // box 64 rows (cta_group 2: each CTA of a pair stages half a tile)
+  CUtensorMap tmap_xt;  // box 32 rows (IVF list tails)
   int32_t* row_ids = nullptr;  // nlist > 0: stored row -> global id (fits 32 bits)
   // IVF coarse quantiser
   float* centroids = nullptr;                // [nlist, d_pad] fp32 (unit norm)

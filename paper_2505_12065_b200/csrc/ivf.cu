@@ -244,6 +244,7 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   idx->X = Xp;
   SA_TRY(make_tmap_bf16(&idx->tmap_x, idx->X, n, dp, FS_BN));
   SA_TRY(make_tmap_bf16(&idx->tmap_x2, idx->X, n, dp, FS_BN / 2));
+  SA_TRY(make_tmap_bf16(&idx->tmap_xt, idx->X, n, dp, FS_TAIL_ROWS));
   idx->h_list_off.resize(nlist + 1);
   SA_CUDA(cudaMemcpy(idx->h_list_off.data(), idx->list_off, (nlist + 1) * sizeof(int64_t),
                      cudaMemcpyDeviceToHost),
@@ -384,7 +385,7 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   a.chunk_rows = chunk_rows;
   a.q_hint = hint;
   prof_begin(SA_KERNEL_IVF_SCAN, s);
-  cudaError_t e = launch_flat_scan(idx->tmap_x, tmap_q, a, 1, sms, s);
+  cudaError_t e = launch_flat_scan(idx->tmap_x, idx->tmap_xt, tmap_q, a, 1, sms, s);
   prof_end(SA_KERNEL_IVF_SCAN, s);
   prof_count(SA_KERNEL_IVF_SCAN);
   SA_CUDA(e, "ivf scan");

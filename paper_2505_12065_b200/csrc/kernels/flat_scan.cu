@@ -52,14 +52,15 @@ constexpr uint32_t kTmemCols = 512;
 constexpr int kASmemKb = FS_BM * FS_BK * 2;  // one 128-row x 64-col K-block of A in smem: 16 KB
 
 constexpr int kKbPerStage = 2;
-constexpr int kLockstepLag = 8;  // tiles a unit may run ahead of units sharing its slice  // K-blocks (64 wide) per ring stage: 8 MMAs per barrier round trip
+constexpr int kLockstepLag = 8;
+constexpr int kTailRows = FS_TAIL_ROWS;  // box rows of the tail tensor map (IVF list tails)  // tiles a unit may run ahead of units sharing its slice  // K-blocks (64 wide) per ring stage: 8 MMAs per barrier round trip
 
 template <int CG>
 struct Cfg {
   static constexpr int kRowsPerCta = kBN / CG;              // corpus rows staged per CTA per tile
   static constexpr int kBoxBytes = kRowsPerCta * kBK * 2;  // one TMA box: rows x 64 bf16
   static constexpr int kStageBytes = kBoxBytes * kKbPerStage;
-  static constexpr int kStages = CG == 1 ? 3 : 7;          // 96 / 112 KB of corpus in flight
+  static constexpr int kStages = CG == 1 ? 4 : 7;          // 128 / 112 KB of corpus in flight
   static constexpr uint32_t kIdesc = ptx::umma_idesc_bf16(kBM * CG, kBN);
 };
 
@@ -164,6 +165,7 @@ __device__ __forceinline__ WorkItem uniform_item(const WorkItem& w) {
 template <int CG>
 __global__ void __launch_bounds__(FS_THREADS, 1)
 flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                      const __grid_constant__ CUtensorMap tmap_tail,
                       const __grid_constant__ CUtensorMap tmap_q, const FlatScanArgs a) {
   using C = Cfg<CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -266,9 +268,22 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const uint32_t dst = ptx::smem_u32(stage_base + stage * C::kStageBytes);
             const uint32_t fb = full0 + stage * 8;
             if (CG == 1) {
-              ptx::mbar_arrive_expect_tx(fb, nkb * C::kBoxBytes);
-              for (int j = 0; j < nkb; ++j)
-                ptx::tma_load_2d(dst + j * C::kBoxBytes, &tmap_x, fb, (kb0 + j) * kBK, row);
+              const int32_t left = wi.row_end - row;
+              if (ivf && left < kBN) {
+                // last tile of an IVF chunk: fetch only ceil(left/32) 32-row boxes instead of
+                // the full 128 rows (the rest of the stage is stale and masked by row_end);
+                // a list's tail otherwise drags in up to 127 rows of the next list
+                const int nbox = (left + kTailRows - 1) / kTailRows;
+                ptx::mbar_arrive_expect_tx(fb, nkb * nbox * kTailRows * kBK * 2);
+                for (int j = 0; j < nkb; ++j)
+                  for (int bx = 0; bx < nbox; ++bx)
+                    ptx::tma_load_2d(dst + j * C::kBoxBytes + bx * kTailRows * kBK * 2, &tmap_tail,
+                                     fb, (kb0 + j) * kBK, row + bx * kTailRows);
+              } else {
+                ptx::mbar_arrive_expect_tx(fb, nkb * C::kBoxBytes);
+                for (int j = 0; j < nkb; ++j)
+                  ptx::tma_load_2d(dst + j * C::kBoxBytes, &tmap_x, fb, (kb0 + j) * kBK, row);
+              }
             } else {
               if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * nkb * C::kBoxBytes);
               const uint32_t fbl = ptx::mapa(fb, 0);
@@ -603,8 +618,9 @@ size_t flat_scan_smem_bytes(int cta_group) {
   return 1024 + (size_t)Cfg<1>::kStages * Cfg<1>::kStageBytes + fixed + sizeof(SmemTail<1>);
 }
 
-cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_q,
-                             const FlatScanArgs& a, int cta_group, int grid, cudaStream_t stream) {
+cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_tail,
+                             const CUtensorMap& tmap_q, const FlatScanArgs& a, int cta_group,
+                             int grid, cudaStream_t stream) {
   const size_t smem = flat_scan_smem_bytes(cta_group);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
@@ -626,7 +642,7 @@ cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_q,
       if (e != cudaSuccess) return e;
       set2 = true;
     }
-    return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<2>, tmap, tmap_q, a);
+    return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<2>, tmap, tmap_tail, tmap_q, a);
   }
   static bool set1 = false;
   if (!set1) {
@@ -635,7 +651,7 @@ cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_q,
     if (e != cudaSuccess) return e;
     set1 = true;
   }
-  return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<1>, tmap, tmap_q, a);
+  return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<1>, tmap, tmap_tail, tmap_q, a);
 }
 
 }  // namespace sa

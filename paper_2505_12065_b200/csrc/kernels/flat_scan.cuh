@@ -18,6 +18,7 @@ constexpr int FS_MAX_DPAD = 768; // queries: up to 8 K-blocks in TMEM + 4 in sme
 constexpr int FS_KB_TMEM = 8;    // K-blocks of the A operand held in TMEM (256 columns)
 constexpr int FS_KB_SMEM = 4;    // K-blocks of the A operand held in smem (64 KB)
 constexpr int FS_KSMEM = 16;     // running heaps in smem for k <= 16, else in global scratch
+constexpr int FS_TAIL_ROWS = 32;  // box rows of the tail tensor map (IVF list tails)
 constexpr int FS_LISTS_PER_ITEM = 2;  // partial lists per (query, work item): one per column half
 
 enum FlatScanMode : int32_t {
@@ -63,7 +64,9 @@ struct FlatScanArgs {
 size_t flat_scan_smem_bytes(int cta_group);
 // tmap: corpus rows (box 128 rows for cta_group 1, 64 for 2); tmap_q: the staged queries
 // (box 128 rows, rows = nq), used for the K-blocks of the A operand that live in smem.
-cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_q,
-                             const FlatScanArgs& a, int cta_group, int grid, cudaStream_t stream);
+// tmap_tail: the corpus with FS_TAIL_ROWS-row boxes (IVF tails, cta_group 1; else unused).
+cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_tail,
+                             const CUtensorMap& tmap_q, const FlatScanArgs& a, int cta_group,
+                             int grid, cudaStream_t stream);
 
 }  // namespace sa

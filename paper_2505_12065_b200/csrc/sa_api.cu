@@ -210,7 +210,8 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
     return st;
   }
   prof_begin(SA_KERNEL_FLAT_SCAN, s);
-  cudaError_t e = launch_flat_scan(p.cg == 2 ? *cv.tmap2 : *cv.tmap1, tmap_q, a, p.cg, p.grid, s);
+  const CUtensorMap& tm = p.cg == 2 ? *cv.tmap2 : *cv.tmap1;
+  cudaError_t e = launch_flat_scan(tm, tm, tmap_q, a, p.cg, p.grid, s);
   prof_end(SA_KERNEL_FLAT_SCAN, s);
   prof_count(SA_KERNEL_FLAT_SCAN);
   if (e == cudaSuccess) {
@@ -254,7 +255,8 @@ sa_status flat_scores_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   CUtensorMap tmap_q;
   sa_status st = make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM);
   if (st != SA_OK) return st;
-  cudaError_t e = launch_flat_scan(p.cg == 2 ? *cv.tmap2 : *cv.tmap1, tmap_q, a, p.cg, p.grid, s);
+  const CUtensorMap& tm = p.cg == 2 ? *cv.tmap2 : *cv.tmap1;
+  cudaError_t e = launch_flat_scan(tm, tm, tmap_q, a, p.cg, p.grid, s);
   prof_count(SA_KERNEL_FLAT_SCAN);
   return cuda_status(e, "score scan");
 }
@@ -477,6 +479,7 @@ sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nl
   }
   if (st == SA_OK) st = make_tmap_bf16(&idx->tmap_x, idx->X, n, d_pad, FS_BN);
   if (st == SA_OK) st = make_tmap_bf16(&idx->tmap_x2, idx->X, n, d_pad, FS_BN / 2);
+  if (st == SA_OK) st = make_tmap_bf16(&idx->tmap_xt, idx->X, n, d_pad, FS_TAIL_ROWS);
   // ivf_build permutes X list-major and re-encodes the tensor maps
   if (st == SA_OK && nlist > 0) st = ivf_build(idx, *opts, s);
   if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "build sync");
