@@ -358,10 +358,10 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
     SA_TRY(dalloc(&heap, (size_t)sms * k * FS_EPI_THREADS, s, "ivf heaps"));
     f.add(heap);
   }
-  uint32_t* hint;
-  SA_TRY(dalloc(&hint, nq, s, "ivf hints"));
+  uint32_t* hint;   // [nq] pruning bounds + [1] dynamic item counter
+  SA_TRY(dalloc(&hint, nq + 1, s, "ivf hints"));
   f.add(hint);
-  SA_CUDA(cudaMemsetAsync(hint, 0, sizeof(uint32_t) * nq, s), "memset hints");
+  SA_CUDA(cudaMemsetAsync(hint, 0, sizeof(uint32_t) * (nq + 1), s), "memset hints");
   CUtensorMap tmap_q;
   SA_TRY(make_tmap_bf16(&tmap_q, Qs, nq, idx->d_pad, FS_BM));
   FlatScanArgs a{};
@@ -384,6 +384,7 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   a.nprobe = nprobe;
   a.chunk_rows = chunk_rows;
   a.q_hint = hint;
+  a.item_counter = reinterpret_cast<int32_t*>(hint + nq);
   prof_begin(SA_KERNEL_IVF_SCAN, s);
   cudaError_t e = launch_flat_scan(idx->tmap_x, idx->tmap_xt, tmap_q, a, 1, sms, s);
   prof_end(SA_KERNEL_IVF_SCAN, s);

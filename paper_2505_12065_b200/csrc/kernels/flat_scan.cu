@@ -53,7 +53,8 @@ constexpr int kASmemKb = FS_BM * FS_BK * 2;  // one 128-row x 64-col K-block of 
 
 constexpr int kKbPerStage = 2;
 constexpr int kLockstepLag = 8;
-constexpr int kTailRows = FS_TAIL_ROWS;  // box rows of the tail tensor map (IVF list tails)  // tiles a unit may run ahead of units sharing its slice  // K-blocks (64 wide) per ring stage: 8 MMAs per barrier round trip
+constexpr int kTailRows = FS_TAIL_ROWS;
+constexpr int kItemQ = 4;                // depth of the dynamic work-item queue  // box rows of the tail tensor map (IVF list tails)  // tiles a unit may run ahead of units sharing its slice  // K-blocks (64 wide) per ring stage: 8 MMAs per barrier round trip
 
 template <int CG>
 struct Cfg {
@@ -72,6 +73,9 @@ struct __align__(8) SmemTail {
   uint64_t tmem_empty[2];
   uint64_t a_full;
   uint64_t a_tma;
+  uint64_t iq_full[kItemQ];   // dynamic work queue (IVF): producer -> MMA + epilogue warps
+  uint64_t iq_empty[kItemQ];
+  int32_t iq_w[kItemQ];
   uint32_t tmem_base;
 };
 
@@ -194,6 +198,19 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
   const int S = a.S;
   const bool ivf = a.mode == FS_MODE_IVF;
   const int n_work = ivf ? *a.n_items : a.QP * S;
+  // IVF items differ in size (list lengths): hand them out dynamically from a global counter
+  // (the producer fetches, the MMA warp and the epilogue warps follow through a small smem
+  // queue) instead of a static round robin whose slowest CTA sets the kernel time.
+  const bool dyn = ivf && CG == 1 && a.item_counter != nullptr;
+  // consumer side of the queue: item #i of this CTA (-1 = no more work)
+  auto take_item = [&](int i, bool arrive_lane) __attribute__((always_inline)) -> int {
+    const int slot = i % kItemQ;
+    ptx::mbar_wait(ptx::smem_u32(&tail->iq_full[slot]), (uint32_t)((i / kItemQ) & 1));
+    const int w = *reinterpret_cast<volatile int32_t*>(&tail->iq_w[slot]);
+    __syncwarp();
+    if (arrive_lane) ptx::mbar_arrive(ptx::smem_u32(&tail->iq_empty[slot]));
+    return w;
+  };
   const int32_t T = (int32_t)((a.n_rows + kBN - 1) / kBN);
   const int num_kb = a.d_pad / kBK;
   const int nacc = 2;
@@ -212,6 +229,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     }
     ptx::mbar_init(ptx::smem_u32(&tail->a_full), FS_EPI_WARPS * CG);
     ptx::mbar_init(ptx::smem_u32(&tail->a_tma), 1);
+    for (int i = 0; i < kItemQ; ++i) {
+      ptx::mbar_init(ptx::smem_u32(&tail->iq_full[i]), 1);
+      ptx::mbar_init(ptx::smem_u32(&tail->iq_empty[i]), 1 + FS_EPI_WARPS);
+    }
     ptx::fence_mbar_init();
     ptx::fence_proxy_async_smem();
   }
@@ -246,7 +267,19 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       // from HBM once and served from L2 to the other groups (37 slices x lag x 192 KB
       // stays well inside the 126 MB L2).  Only the pair leader's producer paces.
       const bool lockstep = a.progress != nullptr && leader;
-      for (int w = unit; w < n_work; w += n_units) {
+      int fetched = 0;
+      auto next_w = [&](int w_prev) -> int {
+        if (!dyn) return w_prev < 0 ? unit : w_prev + n_units;
+        const int slot = fetched % kItemQ;
+        ptx::mbar_wait(ptx::smem_u32(&tail->iq_empty[slot]), (uint32_t)(((fetched / kItemQ) & 1) ^ 1));
+        int w = atomicAdd(a.item_counter, 1);
+        if (w >= n_work) w = -1;
+        *reinterpret_cast<volatile int32_t*>(&tail->iq_w[slot]) = w;
+        ptx::mbar_arrive(ptx::smem_u32(&tail->iq_full[slot]));
+        ++fetched;
+        return w;
+      };
+      for (int w = next_w(-1); w >= 0 && w < n_work; w = next_w(w)) {
         const WorkItem wi = work_item(w, a, T);
         for (int32_t t = wi.t0; t < wi.t1; ++t) {
           if (lockstep) {
@@ -316,7 +349,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(a_smem));
       const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
       const uint32_t empty0 = ptx::smem_u32(&tail->empty[0]);
-      for (int w = unit; w < n_work_u; w += n_units) {
+      int taken = 0;
+      int w = dyn ? __shfl_sync(0xffffffffu, take_item(taken++, lane == 0), 0) : unit;
+      for (; w >= 0 && w < n_work_u;
+           w = dyn ? __shfl_sync(0xffffffffu, take_item(taken++, lane == 0), 0) : w + n_units) {
         const WorkItem wi = uniform_item(work_item(w, a, T));
         if (wi.qkey < 0 || wi.qkey != cur_qp) {
           ptx::mbar_wait(ptx::smem_u32(&tail->a_full), a_phase);
@@ -465,17 +501,21 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       cur_qp = wi.qkey;
     };
 
-    int w = unit;
+    int taken = 0;
+    int w = dyn ? take_item(taken++, lane == 0) : unit;
     WorkItem wi{};
     QSel cs{};
-    if (w < n_work) {
+    if (w >= 0 && w < n_work) {
       wi = work_item(w, a, T);
       cs = qsel(wi);
       stage_a(wi, cs);
     }
-    while (w < n_work) {
-      const int wn = w + n_units;
-      const bool has_next = wn < n_work;
+    while (w >= 0 && w < n_work) {
+      // next item: static -> known now; dynamic -> taken at this item's last tile, when the
+      // producer (which runs ahead) has certainly fetched it
+      int wn = dyn ? -2 : w + n_units;
+      if (dyn && wi.t1 <= wi.t0) wn = take_item(taken++, lane == 0);
+      bool has_next = wn >= 0 && wn < n_work;
       // The next item is decoded only when needed (at this item's last tile) to keep its
       // state out of the registers of the tile loop.
       WorkItem nx{};
@@ -530,6 +570,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         // The last accumulator of this item is in registers, so every MMA that read this
         // item's A operand has completed: stage the next item's queries now, before the
         // score processing, so the tensor core restarts as early as possible.
+        if (t == wi.t1 - 1 && wn == -2) {
+          wn = take_item(taken++, lane == 0);
+          has_next = wn >= 0 && wn < n_work;
+        }
         if (t == wi.t1 - 1 && has_next) {
           nx = work_item(wn, a, T);
           ns = qsel(nx);
@@ -591,6 +635,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         }
         for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
         thr = heap_threshold(0ull);
+      }
+      if (wn == -2) {
+        wn = take_item(taken++, lane == 0);
+        has_next = wn >= 0 && wn < n_work;
       }
       if (has_next && !nx_ready) {
         nx = work_item(wn, a, T);

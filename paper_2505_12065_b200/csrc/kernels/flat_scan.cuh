@@ -53,6 +53,7 @@ struct FlatScanArgs {
   int32_t chunk_rows;      // rows per IVF work item (multiple of FS_BN)
   uint32_t* q_hint;        // optional [nq] ordered-fp32 lower bound of each query's k-th score
                            // (zero-initialised by the caller; 0 = none)
+  int32_t* item_counter;   // IVF: zeroed global counter -> dynamic item scheduling (or nullptr)
   int32_t* progress;       // optional [units] tile progress for soft lockstep (zeroed; flat
                            // mode with one work item per unit and QP > 1)
   int32_t experiment;      // timing experiments only (env SA_EXPERIMENT): 1 = skip score
