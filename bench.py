@@ -195,6 +195,9 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override corpus rows (experiments)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true",
+                    help="BASELINE config 4/5 sweep: recall@k vs q/s over nprobe (batch 512 and "
+                         "64) and agent-step latency; prints one JSON line and exits")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config])
@@ -294,6 +297,10 @@ def main():
         for i in range(args.warmup, nb):
             gi, _ = idx.search(batches[i], k, 0)
             gt[i] = gi.clone()
+
+    if args.sweep:
+        return run_sweep(args, sa, idx, batches, gt, k, nq, d, nlist, n, world, rank, barrier,
+                         max_over_ranks, stream)
 
     # ---- pick nprobe: smallest on the ladder with recall@k >= target on the first batch
     sweep = []
@@ -454,6 +461,53 @@ def main():
         comm.free()
     if dist is not None:
         dist.destroy_process_group()
+    return 0
+
+
+def run_sweep(args, sa, idx, batches, gt, k, nq, d, nlist, n, world, rank, barrier,
+              max_over_ranks, stream):
+    """C4: recall@k and q/s per nprobe at batch nq (and 64); C5: agent-step latency."""
+    out = {"sweep": "recall@k vs queries/s (BASELINE configs 4 and 5)", "n": n, "d": d, "k": k,
+           "nlist": nlist, "n_gpus": world, "rows": [], "agent_step": []}
+    nb = args.warmup + args.steps
+    for batch in (nq, 64):
+        for p in (0, 8, 16, 32, 48, 64, 96, 128, 192, 256):
+            if p > nlist:
+                continue
+            qs = [b[:batch].contiguous() for b in batches]
+            for i in range(args.warmup):
+                idx.search(qs[i], k, p)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(args.warmup, nb):
+                idx.search(qs[i], k, p)
+            e1.record(stream)
+            barrier()
+            ms = max_over_ranks(e0.elapsed_time(e1))
+            rec = float(np.mean([recall_at_k(idx.search(qs[i], k, p)[0], gt[i][:batch])
+                                 for i in range(args.warmup, min(nb, args.warmup + 4))])) if p else 1.0
+            out["rows"].append({"batch": batch, "nprobe": p, "recall": rec,
+                                "qps": args.steps * batch / (ms / 1e3),
+                                "ms_per_batch": ms / args.steps})
+    for p in (48, 0):
+        for b in (1, 2, 4, 8, 16, 32, 64):
+            qh = [batches[(args.warmup + i) % nb][:b].float().cpu().pin_memory() for i in range(8)]
+            ih = torch.empty(b, 5, dtype=torch.int64).pin_memory()
+            sh = torch.empty(b, 5, dtype=torch.float32).pin_memory()
+            for i in range(5):
+                idx.search_host(qh[i % 8], 5, p, out=(ih, sh))
+            ts = []
+            for i in range(200 if p else 20):
+                t_s = time.perf_counter()
+                idx.search_host(qh[i % 8], 5, p, out=(ih, sh))
+                ts.append(time.perf_counter() - t_s)
+            out["agent_step"].append({"batch": b, "k": 5, "nprobe": p,
+                                      "p50_ms": 1e3 * float(np.percentile(ts, 50)),
+                                      "p99_ms": 1e3 * float(np.percentile(ts, 99))})
+    if rank == 0:
+        print(json.dumps(out))
+    idx.free()
     return 0
 
 
