@@ -21,9 +21,9 @@
 namespace sa {
 
 namespace {
-// Rows per IVF work item (multiple of FS_BN).  Big batches have many lists to spread over the
-// SMs; small (agent-step) batches probe only a few dozen lists, so lists are cut into short
-// chunks to put every SM on the few lists there are.
+// Rows per IVF work item (multiple of FS_BN), between these bounds: big batches have many
+// lists to spread over the SMs; small (agent-step) batches probe only a few dozen lists, so
+// lists are cut into short chunks to put every SM on the few lists there are.
 constexpr int kChunkRows = 4096;
 constexpr int kChunkRowsSmall = 256;
 
@@ -314,7 +314,11 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   prof_count(SA_KERNEL_OTHER);
 
   // ---- invert: lists -> probing queries, output slots, work items
-  const int chunk_rows = np < 4 * (int64_t)sms ? kChunkRowsSmall : kChunkRows;
+  // aim for ~4 work items per SM: rows probed ~= np * mean list length
+  const int64_t mean_list = std::max<int64_t>(1, idx->n_local / nlist);
+  int64_t want = np * mean_list / (4 * (int64_t)sms);
+  want = (want + FS_BN - 1) / FS_BN * FS_BN;
+  const int chunk_rows = (int)std::min<int64_t>(kChunkRows, std::max<int64_t>(kChunkRowsSmall, want));
   const int64_t max_chunks = std::max<int64_t>(1, (idx->max_list + chunk_rows - 1) / chunk_rows);
   IvfSearchScratch w{};
   SA_TRY(dalloc(&w.cnt, nlist, s, "ivf scratch"));
