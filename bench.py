@@ -195,6 +195,9 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override corpus rows (experiments)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--simulate-world", type=int, default=0,
+                    help="one-GPU projection of a W-GPU row-sharded run: time rank 0's shard "
+                         "(n/W rows; IVF with the full-corpus centroids) and report per-rank ms")
     ap.add_argument("--sweep", action="store_true",
                     help="BASELINE config 4/5 sweep: recall@k vs q/s over nprobe (batch 512 and "
                          "64) and agent-step latency; prints one JSON line and exits")
@@ -213,6 +216,9 @@ def main():
         return run_reference(args, cfg, args.config)
 
     import paper_2505_12065_b200 as sa
+
+    if args.simulate_world:
+        return run_simulated(args, cfg, sa)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -507,6 +513,52 @@ def run_sweep(args, sa, idx, batches, gt, k, nq, d, nlist, n, world, rank, barri
                                       "p99_ms": 1e3 * float(np.percentile(ts, 99))})
     if rank == 0:
         print(json.dumps(out))
+    idx.free()
+    return 0
+
+
+def run_simulated(args, cfg, sa):
+    """Per-rank work of a W-GPU row-sharded run, measured on one GPU (no NCCL): rank 0's
+    shard of n/W rows, exact and IVF (nprobe = --nprobe or 48, centroids trained on the full
+    corpus as the sharded build would).  The all-gather of [nq, k] keys (40 KB/rank) and the
+    final merge are not included."""
+    W = args.simulate_world
+    n, d, nq, k = cfg["n"], cfg["d"], cfg["nq"], cfg["k"]
+    nprobe = args.nprobe or 48
+    mix = make_mixture(d, cfg["C"], cfg["r"], cfg["s_sub"], cfg["s_n"], CORPUS_SEED, "cuda")
+    X = torch.empty(n, d, dtype=torch.bfloat16, device="cuda")
+    draw_rows_into(mix, X, CORPUS_SEED, 0)
+    full = sa.Index.build(X, args.nlist)
+    C = torch.from_numpy(full.export_centroids()).cuda()
+    full.free()
+    off, ln = sa.shard_range(n, 0, W)
+    Xs = X[off:off + ln].contiguous()
+    del X
+    torch.cuda.empty_cache()
+    idx = sa.Index.build(Xs, args.nlist, row_offset=off, n_total=n, centroids=C)
+    del Xs
+    nb = args.warmup + args.steps
+    Q = torch.empty(nb * nq, d, dtype=torch.bfloat16, device="cuda")
+    draw_rows_into(mix, Q, QUERY_SEED, 0)
+    batches = [Q[i * nq:(i + 1) * nq] for i in range(nb)]
+    stream = torch.cuda.current_stream()
+    res = {"simulated_world": W, "rank_rows": ln, "n": n, "nq": nq, "k": k, "nlist": args.nlist,
+           "note": "rank 0's shard timed alone on one B200; excludes the NCCL all-gather "
+                   "(nq*k*8 B per rank) and the final merge"}
+    for p in (0, nprobe):
+        for i in range(args.warmup):
+            idx.search(batches[i], k, p)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.warmup, nb):
+            idx.search(batches[i], k, p)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        res["exact" if p == 0 else f"ivf_nprobe{p}"] = {"ms_per_batch_per_rank": ms,
+                                                       "projected_job_qps": nq / (ms / 1e3)}
+    print(json.dumps(res))
     idx.free()
     return 0
 
