@@ -372,7 +372,7 @@ def main():
             "kernel_ms": {kk: v[0] for kk, v in kern_i.items()},
             "kernel_launches": {kk: v[1] for kk, v in kern_i.items()},
             "algorithmic_bytes_per_step": alg_bytes,
-            "roofline": {"kernel": "flat_scan_topk_kernel (FS_MODE_IVF list scan)", "bound": "hbm",
+            "roofline": {"kernel": "ivf_scan_kernel", "bound": "hbm",
                          "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
                          "frac": achieved / pk["hbm"],
                          "peak_kind": f"HBM copy, {pk['src']} (MEASURED_PEAKS.json)",
@@ -549,15 +549,19 @@ def run_simulated(args, cfg, sa):
         for i in range(args.warmup):
             idx.search(batches[i], k, p)
         torch.cuda.synchronize()
+        sa.profile_enable(True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.warmup, nb):
             idx.search(batches[i], k, p)
         e1.record(stream)
         torch.cuda.synchronize()
+        kern = {kind: round(sa.profile_read(kind)[0] / args.steps, 4) for kind in sa.KERNEL_KINDS}
+        sa.profile_enable(False)
         ms = e0.elapsed_time(e1) / args.steps
         res["exact" if p == 0 else f"ivf_nprobe{p}"] = {"ms_per_batch_per_rank": ms,
-                                                       "projected_job_qps": nq / (ms / 1e3)}
+                                                       "projected_job_qps": nq / (ms / 1e3),
+                                                       "kernel_ms_per_batch": kern}
     print(json.dumps(res))
     idx.free()
     return 0

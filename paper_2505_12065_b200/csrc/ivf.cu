@@ -7,7 +7,9 @@
 //   * k-means assignment (a2) and the full assignment (a3): queries = rows,
 //     corpus = the bf16 centroids, k = 1 (ties -> lowest list id, R8);
 //   * the probe (a7): queries x centroids, k = nprobe (ties -> lowest id, R11);
-//   * the list scan (a8): the flat kernel's list-major IVF mode.
+//   * the list scan (a8): ivf_scan.cu (list rows on the MMA M side, the probing
+//     queries of a list on N); SA_IVF_LEGACY=1 selects the flat kernel's older
+//     list-major mode (queries on M) for comparison.
 // The rest (sample gather, stable sort by list, deterministic centroid update,
 // empty-list repair, probe inversion) is SIMT glue in ivf_kernels.cu.
 #include <algorithm>
@@ -16,6 +18,7 @@
 #include "internal.h"
 #include "kernels/flat_scan.cuh"
 #include "kernels/ivf_kernels.cuh"
+#include "kernels/ivf_scan.cuh"
 #include "kernels/merge.cuh"
 
 namespace sa {
@@ -320,6 +323,12 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   want = (want + FS_BN - 1) / FS_BN * FS_BN;
   const int chunk_rows = (int)std::min<int64_t>(kChunkRows, std::max<int64_t>(kChunkRowsSmall, want));
   const int64_t max_chunks = std::max<int64_t>(1, (idx->max_list + chunk_rows - 1) / chunk_rows);
+  static const bool legacy = [] {
+    const char* e = getenv("SA_IVF_LEGACY");
+    return e && e[0] == '1';
+  }();
+  const int qblock = legacy ? FS_BM : IVS_NQ;
+  const int parts = legacy ? FS_LISTS_PER_ITEM : IVS_PARTS;
   IvfSearchScratch w{};
   SA_TRY(dalloc(&w.cnt, nlist, s, "ivf scratch"));
   f.add(w.cnt);
@@ -344,11 +353,11 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   SA_TRY(dalloc(&w.scratch, std::max<int64_t>(nlist, np) / 1024 + 4, s, "ivf scratch"));
   f.add(w.scratch);
   if (np <= kInvertSmallMax) {
-    SA_CUDA(launch_invert_small(probes, (int)nq, nprobe, idx->list_off, chunk_rows, w, s),
+    SA_CUDA(launch_invert_small(probes, (int)nq, nprobe, idx->list_off, chunk_rows, qblock, w, s),
             "probe inversion");
     prof_count(SA_KERNEL_OTHER);
   } else {
-    SA_CUDA(launch_probe_invert(probes, nq, nprobe, nlist, idx->list_off, chunk_rows, w, sms, s),
+    SA_CUDA(launch_probe_invert(probes, nq, nprobe, nlist, idx->list_off, chunk_rows, qblock, w, sms, s),
             "probe inversion");
     for (int i = 0; i < 10; ++i) prof_count(SA_KERNEL_OTHER);
   }
@@ -356,16 +365,40 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   // ---- a8: list-major scan on the tensor cores
   const size_t max_slots = (size_t)np * max_chunks;
   uint64_t *part, *heap = nullptr;
-  SA_TRY(dalloc(&part, max_slots * FS_LISTS_PER_ITEM * k, s, "ivf partials"));
+  SA_TRY(dalloc(&part, max_slots * parts * k, s, "ivf partials"));
   f.add(part);
-  if (k > FS_KSMEM) {
-    SA_TRY(dalloc(&heap, (size_t)sms * k * FS_EPI_THREADS, s, "ivf heaps"));
+  if (k > (legacy ? FS_KSMEM : IVS_KSMEM)) {
+    SA_TRY(dalloc(&heap, (size_t)sms * k * (legacy ? FS_EPI_THREADS : IVS_HEAPS), s, "ivf heaps"));
     f.add(heap);
   }
   uint32_t* hint;   // [nq] pruning bounds + [1] dynamic item counter
   SA_TRY(dalloc(&hint, nq + 1, s, "ivf hints"));
   f.add(hint);
   SA_CUDA(cudaMemsetAsync(hint, 0, sizeof(uint32_t) * (nq + 1), s), "memset hints");
+  cudaError_t e;
+  if (!legacy) {
+    IvfScanArgs v{};
+    v.Q = Qs;
+    v.d_pad = idx->d_pad;
+    v.k = k;
+    v.row_ids = idx->row_ids;
+    v.part = part;
+    v.heap_g = heap;
+    v.items = w.items;
+    v.n_items = w.n_items;
+    v.list_off = idx->list_off;
+    v.lq_ent = w.lq_ent;
+    v.q_slot = w.q_slot;
+    v.nprobe = nprobe;
+    v.chunk_rows = chunk_rows;
+    v.q_hint = hint;
+    v.item_counter = reinterpret_cast<int32_t*>(hint + nq);
+    prof_begin(SA_KERNEL_IVF_SCAN, s);
+    e = launch_ivf_scan(idx->tmap_x, idx->tmap_xt, v, sms, s);
+    prof_end(SA_KERNEL_IVF_SCAN, s);
+    prof_count(SA_KERNEL_IVF_SCAN);
+    SA_CUDA(e, "ivf scan");
+  } else {
   CUtensorMap tmap_q;
   SA_TRY(make_tmap_bf16(&tmap_q, Qs, nq, idx->d_pad, FS_BM));
   FlatScanArgs a{};
@@ -390,17 +423,18 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   a.q_hint = hint;
   a.item_counter = reinterpret_cast<int32_t*>(hint + nq);
   prof_begin(SA_KERNEL_IVF_SCAN, s);
-  cudaError_t e = launch_flat_scan(idx->tmap_x, idx->tmap_xt, tmap_q, a, 1, sms, s);
+  e = launch_flat_scan(idx->tmap_x, idx->tmap_xt, tmap_q, a, 1, sms, s);
   prof_end(SA_KERNEL_IVF_SCAN, s);
   prof_count(SA_KERNEL_IVF_SCAN);
   SA_CUDA(e, "ivf scan");
+  }
 
   MergeArgs m{};
   m.cand = part;
   m.k = k;
   m.slot_off = w.q_slot;
   m.slot_stride = nprobe;
-  m.slot_keys = FS_LISTS_PER_ITEM * k;
+  m.slot_keys = parts * k;
   m.out_keys = out.keys;
   m.out_ids = out.ids;
   m.out_scores = out.scores;

@@ -366,11 +366,11 @@ __global__ void probe_slots_kernel(const int64_t* __restrict__ probes, int64_t n
 // Per list: work items = query blocks x chunks (0 if unprobed or empty).
 __global__ void list_items_kernel(const int32_t* __restrict__ cnt, int nlist,
                                   const int64_t* __restrict__ list_off, int chunk_rows,
-                                  int64_t* __restrict__ nitems) {
+                                  int qblock, int64_t* __restrict__ nitems) {
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlist; l += gridDim.x * blockDim.x) {
     const int64_t len = list_off[l + 1] - list_off[l];
     const int64_t nch = (len + chunk_rows - 1) / chunk_rows;
-    const int64_t nqb = (cnt[l] + 127) / 128;
+    const int64_t nqb = (cnt[l] + qblock - 1) / qblock;
     nitems[l] = nch * nqb;
   }
 }
@@ -388,18 +388,18 @@ __global__ void probe_fill_kernel(const int64_t* __restrict__ probes, int64_t nq
   }
 }
 __global__ void items_fill_kernel(const int32_t* __restrict__ cnt, int nlist,
-                                  const int64_t* __restrict__ list_off, int chunk_rows,
+                                  const int64_t* __restrict__ list_off, int chunk_rows, int qblock,
                                   const int64_t* __restrict__ lq_off64,
                                   const int64_t* __restrict__ item_off, int4* __restrict__ items,
                                   int32_t* __restrict__ n_items) {
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nlist; l += gridDim.x * blockDim.x) {
     const int64_t len = list_off[l + 1] - list_off[l];
     const int nch = (int)((len + chunk_rows - 1) / chunk_rows);
-    const int nqb = (cnt[l] + 127) / 128;
+    const int nqb = (cnt[l] + qblock - 1) / qblock;
     int64_t o = item_off[l];
     for (int b = 0; b < nqb; ++b) {
-      const int e0 = (int)lq_off64[l] + b * 128;
-      const int c_b = cnt[l] - b * 128 < 128 ? cnt[l] - b * 128 : 128;
+      const int e0 = (int)lq_off64[l] + b * qblock;
+      const int c_b = cnt[l] - b * qblock < qblock ? cnt[l] - b * qblock : qblock;
       for (int c = 0; c < nch; ++c) items[o++] = make_int4(l, e0, c, c_b);
     }
     if (l == nlist - 1) *n_items = (int32_t)item_off[nlist];
@@ -411,7 +411,7 @@ __global__ void items_fill_kernel(const int32_t* __restrict__ cnt, int nlist,
 // per-(query, probe) output slots and the work items -- one launch instead of ~13.
 __global__ void __launch_bounds__(1024)
 invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
-                    const int64_t* __restrict__ list_off, int chunk_rows,
+                    const int64_t* __restrict__ list_off, int chunk_rows, int qblock,
                     int2* __restrict__ lq_ent, int64_t* __restrict__ q_slot,
                     int4* __restrict__ items, int32_t* __restrict__ n_items) {
   extern __shared__ uint64_t ent[];  // [P2] (list << 32 | entry index)
@@ -477,7 +477,7 @@ invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
       while (i + c < n && (uint32_t)(ent[i + c] >> 32) == l) ++c;
       const int64_t len = list_off[l + 1] - list_off[l];
       const int nch = (int)((len + chunk_rows - 1) / chunk_rows);
-      my_items += ((c + 127) / 128) * nch;
+      my_items += ((c + qblock - 1) / qblock) * nch;
     }
   }
   int total_items;
@@ -489,9 +489,10 @@ invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
       while (i + c < n && (uint32_t)(ent[i + c] >> 32) == l) ++c;
       const int64_t len = list_off[l + 1] - list_off[l];
       const int nch = (int)((len + chunk_rows - 1) / chunk_rows);
-      for (int b = 0; b * 128 < c; ++b)
+      for (int b = 0; b * qblock < c; ++b)
         for (int ch = 0; ch < nch; ++ch)
-          items[o++] = make_int4((int)l, i + b * 128, ch, c - b * 128 < 128 ? c - b * 128 : 128);
+          items[o++] = make_int4((int)l, i + b * qblock, ch,
+                                 c - b * qblock < qblock ? c - b * qblock : qblock);
     }
   }
   // output slots per (q, j), original order: chunks of the probed list
@@ -516,11 +517,11 @@ invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
 }
 
 cudaError_t launch_invert_small(const int64_t* probes, int nq, int nprobe, const int64_t* list_off,
-                                int chunk_rows, IvfSearchScratch& w, cudaStream_t s) {
+                                int chunk_rows, int qblock, IvfSearchScratch& w, cudaStream_t s) {
   int P2 = 1;
   while (P2 < nq * nprobe) P2 <<= 1;
   invert_small_kernel<<<1, 1024, P2 * sizeof(uint64_t), s>>>(probes, nq, nprobe, list_off,
-                                                              chunk_rows, w.lq_ent, w.q_slot,
+                                                              chunk_rows, qblock, w.lq_ent, w.q_slot,
                                                               w.items, w.n_items);
   return cudaGetLastError();
 }
@@ -532,8 +533,8 @@ __global__ void i32_to_i64_kernel(const int32_t* __restrict__ in, int64_t n,
 }
 
 cudaError_t launch_probe_invert(const int64_t* probes, int64_t nq, int nprobe, int nlist,
-                                const int64_t* list_off, int chunk_rows, IvfSearchScratch& w,
-                                int num_sms, cudaStream_t s) {
+                                const int64_t* list_off, int chunk_rows, int qblock,
+                                IvfSearchScratch& w, int num_sms, cudaStream_t s) {
   const int64_t n = nq * nprobe;
   unsigned b = (unsigned)((n + 255) / 256);
   if (b > (unsigned)num_sms * 8) b = (unsigned)num_sms * 8;
@@ -547,9 +548,9 @@ cudaError_t launch_probe_invert(const int64_t* probes, int64_t nq, int nprobe, i
   probe_fill_kernel<<<b, 256, 0, s>>>(probes, nq, nprobe, w.lq_off64, w.cursor, w.lq_ent);
   probe_slots_kernel<<<b, 256, 0, s>>>(probes, n, list_off, chunk_rows, w.tmp64b);
   exclusive_scan_i64(w.tmp64b, n, w.q_slot, w.scratch, s);
-  list_items_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, list_off, chunk_rows, w.tmp64);
+  list_items_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, list_off, chunk_rows, qblock, w.tmp64);
   exclusive_scan_i64(w.tmp64, nlist, w.item_off, w.scratch, s);
-  items_fill_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, list_off, chunk_rows, w.lq_off64, w.item_off,
+  items_fill_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, list_off, chunk_rows, qblock, w.lq_off64, w.item_off,
                                        w.items, w.n_items);
   return cudaGetLastError();
 }

@@ -58,10 +58,11 @@ struct IvfSearchScratch {
   int64_t* scratch;    // [ceil(max(nlist, nq*nprobe) / 1024) + 2]
 };
 constexpr int kInvertSmallMax = 4096;  // nq * nprobe handled by one-CTA inversion
+// Work items = (list, block of <= qblock probers, chunk of chunk_rows rows).
 cudaError_t launch_invert_small(const int64_t* probes, int nq, int nprobe, const int64_t* list_off,
-                                int chunk_rows, IvfSearchScratch& w, cudaStream_t s);
+                                int chunk_rows, int qblock, IvfSearchScratch& w, cudaStream_t s);
 cudaError_t launch_probe_invert(const int64_t* probes, int64_t nq, int nprobe, int nlist,
-                                const int64_t* list_off, int chunk_rows, IvfSearchScratch& w,
-                                int num_sms, cudaStream_t s);
+                                const int64_t* list_off, int chunk_rows, int qblock,
+                                IvfSearchScratch& w, int num_sms, cudaStream_t s);
 
 }  // namespace sa

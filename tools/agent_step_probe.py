@@ -30,4 +30,9 @@ for _ in range(50):
     t0 = time.perf_counter()
     idx.search_host(qh, 5, nprobe)
     ts.append(time.perf_counter() - t0)
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_push("agent")
+for _ in range(3):
+    idx.search_host(qh, 5, nprobe)
+torch.cuda.nvtx.range_pop()
 print(f"batch {b} nprobe {nprobe}: p50 {1e3*np.median(ts):.3f} ms  p99 {1e3*np.percentile(ts, 99):.3f} ms")
