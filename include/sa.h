@@ -136,6 +136,47 @@ sa_status sa_comm_free(sa_comm* c);
 const char* sa_status_string(sa_status s);
 const char* sa_last_error(void);
 
+/* ---- non-stall retrieval: IVF search with the maturity exit ----
+ * PAPER.md §3.3 "Non-Stall Retrieval" and App. B.2: the search
+ * watches RQ_t = (d_t - d_best)/(d_worst - d_best) of the newly discovered candidates,
+ * smooths it with an EMA and halts once the EMA exceeds tau AND the LLM engine is ready;
+ * otherwise it stops naturally.  Carried to IVF (readings R14-R19):
+ *   - a step t is one probed list, in probe-rank order (best centroid first);
+ *   - s_t = the best score of list t; after inserting the list into the running top-k R,
+ *     RQ_t = (s_best - s_t) / (s_best - s_worst) over R's first / last entries (1.0 when
+ *     s_best == s_worst or the list is empty; not clamped);
+ *   - EMA_1 = RQ_1, EMA_t = a*RQ_t + (1-a)*EMA_{t-1}, a = 2/(window+1) (fp64);
+ *   - after every check_every lists the device reads *engine_ready; the query stops there
+ *     if EMA_t >= tau and the flag is nonzero, else it goes on, up to nprobe_max lists;
+ *   - the result is R after the last scanned list (score desc, id asc; padded -1/-INF).
+ * The device makes every decision (one captured graph with a conditional WHILE node per
+ * shape); no host round trip sits between stages. */
+typedef struct {
+  double tau;              /* EMA threshold (the paper's HNSW value is 0.9) */
+  int32_t window;          /* EMA window in lists, >= 1 (the paper's is 500 candidates) */
+  int32_t check_every;     /* g >= 1: exit test after every g lists (values > nprobe_max are
+                              clamped to nprobe_max) */
+  const int32_t* engine_ready; /* readiness flag, read by the device at every checkpoint:
+                              pinned HOST memory (cudaHostAlloc / torch pin_memory) or DEVICE
+                              memory; nonzero = the LLM engine is ready for its next step
+                              (P:177).  The caller may change it while the search runs.
+                              NULL = always ready. */
+} sa_maturity_opts;
+/*
+ * queries: DEVICE [nq, d] of qdtype.  out_ids DEVICE int64 [nq, k], out_scores DEVICE fp32
+ * [nq, k], out_lists_scanned DEVICE int32 [nq] (lists scanned per query; may be NULL),
+ * out_rq / out_ema DEVICE fp64 [nq, nprobe_max] per-step signal (NaN past the exit; both
+ * NULL or both set).  Stream-ordered and asynchronous like sa_search.
+ * Limits: unsharded IVF index (SA_ERR_STATE on a flat-only index, SA_ERR_UNSUPPORTED on a
+ * sharded one); nq * min(check_every, nprobe_max) <= 4096 (agent-step batches), else
+ * SA_ERR_UNSUPPORTED.  Per (shape, opts, stream) the library keeps the captured graph and
+ * its buffers (freed with the index); concurrent calls must use different streams.
+ */
+sa_status sa_search_mature(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                           int32_t k, int32_t nprobe_max, const sa_maturity_opts* opts,
+                           int64_t* out_ids, float* out_scores, int32_t* out_lists_scanned,
+                           double* out_rq, double* out_ema, void* stream);
+
 /* ---- introspection (tests); HOST outputs, synchronous ---- */
 sa_status sa_index_info(const sa_index* idx, int64_t* n_local, int32_t* d, int32_t* nlist,
                         int64_t* row_offset);

@@ -73,12 +73,12 @@ def search_query(X_bits: np.ndarray, lists, probe_order, q_bits: np.ndarray, k: 
                  tau: float, window: int, g: int = 1, ready=True):
     """One query.  probe_order: list ids best first (nprobe_max of them).
     ready(t) -> bool (or a constant): is the engine ready at checkpoint t.
-    Returns dict(ids, scores, t_exit, rq [T], ema [T], s_t [T])."""
+    Returns dict(ids, scores, t_exit, rq [T], ema [T], s_t [T], s_best [T], s_worst [T])."""
     q = bf16_to_f64(q_bits)
     R_ids = np.empty(0, dtype=np.int64)
     R_sc = np.empty(0, dtype=np.float64)
     ema = None
-    rqs, emas, sts = [], [], []
+    rqs, emas, sts, sbs, sws = [], [], [], [], []
     t_exit = len(probe_order)
     for t, l in enumerate(probe_order, start=1):
         rows = np.asarray(lists[l], dtype=np.int64)
@@ -91,6 +91,8 @@ def search_query(X_bits: np.ndarray, lists, probe_order, q_bits: np.ndarray, k: 
         else:
             s_t = -math.inf
             r = 1.0
+        sbs.append(float(R_sc[0]) if R_sc.size else -math.inf)
+        sws.append(float(R_sc[-1]) if R_sc.size else -math.inf)
         ema = ema_update(ema, r, window)
         rqs.append(r)
         emas.append(ema)
@@ -104,7 +106,8 @@ def search_query(X_bits: np.ndarray, lists, probe_order, q_bits: np.ndarray, k: 
     ids[:R_ids.size] = R_ids
     sc[:R_sc.size] = R_sc
     return {"ids": ids, "scores": sc, "t_exit": t_exit, "rq": np.array(rqs),
-            "ema": np.array(emas), "s_t": np.array(sts)}
+            "ema": np.array(emas), "s_t": np.array(sts), "s_best": np.array(sbs),
+            "s_worst": np.array(sws)}
 
 
 def search(X_bits, lists, P, Q_bits, k, tau, window, g=1, ready=True):

@@ -45,6 +45,15 @@ class _BuildOpts(ctypes.Structure):
     ]
 
 
+class _MaturityOpts(ctypes.Structure):
+    _fields_ = [
+        ("tau", ctypes.c_double),
+        ("window", ctypes.c_int32),
+        ("check_every", ctypes.c_int32),
+        ("engine_ready", ctypes.c_void_p),
+    ]
+
+
 _lib = None
 
 
@@ -79,6 +88,8 @@ def lib() -> ctypes.CDLL:
         "sa_index_export_centroids": (st, [P, P]),
         "sa_index_export_lists": (st, [P, P, P]),
         "sa_search_probes": (st, [P, P, i64, i32, P, P]),
+        "sa_search_mature": (st, [P, P, ctypes.c_int, i64, i32, i32, ctypes.POINTER(_MaturityOpts),
+                                  P, P, P, P, P, P]),
         "sa_debug_scores": (st, [P, P, i64, P, P]),
         "sa_profile_enable": (st, [i32]),
         "sa_profile_read": (st, [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]),
@@ -252,6 +263,42 @@ class Index:
                                     _ptr(ids), _ptr(scores), _stream_ptr(stream)))
         return ids, scores
 
+    # sa_search_mature: IVF search with the non-stall maturity exit (PAPER §3.3)
+    def search_mature(self, queries: torch.Tensor, k: int, nprobe_max: int, *, tau: float,
+                      window: int, check_every: int = 1, engine_ready: torch.Tensor | None = None,
+                      trace: bool = False, stream=None):
+        """Returns (ids, scores, lists_scanned[, rq, ema]).  engine_ready: an int32 tensor of
+        one element, pinned host (pin_memory()) or CUDA; None = always ready."""
+        if not queries.is_cuda or queries.dim() != 2 or not queries.is_contiguous():
+            raise ValueError("queries must be a contiguous 2-D CUDA tensor")
+        if queries.shape[1] != self.d:
+            raise SAError(SA_ERR_INVALID_ARG, f"queries have d={queries.shape[1]}, index d={self.d}")
+        nq = queries.shape[0]
+        dev = queries.device
+        ids = torch.empty(nq, k, dtype=torch.int64, device=dev)
+        scores = torch.empty(nq, k, dtype=torch.float32, device=dev)
+        t = torch.empty(nq, dtype=torch.int32, device=dev)
+        rq = ema = None
+        if trace:
+            rq = torch.empty(nq, nprobe_max, dtype=torch.float64, device=dev)
+            ema = torch.empty(nq, nprobe_max, dtype=torch.float64, device=dev)
+        o = _MaturityOpts()
+        o.tau = float(tau)
+        o.window = int(window)
+        o.check_every = int(check_every)
+        if engine_ready is not None:
+            if engine_ready.dtype != torch.int32 or engine_ready.numel() < 1 or \
+                    not (engine_ready.is_cuda or engine_ready.is_pinned()):
+                raise ValueError("engine_ready must be an int32 CUDA or pinned host tensor")
+            o.engine_ready = engine_ready.data_ptr()
+        _check(lib().sa_search_mature(self.handle, _ptr(queries), _dtype_code(queries), nq, k,
+                                      nprobe_max, ctypes.byref(o), _ptr(ids), _ptr(scores), _ptr(t),
+                                      _ptr(rq) if trace else None, _ptr(ema) if trace else None,
+                                      _stream_ptr(stream)))
+        if trace:
+            return ids, scores, t, rq, ema
+        return ids, scores, t
+
     def info(self):
         n = ctypes.c_int64()
         d = ctypes.c_int32()
@@ -321,6 +368,10 @@ def sa_search(index: Index, queries, k, nprobe=0, out=None, stream=None):
 
 def sa_search_host(index: Index, queries, k, nprobe=0, out=None, stream=None):
     return index.search_host(queries, k, nprobe, out, stream)
+
+
+def sa_search_mature(index: Index, queries, k, nprobe_max, **kw):
+    return index.search_mature(queries, k, nprobe_max, **kw)
 
 
 def sa_index_free(index: Index):

@@ -32,6 +32,11 @@ struct sa_graph_entry {
   int64_t kernels = 0;
 };
 
+namespace sa {
+struct MaturePlan;
+void free_mature_plan(MaturePlan* p);
+}  // namespace sa
+
 struct sa_index {
   int device = 0;
   int num_sms = 148;
@@ -56,6 +61,8 @@ struct sa_index {
   // captured small-batch searches (host-buffer path), guarded by graph_mu
   std::mutex graph_mu;
   std::vector<sa_graph_entry> graphs;
+  // captured progressive (maturity-exit) searches, guarded by graph_mu (mature.cu)
+  std::vector<std::unique_ptr<sa::MaturePlan, void (*)(sa::MaturePlan*)>> mature_plans;
 };
 
 namespace sa {
@@ -77,7 +84,9 @@ inline void shard_range(int64_t n, int world, int rank, int64_t* off, int64_t* l
   *len = base + (rank < rem ? 1 : 0);
 }
 
-// profiler hooks
+// profiler hooks (no events and no counting while a graph is being captured)
+void set_capturing(bool on);
+void prof_count_n(int kind, int64_t n);
 void prof_count(int kind);
 void prof_begin(int kind, cudaStream_t s);
 void prof_end(int kind, cudaStream_t s);

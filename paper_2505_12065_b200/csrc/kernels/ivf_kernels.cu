@@ -409,6 +409,8 @@ __global__ void items_fill_kernel(const int32_t* __restrict__ cnt, int nlist,
 // Whole inversion in one CTA for small batches (nq * nprobe <= kInvertSmallMax): sort the
 // (list, query, probe rank) entries by list in smem, emit probers grouped by list, the
 // per-(query, probe) output slots and the work items -- one launch instead of ~13.
+// probes[i] < 0 = no list (a finished query of a maturity stage): no items, an empty slot.
+constexpr uint32_t kNoList = 0xFFFFFFFFu;
 __global__ void __launch_bounds__(1024)
 invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
                     const int64_t* __restrict__ list_off, int chunk_rows, int qblock,
@@ -472,7 +474,7 @@ invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
     const uint32_t e = (uint32_t)ent[i];
     lq_ent[i] = make_int2((int)(e / nprobe), (int)(e % nprobe));
     const uint32_t l = (uint32_t)(ent[i] >> 32);
-    if (i == 0 || (uint32_t)(ent[i - 1] >> 32) != l) {
+    if (l != kNoList && (i == 0 || (uint32_t)(ent[i - 1] >> 32) != l)) {
       int c = 1;
       while (i + c < n && (uint32_t)(ent[i + c] >> 32) == l) ++c;
       const int64_t len = list_off[l + 1] - list_off[l];
@@ -484,7 +486,7 @@ invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
   int o = block_scan(my_items, &total_items);
   for (int i = lo; i < hi; ++i) {
     const uint32_t l = (uint32_t)(ent[i] >> 32);
-    if (i == 0 || (uint32_t)(ent[i - 1] >> 32) != l) {
+    if (l != kNoList && (i == 0 || (uint32_t)(ent[i - 1] >> 32) != l)) {
       int c = 1;
       while (i + c < n && (uint32_t)(ent[i + c] >> 32) == l) ++c;
       const int64_t len = list_off[l + 1] - list_off[l];
@@ -499,6 +501,7 @@ invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
   int my_slots = 0;
   for (int i = lo; i < hi; ++i) {
     const int64_t l = probes[i];
+    if (l < 0) continue;  // no list (maturity stages: finished query)
     const int64_t len = list_off[l + 1] - list_off[l];
     my_slots += (int)((len + chunk_rows - 1) / chunk_rows);
   }
@@ -507,6 +510,7 @@ invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
   for (int i = lo; i < hi; ++i) {
     q_slot[i] = so;
     const int64_t l = probes[i];
+    if (l < 0) continue;
     const int64_t len = list_off[l + 1] - list_off[l];
     so += (int)((len + chunk_rows - 1) / chunk_rows);
   }

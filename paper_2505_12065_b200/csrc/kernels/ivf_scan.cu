@@ -290,6 +290,7 @@ ivf_scan_kernel(const __grid_constant__ CUtensorMap tmap_x,
     const int et = ew * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const int k = a.k;
+    const bool use_hint = a.q_hint != nullptr;  // shared pruning bound (off: exact per-item top-k)
     const int col = half * 16 + lane;  // prober owned by this lane (lanes 0..15)
     uint64_t* heap = (k <= IVS_KSMEM)
                          ? heap_s + (ew * 16 + (lane & 15))
@@ -347,7 +348,7 @@ ivf_scan_kernel(const __grid_constant__ CUtensorMap tmap_x,
         const int2 e = a.lq_ent[it.e0 + col];
         q = e.x;
         pj = e.y;
-        const uint32_t h = __ldcg(a.q_hint + q);
+        const uint32_t h = use_hint ? __ldcg(a.q_hint + q) : 0u;
         if (h != 0u) hint = float_from_ordered(h);
       }
       float thr = hint;
@@ -366,7 +367,7 @@ ivf_scan_kernel(const __grid_constant__ CUtensorMap tmap_x,
         if (lane == 0) ptx::mbar_arrive(ptx::smem_u32(&tail->acc_empty[acc]));
         if (++acc == kNAcc) { acc = 0; acc_phase ^= 1; }
         if (ncol <= 0) continue;
-        if (own && (t & 3) == 3) {
+        if (use_hint && own && (t & 3) == 3) {
           const uint32_t h = __ldcg(a.q_hint + q);
           if (h != 0u) {
             hint = fmaxf(hint, float_from_ordered(h));
@@ -399,7 +400,7 @@ ivf_scan_kernel(const __grid_constant__ CUtensorMap tmap_x,
             if (lane == j) {
               const uint64_t root = heap[0];
               const uint32_t o = (uint32_t)(root >> 32);
-              if (root != 0ull && o > published) {
+              if (use_hint && root != 0ull && o > published) {
                 atomicMax(a.q_hint + q, o);
                 published = o;
               }

@@ -28,7 +28,8 @@ struct IvfScanArgs {
   const int64_t* q_slot;   // [nq * nprobe] first output slot of (query, probe rank)
   int32_t nprobe;
   int32_t chunk_rows;      // rows per work item (multiple of IVS_BM)
-  uint32_t* q_hint;        // [nq] ordered-fp32 lower bound of each query's k-th score (zeroed)
+  uint32_t* q_hint;        // [nq] ordered-fp32 lower bound of each query's k-th score (zeroed);
+                           // nullptr: no shared bound (every partial list is its exact top-k)
   int32_t* item_counter;   // zeroed global counter: dynamic item scheduling
 };
 

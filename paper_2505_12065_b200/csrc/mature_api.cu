@@ -1,0 +1,335 @@
+// mature_api.cu -- sa_search_mature: IVF search with the non-stall maturity exit
+// (§3.3 "Non-Stall Retrieval"; App. B.2; SURVEY.md §8(f)1;
+// DESIGN.md §4.5).
+//
+// The whole progressive search is ONE captured CUDA graph per shape:
+//   prologue  cast/pad the queries, probe (tensor-core centroid scores + exact top-nprobe),
+//             init the running results;
+//   WHILE     (a conditional graph node; the device decides when to stop)
+//               stage lists -> one-CTA probe inversion -> ivf_scan_kernel (no shared bound)
+//               -> in-order merge + RQ/EMA + exit test (reads the engine-ready flag)
+//               -> advance (sets the loop condition to 0 once every query has finished)
+//   epilogue  unpack the results.
+// No host round trip decides anything: a query leaves the loop at the first checkpoint where
+// its EMA >= tau while the flag is set, or after nprobe_max lists.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+
+#include "internal.h"
+#include "kernels/ivf_kernels.cuh"
+#include "kernels/ivf_scan.cuh"
+#include "kernels/mature.cuh"
+#include "kernels/merge.cuh"
+
+namespace sa {
+
+struct MaturePlan {
+  // key
+  int64_t nq = 0;
+  int32_t k = 0, nprobe_max = 0, g = 0, window = 0, qdtype = 0;
+  double tau = 0;
+  const int32_t* ready = nullptr;
+  bool trace = false;
+  cudaStream_t stream = nullptr;
+  // buffers
+  void* d_q = nullptr;
+  __nv_bfloat16* Qs = nullptr;
+  float* psc = nullptr;
+  uint64_t* pkeys = nullptr;
+  int64_t* probes = nullptr;
+  int64_t* stage_probes = nullptr;
+  IvfSearchScratch w{};
+  uint64_t* part = nullptr;
+  uint64_t* heap = nullptr;
+  uint64_t* R = nullptr;
+  double* ema = nullptr;
+  int32_t *active = nullptr, *t_done = nullptr, *ctrl = nullptr;
+  double *trace_rq = nullptr, *trace_ema = nullptr;
+  int64_t* out_ids = nullptr;
+  float* out_sc = nullptr;
+  int32_t* out_t = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<void*> allocs;
+};
+
+void free_mature_plan(MaturePlan* p) {
+  if (!p) return;
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  for (void* a : p->allocs) cudaFree(a);
+  delete p;
+}
+
+namespace {
+
+template <typename T>
+sa_status palloc(MaturePlan& p, T** ptr, size_t count, const char* what) {
+  *ptr = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), count * sizeof(T));
+  if (e != cudaSuccess) return cuda_status(e, what);
+  p.allocs.push_back(*ptr);
+  return SA_OK;
+}
+
+#define SA_TRY(expr)              \
+  do {                            \
+    sa_status _st = (expr);       \
+    if (_st != SA_OK) return _st; \
+  } while (0)
+
+struct CaptureFlag {
+  CaptureFlag() { set_capturing(true); }
+  ~CaptureFlag() { set_capturing(false); }
+};
+
+sa_status make_plan(const sa_index* idx, MaturePlan& p) {
+  const int64_t nq = p.nq, P = p.nprobe_max, g = p.g;
+  const int64_t np = nq * g;
+  const int sms = idx->num_sms;
+  const int64_t nq_pad = padded_nq(nq);
+  const size_t qbytes = (size_t)nq * idx->d * (p.qdtype == SA_F32 ? 4 : 2);
+  // work-item size as in ivf_search: ~4 items per SM from the rows one stage probes
+  const int64_t mean_list = std::max<int64_t>(1, idx->n_local / idx->nlist);
+  int64_t want = np * mean_list / (4 * (int64_t)sms);
+  want = (want + IVS_BM - 1) / IVS_BM * IVS_BM;
+  const int chunk_rows = (int)std::min<int64_t>(4096, std::max<int64_t>(256, want));
+  const int64_t max_chunks = std::max<int64_t>(1, (idx->max_list + chunk_rows - 1) / chunk_rows);
+  const size_t max_slots = (size_t)np * max_chunks;
+
+  SA_TRY(palloc(p, reinterpret_cast<uint8_t**>(&p.d_q), qbytes, "mature plan"));
+  SA_TRY(palloc(p, &p.Qs, (size_t)nq_pad * idx->d_pad, "mature plan"));
+  SA_TRY(palloc(p, &p.psc, (size_t)nq * idx->nlist, "mature plan"));
+  SA_TRY(palloc(p, &p.pkeys, (size_t)nq * P, "mature plan"));
+  SA_TRY(palloc(p, &p.probes, (size_t)nq * P, "mature plan"));
+  SA_TRY(palloc(p, &p.stage_probes, (size_t)np, "mature plan"));
+  SA_TRY(palloc(p, &p.w.lq_ent, (size_t)np, "mature plan"));
+  SA_TRY(palloc(p, &p.w.q_slot, (size_t)np + 1, "mature plan"));
+  SA_TRY(palloc(p, &p.w.items, max_slots, "mature plan"));
+  SA_TRY(palloc(p, &p.w.n_items, 1, "mature plan"));
+  SA_TRY(palloc(p, &p.part, max_slots * IVS_PARTS * p.k, "mature partials"));
+  if (p.k > IVS_KSMEM) SA_TRY(palloc(p, &p.heap, (size_t)sms * p.k * IVS_HEAPS, "mature heaps"));
+  SA_TRY(palloc(p, &p.R, (size_t)nq * p.k, "mature plan"));
+  SA_TRY(palloc(p, &p.ema, (size_t)nq, "mature plan"));
+  SA_TRY(palloc(p, &p.active, (size_t)nq, "mature plan"));
+  SA_TRY(palloc(p, &p.t_done, (size_t)nq, "mature plan"));
+  SA_TRY(palloc(p, &p.ctrl, 4, "mature plan"));
+  if (p.trace) {
+    SA_TRY(palloc(p, &p.trace_rq, (size_t)nq * P, "mature plan"));
+    SA_TRY(palloc(p, &p.trace_ema, (size_t)nq * P, "mature plan"));
+  }
+  SA_TRY(palloc(p, &p.out_ids, (size_t)nq * p.k, "mature plan"));
+  SA_TRY(palloc(p, &p.out_sc, (size_t)nq * p.k, "mature plan"));
+  SA_TRY(palloc(p, &p.out_t, (size_t)nq, "mature plan"));
+
+  MatureArgs m{};
+  m.nq = (int32_t)nq;
+  m.k = p.k;
+  m.nprobe_max = p.nprobe_max;
+  m.g = p.g;
+  m.tau = p.tau;
+  m.alpha = 2.0 / ((double)p.window + 1.0);
+  m.ready = p.ready;
+  m.probes = p.probes;
+  m.stage_probes = p.stage_probes;
+  m.q_slot = p.w.q_slot;
+  m.part = p.part;
+  m.parts = IVS_PARTS;
+  m.R = p.R;
+  m.ema = p.ema;
+  m.active = p.active;
+  m.t_done = p.t_done;
+  m.ctrl = p.ctrl;
+  m.trace_rq = p.trace_rq;
+  m.trace_ema = p.trace_ema;
+
+  IvfScanArgs v{};
+  v.Q = p.Qs;
+  v.d_pad = idx->d_pad;
+  v.k = p.k;
+  v.row_ids = idx->row_ids;
+  v.part = p.part;
+  v.heap_g = p.heap;
+  v.items = p.w.items;
+  v.n_items = p.w.n_items;
+  v.list_off = idx->list_off;
+  v.lq_ent = p.w.lq_ent;
+  v.q_slot = p.w.q_slot;
+  v.nprobe = p.g;
+  v.chunk_rows = chunk_rows;
+  v.q_hint = nullptr;  // exact per-(query, list) top-k: RQ needs every list's best score
+  v.item_counter = p.ctrl + 2;
+
+  cudaStream_t cs;
+  SA_TRY(cuda_status(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream"));
+  std::unique_ptr<CUstream_st, cudaError_t (*)(cudaStream_t)> cs_guard(cs, cudaStreamDestroy);
+  cudaGraph_t graph = nullptr;
+  SA_TRY(cuda_status(cudaGraphCreate(&graph, 0), "graph create"));
+  std::unique_ptr<CUgraph_st, cudaError_t (*)(cudaGraph_t)> graph_guard(graph, cudaGraphDestroy);
+  CaptureFlag cap;
+  const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
+
+  // ---- prologue: stage queries, probe, init
+  std::vector<cudaGraphNode_t> tail;
+  {
+    SA_TRY(cuda_status(cudaStreamBeginCaptureToGraph(cs, graph, nullptr, nullptr, 0, mode),
+                       "begin capture"));
+    sa_status st = cuda_status(launch_cast_pad(p.d_q, p.qdtype == SA_F32, nq, idx->d, p.Qs, nq_pad,
+                                               idx->d_pad, sms, cs),
+                               "stage queries");
+    if (st == SA_OK) {
+      const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, idx->nlist, idx->d_pad, nullptr, 0u};
+      st = flat_scores_view(cvc, sms, p.Qs, nq, p.psc, cs);
+    }
+    if (st == SA_OK) {
+      MergeArgs mg{};
+      mg.cand_scores = p.psc;
+      mg.m_flat = idx->nlist;
+      mg.qstride = idx->nlist;
+      mg.k = p.nprobe_max;
+      mg.out_keys = p.pkeys;
+      st = cuda_status(launch_merge(mg, nq, cs), "probe select");
+    }
+    if (st == SA_OK)
+      st = cuda_status(launch_keys_to_lists(p.pkeys, nq * P, p.probes, nullptr, sms, cs),
+                       "probe lists");
+    if (st == SA_OK) st = cuda_status(launch_mature_init(m, cs), "mature init");
+    if (st == SA_OK) {
+      cudaStreamCaptureStatus cst;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      st = cuda_status(cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &nd),
+                       "capture info");
+      if (st == SA_OK) tail.assign(deps, deps + nd);
+    }
+    cudaGraph_t g2 = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &g2);
+    if (st != SA_OK) return st;
+    SA_TRY(cuda_status(e, "end capture (prologue)"));
+  }
+
+  // ---- the WHILE node
+  cudaGraphConditionalHandle handle;
+  SA_TRY(cuda_status(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault),
+                     "conditional handle"));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode;
+  SA_TRY(cuda_status(cudaGraphAddNode(&cnode, graph, tail.data(), tail.size(), &cp),
+                     "conditional node"));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  {
+    SA_TRY(cuda_status(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, mode),
+                       "begin capture (body)"));
+    sa_status st = cuda_status(launch_mature_stage(m, cs), "mature stage");
+    if (st == SA_OK)
+      st = cuda_status(launch_invert_small(p.stage_probes, (int)nq, p.g, idx->list_off, chunk_rows,
+                                           IVS_NQ, p.w, cs),
+                       "stage inversion");
+    if (st == SA_OK)
+      st = cuda_status(launch_ivf_scan(idx->tmap_x, idx->tmap_xt, v, sms, cs), "stage scan");
+    if (st == SA_OK) st = cuda_status(launch_mature_update(m, cs), "mature update");
+    if (st == SA_OK) st = cuda_status(launch_mature_advance(m, handle, cs), "mature advance");
+    cudaGraph_t g2 = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &g2);
+    if (st != SA_OK) return st;
+    SA_TRY(cuda_status(e, "end capture (body)"));
+  }
+
+  // ---- epilogue
+  {
+    SA_TRY(cuda_status(cudaStreamBeginCaptureToGraph(cs, graph, &cnode, nullptr, 1, mode),
+                       "begin capture (epilogue)"));
+    sa_status st = cuda_status(launch_mature_final(m, p.out_ids, p.out_sc, p.out_t, cs),
+                               "mature final");
+    cudaGraph_t g2 = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &g2);
+    if (st != SA_OK) return st;
+    SA_TRY(cuda_status(e, "end capture (epilogue)"));
+  }
+  SA_TRY(cuda_status(cudaGraphInstantiate(&p.exec, graph, 0), "instantiate"));
+  return SA_OK;
+}
+
+}  // namespace
+}  // namespace sa
+
+using namespace sa;
+
+extern "C" sa_status sa_search_mature(const sa_index* idx, const void* queries, sa_dtype qdtype,
+                                      int64_t nq, int32_t k, int32_t nprobe_max,
+                                      const sa_maturity_opts* opts, int64_t* out_ids,
+                                      float* out_scores, int32_t* out_lists_scanned,
+                                      double* out_rq, double* out_ema, void* stream) {
+  if (!idx || !queries || !opts || !out_ids || !out_scores)
+    return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
+  if (nq < 1) return set_error(SA_ERR_INVALID_ARG, "nq must be >= 1");
+  if (k < 1 || k > 256) return set_error(SA_ERR_INVALID_ARG, "k must be in [1, 256]");
+  if (idx->nlist == 0) return set_error(SA_ERR_STATE, "maturity exit needs an IVF index");
+  if (nprobe_max < 1 || nprobe_max > idx->nlist)
+    return set_error(SA_ERR_INVALID_ARG, "nprobe_max must be in [1, nlist]");
+  if (opts->check_every < 1 || opts->window < 1)
+    return set_error(SA_ERR_INVALID_ARG, "check_every and window must be >= 1");
+  if (opts->tau != opts->tau) return set_error(SA_ERR_INVALID_ARG, "tau is NaN");
+  if ((out_rq == nullptr) != (out_ema == nullptr))
+    return set_error(SA_ERR_INVALID_ARG, "out_rq and out_ema go together");
+  const int32_t g = std::min(opts->check_every, nprobe_max);
+  if (nq * (int64_t)g > kInvertSmallMax)
+    return set_error(SA_ERR_UNSUPPORTED, "nq * check_every > 4096 (agent-step batches)");
+  if (idx->comm && idx->comm->world > 1)
+    return set_error(SA_ERR_UNSUPPORTED, "maturity exit on a sharded index");
+  cudaStream_t s = (cudaStream_t)stream;
+  sa_index* mi = const_cast<sa_index*>(idx);
+  std::lock_guard<std::mutex> lock(mi->graph_mu);
+  MaturePlan* p = nullptr;
+  const bool trace = out_rq != nullptr;
+  for (auto& e : mi->mature_plans)
+    if (e->nq == nq && e->k == k && e->nprobe_max == nprobe_max && e->g == g &&
+        e->window == opts->window && e->tau == opts->tau && e->ready == opts->engine_ready &&
+        e->qdtype == (int32_t)qdtype && e->trace == trace && e->stream == s)
+      p = e.get();
+  if (!p) {
+    std::unique_ptr<MaturePlan, void (*)(MaturePlan*)> np(new MaturePlan, free_mature_plan);
+    np->nq = nq;
+    np->k = k;
+    np->nprobe_max = nprobe_max;
+    np->g = g;
+    np->window = opts->window;
+    np->tau = opts->tau;
+    np->ready = opts->engine_ready;
+    np->qdtype = (int32_t)qdtype;
+    np->trace = trace;
+    np->stream = s;
+    sa_status st = make_plan(idx, *np);
+    if (st != SA_OK) return st;
+    p = np.get();
+    mi->mature_plans.push_back(std::move(np));
+  }
+  const size_t qbytes = (size_t)nq * idx->d * (qdtype == SA_F32 ? 4 : 2);
+  sa_status st = cuda_status(cudaMemcpyAsync(p->d_q, queries, qbytes, cudaMemcpyDefault, s),
+                             "queries in");
+  if (st == SA_OK) st = cuda_status(cudaGraphLaunch(p->exec, s), "graph launch");
+  const size_t nk = (size_t)nq * k;
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(out_ids, p->out_ids, nk * 8, cudaMemcpyDefault, s), "ids out");
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(out_scores, p->out_sc, nk * 4, cudaMemcpyDefault, s),
+                     "scores out");
+  if (st == SA_OK && out_lists_scanned)
+    st = cuda_status(cudaMemcpyAsync(out_lists_scanned, p->out_t, (size_t)nq * 4,
+                                     cudaMemcpyDefault, s),
+                     "lists out");
+  if (st == SA_OK && trace) {
+    const size_t nt = (size_t)nq * nprobe_max * 8;
+    st = cuda_status(cudaMemcpyAsync(out_rq, p->trace_rq, nt, cudaMemcpyDefault, s), "trace out");
+    if (st == SA_OK)
+      st = cuda_status(cudaMemcpyAsync(out_ema, p->trace_ema, nt, cudaMemcpyDefault, s),
+                       "trace out");
+  }
+  prof_count_n(SA_KERNEL_OTHER, 7);
+  return st;
+}

@@ -87,12 +87,14 @@ thread_local cudaEvent_t t_open[SA_KERNEL_KINDS];
 thread_local bool t_capturing = false;  // inside a graph capture: no events, no counting
 }  // namespace
 
+void set_capturing(bool on) { t_capturing = on; }
+
 void prof_count(int kind) {
   if (t_capturing) return;
   std::lock_guard<std::mutex> l(g_prof.mu);
   g_prof.launches[kind]++;
 }
-static void prof_count_n(int kind, int64_t n) {
+void prof_count_n(int kind, int64_t n) {
   std::lock_guard<std::mutex> l(g_prof.mu);
   g_prof.launches[kind] += n;
 }

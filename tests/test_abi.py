@@ -45,3 +45,14 @@ def test_header_documents_each_entry_point():
     assert "PAPER.md" in hdr
     for fn in re.findall(r"\b(sa_[a-z_0-9]+)\s*\(", hdr):
         assert fn.startswith("sa_")
+
+
+def test_search_mature_validates_before_device_work(sa):
+    L = sa.lib()
+    buf = ctypes.c_void_p(1)
+    o = sa._MaturityOpts()
+    o.tau, o.window, o.check_every = 0.9, 8, 1
+    assert L.sa_search_mature(None, buf, 0, 1, 10, 8, ctypes.byref(o), buf, buf, None, None, None,
+                              None) == sa.SA_ERR_INVALID_ARG
+    assert L.sa_search_mature(buf, buf, 0, 1, 10, 8, None, buf, buf, None, None, None,
+                              None) == sa.SA_ERR_INVALID_ARG
