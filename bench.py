@@ -198,6 +198,10 @@ def main():
     ap.add_argument("--simulate-world", type=int, default=0,
                     help="one-GPU projection of a W-GPU row-sharded run: time rank 0's shard "
                          "(n/W rows; IVF with the full-corpus centroids) and report per-rank ms")
+    ap.add_argument("--maturity", action="store_true",
+                    help="non-stall maturity exit (PAPER §3.3): recall / lists scanned / latency "
+                         "over (tau, window, check_every) at agent-step batches, against fixed "
+                         "nprobe; engine-flag stop latency; prints one JSON line and exits")
     ap.add_argument("--sweep", action="store_true",
                     help="BASELINE config 4/5 sweep: recall@k vs q/s over nprobe (batch 512 and "
                          "64) and agent-step latency; prints one JSON line and exits")
@@ -304,6 +308,8 @@ def main():
             gi, _ = idx.search(batches[i], k, 0)
             gt[i] = gi.clone()
 
+    if args.maturity:
+        return run_maturity(args, sa, idx, batches, k, nq, d, nlist, n, rank)
     if args.sweep:
         return run_sweep(args, sa, idx, batches, gt, k, nq, d, nlist, n, world, rank, barrier,
                          max_over_ranks, stream)
@@ -448,6 +454,15 @@ def main():
                       "p50_ms": 1e3 * float(np.percentile(ts, 50)),
                       "p99_ms": 1e3 * float(np.percentile(ts, 99))})
     line["agent_step_latency"] = agent
+    # ---- non-stall maturity exit (PAPER §3.3; full grid: bench.py --maturity), batch 1, k=5
+    if use_ivf and nlist >= 128:
+        qs = [batches[i][:1].contiguous() for i in range(args.warmup, min(nb, args.warmup + 16))]
+        gt5 = [idx.search(q, 5, 0)[0] for q in qs]
+        m = mature_point(sa, idx, qs, 5, 128, 3.0, 32, 8, gt5)
+        fx = fixed_point(idx, qs, 5, 64, gt5)
+        st = stop_latency(sa, idx, qs[0], 5, 128, 0.0, 16, 1, 0.0002)
+        line["maturity_exit"] = {"batch": 1, "k": 5, "mature": m, "fixed_nprobe64": fx,
+                                 "engine_flag_stop": st}
     if build_error:
         line["ivf_build_error"] = build_error
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -511,6 +526,92 @@ def run_sweep(args, sa, idx, batches, gt, k, nq, d, nlist, n, world, rank, barri
             out["agent_step"].append({"batch": b, "k": 5, "nprobe": p,
                                       "p50_ms": 1e3 * float(np.percentile(ts, 50)),
                                       "p99_ms": 1e3 * float(np.percentile(ts, 99))})
+    if rank == 0:
+        print(json.dumps(out))
+    idx.free()
+    return 0
+
+
+def mature_point(sa, idx, qs, k, P, tau, window, g, gt, reps=30):
+    """One maturity-exit setting: recall vs exact, mean lists, p50 latency (host wall clock
+    around the call + sync; the graph is captured before timing)."""
+    rec, lists = [], []
+    for q, t in zip(qs, gt):
+        gi, _, gt_ = idx.search_mature(q, k, P, tau=tau, window=window, check_every=g)
+        rec.append(recall_at_k(gi, t))
+        lists.append(gt_.float().mean().item())
+    ts = []
+    for i in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        idx.search_mature(qs[i % len(qs)], k, P, tau=tau, window=window, check_every=g)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    return {"tau": tau, "window": window, "check_every": g, "nprobe_max": P,
+            "recall": float(np.mean(rec)), "mean_lists": float(np.mean(lists)),
+            "p50_ms": 1e3 * float(np.percentile(ts, 50))}
+
+
+def fixed_point(idx, qs, k, p, gt, reps=30):
+    rec = [recall_at_k(idx.search(q, k, p)[0], t) for q, t in zip(qs, gt)]
+    ts = []
+    for i in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        idx.search(qs[i % len(qs)], k, p)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    return {"nprobe": p, "recall": float(np.mean(rec)), "p50_ms": 1e3 * float(np.percentile(ts, 50))}
+
+
+def stop_latency(sa, idx, q, k, P, tau, window, g, delay_s, reps=20):
+    """Non-stall responsiveness: the engine flag is raised delay_s after the search is
+    launched; time from the raise to the results being complete, and lists scanned."""
+    flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+    idx.search_mature(q, k, P, tau=tau, window=window, check_every=g, engine_ready=flag)
+    torch.cuda.synchronize()
+    out, lists = [], []
+    for _ in range(reps):
+        flag[0] = 0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, _, gt_ = idx.search_mature(q, k, P, tau=tau, window=window, check_every=g,
+                                      engine_ready=flag)
+        while time.perf_counter() - t0 < delay_s:
+            pass
+        t1 = time.perf_counter()
+        flag[0] = 1
+        torch.cuda.synchronize()
+        out.append(time.perf_counter() - t1)
+        lists.append(gt_.float().mean().item())
+    return {"flag_after_ms": 1e3 * delay_s, "stop_p50_ms": 1e3 * float(np.percentile(out, 50)),
+            "stop_p99_ms": 1e3 * float(np.percentile(out, 99)), "mean_lists": float(np.mean(lists))}
+
+
+def run_maturity(args, sa, idx, batches, k, nq, d, nlist, n, rank):
+    """Non-stall maturity exit on the C3 IVF index: per agent-step batch,
+    recall@k (vs the exact mode) / mean lists scanned / latency over a (tau, window, g) grid,
+    fixed-nprobe points for the same effort, and the stop latency after the engine flag."""
+    nb = args.warmup + args.steps
+    P = 128
+    out = {"maturity": "non-stall maturity exit on IVF list order (PAPER §3.3, App. B.2)",
+           "n": n, "d": d, "nlist": nlist, "nprobe_max": P, "rows": [], "fixed": [], "stop": []}
+    for b, kk in ((1, 5), (8, 5), (64, 10)):
+        qs = [batches[i][:b].contiguous() for i in range(args.warmup, min(nb, args.warmup + 16))]
+        gt = [idx.search(q, kk, 0)[0] for q in qs]
+        for (tau, window, g) in ((0.9, 8, 1), (2.0, 16, 1), (2.0, 16, 4), (3.0, 16, 4),
+                                 (2.0, 32, 8), (3.0, 32, 8)):
+            r = mature_point(sa, idx, qs, kk, P, tau, window, g, gt)
+            r.update(batch=b, k=kk)
+            out["rows"].append(r)
+        for p in (8, 16, 32, 48, 64, 96, 128):
+            r = fixed_point(idx, qs, kk, p, gt)
+            r.update(batch=b, k=kk)
+            out["fixed"].append(r)
+        for delay in (0.0, 0.0002, 0.001):
+            r = stop_latency(sa, idx, qs[0], kk, P, 0.0, 16, 1, delay)
+            r.update(batch=b, k=kk, check_every=1)
+            out["stop"].append(r)
     if rank == 0:
         print(json.dumps(out))
     idx.free()

@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(1024)
 invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
                     const int64_t* __restrict__ list_off, int chunk_rows, int qblock,
                     int2* __restrict__ lq_ent, int64_t* __restrict__ q_slot,
-                    int4* __restrict__ items, int32_t* __restrict__ n_items) {
+                    int4* __restrict__ items, int32_t* __restrict__ n_items, StageSrc src) {
   extern __shared__ uint64_t ent[];  // [P2] (list << 32 | entry index)
   __shared__ int wtot[32];
   __shared__ int s_total;
@@ -424,6 +424,17 @@ invert_small_kernel(const int64_t* __restrict__ probes, int nq, int nprobe,
   while (P2 < n) P2 <<= 1;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5;
+  if (src.probes_full) {
+    // maturity stage: entry (q, j) probes rank stage*nprobe + j of a still-active query
+    const int stage = src.ctrl[0];
+    int64_t* sp = const_cast<int64_t*>(probes);
+    for (int i = tid; i < n; i += nt) {
+      const int q = i / nprobe, r = stage * nprobe + i % nprobe;
+      sp[i] = (src.active[q] && r < src.P) ? src.probes_full[(int64_t)q * src.P + r] : -1;
+    }
+    if (tid == 0) *src.item_counter = 0;
+    __syncthreads();
+  }
   for (int i = tid; i < P2; i += nt)
     ent[i] = i < n ? (((uint64_t)(uint32_t)probes[i] << 32) | (uint32_t)i) : ~0ull;
   __syncthreads();
@@ -526,7 +537,18 @@ cudaError_t launch_invert_small(const int64_t* probes, int nq, int nprobe, const
   while (P2 < nq * nprobe) P2 <<= 1;
   invert_small_kernel<<<1, 1024, P2 * sizeof(uint64_t), s>>>(probes, nq, nprobe, list_off,
                                                               chunk_rows, qblock, w.lq_ent, w.q_slot,
-                                                              w.items, w.n_items);
+                                                              w.items, w.n_items, StageSrc{});
+  return cudaGetLastError();
+}
+
+cudaError_t launch_invert_stage(int64_t* stage_probes, int nq, int g, const StageSrc& src,
+                                const int64_t* list_off, int chunk_rows, int qblock,
+                                IvfSearchScratch& w, cudaStream_t s) {
+  int P2 = 1;
+  while (P2 < nq * g) P2 <<= 1;
+  invert_small_kernel<<<1, 1024, P2 * sizeof(uint64_t), s>>>(stage_probes, nq, g, list_off,
+                                                              chunk_rows, qblock, w.lq_ent, w.q_slot,
+                                                              w.items, w.n_items, src);
   return cudaGetLastError();
 }
 __global__ void i32_to_i64_kernel(const int32_t* __restrict__ in, int64_t n,

@@ -61,6 +61,19 @@ constexpr int kInvertSmallMax = 4096;  // nq * nprobe handled by one-CTA inversi
 // Work items = (list, block of <= qblock probers, chunk of chunk_rows rows).
 cudaError_t launch_invert_small(const int64_t* probes, int nq, int nprobe, const int64_t* list_off,
                                 int chunk_rows, int qblock, IvfSearchScratch& w, cudaStream_t s);
+// Maturity stages (mature.cu): the inversion computes its own probe table -- entry (q, j) of
+// stage s = ctrl[0] probes list probes_full[q, s*g + j] if active[q] and s*g + j < P, else none
+// (-1) -- into `stage_probes`, and zeroes the scan's item counter.
+struct StageSrc {
+  const int64_t* probes_full = nullptr;  // [nq, P] probe order
+  int32_t P = 0;
+  const int32_t* ctrl = nullptr;         // [0] = stage
+  const int32_t* active = nullptr;       // [nq]
+  int32_t* item_counter = nullptr;
+};
+cudaError_t launch_invert_stage(int64_t* stage_probes, int nq, int g, const StageSrc& src,
+                                const int64_t* list_off, int chunk_rows, int qblock,
+                                IvfSearchScratch& w, cudaStream_t s);
 cudaError_t launch_probe_invert(const int64_t* probes, int64_t nq, int nprobe, int nlist,
                                 const int64_t* list_off, int chunk_rows, int qblock,
                                 IvfSearchScratch& w, int num_sms, cudaStream_t s);

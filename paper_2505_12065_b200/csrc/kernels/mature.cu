@@ -54,19 +54,8 @@ __global__ void mature_init_kernel(MatureArgs a) {
     a.ctrl[0] = 0;
     a.ctrl[1] = a.nq;
     a.ctrl[2] = 0;
+    a.ctrl[3] = 0;
   }
-}
-
-__global__ void mature_stage_kernel(MatureArgs a) {
-  const int s = a.ctrl[0];
-  const int64_t n = (int64_t)a.nq * a.g;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = i / a.g;
-    const int r = s * a.g + (int)(i % a.g);
-    a.stage_probes[i] = (a.active[q] && r < a.nprobe_max) ? a.probes[q * a.nprobe_max + r] : -1;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.ctrl[2] = 0;
 }
 
 // Bitonic sort of buf[0, n2) descending (n2 a power of two), whole block.
@@ -88,13 +77,36 @@ __device__ void sort_desc(uint64_t* buf, int n2) {
     }
 }
 
+// The last CTA of the update advances the stage and sets the WHILE condition.
+__device__ void advance(const MatureArgs& a, cudaGraphConditionalHandle h) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&a.ctrl[3], 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    a.ctrl[3] = 0;
+    const int s = a.ctrl[0] + 1;
+    a.ctrl[0] = s;
+    const bool more = atomicAdd(&a.ctrl[1], 0) > 0 && (int64_t)s * a.g < a.nprobe_max;
+    cudaGraphSetConditional(h, more ? 1u : 0u);
+  }
+}
+
 // One CTA per query: the stage's lists in probe-rank order.
-__global__ void __launch_bounds__(kUpdThreads) mature_update_kernel(MatureArgs a) {
+__global__ void __launch_bounds__(kUpdThreads)
+mature_update_kernel(MatureArgs a, cudaGraphConditionalHandle h) {
   extern __shared__ uint64_t buf[];  // [pow2 >= k + kCandBlock]
   __shared__ int s_cnt;
   __shared__ unsigned long long s_max;
   const int q = blockIdx.x;
-  if (!a.active[q]) return;
+  if (!a.active[q]) {
+    advance(a, h);
+    return;
+  }
   const int s = a.ctrl[0];
   const int k = a.k;
   uint64_t* Rq = a.R + (size_t)q * k;
@@ -166,13 +178,7 @@ __global__ void __launch_bounds__(kUpdThreads) mature_update_kernel(MatureArgs a
       atomicSub(&a.ctrl[1], 1);
     }
   }
-}
-
-__global__ void mature_advance_kernel(MatureArgs a, cudaGraphConditionalHandle h) {
-  const int s = a.ctrl[0] + 1;
-  a.ctrl[0] = s;
-  const bool more = a.ctrl[1] > 0 && (int64_t)s * a.g < a.nprobe_max;
-  cudaGraphSetConditional(h, more ? 1u : 0u);
+  advance(a, h);
 }
 
 __global__ void mature_final_kernel(MatureArgs a, int64_t* out_ids, float* out_scores,
@@ -204,12 +210,8 @@ cudaError_t launch_mature_init(const MatureArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_mature_stage(const MatureArgs& a, cudaStream_t s) {
-  mature_stage_kernel<<<blocks_for((int64_t)a.nq * a.g), 256, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_mature_update(const MatureArgs& a, cudaStream_t s) {
+cudaError_t launch_mature_update(const MatureArgs& a, cudaGraphConditionalHandle h,
+                                 cudaStream_t s) {
   int n2 = 1;
   while (n2 < a.k + kCandBlock) n2 <<= 1;
   const size_t smem = (size_t)n2 * sizeof(uint64_t);
@@ -220,13 +222,7 @@ cudaError_t launch_mature_update(const MatureArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     set = true;
   }
-  mature_update_kernel<<<a.nq, kUpdThreads, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_mature_advance(const MatureArgs& a, cudaGraphConditionalHandle h,
-                                  cudaStream_t s) {
-  mature_advance_kernel<<<1, 1, 0, s>>>(a, h);
+  mature_update_kernel<<<a.nq, kUpdThreads, smem, s>>>(a, h);
   return cudaGetLastError();
 }
 

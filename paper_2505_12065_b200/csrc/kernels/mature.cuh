@@ -22,19 +22,17 @@ struct MatureArgs {
   double* ema;                   // [nq]
   int32_t* active;               // [nq] 1 while the query is still searching
   int32_t* t_done;               // [nq] lists scanned when the query finished
-  int32_t* ctrl;                 // [0] stage, [1] active queries, [2] ivf_scan item counter
+  int32_t* ctrl;                 // [0] stage, [1] active queries, [2] ivf_scan item counter,
+                                 // [3] update CTAs done
   double* trace_rq;              // optional [nq, nprobe_max] RQ_t (NaN when not scanned)
   double* trace_ema;             // optional [nq, nprobe_max] EMA_t
 };
 
 cudaError_t launch_mature_init(const MatureArgs& a, cudaStream_t s);
-// stage_probes for the current stage + zero the scan's item counter
-cudaError_t launch_mature_stage(const MatureArgs& a, cudaStream_t s);
-// merge the stage's partial lists into R list by list, RQ/EMA, exit decisions
-cudaError_t launch_mature_update(const MatureArgs& a, cudaStream_t s);
-// next stage; sets the WHILE condition of the enclosing graph (0 = all queries finished)
-cudaError_t launch_mature_advance(const MatureArgs& a, cudaGraphConditionalHandle h,
-                                  cudaStream_t s);
+// merge the stage's partial lists into R list by list, RQ/EMA, exit decisions; the last CTA
+// advances the stage and sets the WHILE condition h (0 = every query finished)
+cudaError_t launch_mature_update(const MatureArgs& a, cudaGraphConditionalHandle h,
+                                 cudaStream_t s);
 // R -> out_ids int64 [nq, k] / out_scores fp32 [nq, k] (padded -1 / -inf), t_done -> out_t
 cudaError_t launch_mature_final(const MatureArgs& a, int64_t* out_ids, float* out_scores,
                                 int32_t* out_t, cudaStream_t s);

@@ -6,9 +6,10 @@
 //   prologue  cast/pad the queries, probe (tensor-core centroid scores + exact top-nprobe),
 //             init the running results;
 //   WHILE     (a conditional graph node; the device decides when to stop)
-//               stage lists -> one-CTA probe inversion -> ivf_scan_kernel (no shared bound)
-//               -> in-order merge + RQ/EMA + exit test (reads the engine-ready flag)
-//               -> advance (sets the loop condition to 0 once every query has finished)
+//               one-CTA stage lists + probe inversion -> ivf_scan_kernel (no shared bound,
+//               grid sized to the stage) -> in-order merge + RQ/EMA + exit test (reads the
+//               engine-ready flag); its last CTA advances the stage and sets the loop
+//               condition to 0 once every query has finished
 //   epilogue  unpack the results.
 // No host round trip decides anything: a query leaves the loop at the first checkpoint where
 // its EMA >= tau while the flag is set, or after nprobe_max lists.
@@ -96,6 +97,10 @@ sa_status make_plan(const sa_index* idx, MaturePlan& p) {
   const int chunk_rows = (int)std::min<int64_t>(4096, std::max<int64_t>(256, want));
   const int64_t max_chunks = std::max<int64_t>(1, (idx->max_list + chunk_rows - 1) / chunk_rows);
   const size_t max_slots = (size_t)np * max_chunks;
+  // a stage probes ~np lists of ~mean_list rows: a grid of ~2 CTAs per expected work item
+  // (items are taken dynamically, so any grid is correct; a small one launches faster)
+  const int64_t exp_items = np * ((mean_list + chunk_rows - 1) / chunk_rows);
+  const int scan_grid = (int)std::max<int64_t>(8, std::min<int64_t>(sms, 2 * exp_items));
 
   SA_TRY(palloc(p, reinterpret_cast<uint8_t**>(&p.d_q), qbytes, "mature plan"));
   SA_TRY(palloc(p, &p.Qs, (size_t)nq_pad * idx->d_pad, "mature plan"));
@@ -113,7 +118,7 @@ sa_status make_plan(const sa_index* idx, MaturePlan& p) {
   SA_TRY(palloc(p, &p.ema, (size_t)nq, "mature plan"));
   SA_TRY(palloc(p, &p.active, (size_t)nq, "mature plan"));
   SA_TRY(palloc(p, &p.t_done, (size_t)nq, "mature plan"));
-  SA_TRY(palloc(p, &p.ctrl, 4, "mature plan"));
+  SA_TRY(palloc(p, &p.ctrl, 4, "mature plan"));  // stage, active, item counter, update CTAs
   if (p.trace) {
     SA_TRY(palloc(p, &p.trace_rq, (size_t)nq * P, "mature plan"));
     SA_TRY(palloc(p, &p.trace_ema, (size_t)nq * P, "mature plan"));
@@ -224,15 +229,18 @@ sa_status make_plan(const sa_index* idx, MaturePlan& p) {
   {
     SA_TRY(cuda_status(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, mode),
                        "begin capture (body)"));
-    sa_status st = cuda_status(launch_mature_stage(m, cs), "mature stage");
+    StageSrc src;
+    src.probes_full = p.probes;
+    src.P = p.nprobe_max;
+    src.ctrl = p.ctrl;
+    src.active = p.active;
+    src.item_counter = p.ctrl + 2;
+    sa_status st = cuda_status(launch_invert_stage(p.stage_probes, (int)nq, p.g, src,
+                                                   idx->list_off, chunk_rows, IVS_NQ, p.w, cs),
+                               "stage inversion");
     if (st == SA_OK)
-      st = cuda_status(launch_invert_small(p.stage_probes, (int)nq, p.g, idx->list_off, chunk_rows,
-                                           IVS_NQ, p.w, cs),
-                       "stage inversion");
-    if (st == SA_OK)
-      st = cuda_status(launch_ivf_scan(idx->tmap_x, idx->tmap_xt, v, sms, cs), "stage scan");
-    if (st == SA_OK) st = cuda_status(launch_mature_update(m, cs), "mature update");
-    if (st == SA_OK) st = cuda_status(launch_mature_advance(m, handle, cs), "mature advance");
+      st = cuda_status(launch_ivf_scan(idx->tmap_x, idx->tmap_xt, v, scan_grid, cs), "stage scan");
+    if (st == SA_OK) st = cuda_status(launch_mature_update(m, handle, cs), "mature update");
     cudaGraph_t g2 = nullptr;
     cudaError_t e = cudaStreamEndCapture(cs, &g2);
     if (st != SA_OK) return st;
