@@ -177,6 +177,49 @@ sa_status sa_search_mature(const sa_index* idx, const void* queries, sa_dtype qd
                            int64_t* out_ids, float* out_scores, int32_t* out_lists_scanned,
                            double* out_rq, double* out_ema, void* stream);
 
+/* ---- agent loop support (Alg. 1, App. A.1) ---- */
+
+/*
+ * Priority scheduling (§3.2, Eq. 1-2): orders the engine's n waiting
+ * sequences.  Per sequence i (HOST arrays, length n): R[i] = retrievals completed, W_us[i] =
+ * microseconds since the request first arrived, C[i] = context length in tokens, Wcur_us[i] =
+ * microseconds since the current sequence became ready, ids[i] = request id.  With min/max
+ * over these n sequences (reading R20), Eq. 1 thresholds T_{M,k} = min(M) + (k/G)(max(M) -
+ * min(M)) and Eq. 2 level_i = the largest k with R_i > T_{R,k} or W_i > T_{W,k} or C_i >
+ * T_{C,k} (0 if none; evaluated exactly in integers).  out_order (HOST int64 [n]) receives
+ * the input positions in execution order: level descending, Wcur descending, id ascending
+ * (R21); out_level (HOST int32 [n], may be NULL) the levels.  Metrics must lie in [0, 2^50]
+ * and G >= 1 (the paper uses G = 6), else SA_ERR_INVALID_ARG.  Host only, synchronous.
+ */
+sa_status sa_priority_order(int64_t n, const int64_t* R, const int64_t* W_us, const int64_t* C,
+                            const int64_t* Wcur_us, const int64_t* ids, int32_t G,
+                            int32_t* out_level, int64_t* out_order);
+
+/*
+ * Asynchronous retrieval tasks (Alg. 1: LaunchAsyncRetrievalTask, ActiveSearchTasks,
+ * CheckExternalNonStallSignal, getResult).  A retriever owns `streams` CUDA
+ * streams, a pinned engine-ready flag and `slots` task slots with pinned staging buffers for
+ * up to max_nq queries of d = the index's d.  submit copies fp32 HOST queries [nq, d] into a
+ * slot and enqueues H2D + search + D2H on the next stream without blocking: nprobe_max = 0 ->
+ * exact search; mature = 0 -> fixed-nprobe IVF (sa_search); mature = 1 -> maturity exit
+ * (sa_search_mature with *opts and the retriever's flag).  poll never blocks; result copies
+ * a finished task's ids int64 [nq, k] / scores fp32 [nq, k] / lists scanned int32 [nq] (may
+ * be NULL) to HOST memory and frees the slot.  set_engine_ready writes the flag every running
+ * maturity search reads at its checkpoints.  Errors: SA_ERR_STATE when no slot is free
+ * (submit) or the task is unknown / not finished (result); SA_ERR_INVALID_ARG on bad sizes.
+ */
+typedef struct sa_retriever sa_retriever;
+sa_status sa_retriever_create(const sa_index* idx, int32_t streams, int32_t slots, int32_t max_nq,
+                              int32_t max_k, sa_retriever** out);
+sa_status sa_retriever_submit(sa_retriever* r, const float* queries_host, int32_t nq, int32_t k,
+                              int32_t nprobe_max, int32_t mature, const sa_maturity_opts* opts,
+                              int64_t* task_id);
+sa_status sa_retriever_poll(sa_retriever* r, int64_t task_id, int32_t* done);
+sa_status sa_retriever_result(sa_retriever* r, int64_t task_id, int64_t* ids_host,
+                              float* scores_host, int32_t* lists_host);
+sa_status sa_retriever_set_engine_ready(sa_retriever* r, int32_t ready);
+sa_status sa_retriever_free(sa_retriever* r);
+
 /* ---- introspection (tests); HOST outputs, synchronous ---- */
 sa_status sa_index_info(const sa_index* idx, int64_t* n_local, int32_t* d, int32_t* nlist,
                         int64_t* row_offset);

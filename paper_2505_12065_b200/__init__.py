@@ -88,6 +88,14 @@ def lib() -> ctypes.CDLL:
         "sa_index_export_centroids": (st, [P, P]),
         "sa_index_export_lists": (st, [P, P, P]),
         "sa_search_probes": (st, [P, P, i64, i32, P, P]),
+        "sa_priority_order": (st, [i64, P, P, P, P, P, i32, P, P]),
+        "sa_retriever_create": (st, [P, i32, i32, i32, i32, ctypes.POINTER(P)]),
+        "sa_retriever_submit": (st, [P, P, i32, i32, i32, i32, ctypes.POINTER(_MaturityOpts),
+                                     ctypes.POINTER(i64)]),
+        "sa_retriever_poll": (st, [P, i64, ctypes.POINTER(i32)]),
+        "sa_retriever_result": (st, [P, i64, P, P, P]),
+        "sa_retriever_set_engine_ready": (st, [P, i32]),
+        "sa_retriever_free": (st, [P]),
         "sa_search_mature": (st, [P, P, ctypes.c_int, i64, i32, i32, ctypes.POINTER(_MaturityOpts),
                                   P, P, P, P, P, P]),
         "sa_debug_scores": (st, [P, P, i64, P, P]),
@@ -372,6 +380,73 @@ def sa_search_host(index: Index, queries, k, nprobe=0, out=None, stream=None):
 
 def sa_search_mature(index: Index, queries, k, nprobe_max, **kw):
     return index.search_mature(queries, k, nprobe_max, **kw)
+
+
+def sa_priority_order(R, W_us, C, Wcur_us, ids, G: int = 6):
+    """PAPER §3.2 Eq. 1-2 priority order of waiting sequences (host).  Returns (order as
+    input positions, levels)."""
+    arrs = [np.ascontiguousarray(a, dtype=np.int64) for a in (R, W_us, C, Wcur_us, ids)]
+    n = arrs[0].shape[0]
+    lv = np.empty(n, dtype=np.int32)
+    order = np.empty(n, dtype=np.int64)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    _check(lib().sa_priority_order(n, *[ptr(a) for a in arrs], G, ptr(lv), ptr(order)))
+    return order, lv
+
+
+class Retriever:
+    """Asynchronous retrieval tasks (Alg. 1 LaunchAsyncRetrievalTask / getResult) over an
+    index: submit() never blocks; poll() is an event query; result() copies out."""
+
+    def __init__(self, index: Index, streams: int = 1, slots: int = 8, max_nq: int = 64,
+                 max_k: int = 16):
+        self.index = index
+        self.max_k = max_k
+        h = ctypes.c_void_p()
+        _check(lib().sa_retriever_create(index.handle, streams, slots, max_nq, max_k,
+                                         ctypes.byref(h)))
+        self.handle = h
+        self._shape = {}
+
+    def submit(self, queries: np.ndarray, k: int, nprobe_max: int, *, mature: bool = False,
+               tau: float = 0.0, window: int = 1, check_every: int = 1) -> int:
+        q = np.ascontiguousarray(queries, dtype=np.float32)
+        o = _MaturityOpts()
+        o.tau, o.window, o.check_every = float(tau), int(window), int(check_every)
+        t = ctypes.c_int64()
+        _check(lib().sa_retriever_submit(self.handle, q.ctypes.data_as(ctypes.c_void_p),
+                                         q.shape[0], k, nprobe_max, int(mature), ctypes.byref(o),
+                                         ctypes.byref(t)))
+        self._shape[t.value] = (q.shape[0], k)
+        return t.value
+
+    def poll(self, task: int) -> bool:
+        done = ctypes.c_int32()
+        _check(lib().sa_retriever_poll(self.handle, task, ctypes.byref(done)))
+        return bool(done.value)
+
+    def result(self, task: int):
+        nq, k = self._shape.pop(task)
+        ids = np.empty((nq, k), dtype=np.int64)
+        sc = np.empty((nq, k), dtype=np.float32)
+        lists = np.empty(nq, dtype=np.int32)
+        ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        _check(lib().sa_retriever_result(self.handle, task, ptr(ids), ptr(sc), ptr(lists)))
+        return ids, sc, lists
+
+    def set_engine_ready(self, ready: bool):
+        _check(lib().sa_retriever_set_engine_ready(self.handle, int(bool(ready))))
+
+    def free(self):
+        if self.handle:
+            lib().sa_retriever_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def sa_index_free(index: Index):

@@ -25,7 +25,8 @@ PER_FILE_FLAGS = {"flat_scan.cu": ["-maxrregcount=200"]}
 
 
 def sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "kernels", "*.cu")))
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp"))
+                  + glob.glob(os.path.join(CSRC, "kernels", "*.cu")))
 
 
 def headers():
