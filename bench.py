@@ -455,7 +455,7 @@ def main():
                       "p99_ms": 1e3 * float(np.percentile(ts, 99))})
     line["agent_step_latency"] = agent
     # ---- non-stall maturity exit (PAPER §3.3; full grid: bench.py --maturity), batch 1, k=5
-    if use_ivf and nlist >= 128:
+    if use_ivf and nlist >= 128 and world == 1:   # maturity exit: unsharded indexes only
         qs = [batches[i][:1].contiguous() for i in range(args.warmup, min(nb, args.warmup + 16))]
         gt5 = [idx.search(q, 5, 0)[0] for q in qs]
         m = mature_point(sa, idx, qs, 5, 128, 3.0, 32, 8, gt5)
