@@ -1,0 +1,152 @@
+"""oracle/graph.py -- TEST INFRASTRUCTURE ONLY.  Proximity-graph ANN (build + beam search),
+step by step.
+
+The paper's retriever is a graph index (HNSW, §2, App. B.3) whose
+"search range" (efSearch) trades recall for effort (§2.2.1).  SURVEY.md §8(f)3 asks
+for a GPU graph index with that knob.  The build follows the rank-based recipe of GPU graph
+indexes (an approximate kNN graph, detour-count pruning, reverse edges); the search is
+best-first beam search over a candidate list of size L (the search range).  Readings
+(R22-R27), in order:
+
+  R22  knn(i): the K best rows by inner product (score desc, id asc) among the candidates
+       of row i, excluding i itself (candidates: every row, or a given set such as the
+       union of i's probed IVF lists);
+  R23  detour(i, j) for the neighbour c_j at 0-based rank j of knn(i):
+           #{ k < j : c_j occurs in knn(c_k) at a 0-based rank r < j };
+  R24  fwd(i): knn(i) reordered by (detour asc, rank asc), first R entries;
+  R25  rev(c): every (p, i) with fwd(i)[p] == c, ordered by (p asc, i asc);
+  R26  nbr(c): the first R/2 entries of fwd(c); then rev(c) ids not yet present, in order,
+       up to R; then the remaining fwd(c) entries not yet present, up to R;
+  R27  search(q, L, w, E, T): the list holds at most L (score, id) entries in c1 order with
+       an "expanded" mark; the visited set starts as the entry ids; entries are scored and
+       the list is the top-L of them.  Repeat at most T times: take the first w unexpanded
+       list entries (stop if there are none), mark them expanded, collect their neighbours
+       not yet visited (mark visited), score them and keep the top-L of list + new ones.
+       Result: the first k list entries, padded (-1, -inf).
+
+Scores are fp64 dot products of the stored bf16 values (numpy matmul as a library step).
+Graph-building steps R23-R26 are integer logic on the kNN lists.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import bf16_to_f64
+
+
+def knn(X_bits: np.ndarray, K: int, candidates=None) -> np.ndarray:
+    """R22.  Returns int64 [n, K] (padded -1 when fewer than K candidates)."""
+    X = bf16_to_f64(X_bits)
+    n = X.shape[0]
+    out = np.full((n, K), -1, dtype=np.int64)
+    for i in range(n):
+        cand = np.arange(n) if candidates is None else np.asarray(candidates[i], dtype=np.int64)
+        cand = cand[cand != i]
+        s = X[cand] @ X[i]
+        order = np.lexsort((cand, -s))[:K]
+        out[i, :order.size] = cand[order]
+    return out
+
+
+def prune(knn_lists: np.ndarray, R: int) -> np.ndarray:
+    """R23 + R24.  knn_lists int64 [n, K] (-1 padded) -> fwd int64 [n, R] (-1 padded)."""
+    n, K = knn_lists.shape
+    rank_of = [dict() for _ in range(n)]
+    for i in range(n):
+        for r, c in enumerate(knn_lists[i]):
+            if c >= 0:
+                rank_of[i][int(c)] = r
+    fwd = np.full((n, R), -1, dtype=np.int64)
+    for i in range(n):
+        lst = [int(c) for c in knn_lists[i] if c >= 0]
+        det = []
+        for j, cj in enumerate(lst):
+            cnt = 0
+            for k in range(j):
+                r = rank_of[lst[k]].get(cj)
+                if r is not None and r < j:
+                    cnt += 1
+            det.append((cnt, j, cj))
+        det.sort()
+        keep = [c for _, _, c in det[:R]]
+        fwd[i, :len(keep)] = keep
+    return fwd
+
+
+def reverse_merge(fwd: np.ndarray) -> np.ndarray:
+    """R25 + R26.  fwd int64 [n, R] -> final neighbour lists int64 [n, R] (-1 padded)."""
+    n, R = fwd.shape
+    rev = [[] for _ in range(n)]
+    for i in range(n):
+        for p, c in enumerate(fwd[i]):
+            if c >= 0:
+                rev[int(c)].append((p, i))
+    out = np.full((n, R), -1, dtype=np.int64)
+    for c in range(n):
+        f = [int(x) for x in fwd[c] if x >= 0]
+        lst = f[:R // 2]
+        seen = set(lst)
+        for _, i in sorted(rev[c]):
+            if len(lst) >= R:
+                break
+            if i not in seen:
+                lst.append(i)
+                seen.add(i)
+        for x in f[R // 2:]:
+            if len(lst) >= R:
+                break
+            if x not in seen:
+                lst.append(x)
+                seen.add(x)
+        out[c, :len(lst)] = lst
+    return out
+
+
+def build(X_bits: np.ndarray, K: int, R: int, candidates=None):
+    kn = knn(X_bits, K, candidates)
+    return reverse_merge(prune(kn, R)), kn
+
+
+def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: int, w: int,
+           entries, T: int):
+    """R27 for one query.  Returns dict(ids, scores, expanded, iterations)."""
+    X = bf16_to_f64(X_bits)
+    q = bf16_to_f64(q_bits)
+    visited = set()
+    ent = []
+    for e in entries:
+        if e >= 0 and e not in visited:
+            visited.add(int(e))
+            ent.append(int(e))
+    ids = np.array(ent, dtype=np.int64)
+    sc = X[ids] @ q if ids.size else np.empty(0)
+    order = np.lexsort((ids, -sc))[:L]
+    lst = [[float(sc[o]), int(ids[o]), False] for o in order]
+    it = 0
+    expanded = 0
+    while it < T:
+        pick = [e for e in lst if not e[2]][:w]
+        if not pick:
+            break
+        it += 1
+        new = []
+        for e in pick:
+            e[2] = True
+            expanded += 1
+            for c in nbr[e[1]]:
+                c = int(c)
+                if c >= 0 and c not in visited:
+                    visited.add(c)
+                    new.append(c)
+        if new:
+            nid = np.array(new, dtype=np.int64)
+            ns = X[nid] @ q
+            allv = lst + [[float(s), int(i), False] for s, i in zip(ns, nid)]
+            allv.sort(key=lambda e: (-e[0], e[1]))
+            lst = allv[:L]
+    out_ids = np.full(k, -1, dtype=np.int64)
+    out_sc = np.full(k, -np.inf)
+    for j, e in enumerate(lst[:k]):
+        out_ids[j] = e[1]
+        out_sc[j] = e[0]
+    return {"ids": out_ids, "scores": out_sc, "expanded": expanded, "iterations": it}
