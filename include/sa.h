@@ -177,6 +177,40 @@ sa_status sa_search_mature(const sa_index* idx, const void* queries, sa_dtype qd
                            int64_t* out_ids, float* out_scores, int32_t* out_lists_scanned,
                            double* out_rq, double* out_ema, void* stream);
 
+/* ---- proximity-graph index (readings R22-R27) ----
+ * The paper's retriever is a graph index (HNSW, App. B.3) whose
+ * "search range" (efSearch) trades recall for effort.  Built on an IVF index:
+ *   R22 knn(i): the knn_k best rows (score desc, id asc) over the union of the nprobe_build
+ *       lists row i probes, excluding i (the IVF search with each stored row as a query);
+ *   R23/R24 fwd(i): knn(i) reordered by (detour count, rank), first `degree`, where the
+ *       detour count of the rank-j neighbour c_j is #{k < j : c_j is in knn(c_k) at rank < j};
+ *   R25/R26 final list: the first degree/2 of fwd(c), then reverse edges (p, i) with
+ *       fwd(i)[p] == c in (p, i) order, then the rest of fwd(c), without repeats.
+ * sa_index_build_graph: idx must be an unsharded IVF index; 1 <= degree <= 64,
+ * degree <= knn_k <= 64, knn_k < n, 1 <= nprobe_build <= nlist; flags bit 0 keeps the kNN
+ * lists for sa_index_export_graph.  Synchronous.  Memory: n*degree*4 bytes kept (+ transient
+ * n*(knn_k*4 + degree*12)).
+ * sa_search_graph (R27): beam search per query over a list of search_range (L) entries,
+ * expanding the search_width (w) best unexpanded entries per iteration, at most max_iters
+ * iterations (also capped so the visited set fits: iterations <= (8192 - E) / (w*degree));
+ * entry points = the first stored row (lowest id) of each of the n_entries (E) best IVF
+ * lists of the query.  queries DEVICE [nq, d] of qdtype; out_ids DEVICE int64 [nq, k],
+ * out_scores DEVICE fp32 [nq, k] (score desc, id asc; padded -1 / -INF), out_expanded
+ * DEVICE int32 [nq] (entries expanded; may be NULL).  1 <= k <= L <= 256,
+ * w*degree <= 256, 1 <= E <= min(nlist, 256).  Stream-ordered, asynchronous.
+ * sa_index_export_graph: *degree, host_nbr HOST int64 [n_local, degree] (row = global id -
+ * row_offset, entries global ids, -1 padded), host_knn HOST int64 [n_local, knn_k] likewise
+ * (NULL, or the kept kNN lists), *knn_k.
+ */
+sa_status sa_index_build_graph(sa_index* idx, int32_t knn_k, int32_t degree, int32_t nprobe_build,
+                               int32_t flags, void* stream);
+sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                          int32_t k, int32_t search_range, int32_t search_width,
+                          int32_t n_entries, int32_t max_iters, int64_t* out_ids,
+                          float* out_scores, int32_t* out_expanded, void* stream);
+sa_status sa_index_export_graph(const sa_index* idx, int32_t* degree, int32_t* knn_k,
+                                int64_t* host_nbr, int64_t* host_knn);
+
 /* ---- agent loop support (Alg. 1, App. A.1) ---- */
 
 /*
@@ -246,7 +280,8 @@ typedef enum {
   SA_KERNEL_IVF_PROBE = 3, /* centroid scoring + top-nprobe */
   SA_KERNEL_IVF_SCAN = 4,  /* inverted-list scan + partial top-k */
   SA_KERNEL_OTHER = 5,
-  SA_KERNEL_KINDS = 6
+  SA_KERNEL_GRAPH_SEARCH = 6, /* proximity-graph beam search */
+  SA_KERNEL_KINDS = 7
 } sa_kernel_kind;
 sa_status sa_profile_enable(int32_t on); /* also resets the counters */
 /* Synchronises the recorded events; ms_total = summed event time of that kind,

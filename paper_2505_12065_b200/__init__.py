@@ -22,7 +22,7 @@ _SO = os.path.join(_PKG, "libsa.so")
 
 SA_OK, SA_ERR_INVALID_ARG, SA_ERR_STATE, SA_ERR_OOM, SA_ERR_CUDA, SA_ERR_NCCL, SA_ERR_UNSUPPORTED = range(7)
 SA_BF16, SA_F32 = 0, 1
-KERNEL_KINDS = ("flat_scan", "merge", "stage", "ivf_probe", "ivf_scan", "other")
+KERNEL_KINDS = ("flat_scan", "merge", "stage", "ivf_probe", "ivf_scan", "other", "graph_search")
 
 
 class SAError(RuntimeError):
@@ -89,6 +89,9 @@ def lib() -> ctypes.CDLL:
         "sa_index_export_lists": (st, [P, P, P]),
         "sa_search_probes": (st, [P, P, i64, i32, P, P]),
         "sa_priority_order": (st, [i64, P, P, P, P, P, i32, P, P]),
+        "sa_index_build_graph": (st, [P, i32, i32, i32, i32, P]),
+        "sa_search_graph": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, i32, i32, P, P, P, P]),
+        "sa_index_export_graph": (st, [P, ctypes.POINTER(i32), ctypes.POINTER(i32), P, P]),
         "sa_retriever_create": (st, [P, i32, i32, i32, i32, ctypes.POINTER(P)]),
         "sa_retriever_submit": (st, [P, P, i32, i32, i32, i32, ctypes.POINTER(_MaturityOpts),
                                      ctypes.POINTER(i64)]),
@@ -306,6 +309,40 @@ class Index:
         if trace:
             return ids, scores, t, rq, ema
         return ids, scores, t
+
+    # sa_index_build_graph / sa_search_graph / sa_index_export_graph (proximity graph)
+    def build_graph(self, knn_k: int = 64, degree: int = 32, nprobe_build: int = 8,
+                    keep_knn: bool = False, stream=None):
+        _check(lib().sa_index_build_graph(self.handle, knn_k, degree, nprobe_build,
+                                          1 if keep_knn else 0, _stream_ptr(stream)))
+        return self
+
+    def search_graph(self, queries: torch.Tensor, k: int, search_range: int, *,
+                     search_width: int = 4, n_entries: int = 8, max_iters: int = 1 << 30,
+                     expanded: bool = False, stream=None):
+        if not queries.is_cuda or queries.dim() != 2 or not queries.is_contiguous():
+            raise ValueError("queries must be a contiguous 2-D CUDA tensor")
+        nq = queries.shape[0]
+        ids = torch.empty(nq, k, dtype=torch.int64, device=queries.device)
+        scores = torch.empty(nq, k, dtype=torch.float32, device=queries.device)
+        ex = torch.empty(nq, dtype=torch.int32, device=queries.device) if expanded else None
+        _check(lib().sa_search_graph(self.handle, _ptr(queries), _dtype_code(queries), nq, k,
+                                     search_range, search_width, n_entries,
+                                     min(max_iters, 2**31 - 1), _ptr(ids), _ptr(scores),
+                                     _ptr(ex) if expanded else None, _stream_ptr(stream)))
+        return (ids, scores, ex) if expanded else (ids, scores)
+
+    def export_graph(self, knn: bool = False):
+        inf = self.info()
+        deg, kk = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().sa_index_export_graph(self.handle, ctypes.byref(deg), ctypes.byref(kk),
+                                           None, None))
+        nbr = np.empty((inf["n_local"], deg.value), dtype=np.int64)
+        kn = np.empty((inf["n_local"], kk.value), dtype=np.int64) if knn else None
+        _check(lib().sa_index_export_graph(self.handle, ctypes.byref(deg), ctypes.byref(kk),
+                                           nbr.ctypes.data_as(ctypes.c_void_p),
+                                           kn.ctypes.data_as(ctypes.c_void_p) if knn else None))
+        return (nbr, kn) if knn else nbr
 
     def info(self):
         n = ctypes.c_int64()

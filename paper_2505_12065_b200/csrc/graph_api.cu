@@ -1,0 +1,220 @@
+// graph_api.cu -- proximity-graph index build + search entry points (
+// DESIGN.md §4.7; include/sa.h for the contract).
+//
+// Build: the kNN lists come from the IVF search itself -- every stored row, in list-major
+// order, is a query of ivf_search (tcgen05 list scan; consecutive stored rows probe nearly the
+// same lists, so a batch reads few distinct lists); then the rank-only prune / reverse / merge
+// kernels of graph.cu.  Search: stage queries, probe the IVF centroids for entry points
+// (tensor-core scores + exact top-E select), beam search (graph.cu).
+#include <algorithm>
+#include <vector>
+
+#include "internal.h"
+#include "kernels/graph.cuh"
+#include "kernels/merge.cuh"
+
+using namespace sa;
+
+namespace {
+
+#define SA_TRY(expr)              \
+  do {                            \
+    sa_status _st = (expr);       \
+    if (_st != SA_OK) return _st; \
+  } while (0)
+
+struct DevFree {
+  std::vector<void*> p;
+  ~DevFree() {
+    for (void* x : p) cudaFree(x);
+  }
+};
+
+template <typename T>
+sa_status galloc(DevFree& f, T** ptr, size_t count, const char* what) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(ptr), std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess) return cuda_status(e, what);
+  f.p.push_back(*ptr);
+  return SA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sa_status sa_index_build_graph(sa_index* idx, int32_t knn_k, int32_t degree, int32_t nprobe_build,
+                               int32_t flags, void* stream) {
+  if (!idx) return set_error(SA_ERR_INVALID_ARG, "null index");
+  if (idx->nlist == 0) return set_error(SA_ERR_STATE, "the graph is built on an IVF index");
+  if (idx->comm && idx->comm->world > 1)
+    return set_error(SA_ERR_UNSUPPORTED, "graph index on a sharded index");
+  const int64_t n = idx->n_local;
+  if (degree < 1 || degree > GR_MAX_R || knn_k < degree || knn_k > GR_MAX_K || knn_k >= n)
+    return set_error(SA_ERR_INVALID_ARG, "need 1 <= degree <= knn_k <= 64 and knn_k < n");
+  if (nprobe_build < 1 || nprobe_build > idx->nlist)
+    return set_error(SA_ERR_INVALID_ARG, "nprobe_build must be in [1, nlist]");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int K = knn_k, R = degree, kk = K + 1;
+  DevFree f;
+  int32_t *pos_of, *knn, *fwd, *nbr = nullptr;
+  uint64_t* rev;
+  int64_t* ids;
+  float* sc;
+  const int64_t B = 16384;
+  SA_TRY(galloc(f, &pos_of, n, "graph build"));
+  SA_TRY(galloc(f, &knn, (size_t)n * K, "graph kNN lists"));
+  SA_TRY(galloc(f, &fwd, (size_t)n * R, "graph build"));
+  SA_TRY(galloc(f, &rev, (size_t)n * R, "graph build"));
+  SA_TRY(galloc(f, &ids, (size_t)B * kk, "graph build"));
+  SA_TRY(galloc(f, &sc, (size_t)B * kk, "graph build"));
+  SA_TRY(cuda_status(cudaMalloc(&nbr, (size_t)n * R * sizeof(int32_t)), "graph"));
+  auto fail = [&](sa_status st) {
+    cudaFree(nbr);
+    return st;
+  };
+  sa_status st = cuda_status(launch_inverse_ids(idx->row_ids, n, idx->row_offset, pos_of, s),
+                             "inverse ids");
+  // R22: kNN lists, batch by batch of consecutive stored rows
+  for (int64_t p0 = 0; st == SA_OK && p0 < n; p0 += B) {
+    const int64_t nb = std::min(B, n - p0);
+    SearchOut out;
+    out.ids = ids;
+    out.scores = sc;
+    st = ivf_search(idx, idx->X + (size_t)p0 * idx->d_pad, nb, nb, kk, nprobe_build, out, s);
+    if (st == SA_OK)
+      st = cuda_status(launch_knn_to_pos(ids, nb, kk, p0, pos_of, idx->row_offset, K, knn, s),
+                       "kNN lists");
+  }
+  if (st == SA_OK) st = cuda_status(launch_graph_prune(knn, n, K, R, fwd, s), "graph prune");
+  if (st == SA_OK)
+    st = cuda_status(cudaMemsetAsync(rev, 0xff, (size_t)n * R * sizeof(uint64_t), s), "memset");
+  if (st == SA_OK) st = cuda_status(launch_graph_reverse(fwd, n, R, idx->row_ids, rev, s), "graph reverse");
+  if (st == SA_OK) st = cuda_status(launch_graph_merge(fwd, rev, n, R, pos_of, idx->row_offset, nbr, s), "graph merge");
+  if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "graph build sync");
+  if (st != SA_OK) return fail(st);
+  cudaFree(idx->graph);
+  cudaFree(idx->graph_knn);
+  idx->graph = nbr;
+  idx->graph_knn = nullptr;
+  if (flags & 1) {
+    // keep the kNN lists (tests): hand the buffer over instead of freeing it
+    f.p.erase(std::find(f.p.begin(), f.p.end(), (void*)knn));
+    idx->graph_knn = knn;
+  }
+  idx->graph_R = R;
+  idx->graph_K = K;
+  return SA_OK;
+}
+
+sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                          int32_t k, int32_t search_range, int32_t search_width,
+                          int32_t n_entries, int32_t max_iters, int64_t* out_ids,
+                          float* out_scores, int32_t* out_expanded, void* stream) {
+  if (!idx || !queries || !out_ids || !out_scores)
+    return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (!idx->graph) return set_error(SA_ERR_STATE, "no graph: call sa_index_build_graph");
+  if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
+  if (nq < 1 || nq > (1ll << 31) - 1) return set_error(SA_ERR_INVALID_ARG, "bad nq");
+  const int L = search_range, w = search_width, E = n_entries, R = idx->graph_R;
+  if (k < 1 || k > L || L > GR_MAX_L)
+    return set_error(SA_ERR_INVALID_ARG, "need 1 <= k <= search_range <= 256");
+  if (w < 1 || w * R > GR_MAX_NEW || w > 8)
+    return set_error(SA_ERR_INVALID_ARG, "need 1 <= search_width <= 8, search_width*degree <= 256");
+  if (E < 1 || E > std::min(idx->nlist, 256))
+    return set_error(SA_ERR_INVALID_ARG, "need 1 <= n_entries <= min(nlist, 256)");
+  if (max_iters < 0) return set_error(SA_ERR_INVALID_ARG, "max_iters must be >= 0");
+  const int T = std::min(max_iters, (GR_HASH / 2 - E) / (w * R));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nq_pad = padded_nq(nq);
+  __nv_bfloat16* Qs = nullptr;
+  float* psc = nullptr;
+  uint64_t* pkeys = nullptr;
+  sa_status st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "graph search");
+  if (st == SA_OK) st = dalloc(&psc, (size_t)nq * idx->nlist, s, "graph search");
+  if (st == SA_OK) st = dalloc(&pkeys, (size_t)nq * E, s, "graph search");
+  if (st == SA_OK) {
+    prof_begin(SA_KERNEL_STAGE, s);
+    st = cuda_status(launch_cast_pad(queries, qdtype == SA_F32, nq, idx->d, Qs, nq_pad,
+                                     idx->d_pad, idx->num_sms, s),
+                     "stage queries");
+    prof_end(SA_KERNEL_STAGE, s);
+    prof_count(SA_KERNEL_STAGE);
+  }
+  if (st == SA_OK) {
+    // entry points: the E best IVF lists (tensor-core centroid scores + exact select)
+    prof_begin(SA_KERNEL_IVF_PROBE, s);
+    const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, idx->nlist, idx->d_pad, nullptr, 0u};
+    st = flat_scores_view(cvc, idx->num_sms, Qs, nq, psc, s);
+    if (st == SA_OK) {
+      MergeArgs m{};
+      m.cand_scores = psc;
+      m.m_flat = idx->nlist;
+      m.qstride = idx->nlist;
+      m.k = E;
+      m.out_keys = pkeys;
+      st = cuda_status(launch_merge(m, nq, s), "entry select");
+      prof_count(SA_KERNEL_MERGE);
+    }
+    prof_end(SA_KERNEL_IVF_PROBE, s);
+  }
+  if (st == SA_OK) {
+    GraphSearchArgs a{};
+    a.X = idx->X;
+    a.row_ids = idx->row_ids;
+    a.nbr = idx->graph;
+    a.Q = Qs;
+    a.entry_keys = pkeys;
+    a.list_off = idx->list_off;
+    a.d_pad = idx->d_pad;
+    a.R = R;
+    a.L = L;
+    a.w = w;
+    a.E = E;
+    a.T = T;
+    a.k = k;
+    a.out_ids = out_ids;
+    a.out_scores = out_scores;
+    a.out_expanded = out_expanded;
+    prof_begin(SA_KERNEL_GRAPH_SEARCH, s);
+    st = cuda_status(launch_graph_search(a, nq, s), "graph search");
+    prof_end(SA_KERNEL_GRAPH_SEARCH, s);
+    prof_count(SA_KERNEL_GRAPH_SEARCH);
+  }
+  if (Qs) cudaFreeAsync(Qs, s);
+  if (psc) cudaFreeAsync(psc, s);
+  if (pkeys) cudaFreeAsync(pkeys, s);
+  return st;
+}
+
+sa_status sa_index_export_graph(const sa_index* idx, int32_t* degree, int32_t* knn_k,
+                                int64_t* host_nbr, int64_t* host_knn) {
+  if (!idx || !degree) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  *degree = idx->graph_R;
+  if (knn_k) *knn_k = idx->graph_K;
+  if (!idx->graph) return set_error(SA_ERR_STATE, "no graph");
+  const int64_t n = idx->n_local;
+  std::vector<int32_t> ids(n), buf;
+  cudaError_t e = cudaMemcpy(ids.data(), idx->row_ids, n * 4, cudaMemcpyDeviceToHost);
+  auto conv = [&](const int32_t* dev, int cols, int64_t* out) -> cudaError_t {
+    buf.resize((size_t)n * cols);
+    cudaError_t e2 = cudaMemcpy(buf.data(), dev, buf.size() * 4, cudaMemcpyDeviceToHost);
+    if (e2 != cudaSuccess) return e2;
+    // rows in local-id order (global id - row_offset), entries as global ids
+    for (int64_t p = 0; p < n; ++p) {
+      int64_t* o = out + ((int64_t)(uint32_t)ids[p] - idx->row_offset) * cols;
+      for (int j = 0; j < cols; ++j) {
+        const int32_t v = buf[(size_t)p * cols + j];
+        o[j] = v < 0 ? -1 : (int64_t)(uint32_t)ids[v];
+      }
+    }
+    return cudaSuccess;
+  };
+  if (e == cudaSuccess && host_nbr) e = conv(idx->graph, idx->graph_R, host_nbr);
+  if (e == cudaSuccess && host_knn) {
+    if (!idx->graph_knn) return set_error(SA_ERR_STATE, "kNN lists not kept (build flag bit 0)");
+    e = conv(idx->graph_knn, idx->graph_K, host_knn);
+  }
+  return cuda_status(e, "export graph");
+}
+
+}  // extern "C"

@@ -61,6 +61,10 @@ struct sa_index {
   // captured small-batch searches (host-buffer path), guarded by graph_mu
   std::mutex graph_mu;
   std::vector<sa_graph_entry> graphs;
+  // proximity graph (graph_api.cu): neighbour lists in stored positions [n_local, graph_R]
+  int32_t graph_R = 0, graph_K = 0;
+  int32_t* graph = nullptr;
+  int32_t* graph_knn = nullptr;  // kept kNN lists [n_local, graph_K] (build flag bit 0)
   // captured progressive (maturity-exit) searches, guarded by graph_mu (mature.cu)
   std::vector<std::unique_ptr<sa::MaturePlan, void (*)(sa::MaturePlan*)>> mature_plans;
 };

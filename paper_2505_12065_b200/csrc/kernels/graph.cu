@@ -1,0 +1,504 @@
+// graph.cu -- proximity-graph ANN on B200.
+//
+// The paper's retriever is a graph index (HNSW) whose search range
+// trades recall for effort.  Build (readings R22-R26): an approximate kNN graph
+// from the IVF index (every stored row searched as a query on the tcgen05 list scan), then
+// rank-only pruning by detour counts and a reverse-edge merge -- integer work on the kNN
+// lists, no distances.  Search (R27): one CTA per query runs best-first beam search over a
+// candidate list of L entries (the search range), expanding the w best unexpanded entries
+// per iteration; neighbour rows (1.5 KB bf16 each) are gathered by whole warps with 16-byte
+// loads, 4 rows in flight per warp; the visited set is an exact open-addressing table in
+// shared memory; the list is kept sorted by merge path.  Memory-latency bound: a query's
+// iterations are dependent gathers, so several CTAs per SM hide each other's latency.
+#include <cuda_bf16.h>
+
+#include "graph.cuh"
+#include "keys.cuh"
+
+namespace sa {
+
+namespace {
+
+unsigned grid_for(int64_t n, int per_block) {
+  int64_t b = (n + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > 148 * 64) b = 148 * 64;
+  return (unsigned)b;
+}
+
+__global__ void inverse_ids_kernel(const int32_t* __restrict__ row_ids, int64_t n,
+                                   int64_t row_offset, int32_t* __restrict__ pos_of) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    pos_of[(int64_t)(uint32_t)row_ids[p] - row_offset] = (int32_t)p;
+}
+
+__global__ void knn_to_pos_kernel(const int64_t* __restrict__ ids, int64_t nb, int kk, int64_t p0,
+                                  const int32_t* __restrict__ pos_of, int64_t row_offset, int K,
+                                  int32_t* __restrict__ knn) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t self = p0 + b;
+    int32_t* out = knn + self * K;
+    int cnt = 0;
+    for (int j = 0; j < kk && cnt < K; ++j) {
+      const int64_t id = ids[b * kk + j];
+      if (id < 0) break;
+      const int32_t pos = pos_of[id - row_offset];
+      if (pos == self) continue;
+      out[cnt++] = pos;
+    }
+    for (; cnt < K; ++cnt) out[cnt] = -1;
+  }
+}
+
+constexpr int kHashW = 128;  // per-warp rank table slots (>= 2 * GR_MAX_K)
+
+__device__ __forceinline__ uint32_t hslot(int32_t y) {
+  return ((uint32_t)y * 2654435761u) >> (32 - 7);
+}
+
+// R23 + R24.  One warp per node; lanes own ranks j = lane and lane + 32.
+__global__ void __launch_bounds__(256) graph_prune_kernel(const int32_t* __restrict__ knn,
+                                                          int64_t n, int K, int R,
+                                                          int32_t* __restrict__ fwd) {
+  __shared__ int32_t hkey[8][kHashW];
+  __shared__ int32_t hval[8][kHashW];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int32_t* hk = hkey[warp];
+  int32_t* hv = hval[warp];
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t i = blockIdx.x * 8 + warp; i < n; i += nw) {
+    const int j0 = lane, j1 = lane + 32;
+    const int32_t c0 = j0 < K ? knn[i * K + j0] : -1;
+    const int32_t c1 = j1 < K ? knn[i * K + j1] : -1;
+    int det0 = 0, det1 = 0;
+    for (int k = 0; k < K - 1; ++k) {
+      const int32_t ck = __shfl_sync(0xffffffffu, k < 32 ? c0 : c1, k & 31);
+      if (ck < 0) break;
+      for (int s = lane; s < kHashW; s += 32) hk[s] = -1;
+      __syncwarp();
+      const int32_t y0 = j0 < K ? knn[(int64_t)ck * K + j0] : -1;
+      const int32_t y1 = j1 < K ? knn[(int64_t)ck * K + j1] : -1;
+      if (y0 >= 0) {
+        uint32_t h = hslot(y0);
+        while (atomicCAS(&hk[h], -1, y0) != -1) h = (h + 1) & (kHashW - 1);
+        hv[h] = j0;
+      }
+      if (y1 >= 0) {
+        uint32_t h = hslot(y1);
+        while (atomicCAS(&hk[h], -1, y1) != -1) h = (h + 1) & (kHashW - 1);
+        hv[h] = j1;
+      }
+      __syncwarp();
+      // c_j occurs in knn(c_k) at rank r < j, with k < j
+      if (c0 >= 0 && k < j0) {
+        uint32_t h = hslot(c0);
+        while (hk[h] != -1) {
+          if (hk[h] == c0) {
+            if (hv[h] < j0) ++det0;
+            break;
+          }
+          h = (h + 1) & (kHashW - 1);
+        }
+      }
+      if (c1 >= 0 && k < j1) {
+        uint32_t h = hslot(c1);
+        while (hk[h] != -1) {
+          if (hk[h] == c1) {
+            if (hv[h] < j1) ++det1;
+            break;
+          }
+          h = (h + 1) & (kHashW - 1);
+        }
+      }
+      __syncwarp();
+    }
+    // order by (detour, rank): rank of each own entry among the valid ones
+    const uint32_t key0 = c0 >= 0 ? ((uint32_t)det0 << 8) | (uint32_t)j0 : 0xffffffffu;
+    const uint32_t key1 = c1 >= 0 ? ((uint32_t)det1 << 8) | (uint32_t)j1 : 0xffffffffu;
+    int r0 = 0, r1 = 0, valid = 0;
+    for (int m = 0; m < K; ++m) {
+      const uint32_t km = __shfl_sync(0xffffffffu, m < 32 ? key0 : key1, m & 31);
+      if (km == 0xffffffffu) continue;
+      ++valid;
+      r0 += km < key0;
+      r1 += km < key1;
+    }
+    if (c0 >= 0 && r0 < R) fwd[i * R + r0] = c0;
+    if (c1 >= 0 && r1 < R) fwd[i * R + r1] = c1;
+    for (int r = valid + lane; r < R; r += 32) fwd[i * R + r] = -1;
+  }
+}
+
+// R25: insert (p << 32 | i) into node c's R-smallest set (CAS on the current maximum; the
+// final set is the R smallest keys whatever the interleaving -- values only decrease).
+// Keys carry the GLOBAL id of i (R25 orders ties by id, and stored positions are list-major).
+__global__ void graph_reverse_kernel(const int32_t* __restrict__ fwd, int64_t n, int R,
+                                     const int32_t* __restrict__ row_ids,
+                                     unsigned long long* __restrict__ rev) {
+  const int64_t tot = n * R;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / R;
+    const int p = (int)(t % R);
+    const int32_t c = fwd[t];
+    if (c < 0) continue;
+    const unsigned long long key =
+        ((unsigned long long)p << 32) | (unsigned long long)(uint32_t)row_ids[i];
+    unsigned long long* slots = rev + (int64_t)c * R;
+    while (true) {
+      int m = 0;
+      unsigned long long mv = __ldcg(slots);  // L2 reads: other SMs CAS these slots
+      for (int s = 1; s < R; ++s) {
+        const unsigned long long v = __ldcg(slots + s);
+        if (v > mv) {
+          mv = v;
+          m = s;
+        }
+      }
+      if (key >= mv) break;
+      if (atomicCAS(&slots[m], mv, key) == mv) break;
+    }
+  }
+}
+
+// R26: one warp per node.
+__global__ void __launch_bounds__(256) graph_merge_kernel(const int32_t* __restrict__ fwd,
+                                                          const unsigned long long* __restrict__ rev,
+                                                          int64_t n, int R,
+                                                          const int32_t* __restrict__ pos_of,
+                                                          int64_t row_offset,
+                                                          int32_t* __restrict__ nbr) {
+  __shared__ int32_t lst[8][GR_MAX_R];
+  __shared__ unsigned long long srt[8][GR_MAX_R];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int32_t* L = lst[warp];
+  unsigned long long* S = srt[warp];
+  const int64_t nw = (int64_t)gridDim.x * 8;
+  for (int64_t c = blockIdx.x * 8 + warp; c < n; c += nw) {
+    // sort the reverse keys ascending (empty = ~0 sorts last)
+    const unsigned long long k0 = lane < R ? rev[c * R + lane] : ~0ull;
+    const unsigned long long k1 = lane + 32 < R ? rev[c * R + lane + 32] : ~0ull;
+    int r0 = 0, r1 = 0;
+    for (int m = 0; m < R; ++m) {
+      const unsigned long long km = __shfl_sync(0xffffffffu, m < 32 ? k0 : k1, m & 31);
+      r0 += km < k0 || (km == k0 && m < lane);
+      r1 += km < k1 || (km == k1 && m < lane + 32);
+    }
+    if (lane < R) S[r0] = k0;
+    if (lane + 32 < R) S[r1] = k1;
+    __syncwarp();
+    int cnt = 0;
+    auto present = [&](int32_t x) -> bool {
+      const bool hit = (lane < cnt && L[lane] == x) || (lane + 32 < cnt && L[lane + 32] == x);
+      return __ballot_sync(0xffffffffu, hit) != 0;
+    };
+    const int32_t* f = fwd + c * R;
+    for (int t = 0; t < R / 2; ++t) {
+      const int32_t x = f[t];
+      if (x < 0) break;
+      if (lane == 0) L[cnt] = x;
+      ++cnt;
+      __syncwarp();
+    }
+    for (int t = 0; t < R && cnt < R; ++t) {
+      const unsigned long long kk = S[t];
+      if (kk == ~0ull) break;
+      const int32_t x = pos_of[(int64_t)(kk & 0xffffffffull) - row_offset];
+      if (!present(x)) {
+        if (lane == 0) L[cnt] = x;
+        ++cnt;
+      }
+      __syncwarp();
+    }
+    for (int t = R / 2; t < R && cnt < R; ++t) {
+      const int32_t x = f[t];
+      if (x < 0) break;
+      if (!present(x)) {
+        if (lane == 0) L[cnt] = x;
+        ++cnt;
+      }
+      __syncwarp();
+    }
+    for (int t = lane; t < R; t += 32) nbr[c * R + t] = t < cnt ? L[t] : -1;
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ search
+constexpr int kSThreads = 256;
+constexpr int kSWarps = kSThreads / 32;
+constexpr int kRowsPerWarp = 4;
+
+struct SearchSmem {
+  uint32_t hash[GR_HASH];
+  unsigned long long key[2][GR_MAX_L];
+  int32_t pos[2][GR_MAX_L];
+  uint8_t flag[2][GR_MAX_L];
+  unsigned long long nkey[GR_MAX_NEW];
+  int32_t npos[GR_MAX_NEW];
+  int32_t chosen[8];
+  int32_t n_new, n_chosen, cnt;
+};
+
+__device__ __forceinline__ bool visit(uint32_t* hash, int32_t pos) {
+  const uint32_t v = (uint32_t)pos + 1u;
+  uint32_t h = ((uint32_t)pos * 2654435761u) & (GR_HASH - 1);
+  while (true) {
+    const uint32_t old = atomicCAS(&hash[h], 0u, v);
+    if (old == 0u) return true;
+    if (old == v) return false;
+    h = (h + 1) & (GR_HASH - 1);
+  }
+}
+
+__device__ __forceinline__ float bf16x8_dot(const uint4 v, const float* q) {
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+  float acc = 0.f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(b[e]);
+    acc = fmaf(f.x, q[2 * e], acc);
+    acc = fmaf(f.y, q[2 * e + 1], acc);
+  }
+  return acc;
+}
+
+// Score npos[0, cnt) into nkey (warp-cooperative, kRowsPerWarp rows in flight per warp).
+__device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, const float (&qf)[3][8],
+                           int cnt, int nchunk) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint4* X4 = reinterpret_cast<const uint4*>(a.X);
+  for (int j0 = warp * kRowsPerWarp; j0 < cnt; j0 += kSWarps * kRowsPerWarp) {
+    uint4 v[kRowsPerWarp][3];
+    int32_t p[kRowsPerWarp];
+#pragma unroll
+    for (int u = 0; u < kRowsPerWarp; ++u) {
+      p[u] = j0 + u < cnt ? sm.npos[j0 + u] : -1;
+#pragma unroll
+      for (int rd = 0; rd < 3; ++rd) {
+        const int c = rd * 32 + lane;
+        v[u][rd] = (p[u] >= 0 && c < nchunk) ? __ldg(X4 + (int64_t)p[u] * nchunk + c)
+                                             : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kRowsPerWarp; ++u) {
+      float acc = bf16x8_dot(v[u][0], qf[0]) + bf16x8_dot(v[u][1], qf[1]) +
+                  bf16x8_dot(v[u][2], qf[2]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0 && p[u] >= 0) sm.nkey[j0 + u] = make_key(acc, (uint32_t)a.row_ids[p[u]]);
+    }
+  }
+}
+
+// Bitonic sort of (nkey, npos)[0, n2) descending by key.
+__device__ void sort_new(SearchSmem& sm, int n2) {
+  for (int sz = 2; sz <= n2; sz <<= 1)
+    for (int st = sz >> 1; st > 0; st >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += kSThreads) {
+        const int j = i ^ st;
+        if (j > i) {
+          const bool desc = (i & sz) == 0;
+          const unsigned long long x = sm.nkey[i], y = sm.nkey[j];
+          if (desc ? x < y : x > y) {
+            sm.nkey[i] = y;
+            sm.nkey[j] = x;
+            const int32_t t = sm.npos[i];
+            sm.npos[i] = sm.npos[j];
+            sm.npos[j] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+// number of entries of the descending array a[0, n) that are > x
+__device__ __forceinline__ int count_greater(const unsigned long long* a, int n,
+                                             unsigned long long x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] > x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kSThreads) graph_search_kernel(const GraphSearchArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  SearchSmem& sm = *reinterpret_cast<SearchSmem*>(smem_raw);
+  const int q = blockIdx.x;
+  const int lane = threadIdx.x % 32;
+  const int nchunk = a.d_pad / 8;
+  for (int i = threadIdx.x; i < GR_HASH; i += kSThreads) sm.hash[i] = 0u;
+  // query in registers: lane holds 16-byte chunks lane, lane + 32, lane + 64
+  float qf[3][8];
+  {
+    const uint4* Q4 = reinterpret_cast<const uint4*>(a.Q) + (int64_t)q * nchunk;
+#pragma unroll
+    for (int rd = 0; rd < 3; ++rd) {
+      const int c = rd * 32 + lane;
+      const uint4 v = c < nchunk ? Q4[c] : make_uint4(0, 0, 0, 0);
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(b[e]);
+        qf[rd][2 * e] = f.x;
+        qf[rd][2 * e + 1] = f.y;
+      }
+    }
+  }
+  if (threadIdx.x == 0) sm.n_new = 0;
+  __syncthreads();
+  // entries: the first stored row of each probed list (lists hold ascending global ids)
+  if (threadIdx.x < a.E) {
+    const uint64_t pk = a.entry_keys[(int64_t)q * a.E + threadIdx.x];
+    if (pk != 0ull) {
+      const uint32_t l = key_id(pk);
+      const int64_t lo = a.list_off[l], hi = a.list_off[l + 1];
+      if (hi > lo && visit(sm.hash, (int32_t)lo)) sm.npos[atomicAdd(&sm.n_new, 1)] = (int32_t)lo;
+    }
+  }
+  __syncthreads();
+  int cur = 0;
+  int n_new = sm.n_new;
+  score_rows(a, sm, qf, n_new, nchunk);
+  __syncthreads();
+  int cnt = 0;
+  int expanded = 0;
+  for (int it = 0;; ++it) {
+    // ---- merge the scored new rows into the sorted list (top-L)
+    if (n_new > 0) {
+      int n2 = 1;
+      while (n2 < n_new) n2 <<= 1;
+      for (int i = n_new + threadIdx.x; i < n2; i += kSThreads) {
+        sm.nkey[i] = 0ull;
+        sm.npos[i] = -1;
+      }
+      __syncthreads();
+      sort_new(sm, n2);
+      const int nxt = cur ^ 1;
+      for (int i = threadIdx.x; i < cnt; i += kSThreads) {
+        const unsigned long long x = sm.key[cur][i];
+        const int np = i + count_greater(sm.nkey, n_new, x);
+        if (np < a.L) {
+          sm.key[nxt][np] = x;
+          sm.pos[nxt][np] = sm.pos[cur][i];
+          sm.flag[nxt][np] = sm.flag[cur][i];
+        }
+      }
+      for (int j = threadIdx.x; j < n_new; j += kSThreads) {
+        const unsigned long long x = sm.nkey[j];
+        const int np = j + count_greater(sm.key[cur], cnt, x);
+        if (np < a.L) {
+          sm.key[nxt][np] = x;
+          sm.pos[nxt][np] = sm.npos[j];
+          sm.flag[nxt][np] = 0;
+        }
+      }
+      cnt = min(a.L, cnt + n_new);
+      cur = nxt;
+      __syncthreads();
+    }
+    if (it >= a.T) break;
+    // ---- pick the first w unexpanded entries (warp 0)
+    if (threadIdx.x < 32) {
+      int taken = 0;
+      for (int base = 0; base < cnt && taken < a.w; base += 32) {
+        const int i = base + lane;
+        const bool un = i < cnt && sm.flag[cur][i] == 0;
+        unsigned m = __ballot_sync(0xffffffffu, un);
+        while (m && taken < a.w) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          if (lane == 0) {
+            sm.chosen[taken] = sm.pos[cur][base + b];
+            sm.flag[cur][base + b] = 1;
+          }
+          ++taken;
+        }
+      }
+      if (lane == 0) {
+        sm.n_chosen = taken;
+        sm.n_new = 0;
+      }
+    }
+    __syncthreads();
+    const int nc = sm.n_chosen;
+    if (nc == 0) break;
+    expanded += nc;
+    // ---- neighbours not yet visited
+    for (int t = threadIdx.x; t < nc * a.R; t += kSThreads) {
+      const int32_t c = a.nbr[(int64_t)sm.chosen[t / a.R] * a.R + (t % a.R)];
+      if (c >= 0 && visit(sm.hash, c)) sm.npos[atomicAdd(&sm.n_new, 1)] = c;
+    }
+    __syncthreads();
+    n_new = sm.n_new;
+    score_rows(a, sm, qf, n_new, nchunk);
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < a.k; i += kSThreads) {
+    const unsigned long long key = i < cnt ? sm.key[cur][i] : 0ull;
+    a.out_ids[(int64_t)q * a.k + i] = key == 0ull ? -1 : (int64_t)key_id(key);
+    a.out_scores[(int64_t)q * a.k + i] = key == 0ull ? -INFINITY : key_score(key);
+  }
+  if (a.out_expanded && threadIdx.x == 0) a.out_expanded[q] = expanded;
+}
+
+}  // namespace
+
+cudaError_t launch_inverse_ids(const int32_t* row_ids, int64_t n, int64_t row_offset,
+                               int32_t* pos_of, cudaStream_t s) {
+  inverse_ids_kernel<<<grid_for(n, 256), 256, 0, s>>>(row_ids, n, row_offset, pos_of);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_knn_to_pos(const int64_t* ids, int64_t nb, int kk, int64_t p0,
+                              const int32_t* pos_of, int64_t row_offset, int K, int32_t* knn,
+                              cudaStream_t s) {
+  knn_to_pos_kernel<<<grid_for(nb, 128), 128, 0, s>>>(ids, nb, kk, p0, pos_of, row_offset, K,
+                                                      knn);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_graph_prune(const int32_t* knn, int64_t n, int K, int R, int32_t* fwd,
+                               cudaStream_t s) {
+  graph_prune_kernel<<<grid_for(n, 8), 256, 0, s>>>(knn, n, K, R, fwd);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_graph_reverse(const int32_t* fwd, int64_t n, int R, const int32_t* row_ids,
+                                 uint64_t* rev, cudaStream_t s) {
+  graph_reverse_kernel<<<grid_for(n * R, 256), 256, 0, s>>>(
+      fwd, n, R, row_ids, reinterpret_cast<unsigned long long*>(rev));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_graph_merge(const int32_t* fwd, const uint64_t* rev, int64_t n, int R,
+                               const int32_t* pos_of, int64_t row_offset, int32_t* nbr,
+                               cudaStream_t s) {
+  graph_merge_kernel<<<grid_for(n, 8), 256, 0, s>>>(
+      fwd, reinterpret_cast<const unsigned long long*>(rev), n, R, pos_of, row_offset, nbr);
+  return cudaGetLastError();
+}
+
+size_t graph_search_smem(int) { return sizeof(SearchSmem); }
+
+cudaError_t launch_graph_search(const GraphSearchArgs& a, int64_t nq, cudaStream_t s) {
+  const size_t smem = sizeof(SearchSmem);
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(graph_search_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  graph_search_kernel<<<(unsigned)nq, kSThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sa

@@ -1,0 +1,51 @@
+// graph.cuh -- proximity-graph ANN kernels (R22-R27).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sa {
+
+constexpr int GR_MAX_K = 64;       // kNN list length (build)
+constexpr int GR_MAX_R = 64;       // graph degree
+constexpr int GR_MAX_L = 256;      // search list (search range)
+constexpr int GR_MAX_NEW = 256;    // w * R per iteration
+constexpr int GR_HASH = 16384;     // visited-set slots per query (smem, 64 KB)
+
+// kNN ids from the IVF search (global ids [nb, kk], best first, -1 padded) -> stored positions
+// [nb, K] without the row itself (R22).  row p0 + b is row b of the batch.
+cudaError_t launch_knn_to_pos(const int64_t* ids, int64_t nb, int kk, int64_t p0,
+                              const int32_t* pos_of, int64_t row_offset, int K, int32_t* knn,
+                              cudaStream_t s);
+// pos_of[row_ids[p] - row_offset] = p
+cudaError_t launch_inverse_ids(const int32_t* row_ids, int64_t n, int64_t row_offset,
+                               int32_t* pos_of, cudaStream_t s);
+// R23 + R24: detour counts, fwd [n, R]
+cudaError_t launch_graph_prune(const int32_t* knn, int64_t n, int K, int R, int32_t* fwd,
+                               cudaStream_t s);
+// R25: the R smallest (p, global id of i) reverse keys of every node (rev [n, R] u64,
+// pre-filled ~0)
+cudaError_t launch_graph_reverse(const int32_t* fwd, int64_t n, int R, const int32_t* row_ids,
+                                 uint64_t* rev, cudaStream_t s);
+// R26: final lists [n, R] (stored positions; pos_of maps global id - row_offset -> position)
+cudaError_t launch_graph_merge(const int32_t* fwd, const uint64_t* rev, int64_t n, int R,
+                               const int32_t* pos_of, int64_t row_offset, int32_t* nbr,
+                               cudaStream_t s);
+
+struct GraphSearchArgs {
+  const __nv_bfloat16* X;   // stored rows [n, d_pad]
+  const int32_t* row_ids;   // stored row -> global id
+  const int32_t* nbr;       // [n, R] stored positions, -1 padded
+  const __nv_bfloat16* Q;   // staged queries [nq, d_pad]
+  const uint64_t* entry_keys;  // [nq, E] probe keys (list id in the key, 0 = none)
+  const int64_t* list_off;  // [nlist + 1]
+  int32_t d_pad, R, L, w, E, T, k;
+  int64_t* out_ids;         // [nq, k]
+  float* out_scores;        // [nq, k]
+  int32_t* out_expanded;    // optional [nq]
+};
+size_t graph_search_smem(int L);
+cudaError_t launch_graph_search(const GraphSearchArgs& a, int64_t nq, cudaStream_t s);
+
+}  // namespace sa

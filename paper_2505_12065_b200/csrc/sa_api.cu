@@ -423,6 +423,8 @@ sa_status sa_index_free(sa_index* idx) {
   cudaFree(idx->centroids);
   cudaFree(idx->centroids_bf16);
   cudaFree(idx->list_off);
+  cudaFree(idx->graph);
+  cudaFree(idx->graph_knn);
   delete idx;
   return SA_OK;
 }

@@ -1,0 +1,159 @@
+"""Proximity-graph index on the GPU against oracle/graph.py (R22-R27).
+
+  * kNN lists (R22): each row's list is the exact top-K over the union of its probed IVF
+    lists without itself (band rule vs oracle.c);
+  * pruning + reverse merge (R23-R26): the oracle applied to the GPU's own kNN lists gives
+    bit-identical neighbour lists (integer logic);
+  * search (R27): exhaustive beam (L >= n) == brute force over the nodes reachable from the
+    entries, with every reachable node expanded exactly once; on a mixture the GPU beam
+    search reproduces the oracle's beam search on the same graph and entries (identical
+    results for almost all queries -- fp32 vs fp64 scores can reorder near-ties -- and
+    recall against the oracle's result >= 0.99), returned scores within the band.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import graph
+from datagen import make_mixture, draw_rows, to_bf16_bits
+from parity import check
+
+pytestmark = pytest.mark.gpu
+
+
+def bits_to_tensor(b):
+    return torch.from_numpy(np.ascontiguousarray(b).view(np.int16).copy()).view(torch.bfloat16)
+
+
+def lists_of(idx):
+    off, ids = idx.export_lists()
+    return [ids[off[j]:off[j + 1]] for j in range(len(off) - 1)]
+
+
+@pytest.fixture(scope="module")
+def small(sa):
+    mx = make_mixture(d=128, C=16, r=16, s_n=0.7)
+    X = draw_rows(mx, 8_000, row_seed=51)
+    Q = draw_rows(mx, 48, row_seed=52)
+    Xb, Qb = to_bf16_bits(X), to_bf16_bits(Q)
+    idx = sa.Index.build(bits_to_tensor(Xb).cuda(), 16, kmeans_iters=8)
+    idx.build_graph(knn_k=24, degree=16, nprobe_build=3, keep_knn=True)
+    nbr, kn = idx.export_graph(knn=True)
+    yield idx, Xb, Qb, nbr, kn
+    idx.free()
+
+
+def test_knn_lists_exact_over_probed_lists(sa, small):
+    idx, Xb, Qb, nbr, kn = small
+    lists = lists_of(idx)
+    g = np.random.default_rng(0)
+    rows = g.choice(Xb.shape[0], 200, replace=False)
+    P = idx.probes(bits_to_tensor(Xb[rows]).cuda(), 3).cpu().numpy()
+    for t, i in enumerate(rows):
+        cand = np.sort(np.concatenate([lists[j] for j in P[t]]))
+        cand = cand[cand != i]
+        oi, osc = oracle.flat_topk(Xb[cand], Xb[i:i + 1], 24 + 8)
+        oi = np.where(oi >= 0, cand[np.maximum(oi, 0)], -1)
+        gi = kn[i:i + 1]
+        gs = oracle.pair_scores(Xb, Xb[i:i + 1], np.zeros(24, int), np.maximum(gi[0], 0))[None]
+        r = check(gi, gs.astype(np.float32), oi, osc,
+                  lambda _q, ids_: oracle.pair_scores(Xb, Xb[i:i + 1], np.zeros(len(ids_), int), ids_),
+                  24, n_avail=min(24, len(cand)))
+        assert r["ok"], (i, r)
+
+
+def test_prune_and_merge_bit_exact(sa, small):
+    idx, Xb, Qb, nbr, kn = small
+    want = graph.reverse_merge(graph.prune(kn, 16))
+    assert np.array_equal(nbr, want)
+
+
+def entries_of(idx, Q, E):
+    lists = lists_of(idx)
+    P = idx.probes(bits_to_tensor(Q).cuda(), E).cpu().numpy()
+    return [[int(lists[l][0]) for l in P[i] if len(lists[l])] for i in range(len(Q))]
+
+
+def test_beam_search_matches_oracle(sa, small):
+    idx, Xb, Qb, nbr, kn = small
+    ent = entries_of(idx, Qb, 4)
+    same, rec = 0, []
+    for L, w in ((32, 1), (64, 4), (128, 2)):
+        gi, gs, gx = idx.search_graph(bits_to_tensor(Qb).cuda(), 10, L, search_width=w,
+                                      n_entries=4, expanded=True)
+        gi, gs, gx = gi.cpu().numpy(), gs.cpu().numpy(), gx.cpu().numpy()
+        for q in range(len(Qb)):
+            o = graph.search(Xb, nbr, Qb[q], 10, L=L, w=w, entries=ent[q], T=10_000)
+            if np.array_equal(gi[q], o["ids"]) and gx[q] == o["expanded"]:
+                same += 1
+            rec.append(len(set(gi[q]) & set(o["ids"])) / 10)
+            ps = oracle.pair_scores(Xb, Qb[q:q + 1], np.zeros(10, int), gi[q])
+            assert np.all(np.abs(ps - gs[q]) <= 1e-3 * np.maximum(np.abs(ps), 1e-3))
+            assert np.all(np.diff(gs[q]) <= 0) and len(set(gi[q].tolist())) == 10
+    assert same >= 0.9 * 3 * len(Qb), same
+    assert np.mean(rec) >= 0.99
+
+
+def test_exhaustive_beam_is_brute_force_over_reachable(sa):
+    mx = make_mixture(d=64, C=4, r=8, s_n=0.7)
+    X = draw_rows(mx, 200, row_seed=61)
+    Q = draw_rows(mx, 16, row_seed=62)
+    Xb, Qb = to_bf16_bits(X), to_bf16_bits(Q)
+    idx = sa.Index.build(bits_to_tensor(Xb).cuda(), 4, kmeans_iters=5)
+    idx.build_graph(knn_k=16, degree=8, nprobe_build=2)
+    nbr = idx.export_graph()
+    ent = entries_of(idx, Qb, 2)
+    gi, gs, gx = idx.search_graph(bits_to_tensor(Qb).cuda(), 10, 256, search_width=2,
+                                  n_entries=2, expanded=True)
+    gi, gs, gx = gi.cpu().numpy(), gs.cpu().numpy(), gx.cpu().numpy()
+    for q in range(len(Qb)):
+        seen, todo = set(ent[q]), list(ent[q])
+        while todo:
+            u = todo.pop()
+            for v in nbr[u]:
+                if v >= 0 and int(v) not in seen:
+                    seen.add(int(v))
+                    todo.append(int(v))
+        reach = np.array(sorted(seen))
+        assert gx[q] == reach.size
+        oi, osc = oracle.flat_topk(Xb[reach], Qb[q:q + 1], 18)
+        oi = np.where(oi >= 0, reach[np.maximum(oi, 0)], -1)
+        r = check(gi[q:q + 1], gs[q:q + 1], oi, osc,
+                  lambda _q, ids_: oracle.pair_scores(Xb, Qb[q:q + 1], np.zeros(len(ids_), int), ids_),
+                  10, n_avail=min(10, reach.size))
+        assert r["ok"], (q, r)
+    idx.free()
+
+
+def test_recall_grows_with_search_range(sa):
+    mx = make_mixture(d=128, C=16, r=16, s_n=0.7)
+    X = draw_rows(mx, 60_000, row_seed=71)
+    Q = draw_rows(mx, 64, row_seed=72)
+    Xb, Qb = to_bf16_bits(X), to_bf16_bits(Q)
+    idx = sa.Index.build(bits_to_tensor(Xb).cuda(), 64, kmeans_iters=8)
+    idx.build_graph(knn_k=32, degree=16, nprobe_build=4)
+    ei, _ = oracle.flat_topk(Xb, Qb, 10)
+    Qd = bits_to_tensor(Qb).cuda()
+    recs = []
+    for L in (16, 32, 64, 128, 256):
+        gi, _ = idx.search_graph(Qd, 10, L, search_width=2, n_entries=4)
+        gi = gi.cpu().numpy()
+        recs.append(np.mean([len(set(gi[i]) & set(ei[i])) / 10 for i in range(len(Qb))]))
+    assert recs[-1] >= 0.95, recs
+    assert all(b >= a - 0.02 for a, b in zip(recs, recs[1:])), recs
+    idx.free()
+
+
+def test_graph_errors(sa, small):
+    idx, Xb, Qb, nbr, kn = small
+    Qd = bits_to_tensor(Qb).cuda()
+    with pytest.raises(sa.SAError):
+        idx.search_graph(Qd, 10, 8)                   # k > L
+    with pytest.raises(sa.SAError):
+        idx.search_graph(Qd, 10, 64, search_width=32)  # w * R > 256
+    flat = sa.Index.build(bits_to_tensor(Xb[:1000]).cuda(), 0)
+    with pytest.raises(sa.SAError) as e:
+        flat.build_graph()
+    assert e.value.status == sa.SA_ERR_STATE
+    flat.free()

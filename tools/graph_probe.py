@@ -1,0 +1,83 @@
+"""tools/graph_probe.py -- graph index build time, recall@10 and q/s per search range on the
+C3 corpus (or --n rows).  One JSON line.
+
+  python tools/graph_probe.py [--n 21015324] [--knn 64] [--degree 32] [--nprobe-build 8]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2505_12065_b200 as sa  # noqa: E402
+from datagen import CONFIGS, CORPUS_SEED, QUERY_SEED, make_mixture, draw_rows_into  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=CONFIGS["c3"]["n"])
+    ap.add_argument("--nlist", type=int, default=16384)
+    ap.add_argument("--knn", type=int, default=64)
+    ap.add_argument("--degree", type=int, default=32)
+    ap.add_argument("--nprobe-build", type=int, default=8)
+    ap.add_argument("--nq", type=int, default=512)
+    ap.add_argument("--ranges", default="16,32,48,64,96,128,192,256")
+    ap.add_argument("--widths", default="1,2,4")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS["c3"])
+    n, d = args.n, cfg["d"]
+    mix = make_mixture(d, cfg["C"], cfg["r"], cfg["s_sub"], cfg["s_n"], CORPUS_SEED, "cuda")
+    X = torch.empty(n, d, dtype=torch.bfloat16, device="cuda")
+    draw_rows_into(mix, X, CORPUS_SEED, 0)
+    t0 = time.perf_counter()
+    idx = sa.Index.build(X, args.nlist)
+    torch.cuda.synchronize()
+    ivf_s = time.perf_counter() - t0
+    del X
+    torch.cuda.empty_cache()
+    t0 = time.perf_counter()
+    idx.build_graph(knn_k=args.knn, degree=args.degree, nprobe_build=args.nprobe_build)
+    torch.cuda.synchronize()
+    graph_s = time.perf_counter() - t0
+    Q = torch.empty(4 * args.nq, d, dtype=torch.bfloat16, device="cuda")
+    draw_rows_into(mix, Q, QUERY_SEED, 0)
+    qs = [Q[i * args.nq:(i + 1) * args.nq] for i in range(4)]
+    gt = [idx.search(q, 10, 0)[0].cpu().numpy() for q in qs]
+    out = {"n": n, "nlist": args.nlist, "knn": args.knn, "degree": args.degree,
+           "nprobe_build": args.nprobe_build, "ivf_build_s": ivf_s, "graph_build_s": graph_s,
+           "nq": args.nq, "rows": []}
+    stream = torch.cuda.current_stream()
+    for w in [int(x) for x in args.widths.split(",")]:
+        for L in [int(x) for x in args.ranges.split(",")]:
+            rec, exp = [], []
+            for q, t in zip(qs, gt):
+                gi, _, ex = idx.search_graph(q, 10, L, search_width=w, n_entries=8, expanded=True)
+                gi = gi.cpu().numpy()
+                rec.append(np.mean([len(set(gi[i]) & set(t[i])) / 10 for i in range(len(t))]))
+                exp.append(ex.float().mean().item())
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for i in range(8):
+                idx.search_graph(qs[i % 4], 10, L, search_width=w, n_entries=8)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 8
+            out["rows"].append({"L": L, "w": w, "recall": float(np.mean(rec)),
+                                "expanded": float(np.mean(exp)), "ms_per_batch": ms,
+                                "qps": args.nq / (ms / 1e3)})
+            print(json.dumps(out["rows"][-1]), file=sys.stderr, flush=True)
+    print(json.dumps(out))
+    idx.free()
+
+
+if __name__ == "__main__":
+    main()
