@@ -169,6 +169,8 @@ def run_reference(args, cfg, name):
 
 # ------------------------------------------------------------------ GPU arm
 NPROBE_LADDER = (8, 16, 24, 32, 36, 40, 44, 48, 52, 56, 64, 80, 96, 128, 192, 256)
+GRAPH_L = (64, 96, 112, 128, 144, 160, 176, 192, 224, 256)   # search range ladder
+GRAPH_W, GRAPH_E = 4, 16                                     # search width, entry lists
 RECALL_TARGET = 0.95
 CALIBRATION_MARGIN = 0.005   # calibrate at >= 0.955 so the timed batches' mean stays >= 0.95
 
@@ -184,15 +186,21 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
-    ap.add_argument("--mode", default="auto", choices=["auto", "exact", "ivf"],
-                    help="auto: IVF at the smallest nprobe with recall@10 >= 0.95 (headline), "
-                         "plus the exact mode; exact: flat scan only; ivf: fixed --nprobe")
+    ap.add_argument("--mode", default="auto", choices=["auto", "exact", "ivf", "graph"],
+                    help="auto: the fastest of IVF (smallest nprobe with recall@10 >= 0.95), "
+                         "the proximity graph (smallest search range with recall@10 >= 0.95) "
+                         "and the exact mode; exact: flat scan only; ivf: fixed --nprobe; "
+                         "graph: graph only (calibrated search range)")
     ap.add_argument("--nprobe", type=int, default=0)
     ap.add_argument("--nlist", type=int, default=16384)
     ap.add_argument("--nq", type=int, default=None, help="override batch size")
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--d", type=int, default=None, help="override dimension (experiments)")
     ap.add_argument("--n", type=int, default=None, help="override corpus rows (experiments)")
+    ap.add_argument("--no-graph", action="store_true", help="skip the proximity-graph mode")
+    ap.add_argument("--graph-knn", type=int, default=64)
+    ap.add_argument("--graph-degree", type=int, default=32)
+    ap.add_argument("--graph-nprobe-build", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simulate-world", type=int, default=0,
@@ -235,7 +243,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = sa.Comm.from_torch_distributed(local)
     mode = args.mode
-    use_ivf = mode in ("auto", "ivf")
+    use_ivf = mode in ("auto", "ivf", "graph")
+    use_graph = mode in ("auto", "graph") and not args.no_graph and world == 1
     nlist = args.nlist if use_ivf else 0
 
     n, d, nq, k = cfg["n"], cfg["d"], cfg["nq"], cfg["k"]
@@ -261,6 +270,15 @@ def main():
     build_s = time.perf_counter() - t0
     del X
     torch.cuda.empty_cache()
+    graph_build_s = None
+    if use_graph and nlist > 0:
+        t0 = time.perf_counter()
+        idx.build_graph(knn_k=args.graph_knn, degree=args.graph_degree,
+                        nprobe_build=args.graph_nprobe_build)
+        torch.cuda.synchronize()
+        graph_build_s = time.perf_counter() - t0
+    else:
+        use_graph = False
 
     nb = args.warmup + args.steps
     Qall = torch.empty(nb * nq, d, dtype=torch.bfloat16, device="cuda")
@@ -282,10 +300,16 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def run_search(i, nprobe):
+        if isinstance(nprobe, tuple):          # ("graph", L)
+            return idx.search_graph(batches[i], k, nprobe[1], search_width=GRAPH_W,
+                                    n_entries=GRAPH_E)
+        return idx.search(batches[i], k, nprobe, out=(ids, scores))
+
     def timed(nprobe):
         """W warm-up + K timed search steps; returns (ms, per-kind kernel (ms, launches), clocks)."""
         for i in range(args.warmup):
-            idx.search(batches[i], k, nprobe, out=(ids, scores))
+            run_search(i, nprobe)
         barrier()
         sa.profile_enable(True)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -293,7 +317,7 @@ def main():
             barrier()
             ev0.record(stream)
             for i in range(args.steps):
-                idx.search(batches[args.warmup + i], k, nprobe, out=(ids, scores))
+                run_search(args.warmup + i, nprobe)
             ev1.record(stream)
             barrier()
         ms = max_over_ranks(ev0.elapsed_time(ev1))
@@ -353,7 +377,7 @@ def main():
                          "traffic": traffic_from_profiles("flat_scan", args.config, nq)},
         }
     result_ivf = None
-    if use_ivf:
+    if use_ivf and mode != "graph":
         ms_i, kern_i, clk_i = timed(nprobe)
         rec = []
         for i in range(args.warmup, nb):
@@ -387,17 +411,70 @@ def main():
                          "traffic": traffic_from_profiles("ivf_scan", args.config, nq)},
         }
 
-    # headline: the faster of the modes that meet recall@10 >= 0.95
-    cands = [r for r in (result_ivf, result_exact) if r is not None and r["recall"] >= RECALL_TARGET]
+    result_graph = None
+    if use_graph:
+        gsweep, L = [], GRAPH_L[-1]
+        calib = list(range(args.warmup, min(nb, args.warmup + 2)))
+        for Lc in GRAPH_L:
+            r = float(np.mean([recall_at_k(run_search(i, ("graph", Lc))[0], gt[i]) for i in calib]))
+            gsweep.append({"search_range": Lc, "recall": r})
+            if r >= RECALL_TARGET + CALIBRATION_MARGIN:
+                L = Lc
+                break
+        ms_g, kern_g, clk_g = timed(("graph", L))
+        rec, byts = [], []
+        for i in range(args.warmup, nb):
+            gi, _, ex, scd = idx.search_graph(batches[i], k, L, search_width=GRAPH_W,
+                                              n_entries=GRAPH_E, expanded=True)
+            rec.append(recall_at_k(gi, gt[i]))
+            # algorithmic bytes: every scored row (d_pad bf16) + every expanded list (R ids)
+            byts.append(float(scd.sum().item()) * d * 2 + float(ex.sum().item()) * args.graph_degree * 4)
+        gs_ms, gs_n = kern_g["graph_search"]
+        per_launch = gs_ms / max(gs_n, 1)
+        achieved = float(np.mean(byts)) / (per_launch / 1e3) / 1e9
+        result_graph = {
+            "value": args.steps * nq / (ms_g / 1e3), "unit": "queries/s",
+            "recall": float(np.mean(rec)), "search_range": L, "search_width": GRAPH_W,
+            "n_entries": GRAPH_E, "knn_k": args.graph_knn, "degree": args.graph_degree,
+            "nprobe_build": args.graph_nprobe_build, "build_s": graph_build_s, "sweep": gsweep,
+            "ms_per_step": ms_g / args.steps, "clocks": clk_g,
+            "kernel_ms": {kk: v[0] for kk, v in kern_g.items()},
+            "kernel_launches": {kk: v[1] for kk, v in kern_g.items()},
+            "algorithmic_bytes_per_step": float(np.mean(byts)),
+            "roofline": {"kernel": "graph_search_kernel", "bound": "hbm",
+                         "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
+                         "frac": achieved / pk["hbm"],
+                         "peak_kind": f"HBM copy, {pk['src']} (MEASURED_PEAKS.json); the kernel "
+                                      "gathers random 1.5 KB rows",
+                         "frac_of_8TBs": achieved / 8000.0,
+                         "kernel_ms": per_launch, "kernel_share_of_step": gs_ms / ms_g,
+                         "traffic": traffic_from_profiles("graph_search", args.config, nq)},
+        }
+
+    # headline: the fastest of the modes that meet recall@10 >= 0.95
+    cands = [r for r in (result_graph, result_ivf, result_exact)
+             if r is not None and r["recall"] >= RECALL_TARGET]
     head = max(cands, key=lambda r: r["value"]) if cands else (result_ivf or result_exact)
-    head_nprobe = head.get("nprobe", 0)
+    head_is_graph = head is result_graph
+    head_nprobe = result_ivf["nprobe"] if (head_is_graph and result_ivf) else head.get("nprobe", 0)
 
     # ---- end to end through the host-buffer C-ABI call (H2D + search + D2H per step)
     qh = [batches[i].float().cpu().pin_memory() for i in range(nb)]
     ids_h = torch.empty(nq, k, dtype=torch.int64).pin_memory()
     sc_h = torch.empty(nq, k, dtype=torch.float32).pin_memory()
+
+    def host_search(qhost):
+        if head_is_graph:   # public API: pinned host -> device, sa_search_graph, device -> host
+            gi, gs = idx.search_graph(qhost.to("cuda", non_blocking=True), k, head["search_range"],
+                                      search_width=GRAPH_W, n_entries=GRAPH_E)
+            ids_h.copy_(gi, non_blocking=True)
+            sc_h.copy_(gs, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        else:
+            idx.search_host(qhost, k, head_nprobe, out=(ids_h, sc_h))
+
     for i in range(args.warmup):
-        idx.search_host(qh[i], k, head_nprobe, out=(ids_h, sc_h))
+        host_search(qh[i])
     barrier()
     lat = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -405,14 +482,18 @@ def main():
         t_s = time.perf_counter()
         if i == 0:
             e0.record(stream)
-        idx.search_host(qh[args.warmup + i], k, head_nprobe, out=(ids_h, sc_h))
+        host_search(qh[args.warmup + i])
         lat.append(time.perf_counter() - t_s)
     e1.record(stream)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     e2e_value = args.steps * nq / (e2e_ms / 1e3)
 
-    mode_name = "exact flat" if head_nprobe == 0 else f"IVF nlist={nlist} nprobe={head_nprobe}"
+    if head_is_graph:
+        mode_name = (f"graph (kNN {args.graph_knn}, degree {args.graph_degree}) search range "
+                     f"{head['search_range']} width {GRAPH_W}")
+    else:
+        mode_name = "exact flat" if head_nprobe == 0 else f"IVF nlist={nlist} nprobe={head_nprobe}"
     line = {
         "metric": METRIC, "value": head["value"], "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
@@ -420,7 +501,9 @@ def main():
         "data": "synthetic (seeded low-rank Gaussian mixture, unit-norm; DESIGN.md §3)",
         "config": {"workload": f"{args.config}: {mode_name} top-{k}, {n}x{d} bf16 corpus, "
                                f"batch {nq}",
-                   "n": n, "d": d, "nq": nq, "k": k, "nprobe": head_nprobe, "nlist": nlist,
+                   "n": n, "d": d, "nq": nq, "k": k,
+                   "nprobe": None if head_is_graph else head_nprobe, "nlist": nlist,
+                   "search_range": head.get("search_range"),
                    "recall_at_k": head["recall"], "n_local": n_local,
                    "parallelism": f"row-shard x{world}",
                    "l2": "inputs larger than L2 (corpus 32 GB >> 126 MB); no flush"},
@@ -432,8 +515,8 @@ def main():
         "gpu_launches": int(sum(v for v in head["kernel_launches"].values())),
         "kernel_ms": head["kernel_ms"], "kernel_launches": head["kernel_launches"],
         "clocks": head["clocks"],
-        "exact": result_exact, "ivf": result_ivf,
-        "build_s": build_s, "gen_s": gen_s,
+        "exact": result_exact, "ivf": result_ivf, "graph": result_graph,
+        "build_s": build_s, "graph_build_s": graph_build_s, "gen_s": gen_s,
     }
     # ---- agent-step batches (BASELINE config 5 shape): p50/p99 latency of one sa_search_host
     # call (H2D + search + D2H) at the headline nprobe, closed loop, per batch size
@@ -454,6 +537,28 @@ def main():
                       "p50_ms": 1e3 * float(np.percentile(ts, 50)),
                       "p99_ms": 1e3 * float(np.percentile(ts, 99))})
     line["agent_step_latency"] = agent
+    if result_graph is not None:
+        # the same agent-step batches through the graph index (pinned H2D, search, D2H)
+        agent_g = []
+        for b in (1, 8, 64):
+            qb = [batches[(args.warmup + i) % nb][:b].float().cpu().pin_memory() for i in range(8)]
+            ih = torch.empty(b, 5, dtype=torch.int64).pin_memory()
+            sh = torch.empty(b, 5, dtype=torch.float32).pin_memory()
+            Lg = max(5, result_graph["search_range"])
+            ts = []
+            for i in range(105):
+                t_s = time.perf_counter()
+                gi, gs = idx.search_graph(qb[i % 8].to("cuda", non_blocking=True), 5, Lg,
+                                          search_width=GRAPH_W, n_entries=GRAPH_E)
+                ih.copy_(gi, non_blocking=True)
+                sh.copy_(gs, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                if i >= 5:
+                    ts.append(time.perf_counter() - t_s)
+            agent_g.append({"batch": b, "k": 5, "search_range": Lg,
+                            "p50_ms": 1e3 * float(np.percentile(ts, 50)),
+                            "p99_ms": 1e3 * float(np.percentile(ts, 99))})
+        line["agent_step_latency_graph"] = agent_g
     # ---- non-stall maturity exit (PAPER §3.3; full grid: bench.py --maturity), batch 1, k=5
     if use_ivf and nlist >= 128 and world == 1:   # maturity exit: unsharded indexes only
         qs = [batches[i][:1].contiguous() for i in range(args.warmup, min(nb, args.warmup + 16))]

@@ -192,11 +192,11 @@ sa_status sa_search_mature(const sa_index* idx, const void* queries, sa_dtype qd
  * n*(knn_k*4 + degree*12)).
  * sa_search_graph (R27): beam search per query over a list of search_range (L) entries,
  * expanding the search_width (w) best unexpanded entries per iteration, at most max_iters
- * iterations (also capped so the visited set fits: iterations <= (8192 - E) / (w*degree));
+ * iterations (also capped so the visited set fits: iterations <= (6144 - E) / (w*degree));
  * entry points = the first stored row (lowest id) of each of the n_entries (E) best IVF
  * lists of the query.  queries DEVICE [nq, d] of qdtype; out_ids DEVICE int64 [nq, k],
  * out_scores DEVICE fp32 [nq, k] (score desc, id asc; padded -1 / -INF), out_expanded
- * DEVICE int32 [nq] (entries expanded; may be NULL).  1 <= k <= L <= 256,
+ * DEVICE int32 [2, nq] (row 0: list entries expanded, row 1: rows scored; may be NULL).  1 <= k <= L <= 256,
  * w*degree <= 256, 1 <= E <= min(nlist, 256).  Stream-ordered, asynchronous.
  * sa_index_export_graph: *degree, host_nbr HOST int64 [n_local, degree] (row = global id -
  * row_offset, entries global ids, -1 padded), host_knn HOST int64 [n_local, knn_k] likewise

@@ -325,12 +325,13 @@ class Index:
         nq = queries.shape[0]
         ids = torch.empty(nq, k, dtype=torch.int64, device=queries.device)
         scores = torch.empty(nq, k, dtype=torch.float32, device=queries.device)
-        ex = torch.empty(nq, dtype=torch.int32, device=queries.device) if expanded else None
+        ex = torch.empty(2, nq, dtype=torch.int32, device=queries.device) if expanded else None
         _check(lib().sa_search_graph(self.handle, _ptr(queries), _dtype_code(queries), nq, k,
                                      search_range, search_width, n_entries,
                                      min(max_iters, 2**31 - 1), _ptr(ids), _ptr(scores),
                                      _ptr(ex) if expanded else None, _stream_ptr(stream)))
-        return (ids, scores, ex) if expanded else (ids, scores)
+        # expanded: (entries expanded [nq], rows scored [nq])
+        return (ids, scores, ex[0], ex[1]) if expanded else (ids, scores)
 
     def export_graph(self, knn: bool = False):
         inf = self.info()

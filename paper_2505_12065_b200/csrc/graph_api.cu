@@ -123,7 +123,7 @@ sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdt
   if (E < 1 || E > std::min(idx->nlist, 256))
     return set_error(SA_ERR_INVALID_ARG, "need 1 <= n_entries <= min(nlist, 256)");
   if (max_iters < 0) return set_error(SA_ERR_INVALID_ARG, "max_iters must be >= 0");
-  const int T = std::min(max_iters, (GR_HASH / 2 - E) / (w * R));
+  const int T = std::min(max_iters, (GR_VISIT_CAP - E) / (w * R));
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t nq_pad = padded_nq(nq);
   __nv_bfloat16* Qs = nullptr;
@@ -175,6 +175,7 @@ sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdt
     a.out_ids = out_ids;
     a.out_scores = out_scores;
     a.out_expanded = out_expanded;
+    a.nq = (int32_t)nq;
     prof_begin(SA_KERNEL_GRAPH_SEARCH, s);
     st = cuda_status(launch_graph_search(a, nq, s), "graph search");
     prof_end(SA_KERNEL_GRAPH_SEARCH, s);

@@ -229,22 +229,23 @@ __global__ void __launch_bounds__(256) graph_merge_kernel(const int32_t* __restr
 // ------------------------------------------------------------------ search
 constexpr int kSThreads = 256;
 constexpr int kSWarps = kSThreads / 32;
-constexpr int kRowsPerWarp = 4;
+constexpr int kRowsPerWarp = 3;
 
 struct SearchSmem {
   uint32_t hash[GR_HASH];
+  float q[768];
   unsigned long long key[2][GR_MAX_L];
   int32_t pos[2][GR_MAX_L];
   uint8_t flag[2][GR_MAX_L];
   unsigned long long nkey[GR_MAX_NEW];
   int32_t npos[GR_MAX_NEW];
   int32_t chosen[8];
-  int32_t n_new, n_chosen, cnt;
+  int32_t n_new, n_chosen;
 };
 
 __device__ __forceinline__ bool visit(uint32_t* hash, int32_t pos) {
   const uint32_t v = (uint32_t)pos + 1u;
-  uint32_t h = ((uint32_t)pos * 2654435761u) & (GR_HASH - 1);
+  uint32_t h = ((uint32_t)pos * 2654435761u) >> (32 - GR_HASH_LOG);
   while (true) {
     const uint32_t old = atomicCAS(&hash[h], 0u, v);
     if (old == 0u) return true;
@@ -254,20 +255,25 @@ __device__ __forceinline__ bool visit(uint32_t* hash, int32_t pos) {
 }
 
 __device__ __forceinline__ float bf16x8_dot(const uint4 v, const float* q) {
+  const float4 qa = *reinterpret_cast<const float4*>(q);
+  const float4 qb = *reinterpret_cast<const float4*>(q + 4);
   const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
-  float acc = 0.f;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const float2 f = __bfloat1622float2(b[e]);
-    acc = fmaf(f.x, q[2 * e], acc);
-    acc = fmaf(f.y, q[2 * e + 1], acc);
-  }
+  const float2 f0 = __bfloat1622float2(b[0]), f1 = __bfloat1622float2(b[1]);
+  const float2 f2 = __bfloat1622float2(b[2]), f3 = __bfloat1622float2(b[3]);
+  float acc = f0.x * qa.x;
+  acc = fmaf(f0.y, qa.y, acc);
+  acc = fmaf(f1.x, qa.z, acc);
+  acc = fmaf(f1.y, qa.w, acc);
+  acc = fmaf(f2.x, qb.x, acc);
+  acc = fmaf(f2.y, qb.y, acc);
+  acc = fmaf(f3.x, qb.z, acc);
+  acc = fmaf(f3.y, qb.w, acc);
   return acc;
 }
 
-// Score npos[0, cnt) into nkey (warp-cooperative, kRowsPerWarp rows in flight per warp).
-__device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, const float (&qf)[3][8],
-                           int cnt, int nchunk) {
+// Score npos[0, cnt) into nkey (warp-cooperative, kRowsPerWarp rows in flight per warp;
+// lane l holds 16-byte chunks l, l + 32, l + 64 of a row; the query is in smem).
+__device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, int nchunk) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint4* X4 = reinterpret_cast<const uint4*>(a.X);
   for (int j0 = warp * kRowsPerWarp; j0 < cnt; j0 += kSWarps * kRowsPerWarp) {
@@ -285,35 +291,15 @@ __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, const float
     }
 #pragma unroll
     for (int u = 0; u < kRowsPerWarp; ++u) {
-      float acc = bf16x8_dot(v[u][0], qf[0]) + bf16x8_dot(v[u][1], qf[1]) +
-                  bf16x8_dot(v[u][2], qf[2]);
+      float acc = 0.f;
+#pragma unroll
+      for (int rd = 0; rd < 3; ++rd)
+        if (rd * 32 + lane < nchunk) acc += bf16x8_dot(v[u][rd], sm.q + (rd * 32 + lane) * 8);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0 && p[u] >= 0) sm.nkey[j0 + u] = make_key(acc, (uint32_t)a.row_ids[p[u]]);
     }
   }
-}
-
-// Bitonic sort of (nkey, npos)[0, n2) descending by key.
-__device__ void sort_new(SearchSmem& sm, int n2) {
-  for (int sz = 2; sz <= n2; sz <<= 1)
-    for (int st = sz >> 1; st > 0; st >>= 1) {
-      for (int i = threadIdx.x; i < n2; i += kSThreads) {
-        const int j = i ^ st;
-        if (j > i) {
-          const bool desc = (i & sz) == 0;
-          const unsigned long long x = sm.nkey[i], y = sm.nkey[j];
-          if (desc ? x < y : x > y) {
-            sm.nkey[i] = y;
-            sm.nkey[j] = x;
-            const int32_t t = sm.npos[i];
-            sm.npos[i] = sm.npos[j];
-            sm.npos[j] = t;
-          }
-        }
-      }
-      __syncthreads();
-    }
 }
 
 // number of entries of the descending array a[0, n) that are > x
@@ -328,35 +314,20 @@ __device__ __forceinline__ int count_greater(const unsigned long long* a, int n,
   return lo;
 }
 
-__global__ void __launch_bounds__(kSThreads) graph_search_kernel(const GraphSearchArgs a) {
+__global__ void __launch_bounds__(kSThreads, 4) graph_search_kernel(const GraphSearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   SearchSmem& sm = *reinterpret_cast<SearchSmem*>(smem_raw);
   const int q = blockIdx.x;
   const int lane = threadIdx.x % 32;
   const int nchunk = a.d_pad / 8;
   for (int i = threadIdx.x; i < GR_HASH; i += kSThreads) sm.hash[i] = 0u;
-  // query in registers: lane holds 16-byte chunks lane, lane + 32, lane + 64
-  float qf[3][8];
-  {
-    const uint4* Q4 = reinterpret_cast<const uint4*>(a.Q) + (int64_t)q * nchunk;
-#pragma unroll
-    for (int rd = 0; rd < 3; ++rd) {
-      const int c = rd * 32 + lane;
-      const uint4 v = c < nchunk ? Q4[c] : make_uint4(0, 0, 0, 0);
-      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(b[e]);
-        qf[rd][2 * e] = f.x;
-        qf[rd][2 * e + 1] = f.y;
-      }
-    }
-  }
+  for (int i = threadIdx.x; i < a.d_pad; i += kSThreads)
+    sm.q[i] = __bfloat162float(a.Q[(int64_t)q * a.d_pad + i]);
   if (threadIdx.x == 0) sm.n_new = 0;
   __syncthreads();
   // entries: the first stored row of each probed list (lists hold ascending global ids)
-  if (threadIdx.x < a.E) {
-    const uint64_t pk = a.entry_keys[(int64_t)q * a.E + threadIdx.x];
+  for (int e = threadIdx.x; e < a.E; e += kSThreads) {
+    const uint64_t pk = a.entry_keys[(int64_t)q * a.E + e];
     if (pk != 0ull) {
       const uint32_t l = key_id(pk);
       const int64_t lo = a.list_off[l], hi = a.list_off[l + 1];
@@ -366,25 +337,20 @@ __global__ void __launch_bounds__(kSThreads) graph_search_kernel(const GraphSear
   __syncthreads();
   int cur = 0;
   int n_new = sm.n_new;
-  score_rows(a, sm, qf, n_new, nchunk);
+  score_rows(a, sm, n_new, nchunk);
   __syncthreads();
   int cnt = 0;
   int expanded = 0;
+  int scored = n_new;
   for (int it = 0;; ++it) {
-    // ---- merge the scored new rows into the sorted list (top-L)
+    // ---- merge the new rows into the sorted list (top-L); keys are distinct, so an entry's
+    // new position = its rank in the old list + the number of new keys above it (and v.v.)
     if (n_new > 0) {
-      int n2 = 1;
-      while (n2 < n_new) n2 <<= 1;
-      for (int i = n_new + threadIdx.x; i < n2; i += kSThreads) {
-        sm.nkey[i] = 0ull;
-        sm.npos[i] = -1;
-      }
-      __syncthreads();
-      sort_new(sm, n2);
       const int nxt = cur ^ 1;
       for (int i = threadIdx.x; i < cnt; i += kSThreads) {
         const unsigned long long x = sm.key[cur][i];
-        const int np = i + count_greater(sm.nkey, n_new, x);
+        int np = i;
+        for (int j = 0; j < n_new; ++j) np += sm.nkey[j] > x;
         if (np < a.L) {
           sm.key[nxt][np] = x;
           sm.pos[nxt][np] = sm.pos[cur][i];
@@ -393,7 +359,8 @@ __global__ void __launch_bounds__(kSThreads) graph_search_kernel(const GraphSear
       }
       for (int j = threadIdx.x; j < n_new; j += kSThreads) {
         const unsigned long long x = sm.nkey[j];
-        const int np = j + count_greater(sm.key[cur], cnt, x);
+        int np = count_greater(sm.key[cur], cnt, x);
+        for (int t = 0; t < n_new; ++t) np += sm.nkey[t] > x;
         if (np < a.L) {
           sm.key[nxt][np] = x;
           sm.pos[nxt][np] = sm.npos[j];
@@ -438,7 +405,8 @@ __global__ void __launch_bounds__(kSThreads) graph_search_kernel(const GraphSear
     }
     __syncthreads();
     n_new = sm.n_new;
-    score_rows(a, sm, qf, n_new, nchunk);
+    scored += n_new;
+    score_rows(a, sm, n_new, nchunk);
     __syncthreads();
   }
   for (int i = threadIdx.x; i < a.k; i += kSThreads) {
@@ -446,7 +414,10 @@ __global__ void __launch_bounds__(kSThreads) graph_search_kernel(const GraphSear
     a.out_ids[(int64_t)q * a.k + i] = key == 0ull ? -1 : (int64_t)key_id(key);
     a.out_scores[(int64_t)q * a.k + i] = key == 0ull ? -INFINITY : key_score(key);
   }
-  if (a.out_expanded && threadIdx.x == 0) a.out_expanded[q] = expanded;
+  if (a.out_expanded && threadIdx.x == 0) {
+    a.out_expanded[q] = expanded;
+    a.out_expanded[a.nq + q] = scored;
+  }
 }
 
 }  // namespace

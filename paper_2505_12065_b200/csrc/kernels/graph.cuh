@@ -11,7 +11,9 @@ constexpr int GR_MAX_K = 64;       // kNN list length (build)
 constexpr int GR_MAX_R = 64;       // graph degree
 constexpr int GR_MAX_L = 256;      // search list (search range)
 constexpr int GR_MAX_NEW = 256;    // w * R per iteration
-constexpr int GR_HASH = 16384;     // visited-set slots per query (smem, 64 KB)
+constexpr int GR_HASH_LOG = 13;
+constexpr int GR_HASH = 1 << GR_HASH_LOG;  // visited-set slots per query (smem, 32 KB)
+constexpr int GR_VISIT_CAP = GR_HASH * 3 / 4;  // visited nodes per query (load <= 3/4)
 
 // kNN ids from the IVF search (global ids [nb, kk], best first, -1 padded) -> stored positions
 // [nb, K] without the row itself (R22).  row p0 + b is row b of the batch.
@@ -43,7 +45,8 @@ struct GraphSearchArgs {
   int32_t d_pad, R, L, w, E, T, k;
   int64_t* out_ids;         // [nq, k]
   float* out_scores;        // [nq, k]
-  int32_t* out_expanded;    // optional [nq]
+  int32_t* out_expanded;    // optional [2, nq]: entries expanded, rows scored
+  int32_t nq;
 };
 size_t graph_search_smem(int L);
 cudaError_t launch_graph_search(const GraphSearchArgs& a, int64_t nq, cudaStream_t s);

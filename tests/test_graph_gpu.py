@@ -80,7 +80,7 @@ def test_beam_search_matches_oracle(sa, small):
     ent = entries_of(idx, Qb, 4)
     same, rec = 0, []
     for L, w in ((32, 1), (64, 4), (128, 2)):
-        gi, gs, gx = idx.search_graph(bits_to_tensor(Qb).cuda(), 10, L, search_width=w,
+        gi, gs, gx, _ = idx.search_graph(bits_to_tensor(Qb).cuda(), 10, L, search_width=w,
                                       n_entries=4, expanded=True)
         gi, gs, gx = gi.cpu().numpy(), gs.cpu().numpy(), gx.cpu().numpy()
         for q in range(len(Qb)):
@@ -104,9 +104,9 @@ def test_exhaustive_beam_is_brute_force_over_reachable(sa):
     idx.build_graph(knn_k=16, degree=8, nprobe_build=2)
     nbr = idx.export_graph()
     ent = entries_of(idx, Qb, 2)
-    gi, gs, gx = idx.search_graph(bits_to_tensor(Qb).cuda(), 10, 256, search_width=2,
-                                  n_entries=2, expanded=True)
-    gi, gs, gx = gi.cpu().numpy(), gs.cpu().numpy(), gx.cpu().numpy()
+    gi, gs, gx, gsc = idx.search_graph(bits_to_tensor(Qb).cuda(), 10, 256, search_width=2,
+                                       n_entries=2, expanded=True)
+    gi, gs, gx, gsc = gi.cpu().numpy(), gs.cpu().numpy(), gx.cpu().numpy(), gsc.cpu().numpy()
     for q in range(len(Qb)):
         seen, todo = set(ent[q]), list(ent[q])
         while todo:
@@ -116,7 +116,7 @@ def test_exhaustive_beam_is_brute_force_over_reachable(sa):
                     seen.add(int(v))
                     todo.append(int(v))
         reach = np.array(sorted(seen))
-        assert gx[q] == reach.size
+        assert gx[q] == reach.size and gsc[q] == reach.size   # each node expanded/scored once
         oi, osc = oracle.flat_topk(Xb[reach], Qb[q:q + 1], 18)
         oi = np.where(oi >= 0, reach[np.maximum(oi, 0)], -1)
         r = check(gi[q:q + 1], gs[q:q + 1], oi, osc,

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--nq", type=int, default=512)
     ap.add_argument("--ranges", default="16,32,48,64,96,128,192,256")
     ap.add_argument("--widths", default="1,2,4")
+    ap.add_argument("--entries", default="8")
     args = ap.parse_args()
     cfg = dict(CONFIGS["c3"])
     n, d = args.n, cfg["d"]
@@ -55,11 +56,13 @@ def main():
            "nprobe_build": args.nprobe_build, "ivf_build_s": ivf_s, "graph_build_s": graph_s,
            "nq": args.nq, "rows": []}
     stream = torch.cuda.current_stream()
-    for w in [int(x) for x in args.widths.split(",")]:
-        for L in [int(x) for x in args.ranges.split(",")]:
+    for E, w, L in [(E, w, L) for E in [int(x) for x in args.entries.split(",")]
+                    for w in [int(x) for x in args.widths.split(",")]
+                    for L in [int(x) for x in args.ranges.split(",")]]:
+        if True:
             rec, exp = [], []
             for q, t in zip(qs, gt):
-                gi, _, ex = idx.search_graph(q, 10, L, search_width=w, n_entries=8, expanded=True)
+                gi, _, ex, sc_rows = idx.search_graph(q, 10, L, search_width=w, n_entries=E, expanded=True)
                 gi = gi.cpu().numpy()
                 rec.append(np.mean([len(set(gi[i]) & set(t[i])) / 10 for i in range(len(t))]))
                 exp.append(ex.float().mean().item())
@@ -67,11 +70,11 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for i in range(8):
-                idx.search_graph(qs[i % 4], 10, L, search_width=w, n_entries=8)
+                idx.search_graph(qs[i % 4], 10, L, search_width=w, n_entries=E)
             e1.record(stream)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 8
-            out["rows"].append({"L": L, "w": w, "recall": float(np.mean(rec)),
+            out["rows"].append({"L": L, "w": w, "E": E, "recall": float(np.mean(rec)),
                                 "expanded": float(np.mean(exp)), "ms_per_batch": ms,
                                 "qps": args.nq / (ms / 1e3)})
             print(json.dumps(out["rows"][-1]), file=sys.stderr, flush=True)
