@@ -170,7 +170,7 @@ def run_reference(args, cfg, name):
 # ------------------------------------------------------------------ GPU arm
 NPROBE_LADDER = (8, 16, 24, 32, 36, 40, 44, 48, 52, 56, 64, 80, 96, 128, 192, 256)
 GRAPH_L = (64, 96, 112, 128, 144, 160, 176, 192, 224, 256)   # search range ladder
-GRAPH_W, GRAPH_E = 4, 16                                     # search width, entry lists
+GRAPH_W, GRAPH_E = 8, 16                                     # search width, entry lists
 RECALL_TARGET = 0.95
 CALIBRATION_MARGIN = 0.005   # calibrate at >= 0.955 so the timed batches' mean stays >= 0.95
 

@@ -67,13 +67,16 @@ def main():
                 rec.append(np.mean([len(set(gi[i]) & set(t[i])) / 10 for i in range(len(t))]))
                 exp.append(ex.float().mean().item())
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for i in range(8):
-                idx.search_graph(qs[i % 4], 10, L, search_width=w, n_entries=E)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / 8
+            reps = []
+            for rep in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for i in range(8):
+                    idx.search_graph(qs[i % 4], 10, L, search_width=w, n_entries=E)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                reps.append(e0.elapsed_time(e1) / 8)
+            ms = float(np.median(reps))
             out["rows"].append({"L": L, "w": w, "E": E, "recall": float(np.mean(rec)),
                                 "expanded": float(np.mean(exp)), "ms_per_batch": ms,
                                 "qps": args.nq / (ms / 1e3)})
