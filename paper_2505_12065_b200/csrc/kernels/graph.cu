@@ -8,7 +8,8 @@
 // candidate list of L entries (the search range), expanding the w best unexpanded entries
 // per iteration; neighbour rows (1.5 KB bf16 each) are gathered by whole warps with 16-byte
 // loads, 3 rows (and their global ids) in flight per warp; the visited set is an exact open-addressing table in
-// shared memory; the list is kept sorted by merge path.  Memory-latency bound: a query's
+// shared memory; scored rows below the list's L-th key are dropped at once and the few
+// survivors are merged into the sorted list by rank counting.  Memory-latency bound: a query's
 // iterations are dependent gathers, so several CTAs per SM hide each other's latency.
 #include <cuda_bf16.h>
 
@@ -234,10 +235,11 @@ struct SearchSmem {
   unsigned long long key[2][GR_MAX_L];
   int32_t pos[2][GR_MAX_L];
   uint8_t flag[2][GR_MAX_L];
-  unsigned long long nkey[GR_MAX_NEW];
-  int32_t npos[GR_MAX_NEW];
+  int32_t npos[GR_MAX_NEW];               // rows to score this iteration
+  unsigned long long nkey[GR_MAX_NEW];    // scored rows that can enter the list
+  int32_t ipos[GR_MAX_NEW];
   int32_t chosen[8];
-  int32_t n_new, n_chosen;
+  int32_t n_new, n_ins, n_chosen;
 };
 
 __device__ __forceinline__ bool visit(uint32_t* hash, int32_t pos) {
@@ -270,8 +272,11 @@ __device__ __forceinline__ float bf16x8_dot(const uint4 v, const float* q) {
 
 // Score npos[0, cnt) into nkey (warp-cooperative, kRowsPerWarp rows in flight per warp;
 // lane l holds 16-byte chunks l, l + 32, l + 64 of a row; the query is in smem).
+// Rows whose key is not above `floor` (the list's L-th key once the list is full) cannot enter
+// the list and are dropped here; the survivors go to (nkey, ipos)[0, n_ins).
 template <int kSThreads, int kRowsPerWarp>
-__device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, int nchunk) {
+__device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, int nchunk,
+                           unsigned long long floor) {
   constexpr int kSWarps = kSThreads / 32;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint4* X4 = reinterpret_cast<const uint4*>(a.X);
@@ -299,7 +304,14 @@ __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, in
         if (rd * 32 + lane < nchunk) acc += bf16x8_dot(v[u][rd], sm.q + (rd * 32 + lane) * 8);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0 && p[u] >= 0) sm.nkey[j0 + u] = make_key(acc, gid[u]);
+      if (lane == 0 && p[u] >= 0) {
+        const unsigned long long key = make_key(acc, gid[u]);
+        if (key > floor) {
+          const int t = atomicAdd(&sm.n_ins, 1);
+          sm.nkey[t] = key;
+          sm.ipos[t] = p[u];
+        }
+      }
     }
   }
 }
@@ -326,7 +338,10 @@ __global__ void __launch_bounds__(kSThreads, 4) graph_search_kernel(const GraphS
   for (int i = threadIdx.x; i < GR_HASH; i += kSThreads) sm.hash[i] = 0u;
   for (int i = threadIdx.x; i < a.d_pad; i += kSThreads)
     sm.q[i] = __bfloat162float(a.Q[(int64_t)q * a.d_pad + i]);
-  if (threadIdx.x == 0) sm.n_new = 0;
+  if (threadIdx.x == 0) {
+    sm.n_new = 0;
+    sm.n_ins = 0;
+  }
   __syncthreads();
   // entries: the first stored row of each probed list (lists hold ascending global ids)
   for (int e = threadIdx.x; e < a.E; e += kSThreads) {
@@ -340,37 +355,38 @@ __global__ void __launch_bounds__(kSThreads, 4) graph_search_kernel(const GraphS
   __syncthreads();
   int cur = 0;
   int n_new = sm.n_new;
-  score_rows<kSThreads, kRowsPerWarp>(a, sm, n_new, nchunk);
-  __syncthreads();
   int cnt = 0;
+  score_rows<kSThreads, kRowsPerWarp>(a, sm, n_new, nchunk, 0ull);
+  __syncthreads();
   int expanded = 0;
   int scored = n_new;
   for (int it = 0;; ++it) {
-    // ---- merge the new rows into the sorted list (top-L); keys are distinct, so an entry's
-    // new position = its rank in the old list + the number of new keys above it (and v.v.)
-    if (n_new > 0) {
+    // ---- merge the surviving new rows into the sorted list (top-L); keys are distinct, so an
+    // entry's new position = its rank in the old list + the number of new keys above it (v.v.)
+    const int n_ins = sm.n_ins;
+    if (n_ins > 0) {
       const int nxt = cur ^ 1;
       for (int i = threadIdx.x; i < cnt; i += kSThreads) {
         const unsigned long long x = sm.key[cur][i];
         int np = i;
-        for (int j = 0; j < n_new; ++j) np += sm.nkey[j] > x;
+        for (int j = 0; j < n_ins; ++j) np += sm.nkey[j] > x;
         if (np < a.L) {
           sm.key[nxt][np] = x;
           sm.pos[nxt][np] = sm.pos[cur][i];
           sm.flag[nxt][np] = sm.flag[cur][i];
         }
       }
-      for (int j = threadIdx.x; j < n_new; j += kSThreads) {
+      for (int j = threadIdx.x; j < n_ins; j += kSThreads) {
         const unsigned long long x = sm.nkey[j];
         int np = count_greater(sm.key[cur], cnt, x);
-        for (int t = 0; t < n_new; ++t) np += sm.nkey[t] > x;
+        for (int t = 0; t < n_ins; ++t) np += sm.nkey[t] > x;
         if (np < a.L) {
           sm.key[nxt][np] = x;
-          sm.pos[nxt][np] = sm.npos[j];
+          sm.pos[nxt][np] = sm.ipos[j];
           sm.flag[nxt][np] = 0;
         }
       }
-      cnt = min(a.L, cnt + n_new);
+      cnt = min(a.L, cnt + n_ins);
       cur = nxt;
       __syncthreads();
     }
@@ -395,6 +411,7 @@ __global__ void __launch_bounds__(kSThreads, 4) graph_search_kernel(const GraphS
       if (lane == 0) {
         sm.n_chosen = taken;
         sm.n_new = 0;
+        sm.n_ins = 0;
       }
     }
     __syncthreads();
@@ -409,7 +426,8 @@ __global__ void __launch_bounds__(kSThreads, 4) graph_search_kernel(const GraphS
     __syncthreads();
     n_new = sm.n_new;
     scored += n_new;
-    score_rows<kSThreads, kRowsPerWarp>(a, sm, n_new, nchunk);
+    score_rows<kSThreads, kRowsPerWarp>(a, sm, n_new, nchunk,
+                                        cnt == a.L ? sm.key[cur][a.L - 1] : 0ull);
     __syncthreads();
   }
   for (int i = threadIdx.x; i < a.k; i += kSThreads) {
