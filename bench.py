@@ -169,8 +169,8 @@ def run_reference(args, cfg, name):
 
 # ------------------------------------------------------------------ GPU arm
 NPROBE_LADDER = (8, 16, 24, 32, 36, 40, 44, 48, 52, 56, 64, 80, 96, 128, 192, 256)
-GRAPH_L = (64, 96, 112, 128, 144, 160, 176, 192, 224, 256)   # search range ladder
-GRAPH_W, GRAPH_E = 8, 16                                     # search width, entry lists
+GRAPH_L = (64, 80, 96, 104, 112, 120, 128, 144, 160, 192, 256)   # search range ladder
+GRAPH_W, GRAPH_E = 4, 16                                     # search width, entry lists
 RECALL_TARGET = 0.95
 CALIBRATION_MARGIN = 0.005   # calibrate at >= 0.955 so the timed batches' mean stays >= 0.95
 
@@ -199,8 +199,9 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override corpus rows (experiments)")
     ap.add_argument("--no-graph", action="store_true", help="skip the proximity-graph mode")
     ap.add_argument("--graph-knn", type=int, default=64)
-    ap.add_argument("--graph-degree", type=int, default=32)
+    ap.add_argument("--graph-degree", type=int, default=48)
     ap.add_argument("--graph-nprobe-build", type=int, default=8)
+    ap.add_argument("--graph-width", type=int, default=4, help="search width w")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simulate-world", type=int, default=0,
@@ -215,6 +216,8 @@ def main():
                          "64) and agent-step latency; prints one JSON line and exits")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    global GRAPH_W
+    GRAPH_W = args.graph_width
     cfg = dict(CONFIGS[args.config])
     if args.nq:
         cfg["nq"] = args.nq

@@ -7,6 +7,9 @@
 // kernels of graph.cu.  Search: stage queries, probe the IVF centroids for entry points
 // (tensor-core scores + exact top-E select), beam search (graph.cu).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "internal.h"
@@ -72,6 +75,20 @@ sa_status sa_index_build_graph(sa_index* idx, int32_t knn_k, int32_t degree, int
     cudaFree(nbr);
     return st;
   };
+  // SA_VERBOSE=1: phase timings on stderr (synchronises between phases)
+  static const bool verbose = [] {
+    const char* e = getenv("SA_VERBOSE");
+    return e && e[0] == '1';
+  }();
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    if (!verbose) return;
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[sa] graph build %s: %.3f s\n", name,
+            std::chrono::duration<double>(t - t_last).count());
+    t_last = t;
+  };
   sa_status st = cuda_status(launch_inverse_ids(idx->row_ids, n, idx->row_offset, pos_of, s),
                              "inverse ids");
   // R22: kNN lists, batch by batch of consecutive stored rows
@@ -85,11 +102,15 @@ sa_status sa_index_build_graph(sa_index* idx, int32_t knn_k, int32_t degree, int
       st = cuda_status(launch_knn_to_pos(ids, nb, kk, p0, pos_of, idx->row_offset, K, knn, s),
                        "kNN lists");
   }
+  phase("kNN lists (IVF search)");
   if (st == SA_OK) st = cuda_status(launch_graph_prune(knn, n, K, R, fwd, s), "graph prune");
+  phase("prune");
   if (st == SA_OK)
     st = cuda_status(cudaMemsetAsync(rev, 0xff, (size_t)n * R * sizeof(uint64_t), s), "memset");
   if (st == SA_OK) st = cuda_status(launch_graph_reverse(fwd, n, R, idx->row_ids, rev, s), "graph reverse");
+  phase("reverse");
   if (st == SA_OK) st = cuda_status(launch_graph_merge(fwd, rev, n, R, pos_of, idx->row_offset, nbr, s), "graph merge");
+  phase("merge");
   if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "graph build sync");
   if (st != SA_OK) return fail(st);
   cudaFree(idx->graph);
