@@ -146,65 +146,73 @@ sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdt
   if (max_iters < 0) return set_error(SA_ERR_INVALID_ARG, "max_iters must be >= 0");
   const int T = std::min(max_iters, (GR_VISIT_CAP - E) / (w * R));
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t nq_pad = padded_nq(nq);
-  __nv_bfloat16* Qs = nullptr;
-  float* psc = nullptr;
-  uint64_t* pkeys = nullptr;
-  sa_status st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "graph search");
-  if (st == SA_OK) st = dalloc(&psc, (size_t)nq * idx->nlist, s, "graph search");
-  if (st == SA_OK) st = dalloc(&pkeys, (size_t)nq * E, s, "graph search");
-  if (st == SA_OK) {
-    prof_begin(SA_KERNEL_STAGE, s);
-    st = cuda_status(launch_cast_pad(queries, qdtype == SA_F32, nq, idx->d, Qs, nq_pad,
-                                     idx->d_pad, idx->num_sms, s),
-                     "stage queries");
-    prof_end(SA_KERNEL_STAGE, s);
-    prof_count(SA_KERNEL_STAGE);
-  }
-  if (st == SA_OK) {
-    // entry points: the E best IVF lists (tensor-core centroid scores + exact select)
-    prof_begin(SA_KERNEL_IVF_PROBE, s);
-    const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, idx->nlist, idx->d_pad, nullptr, 0u};
-    st = flat_scores_view(cvc, idx->num_sms, Qs, nq, psc, s);
+  // queries in chunks: the probe's dense score buffer is chunk x nlist fp32
+  const int64_t C = 4096;
+  const size_t qsize = (size_t)idx->d * (qdtype == SA_F32 ? 4 : 2);
+  sa_status st = SA_OK;
+  for (int64_t q0 = 0; st == SA_OK && q0 < nq; q0 += C) {
+    const int64_t nc = std::min(C, nq - q0);
+    const int64_t nq_pad = padded_nq(nc);
+    __nv_bfloat16* Qs = nullptr;
+    float* psc = nullptr;
+    uint64_t* pkeys = nullptr;
+    st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "graph search");
+    if (st == SA_OK) st = dalloc(&psc, (size_t)nc * idx->nlist, s, "graph search");
+    if (st == SA_OK) st = dalloc(&pkeys, (size_t)nc * E, s, "graph search");
     if (st == SA_OK) {
-      MergeArgs m{};
-      m.cand_scores = psc;
-      m.m_flat = idx->nlist;
-      m.qstride = idx->nlist;
-      m.k = E;
-      m.out_keys = pkeys;
-      st = cuda_status(launch_merge(m, nq, s), "entry select");
-      prof_count(SA_KERNEL_MERGE);
+      prof_begin(SA_KERNEL_STAGE, s);
+      st = cuda_status(launch_cast_pad(static_cast<const uint8_t*>(queries) + q0 * qsize,
+                                       qdtype == SA_F32, nc, idx->d, Qs, nq_pad, idx->d_pad,
+                                       idx->num_sms, s),
+                       "stage queries");
+      prof_end(SA_KERNEL_STAGE, s);
+      prof_count(SA_KERNEL_STAGE);
     }
-    prof_end(SA_KERNEL_IVF_PROBE, s);
+    if (st == SA_OK) {
+      // entry points: the E best IVF lists (tensor-core centroid scores + exact select)
+      prof_begin(SA_KERNEL_IVF_PROBE, s);
+      const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, idx->nlist, idx->d_pad, nullptr, 0u};
+      st = flat_scores_view(cvc, idx->num_sms, Qs, nc, psc, s);
+      if (st == SA_OK) {
+        MergeArgs m{};
+        m.cand_scores = psc;
+        m.m_flat = idx->nlist;
+        m.qstride = idx->nlist;
+        m.k = E;
+        m.out_keys = pkeys;
+        st = cuda_status(launch_merge(m, nc, s), "entry select");
+        prof_count(SA_KERNEL_MERGE);
+      }
+      prof_end(SA_KERNEL_IVF_PROBE, s);
+    }
+    if (st == SA_OK) {
+      GraphSearchArgs a{};
+      a.X = idx->X;
+      a.row_ids = idx->row_ids;
+      a.nbr = idx->graph;
+      a.Q = Qs;
+      a.entry_keys = pkeys;
+      a.list_off = idx->list_off;
+      a.d_pad = idx->d_pad;
+      a.R = R;
+      a.L = L;
+      a.w = w;
+      a.E = E;
+      a.T = T;
+      a.k = k;
+      a.out_ids = out_ids + q0 * k;
+      a.out_scores = out_scores + q0 * k;
+      a.out_expanded = out_expanded ? out_expanded + q0 : nullptr;
+      a.nq = (int32_t)nq;   // row stride of out_expanded
+      prof_begin(SA_KERNEL_GRAPH_SEARCH, s);
+      st = cuda_status(launch_graph_search(a, nc, s), "graph search");
+      prof_end(SA_KERNEL_GRAPH_SEARCH, s);
+      prof_count(SA_KERNEL_GRAPH_SEARCH);
+    }
+    if (Qs) cudaFreeAsync(Qs, s);
+    if (psc) cudaFreeAsync(psc, s);
+    if (pkeys) cudaFreeAsync(pkeys, s);
   }
-  if (st == SA_OK) {
-    GraphSearchArgs a{};
-    a.X = idx->X;
-    a.row_ids = idx->row_ids;
-    a.nbr = idx->graph;
-    a.Q = Qs;
-    a.entry_keys = pkeys;
-    a.list_off = idx->list_off;
-    a.d_pad = idx->d_pad;
-    a.R = R;
-    a.L = L;
-    a.w = w;
-    a.E = E;
-    a.T = T;
-    a.k = k;
-    a.out_ids = out_ids;
-    a.out_scores = out_scores;
-    a.out_expanded = out_expanded;
-    a.nq = (int32_t)nq;
-    prof_begin(SA_KERNEL_GRAPH_SEARCH, s);
-    st = cuda_status(launch_graph_search(a, nq, s), "graph search");
-    prof_end(SA_KERNEL_GRAPH_SEARCH, s);
-    prof_count(SA_KERNEL_GRAPH_SEARCH);
-  }
-  if (Qs) cudaFreeAsync(Qs, s);
-  if (psc) cudaFreeAsync(psc, s);
-  if (pkeys) cudaFreeAsync(pkeys, s);
   return st;
 }
 

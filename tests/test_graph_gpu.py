@@ -157,3 +157,18 @@ def test_graph_errors(sa, small):
         flat.build_graph()
     assert e.value.status == sa.SA_ERR_STATE
     flat.free()
+
+
+def test_batch_invariance_and_chunking(sa, small):
+    """Each query is searched by its own CTA: alone, inside a batch, or in a later 4096-query
+    chunk, the result is bit-identical."""
+    idx, Xb, Qb, nbr, kn = small
+    Qd = bits_to_tensor(Qb).cuda()
+    big = Qd[torch.arange(48 * 87, device=Qd.device) % Qd.shape[0]].contiguous()
+    gi, gs, gx, gsc = idx.search_graph(big, 10, 48, search_width=2, n_entries=4, expanded=True)
+    for q in (0, 5, 47):
+        si, ss, sx, ssc = idx.search_graph(Qd[q:q + 1].contiguous(), 10, 48, search_width=2,
+                                           n_entries=4, expanded=True)
+        for row in (q, q + 48 * 86):           # first chunk and second chunk (row >= 4096)
+            assert torch.equal(gi[row], si[0]) and torch.equal(gs[row], ss[0])
+            assert int(gx[row]) == int(sx[0]) and int(gsc[row]) == int(ssc[0])
