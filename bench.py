@@ -247,7 +247,9 @@ def main():
         comm = sa.Comm.from_torch_distributed(local)
     mode = args.mode
     use_ivf = mode in ("auto", "ivf", "graph")
-    use_graph = mode in ("auto", "graph") and not args.no_graph and world == 1
+    # graph mode: one full-corpus index + graph per rank (replicas; query batches are split
+    # across ranks, no data-path collective), so it scales weakly; IVF / exact are row-sharded
+    use_graph = mode in ("auto", "graph") and not args.no_graph
     nlist = args.nlist if use_ivf else 0
 
     n, d, nq, k = cfg["n"], cfg["d"], cfg["nq"], cfg["k"]
@@ -274,10 +276,19 @@ def main():
     del X
     torch.cuda.empty_cache()
     graph_build_s = None
+    gidx = None
     if use_graph and nlist > 0:
         t0 = time.perf_counter()
-        idx.build_graph(knn_k=args.graph_knn, degree=args.graph_degree,
-                        nprobe_build=args.graph_nprobe_build)
+        if world == 1:
+            gidx = idx
+        else:
+            Xf = torch.empty(n, d, dtype=torch.bfloat16, device="cuda")
+            draw_rows_into(mix, Xf, CORPUS_SEED, 0)
+            gidx = sa.Index.build(Xf, nlist)
+            del Xf
+            torch.cuda.empty_cache()
+        gidx.build_graph(knn_k=args.graph_knn, degree=args.graph_degree,
+                         nprobe_build=args.graph_nprobe_build)
         torch.cuda.synchronize()
         graph_build_s = time.perf_counter() - t0
     else:
@@ -287,6 +298,11 @@ def main():
     Qall = torch.empty(nb * nq, d, dtype=torch.bfloat16, device="cuda")
     draw_rows_into(mix, Qall, QUERY_SEED, 0)
     batches = [Qall[i * nq:(i + 1) * nq] for i in range(nb)]
+    gbatches = batches
+    if use_graph and world > 1:        # replicas: every rank searches its own query batches
+        Qg = torch.empty(nb * nq, d, dtype=torch.bfloat16, device="cuda")
+        draw_rows_into(mix, Qg, QUERY_SEED, rank * nb * nq)
+        gbatches = [Qg[i * nq:(i + 1) * nq] for i in range(nb)]
     ids = torch.empty(nq, k, dtype=torch.int64, device="cuda")
     scores = torch.empty(nq, k, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
@@ -305,8 +321,8 @@ def main():
 
     def run_search(i, nprobe):
         if isinstance(nprobe, tuple):          # ("graph", L)
-            return idx.search_graph(batches[i], k, nprobe[1], search_width=GRAPH_W,
-                                    n_entries=GRAPH_E)
+            return gidx.search_graph(gbatches[i], k, nprobe[1], search_width=GRAPH_W,
+                                     n_entries=GRAPH_E)
         return idx.search(batches[i], k, nprobe, out=(ids, scores))
 
     def timed(nprobe):
@@ -416,10 +432,12 @@ def main():
 
     result_graph = None
     if use_graph:
+        ggt = gt if world == 1 else {i: gidx.search(gbatches[i], k, 0)[0].clone()
+                                     for i in range(args.warmup, nb)}
         gsweep, L = [], GRAPH_L[-1]
         calib = list(range(args.warmup, min(nb, args.warmup + 2)))
         for Lc in GRAPH_L:
-            r = float(np.mean([recall_at_k(run_search(i, ("graph", Lc))[0], gt[i]) for i in calib]))
+            r = float(np.mean([recall_at_k(run_search(i, ("graph", Lc))[0], ggt[i]) for i in calib]))
             gsweep.append({"search_range": Lc, "recall": r})
             if r >= RECALL_TARGET + CALIBRATION_MARGIN:
                 L = Lc
@@ -427,16 +445,17 @@ def main():
         ms_g, kern_g, clk_g = timed(("graph", L))
         rec, byts = [], []
         for i in range(args.warmup, nb):
-            gi, _, ex, scd = idx.search_graph(batches[i], k, L, search_width=GRAPH_W,
-                                              n_entries=GRAPH_E, expanded=True)
-            rec.append(recall_at_k(gi, gt[i]))
+            gi, _, ex, scd = gidx.search_graph(gbatches[i], k, L, search_width=GRAPH_W,
+                                               n_entries=GRAPH_E, expanded=True)
+            rec.append(recall_at_k(gi, ggt[i]))
             # algorithmic bytes: every scored row (d_pad bf16) + every expanded list (R ids)
             byts.append(float(scd.sum().item()) * d * 2 + float(ex.sum().item()) * args.graph_degree * 4)
         gs_ms, gs_n = kern_g["graph_search"]
         per_launch = gs_ms / max(gs_n, 1)
         achieved = float(np.mean(byts)) / (per_launch / 1e3) / 1e9
         result_graph = {
-            "value": args.steps * nq / (ms_g / 1e3), "unit": "queries/s",
+            "value": world * args.steps * nq / (ms_g / 1e3), "unit": "queries/s",
+            "scaling": "weak", "parallelism": f"replicas x{world}",
             "recall": float(np.mean(rec)), "search_range": L, "search_width": GRAPH_W,
             "n_entries": GRAPH_E, "knn_k": args.graph_knn, "degree": args.graph_degree,
             "nprobe_build": args.graph_nprobe_build, "build_s": graph_build_s, "sweep": gsweep,
@@ -448,7 +467,7 @@ def main():
                          "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
                          "frac": achieved / pk["hbm"],
                          "peak_kind": f"HBM copy, {pk['src']} (MEASURED_PEAKS.json); the kernel "
-                                      "gathers random 1.5 KB rows",
+                                      f"gathers random {d * 2} B rows",
                          "frac_of_8TBs": achieved / 8000.0,
                          "kernel_ms": per_launch, "kernel_share_of_step": gs_ms / ms_g,
                          "traffic": traffic_from_profiles("graph_search", args.config, nq)},
@@ -462,14 +481,16 @@ def main():
     head_nprobe = result_ivf["nprobe"] if (head_is_graph and result_ivf) else head.get("nprobe", 0)
 
     # ---- end to end through the host-buffer C-ABI call (H2D + search + D2H per step)
-    qh = [batches[i].float().cpu().pin_memory() for i in range(nb)]
+    qh = [(gbatches if head_is_graph else batches)[i].float().cpu().pin_memory()
+          for i in range(nb)]
     ids_h = torch.empty(nq, k, dtype=torch.int64).pin_memory()
     sc_h = torch.empty(nq, k, dtype=torch.float32).pin_memory()
 
     def host_search(qhost):
         if head_is_graph:   # public API: pinned host -> device, sa_search_graph, device -> host
-            gi, gs = idx.search_graph(qhost.to("cuda", non_blocking=True), k, head["search_range"],
-                                      search_width=GRAPH_W, n_entries=GRAPH_E)
+            gi, gs = gidx.search_graph(qhost.to("cuda", non_blocking=True), k,
+                                       head["search_range"], search_width=GRAPH_W,
+                                       n_entries=GRAPH_E)
             ids_h.copy_(gi, non_blocking=True)
             sc_h.copy_(gs, non_blocking=True)
             torch.cuda.current_stream().synchronize()
@@ -490,7 +511,7 @@ def main():
     e1.record(stream)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
-    e2e_value = args.steps * nq / (e2e_ms / 1e3)
+    e2e_value = (world if head_is_graph else 1) * args.steps * nq / (e2e_ms / 1e3)
 
     if head_is_graph:
         mode_name = (f"graph (kNN {args.graph_knn}, degree {args.graph_degree}) search range "
@@ -500,7 +521,8 @@ def main():
     line = {
         "metric": METRIC, "value": head["value"], "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": True, "scaling": head.get("scaling", "strong"), "vs_baseline": None,
+        "dtype": "bf16",
         "data": "synthetic (seeded low-rank Gaussian mixture, unit-norm; DESIGN.md §3)",
         "config": {"workload": f"{args.config}: {mode_name} top-{k}, {n}x{d} bf16 corpus, "
                                f"batch {nq}",
@@ -508,8 +530,9 @@ def main():
                    "nprobe": None if head_is_graph else head_nprobe, "nlist": nlist,
                    "search_range": head.get("search_range"),
                    "recall_at_k": head["recall"], "n_local": n_local,
-                   "parallelism": f"row-shard x{world}",
-                   "l2": "inputs larger than L2 (corpus 32 GB >> 126 MB); no flush"},
+                   "parallelism": head.get("parallelism", f"row-shard x{world}"),
+                   "l2": f"inputs larger than L2 (corpus {n * d * 2 / 1e9:.0f} GB >> 126 MB); "
+                         "no flush"},
         "roofline": head["roofline"],
         "e2e": {"value": e2e_value, "unit": "queries/s",
                 "h2d_bytes_per_step": nq * d * 4, "d2h_bytes_per_step": nq * k * (8 + 4),
@@ -544,14 +567,15 @@ def main():
         # the same agent-step batches through the graph index (pinned H2D, search, D2H)
         agent_g = []
         for b in (1, 8, 64):
-            qb = [batches[(args.warmup + i) % nb][:b].float().cpu().pin_memory() for i in range(8)]
+            qb = [gbatches[(args.warmup + i) % nb][:b].float().cpu().pin_memory()
+                  for i in range(8)]
             ih = torch.empty(b, 5, dtype=torch.int64).pin_memory()
             sh = torch.empty(b, 5, dtype=torch.float32).pin_memory()
             Lg = max(5, result_graph["search_range"])
             ts = []
             for i in range(105):
                 t_s = time.perf_counter()
-                gi, gs = idx.search_graph(qb[i % 8].to("cuda", non_blocking=True), 5, Lg,
+                gi, gs = gidx.search_graph(qb[i % 8].to("cuda", non_blocking=True), 5, Lg,
                                           search_width=GRAPH_W, n_entries=GRAPH_E)
                 ih.copy_(gi, non_blocking=True)
                 sh.copy_(gs, non_blocking=True)
@@ -585,6 +609,8 @@ def main():
                       f"fp64; q/s scaled by {rows}/{n} to the full corpus"}
     if rank == 0:
         print(json.dumps(line))
+    if gidx is not None and gidx is not idx:
+        gidx.free()
     idx.free()
     if comm is not None:
         comm.free()

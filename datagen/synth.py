@@ -41,6 +41,10 @@ CONFIGS = {
                corpus_dtype="bf16", nlist=16384),
     "c5": dict(n=21_015_324, d=768, nq=64, k=5, C=128, r=32, s_sub=1.0, s_n=0.7,
                corpus_dtype="bf16"),
+    # paper-shaped: the paper's encoder all-MiniLM-L6-v2 gives 384-d
+    # embeddings (App. B.3) and the agent reads top-1..5 documents
+    "p384": dict(n=21_015_324, d=384, nq=512, k=5, C=128, r=32, s_sub=1.0, s_n=0.7,
+                 corpus_dtype="bf16"),
 }
 CORPUS_SEED = 1234
 QUERY_SEED = 5678
