@@ -329,7 +329,8 @@ __device__ __forceinline__ int count_greater(const unsigned long long* a, int n,
 }
 
 template <int kSThreads, int kRowsPerWarp>
-__global__ void __launch_bounds__(kSThreads, 4) graph_search_kernel(const GraphSearchArgs a) {
+__global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
+    graph_search_kernel(const GraphSearchArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   SearchSmem& sm = *reinterpret_cast<SearchSmem*>(smem_raw);
   const int q = blockIdx.x;
@@ -480,11 +481,8 @@ cudaError_t launch_graph_merge(const int32_t* fwd, const uint64_t* rev, int64_t 
 
 size_t graph_search_smem(int) { return sizeof(SearchSmem); }
 
-cudaError_t launch_graph_search(const GraphSearchArgs& a, int64_t nq, cudaStream_t s) {
-  // 256 threads x 3 rows in flight per warp at 4 CTAs/SM (64 registers, ~45 KB smem): every
-  // query of a 512 batch is resident at once.  Measured alternatives (C3, L=160):
-  // 128 threads x 6 rows 0.84x, 128 x 8 (spills) 0.6x, 256 x 4 (spills) slower.
-  constexpr int TH = 256, RW = 3;
+template <int TH, int RW>
+cudaError_t launch_shape(const GraphSearchArgs& a, int64_t nq, cudaStream_t s) {
   const size_t smem = sizeof(SearchSmem);
   static bool set = false;
   if (!set) {
@@ -495,6 +493,18 @@ cudaError_t launch_graph_search(const GraphSearchArgs& a, int64_t nq, cudaStream
   }
   graph_search_kernel<TH, RW><<<(unsigned)nq, TH, smem, s>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_graph_search(const GraphSearchArgs& a, int64_t nq, cudaStream_t s) {
+  // Throughput shape: 256 threads x 3 rows in flight per warp at 4 CTAs/SM (64 registers,
+  // ~45 KB smem), every query of a 512 batch resident at once.  Measured alternatives (C3,
+  // L=160): 128 threads x 6 rows 0.84x, 128 x 8 (spills) 0.6x, 256 x 4 (spills) slower.
+  // Latency shapes for small batches (agent steps): 1024 threads when at most one query per
+  // SM (an iteration's ~100-200 new rows all in flight at once), 512 threads for two.
+  // (C3, L=104: batch 1 0.32 ms, 64 0.40 ms, 148 0.43 ms vs 0.65 ms with the 256 shape.)
+  if (nq <= 148) return launch_shape<1024, 3>(a, nq, s);
+  if (nq <= 296) return launch_shape<512, 3>(a, nq, s);
+  return launch_shape<256, 3>(a, nq, s);
 }
 
 }  // namespace sa

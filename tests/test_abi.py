@@ -56,3 +56,18 @@ def test_search_mature_validates_before_device_work(sa):
                               None) == sa.SA_ERR_INVALID_ARG
     assert L.sa_search_mature(buf, buf, 0, 1, 10, 8, None, buf, buf, None, None, None,
                               None) == sa.SA_ERR_INVALID_ARG
+
+
+def test_graph_and_retriever_entry_points_validate(sa):
+    L = sa.lib()
+    buf = ctypes.c_void_p(1)
+    assert L.sa_index_build_graph(None, 64, 32, 8, 0, None) == sa.SA_ERR_INVALID_ARG
+    assert L.sa_search_graph(None, buf, 0, 1, 10, 64, 4, 8, 100, buf, buf, None,
+                             None) == sa.SA_ERR_INVALID_ARG
+    deg = ctypes.c_int32()
+    assert L.sa_index_export_graph(None, ctypes.byref(deg), None, None, None) == sa.SA_ERR_INVALID_ARG
+    h = ctypes.c_void_p()
+    assert L.sa_retriever_create(None, 1, 1, 1, 1, ctypes.byref(h)) == sa.SA_ERR_INVALID_ARG
+    assert L.sa_retriever_set_engine_ready(None, 1) == sa.SA_ERR_INVALID_ARG
+    done = ctypes.c_int32()
+    assert L.sa_retriever_poll(None, 0, ctypes.byref(done)) == sa.SA_ERR_INVALID_ARG

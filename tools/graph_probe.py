@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--ranges", default="16,32,48,64,96,128,192,256")
     ap.add_argument("--widths", default="1,2,4")
     ap.add_argument("--entries", default="8")
+    ap.add_argument("--latency", action="store_true", help="also time agent-step batches")
     args = ap.parse_args()
     cfg = dict(CONFIGS["c3"])
     n, d = args.n, cfg["d"]
@@ -81,6 +82,24 @@ def main():
                                 "expanded": float(np.mean(exp)), "ms_per_batch": ms,
                                 "qps": args.nq / (ms / 1e3)})
             print(json.dumps(out["rows"][-1]), file=sys.stderr, flush=True)
+    if args.latency:
+        # agent-step batches: device time per call (stage + probe + search), median of 50
+        out["latency"] = []
+        Lr = int(args.ranges.split(",")[0])
+        for b in (1, 8, 64, 148, 149):
+            q = qs[0][:b].contiguous()
+            ts = []
+            for i in range(55):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                idx.search_graph(q, 5, Lr, search_width=int(args.widths.split(",")[0]),
+                                 n_entries=16)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                if i >= 5:
+                    ts.append(e0.elapsed_time(e1))
+            out["latency"].append({"batch": b, "L": Lr, "p50_ms": float(np.median(ts))})
+            print(json.dumps(out["latency"][-1]), file=sys.stderr, flush=True)
     print(json.dumps(out))
     idx.free()
 
