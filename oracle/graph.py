@@ -108,8 +108,16 @@ def build(X_bits: np.ndarray, K: int, R: int, candidates=None):
 
 
 def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: int, w: int,
-           entries, T: int):
-    """R27 for one query.  Returns dict(ids, scores, expanded, iterations)."""
+           entries, T: int, tau=None, window: int = 1, g: int = 1, ready=True):
+    """R27 for one query.  Returns dict(ids, scores, expanded, iterations[, rq, ema]).
+
+    With tau set, the non-stall maturity exit of PAPER.md §3.3 (App. B.2) runs on
+    the beam search itself -- the paper's own setting (HNSW).  Readings R28-R29: a step is
+    one iteration (w expansions); after its new rows are merged, s_t = the best score among
+    the rows scored in the step (none -> RQ = 1), RQ_t = (s_best - s_t)/(s_best - s_worst)
+    over the list's first / last entries (1 if equal), EMA as R17 (alpha = 2/(window+1),
+    seeded with RQ_1); after every g-th step the search stops if EMA >= tau and the engine is
+    ready (ready(t) or a constant); the result is the list at that point (R19)."""
     X = bf16_to_f64(X_bits)
     q = bf16_to_f64(q_bits)
     visited = set()
@@ -124,6 +132,8 @@ def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: i
     lst = [[float(sc[o]), int(ids[o]), False] for o in order]
     it = 0
     expanded = 0
+    ema = None
+    rqs, emas = [], []
     while it < T:
         pick = [e for e in lst if not e[2]][:w]
         if not pick:
@@ -138,15 +148,31 @@ def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: i
                 if c >= 0 and c not in visited:
                     visited.add(c)
                     new.append(c)
+        s_t = None
         if new:
             nid = np.array(new, dtype=np.int64)
             ns = X[nid] @ q
+            s_t = float(ns.max())
             allv = lst + [[float(s), int(i), False] for s, i in zip(ns, nid)]
             allv.sort(key=lambda e: (-e[0], e[1]))
             lst = allv[:L]
+        if tau is not None:
+            sb, sw = lst[0][0], lst[-1][0]
+            r = 1.0 if (s_t is None or sb == sw) else (sb - s_t) / (sb - sw)
+            a = 2.0 / (window + 1)
+            ema = r if ema is None else a * r + (1.0 - a) * ema
+            rqs.append(r)
+            emas.append(ema)
+            is_ready = ready(it) if callable(ready) else bool(ready)
+            if it % g == 0 and ema >= tau and is_ready:
+                break
     out_ids = np.full(k, -1, dtype=np.int64)
     out_sc = np.full(k, -np.inf)
     for j, e in enumerate(lst[:k]):
         out_ids[j] = e[1]
         out_sc[j] = e[0]
-    return {"ids": out_ids, "scores": out_sc, "expanded": expanded, "iterations": it}
+    out = {"ids": out_ids, "scores": out_sc, "expanded": expanded, "iterations": it}
+    if tau is not None:
+        out["rq"] = np.array(rqs)
+        out["ema"] = np.array(emas)
+    return out

@@ -98,3 +98,23 @@ def test_gr4_knn_is_brute_force_without_self():
         want = [int(x) for x in ids[i] if x != i][:5]
         assert kn[i].tolist() == want
     assert kn[3][0] == 7 and kn[7][0] == 3
+
+
+def test_gr5_maturity_on_beam_search_by_hand():
+    """Maturity exit on the beam search (R28-R29) on the path graph of GR2, by hand:
+    L=2, w=1, entry 0; step 1 scores {1: 0.25} -> list (0.25, 0.125), s_t = s_best -> RQ 0;
+    step 2 scores {2: 0.375} -> list (0.375, 0.25), RQ 0; step 3 scores {3: 0.5}, RQ 0;
+    step 4 scores nothing -> RQ 1.  W=3 (alpha 0.5): EMA 0, 0, 0, 0.5."""
+    X, nbr, q = path_graph()
+    r = graph.search(X, nbr, q[0], 2, L=2, w=1, entries=[0], T=100, tau=float("inf"), window=3)
+    assert r["rq"].tolist() == [0.0, 0.0, 0.0, 1.0]
+    assert r["ema"].tolist() == [0.0, 0.0, 0.0, 0.5]
+    assert r["iterations"] == 4
+    # tau = 0 stops after the first step with the engine ready; never ready -> natural stop
+    r = graph.search(X, nbr, q[0], 2, L=2, w=1, entries=[0], T=100, tau=0.0, window=3)
+    assert r["iterations"] == 1 and r["ids"].tolist() == [1, 0]
+    r = graph.search(X, nbr, q[0], 2, L=2, w=1, entries=[0], T=100, tau=0.0, window=3,
+                     ready=False)
+    assert r["iterations"] == 4 and r["ids"].tolist() == [3, 2]
+    r = graph.search(X, nbr, q[0], 2, L=2, w=1, entries=[0], T=100, tau=0.0, window=3, g=3)
+    assert r["iterations"] == 3 and r["ids"].tolist() == [3, 2]
