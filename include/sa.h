@@ -210,6 +210,37 @@ sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdt
                           float* out_scores, int32_t* out_expanded, void* stream);
 sa_status sa_index_export_graph(const sa_index* idx, int32_t* degree, int32_t* knn_k,
                                 int64_t* host_nbr, int64_t* host_knn);
+/* sa_index_import_graph: replace idx's graph by host_nbr HOST int64 [n_local, degree] in
+ * sa_index_export_graph's layout (row = global id - row_offset, entries global ids of this
+ * index, -1 padded); the inverse of export (a saved graph, or a hand-built one in tests).
+ * Synchronous; the caller keeps host_nbr.  SA_ERR_STATE on a flat-only index,
+ * SA_ERR_INVALID_ARG on degree outside [1, 64] or an id outside the index. */
+sa_status sa_index_import_graph(sa_index* idx, int32_t degree, const int64_t* host_nbr);
+
+/* sa_search_graph_mature: the beam search of sa_search_graph with the non-stall maturity
+ * exit of PAPER.md §3.3 (App. B.2) in the paper's own setting, a graph
+ * search (readings R28-R29):
+ *   - a step t is one iteration (search_width expansions);
+ *   - s_t = the best score among the rows scored in step t; after they are merged into the
+ *     list, RQ_t = (s_best - s_t) / (s_best - s_worst) over the list's first / last entries
+ *     (1.0 when the step scored nothing or s_best == s_worst; not clamped);
+ *   - EMA_1 = RQ_1, EMA_t = a*RQ_t + (1-a)*EMA_{t-1}, a = 2/(opts->window+1), fp64;
+ *   - after every opts->check_every steps the query stops if EMA_t >= opts->tau and
+ *     *opts->engine_ready is nonzero (read by the device at that moment; NULL = always);
+ *     otherwise it runs until no entry is left to expand or max_iters (capped as in
+ *     sa_search_graph);
+ *   - the result is the list's first k entries at that point (R19).
+ * One launch; each query's CTA decides on its own.  out_steps DEVICE int32 [nq] (iterations
+ * run; may be NULL); out_rq / out_ema DEVICE fp64 [nq, trace_cols] per-step signal for steps
+ * 1..trace_cols (NaN past the exit; both NULL, or both set with trace_cols >= 1).  Other
+ * arguments, limits and errors as sa_search_graph; SA_ERR_INVALID_ARG on opts NULL, tau NaN,
+ * window < 1 or check_every < 1. */
+sa_status sa_search_graph_mature(const sa_index* idx, const void* queries, sa_dtype qdtype,
+                                 int64_t nq, int32_t k, int32_t search_range,
+                                 int32_t search_width, int32_t n_entries, int32_t max_iters,
+                                 const sa_maturity_opts* opts, int64_t* out_ids,
+                                 float* out_scores, int32_t* out_steps, double* out_rq,
+                                 double* out_ema, int32_t trace_cols, void* stream);
 
 /* ---- agent loop support (Alg. 1, App. A.1) ---- */
 

@@ -57,6 +57,19 @@ class _MaturityOpts(ctypes.Structure):
 _lib = None
 
 
+def _maturity_opts(tau, window, check_every, engine_ready):
+    o = _MaturityOpts()
+    o.tau = float(tau)
+    o.window = int(window)
+    o.check_every = int(check_every)
+    if engine_ready is not None:
+        if engine_ready.dtype != torch.int32 or engine_ready.numel() < 1 or \
+                not (engine_ready.is_cuda or engine_ready.is_pinned()):
+            raise ValueError("engine_ready must be an int32 CUDA or pinned host tensor")
+        o.engine_ready = engine_ready.data_ptr()
+    return o
+
+
 def lib() -> ctypes.CDLL:
     """Load libsa.so (built in-tree by build.py / __graft_entry__.build())."""
     global _lib
@@ -92,6 +105,9 @@ def lib() -> ctypes.CDLL:
         "sa_index_build_graph": (st, [P, i32, i32, i32, i32, P]),
         "sa_search_graph": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, i32, i32, P, P, P, P]),
         "sa_index_export_graph": (st, [P, ctypes.POINTER(i32), ctypes.POINTER(i32), P, P]),
+        "sa_index_import_graph": (st, [P, i32, P]),
+        "sa_search_graph_mature": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, i32, i32,
+                                        ctypes.POINTER(_MaturityOpts), P, P, P, P, P, i32, P]),
         "sa_retriever_create": (st, [P, i32, i32, i32, i32, ctypes.POINTER(P)]),
         "sa_retriever_submit": (st, [P, P, i32, i32, i32, i32, ctypes.POINTER(_MaturityOpts),
                                      ctypes.POINTER(i64)]),
@@ -293,15 +309,7 @@ class Index:
         if trace:
             rq = torch.empty(nq, nprobe_max, dtype=torch.float64, device=dev)
             ema = torch.empty(nq, nprobe_max, dtype=torch.float64, device=dev)
-        o = _MaturityOpts()
-        o.tau = float(tau)
-        o.window = int(window)
-        o.check_every = int(check_every)
-        if engine_ready is not None:
-            if engine_ready.dtype != torch.int32 or engine_ready.numel() < 1 or \
-                    not (engine_ready.is_cuda or engine_ready.is_pinned()):
-                raise ValueError("engine_ready must be an int32 CUDA or pinned host tensor")
-            o.engine_ready = engine_ready.data_ptr()
+        o = _maturity_opts(tau, window, check_every, engine_ready)
         _check(lib().sa_search_mature(self.handle, _ptr(queries), _dtype_code(queries), nq, k,
                                       nprobe_max, ctypes.byref(o), _ptr(ids), _ptr(scores), _ptr(t),
                                       _ptr(rq) if trace else None, _ptr(ema) if trace else None,
@@ -332,6 +340,41 @@ class Index:
                                      _ptr(ex) if expanded else None, _stream_ptr(stream)))
         # expanded: (entries expanded [nq], rows scored [nq])
         return (ids, scores, ex[0], ex[1]) if expanded else (ids, scores)
+
+    def search_graph_mature(self, queries: torch.Tensor, k: int, search_range: int, *,
+                            tau: float, window: int, check_every: int = 1,
+                            engine_ready: torch.Tensor | None = None, search_width: int = 4,
+                            n_entries: int = 8, max_iters: int = 1 << 30, trace_cols: int = 0,
+                            stream=None):
+        """sa_search_graph_mature.  Returns (ids, scores, steps[, rq, ema]) -- rq / ema
+        [nq, trace_cols] fp64 when trace_cols > 0."""
+        if not queries.is_cuda or queries.dim() != 2 or not queries.is_contiguous():
+            raise ValueError("queries must be a contiguous 2-D CUDA tensor")
+        nq = queries.shape[0]
+        dev = queries.device
+        ids = torch.empty(nq, k, dtype=torch.int64, device=dev)
+        scores = torch.empty(nq, k, dtype=torch.float32, device=dev)
+        steps = torch.empty(nq, dtype=torch.int32, device=dev)
+        rq = ema = None
+        if trace_cols > 0:
+            rq = torch.empty(nq, trace_cols, dtype=torch.float64, device=dev)
+            ema = torch.empty(nq, trace_cols, dtype=torch.float64, device=dev)
+        o = _maturity_opts(tau, window, check_every, engine_ready)
+        _check(lib().sa_search_graph_mature(self.handle, _ptr(queries), _dtype_code(queries), nq, k,
+                                            search_range, search_width, n_entries,
+                                            min(max_iters, 2**31 - 1), ctypes.byref(o), _ptr(ids),
+                                            _ptr(scores), _ptr(steps),
+                                            _ptr(rq) if rq is not None else None,
+                                            _ptr(ema) if ema is not None else None,
+                                            trace_cols, _stream_ptr(stream)))
+        return (ids, scores, steps, rq, ema) if trace_cols > 0 else (ids, scores, steps)
+
+    def import_graph(self, nbr: np.ndarray):
+        """sa_index_import_graph: nbr int64 [n_local, degree] of global ids (-1 padded)."""
+        nbr = np.ascontiguousarray(nbr, dtype=np.int64)
+        _check(lib().sa_index_import_graph(self.handle, nbr.shape[1],
+                                           nbr.ctypes.data_as(ctypes.c_void_p)))
+        return self
 
     def export_graph(self, knn: bool = False):
         inf = self.info()

@@ -127,10 +127,16 @@ sa_status sa_index_build_graph(sa_index* idx, int32_t knn_k, int32_t degree, int
   return SA_OK;
 }
 
-sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
-                          int32_t k, int32_t search_range, int32_t search_width,
-                          int32_t n_entries, int32_t max_iters, int64_t* out_ids,
-                          float* out_scores, int32_t* out_expanded, void* stream) {
+}  // extern "C"
+
+namespace {
+
+// sa_search_graph and sa_search_graph_mature: `mo` NULL = plain beam search (R27)
+sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                       int32_t k, int32_t search_range, int32_t search_width, int32_t n_entries,
+                       int32_t max_iters, const sa_maturity_opts* mo, int64_t* out_ids,
+                       float* out_scores, int32_t* out_expanded, int32_t* out_steps,
+                       double* out_rq, double* out_ema, int32_t trace_cols, void* stream) {
   if (!idx || !queries || !out_ids || !out_scores)
     return set_error(SA_ERR_INVALID_ARG, "null pointer");
   if (!idx->graph) return set_error(SA_ERR_STATE, "no graph: call sa_index_build_graph");
@@ -144,6 +150,14 @@ sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdt
   if (E < 1 || E > std::min(idx->nlist, 256))
     return set_error(SA_ERR_INVALID_ARG, "need 1 <= n_entries <= min(nlist, 256)");
   if (max_iters < 0) return set_error(SA_ERR_INVALID_ARG, "max_iters must be >= 0");
+  if (mo) {
+    if (!(mo->tau == mo->tau)) return set_error(SA_ERR_INVALID_ARG, "tau is NaN");
+    if (mo->window < 1 || mo->check_every < 1)
+      return set_error(SA_ERR_INVALID_ARG, "need window >= 1 and check_every >= 1");
+    if ((out_rq == nullptr) != (out_ema == nullptr) || trace_cols < 0 ||
+        (out_rq && trace_cols < 1))
+      return set_error(SA_ERR_INVALID_ARG, "out_rq / out_ema: both NULL or both [nq, trace_cols >= 1]");
+  }
   const int T = std::min(max_iters, (GR_VISIT_CAP - E) / (w * R));
   cudaStream_t s = (cudaStream_t)stream;
   // queries in chunks: the probe's dense score buffer is chunk x nlist fp32
@@ -204,8 +218,19 @@ sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdt
       a.out_scores = out_scores + q0 * k;
       a.out_expanded = out_expanded ? out_expanded + q0 : nullptr;
       a.nq = (int32_t)nq;   // row stride of out_expanded
+      GraphMatureArgs m{};
+      if (mo) {
+        m.tau = mo->tau;
+        m.alpha = 2.0 / (mo->window + 1.0);
+        m.g = mo->check_every;
+        m.ready = mo->engine_ready;
+        m.out_steps = out_steps ? out_steps + q0 : nullptr;
+        m.trace_cols = out_rq ? trace_cols : 0;
+        m.out_rq = out_rq ? out_rq + q0 * trace_cols : nullptr;
+        m.out_ema = out_rq ? out_ema + q0 * trace_cols : nullptr;
+      }
       prof_begin(SA_KERNEL_GRAPH_SEARCH, s);
-      st = cuda_status(launch_graph_search(a, nc, s), "graph search");
+      st = cuda_status(launch_graph_search(a, mo ? &m : nullptr, nc, s), "graph search");
       prof_end(SA_KERNEL_GRAPH_SEARCH, s);
       prof_count(SA_KERNEL_GRAPH_SEARCH);
     }
@@ -214,6 +239,66 @@ sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdt
     if (pkeys) cudaFreeAsync(pkeys, s);
   }
   return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                          int32_t k, int32_t search_range, int32_t search_width,
+                          int32_t n_entries, int32_t max_iters, int64_t* out_ids,
+                          float* out_scores, int32_t* out_expanded, void* stream) {
+  return graph_search(idx, queries, qdtype, nq, k, search_range, search_width, n_entries,
+                      max_iters, nullptr, out_ids, out_scores, out_expanded, nullptr, nullptr,
+                      nullptr, 0, stream);
+}
+
+sa_status sa_search_graph_mature(const sa_index* idx, const void* queries, sa_dtype qdtype,
+                                 int64_t nq, int32_t k, int32_t search_range,
+                                 int32_t search_width, int32_t n_entries, int32_t max_iters,
+                                 const sa_maturity_opts* opts, int64_t* out_ids,
+                                 float* out_scores, int32_t* out_steps, double* out_rq,
+                                 double* out_ema, int32_t trace_cols, void* stream) {
+  if (!opts) return set_error(SA_ERR_INVALID_ARG, "null maturity options");
+  return graph_search(idx, queries, qdtype, nq, k, search_range, search_width, n_entries,
+                      max_iters, opts, out_ids, out_scores, nullptr, out_steps, out_rq, out_ema,
+                      trace_cols, stream);
+}
+
+sa_status sa_index_import_graph(sa_index* idx, int32_t degree, const int64_t* host_nbr) {
+  if (!idx || !host_nbr) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (idx->nlist == 0) return set_error(SA_ERR_STATE, "the graph is built on an IVF index");
+  if (degree < 1 || degree > GR_MAX_R)
+    return set_error(SA_ERR_INVALID_ARG, "need 1 <= degree <= 64");
+  const int64_t n = idx->n_local;
+  std::vector<int32_t> ids(n), pos_of(n), buf((size_t)n * degree);
+  cudaError_t e = cudaMemcpy(ids.data(), idx->row_ids, n * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_status(e, "import graph");
+  for (int64_t p = 0; p < n; ++p) pos_of[(int64_t)(uint32_t)ids[p] - idx->row_offset] = (int32_t)p;
+  for (int64_t p = 0; p < n; ++p) {
+    const int64_t* src = host_nbr + ((int64_t)(uint32_t)ids[p] - idx->row_offset) * degree;
+    for (int j = 0; j < degree; ++j) {
+      const int64_t v = src[j];
+      if (v >= 0 && (v < idx->row_offset || v >= idx->row_offset + n))
+        return set_error(SA_ERR_INVALID_ARG, "neighbour id outside the index");
+      buf[(size_t)p * degree + j] = v < 0 ? -1 : pos_of[v - idx->row_offset];
+    }
+  }
+  int32_t* nbr = nullptr;
+  e = cudaMalloc(&nbr, buf.size() * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(nbr, buf.data(), buf.size() * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(nbr);
+    return cuda_status(e, "import graph");
+  }
+  cudaFree(idx->graph);
+  cudaFree(idx->graph_knn);
+  idx->graph = nbr;
+  idx->graph_knn = nullptr;
+  idx->graph_R = degree;
+  idx->graph_K = 0;
+  return SA_OK;
 }
 
 sa_status sa_index_export_graph(const sa_index* idx, int32_t* degree, int32_t* knn_k,

@@ -240,7 +240,15 @@ struct SearchSmem {
   int32_t ipos[GR_MAX_NEW];
   int32_t chosen[8];
   int32_t n_new, n_ins, n_chosen;
+  unsigned long long smax;                // best key scored in the step (maturity exit)
 };
+
+__device__ __forceinline__ int32_t read_ready(const int32_t* p) {
+  if (p == nullptr) return 1;
+  int32_t v;
+  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ bool visit(uint32_t* hash, int32_t pos) {
   const uint32_t v = (uint32_t)pos + 1u;
@@ -274,7 +282,7 @@ __device__ __forceinline__ float bf16x8_dot(const uint4 v, const float* q) {
 // lane l holds 16-byte chunks l, l + 32, l + 64 of a row; the query is in smem).
 // Rows whose key is not above `floor` (the list's L-th key once the list is full) cannot enter
 // the list and are dropped here; the survivors go to (nkey, ipos)[0, n_ins).
-template <int kSThreads, int kRowsPerWarp>
+template <int kSThreads, int kRowsPerWarp, bool kMature>
 __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, int nchunk,
                            unsigned long long floor) {
   constexpr int kSWarps = kSThreads / 32;
@@ -306,6 +314,7 @@ __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, in
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0 && p[u] >= 0) {
         const unsigned long long key = make_key(acc, gid[u]);
+        if (kMature) atomicMax(&sm.smax, key);
         if (key > floor) {
           const int t = atomicAdd(&sm.n_ins, 1);
           sm.nkey[t] = key;
@@ -328,9 +337,9 @@ __device__ __forceinline__ int count_greater(const unsigned long long* a, int n,
   return lo;
 }
 
-template <int kSThreads, int kRowsPerWarp>
+template <int kSThreads, int kRowsPerWarp, bool kMature>
 __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
-    graph_search_kernel(const GraphSearchArgs a) {
+    graph_search_kernel(const GraphSearchArgs a, const GraphMatureArgs m) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   SearchSmem& sm = *reinterpret_cast<SearchSmem*>(smem_raw);
   const int q = blockIdx.x;
@@ -357,11 +366,14 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
   int cur = 0;
   int n_new = sm.n_new;
   int cnt = 0;
-  score_rows<kSThreads, kRowsPerWarp>(a, sm, n_new, nchunk, 0ull);
+  score_rows<kSThreads, kRowsPerWarp, false>(a, sm, n_new, nchunk, 0ull);
   __syncthreads();
   int expanded = 0;
   int scored = n_new;
+  double ema = 0.0;  // thread 0 (maturity exit)
+  int steps = 0;     // iterations run (maturity exit)
   for (int it = 0;; ++it) {
+    if (kMature) steps = it;
     // ---- merge the surviving new rows into the sorted list (top-L); keys are distinct, so an
     // entry's new position = its rank in the old list + the number of new keys above it (v.v.)
     const int n_ins = sm.n_ins;
@@ -391,11 +403,29 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
       cur = nxt;
       __syncthreads();
     }
+    // ---- maturity signal of step it (R28-R29): s_t = best key scored in the step, RQ_t over
+    // the list's first / last entries after the merge, EMA in fp64 with the oracle's roundings
+    bool stop = false;
+    if constexpr (kMature) if (it > 0 && threadIdx.x == 0) {
+      double r = 1.0;
+      if (n_new > 0) {
+        const double sb = key_score(sm.key[cur][0]), sw = key_score(sm.key[cur][cnt - 1]);
+        if (sb != sw) r = __ddiv_rn(__dsub_rn(sb, (double)key_score(sm.smax)), __dsub_rn(sb, sw));
+      }
+      ema = it == 1 ? r
+                    : __dadd_rn(__dmul_rn(m.alpha, r), __dmul_rn(__dsub_rn(1.0, m.alpha), ema));
+      if (m.out_rq && it <= m.trace_cols) {
+        m.out_rq[(int64_t)q * m.trace_cols + it - 1] = r;
+        m.out_ema[(int64_t)q * m.trace_cols + it - 1] = ema;
+      }
+      stop = it % m.g == 0 && ema >= m.tau && read_ready(m.ready) != 0;
+    }
     if (it >= a.T) break;
     // ---- pick the first w unexpanded entries (warp 0)
     if (threadIdx.x < 32) {
       int taken = 0;
-      for (int base = 0; base < cnt && taken < a.w; base += 32) {
+      if constexpr (kMature) stop = __shfl_sync(0xffffffffu, stop, 0);
+      for (int base = 0; base < cnt && taken < a.w && !stop; base += 32) {
         const int i = base + lane;
         const bool un = i < cnt && sm.flag[cur][i] == 0;
         unsigned m = __ballot_sync(0xffffffffu, un);
@@ -413,6 +443,7 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
         sm.n_chosen = taken;
         sm.n_new = 0;
         sm.n_ins = 0;
+        if constexpr (kMature) sm.smax = 0ull;
       }
     }
     __syncthreads();
@@ -427,7 +458,7 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
     __syncthreads();
     n_new = sm.n_new;
     scored += n_new;
-    score_rows<kSThreads, kRowsPerWarp>(a, sm, n_new, nchunk,
+    score_rows<kSThreads, kRowsPerWarp, kMature>(a, sm, n_new, nchunk,
                                         cnt == a.L ? sm.key[cur][a.L - 1] : 0ull);
     __syncthreads();
   }
@@ -439,6 +470,14 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
   if (a.out_expanded && threadIdx.x == 0) {
     a.out_expanded[q] = expanded;
     a.out_expanded[a.nq + q] = scored;
+  }
+  if (kMature) {
+    if (m.out_steps && threadIdx.x == 0) m.out_steps[q] = steps;
+    if (m.out_rq)
+      for (int t = steps + threadIdx.x; t < m.trace_cols; t += kSThreads) {
+        m.out_rq[(int64_t)q * m.trace_cols + t] = __longlong_as_double(0x7ff8000000000000ll);
+        m.out_ema[(int64_t)q * m.trace_cols + t] = __longlong_as_double(0x7ff8000000000000ll);
+      }
   }
 }
 
@@ -481,30 +520,38 @@ cudaError_t launch_graph_merge(const int32_t* fwd, const uint64_t* rev, int64_t 
 
 size_t graph_search_smem(int) { return sizeof(SearchSmem); }
 
-template <int TH, int RW>
-cudaError_t launch_shape(const GraphSearchArgs& a, int64_t nq, cudaStream_t s) {
+template <int TH, int RW, bool M>
+cudaError_t launch_shape(const GraphSearchArgs& a, const GraphMatureArgs& m, int64_t nq,
+                         cudaStream_t s) {
   const size_t smem = sizeof(SearchSmem);
   static bool set = false;
   if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(graph_search_kernel<TH, RW>,
+    cudaError_t e = cudaFuncSetAttribute(graph_search_kernel<TH, RW, M>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     set = true;
   }
-  graph_search_kernel<TH, RW><<<(unsigned)nq, TH, smem, s>>>(a);
+  graph_search_kernel<TH, RW, M><<<(unsigned)nq, TH, smem, s>>>(a, m);
   return cudaGetLastError();
 }
 
-cudaError_t launch_graph_search(const GraphSearchArgs& a, int64_t nq, cudaStream_t s) {
+template <bool M>
+cudaError_t launch_shapes(const GraphSearchArgs& a, const GraphMatureArgs& m, int64_t nq,
+                          cudaStream_t s) {
+  if (nq <= 148) return launch_shape<1024, 3, M>(a, m, nq, s);
+  if (nq <= 296) return launch_shape<512, 3, M>(a, m, nq, s);
+  return launch_shape<256, 3, M>(a, m, nq, s);
+}
+
+cudaError_t launch_graph_search(const GraphSearchArgs& a, const GraphMatureArgs* m, int64_t nq,
+                                cudaStream_t s) {
   // Throughput shape: 256 threads x 3 rows in flight per warp at 4 CTAs/SM (64 registers,
   // ~45 KB smem), every query of a 512 batch resident at once.  Measured alternatives (C3,
   // L=160): 128 threads x 6 rows 0.84x, 128 x 8 (spills) 0.6x, 256 x 4 (spills) slower.
   // Latency shapes for small batches (agent steps): 1024 threads when at most one query per
   // SM (an iteration's ~100-200 new rows all in flight at once), 512 threads for two.
   // (C3, L=104: batch 1 0.32 ms, 64 0.40 ms, 148 0.43 ms vs 0.65 ms with the 256 shape.)
-  if (nq <= 148) return launch_shape<1024, 3>(a, nq, s);
-  if (nq <= 296) return launch_shape<512, 3>(a, nq, s);
-  return launch_shape<256, 3>(a, nq, s);
+  return m ? launch_shapes<true>(a, *m, nq, s) : launch_shapes<false>(a, GraphMatureArgs{}, nq, s);
 }
 
 }  // namespace sa

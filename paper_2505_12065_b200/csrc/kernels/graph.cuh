@@ -48,7 +48,21 @@ struct GraphSearchArgs {
   int32_t* out_expanded;    // optional [2, nq]: entries expanded, rows scored
   int32_t nq;
 };
+// non-stall maturity exit on the beam search (§3.3; readings R28-R29): a step is one
+// iteration; RQ_t / EMA_t in fp64; after every g-th step the query stops if EMA_t >= tau and
+// *ready != 0 (NULL = always ready).  A separate kernel argument, so the plain search's
+// argument block (and its register allocation) is unchanged.
+struct GraphMatureArgs {
+  double tau, alpha;
+  int32_t g, trace_cols;
+  const int32_t* ready;
+  int32_t* out_steps;       // optional [nq]: iterations run
+  double* out_rq;           // optional [nq, trace_cols] (NaN past the exit)
+  double* out_ema;
+};
 size_t graph_search_smem(int L);
-cudaError_t launch_graph_search(const GraphSearchArgs& a, int64_t nq, cudaStream_t s);
+// m == nullptr: plain beam search
+cudaError_t launch_graph_search(const GraphSearchArgs& a, const GraphMatureArgs* m, int64_t nq,
+                                cudaStream_t s);
 
 }  // namespace sa
