@@ -722,6 +722,90 @@ def stop_latency(sa, idx, q, k, P, tau, window, g, delay_s, reps=20):
             "stop_p99_ms": 1e3 * float(np.percentile(out, 99)), "mean_lists": float(np.mean(lists))}
 
 
+def graph_point(gidx, qs, k, L, gt, mature=None, reps=30):
+    """One graph-search setting (fixed search range, or the maturity exit when `mature` =
+    (tau, window, g)): recall vs exact, mean iterations, p50 latency (host wall clock around the
+    call + sync)."""
+    def call(q):
+        if mature is None:
+            gi, _, ex, _ = gidx.search_graph(q, k, L, search_width=GRAPH_W, n_entries=GRAPH_E,
+                                             expanded=True)
+            return gi, (ex.float() / GRAPH_W).ceil()
+        tau, window, g = mature
+        gi, _, st = gidx.search_graph_mature(q, k, L, tau=tau, window=window, check_every=g,
+                                             search_width=GRAPH_W, n_entries=GRAPH_E)
+        return gi, st.float()
+    rec, its = [], []
+    for q, t in zip(qs, gt):
+        gi, it = call(q)
+        rec.append(recall_at_k(gi, t))
+        its.append(it.mean().item())
+    ts = []
+    for i in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        call(qs[i % len(qs)])
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    out = {"search_range": L, "recall": float(np.mean(rec)), "mean_iterations": float(np.mean(its)),
+           "p50_ms": 1e3 * float(np.percentile(ts, 50))}
+    if mature is not None:
+        out.update(tau=mature[0], window=mature[1], check_every=mature[2])
+    return out
+
+
+def graph_stop_latency(gidx, q, k, L, delay_s, reps=20):
+    """Non-stall responsiveness on the graph search: tau = 0, the engine flag raised delay_s
+    after the launch; time from the raise to the results being complete, iterations run."""
+    flag = torch.zeros(1, dtype=torch.int32).pin_memory()
+    kw = dict(tau=0.0, window=4, check_every=1, engine_ready=flag, search_width=GRAPH_W,
+              n_entries=GRAPH_E)
+    gidx.search_graph_mature(q, k, L, **kw)
+    torch.cuda.synchronize()
+    out, its = [], []
+    for _ in range(reps):
+        flag[0] = 0
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, _, st = gidx.search_graph_mature(q, k, L, **kw)
+        while time.perf_counter() - t0 < delay_s:
+            pass
+        t1 = time.perf_counter()
+        flag[0] = 1
+        torch.cuda.synchronize()
+        out.append(time.perf_counter() - t1)
+        its.append(st.float().mean().item())
+    return {"flag_after_ms": 1e3 * delay_s, "stop_p50_ms": 1e3 * float(np.percentile(out, 50)),
+            "stop_p99_ms": 1e3 * float(np.percentile(out, 99)),
+            "mean_iterations": float(np.mean(its))}
+
+
+def run_maturity_graph(args, gidx, batches, nb):
+    """Maturity exit on the graph search -- the paper's own setting (HNSW):
+    per agent-step batch and at batch 512, recall / iterations / latency over (tau, window, g)
+    with a generous search range, against fixed search ranges."""
+    out = {"rows": [], "fixed": [], "stop": []}
+    Lmax = 256
+    for b, kk in ((1, 5), (8, 5), (64, 10), (512, 10)):
+        qs = [batches[i][:b].contiguous() for i in range(args.warmup, min(nb, args.warmup + 16))]
+        gt = [gidx.search(q, kk, 0)[0] for q in qs]
+        for m in ((0.9, 4, 1), (0.9, 16, 1), (1.0, 8, 1), (1.1, 8, 1), (1.25, 8, 1),
+                  (1.5, 8, 1), (2.0, 8, 1)):
+            r = graph_point(gidx, qs, kk, Lmax, gt, mature=m)
+            r.update(batch=b, k=kk)
+            out["rows"].append(r)
+        for L in (32, 64, 96, 128, 160, 256):
+            r = graph_point(gidx, qs, kk, max(L, kk), gt)
+            r.update(batch=b, k=kk)
+            out["fixed"].append(r)
+        if b <= 64:
+            for delay in (0.0, 0.0002):
+                r = graph_stop_latency(gidx, qs[0], kk, Lmax, delay)
+                r.update(batch=b, k=kk)
+                out["stop"].append(r)
+    return out
+
+
 def run_maturity(args, sa, idx, batches, k, nq, d, nlist, n, rank):
     """Non-stall maturity exit on the C3 IVF index: per agent-step batch,
     recall@k (vs the exact mode) / mean lists scanned / latency over a (tau, window, g) grid,
@@ -746,6 +830,14 @@ def run_maturity(args, sa, idx, batches, k, nq, d, nlist, n, rank):
             r = stop_latency(sa, idx, qs[0], kk, P, 0.0, 16, 1, delay)
             r.update(batch=b, k=kk, check_every=1)
             out["stop"].append(r)
+    if not args.no_graph:
+        t0 = time.perf_counter()
+        idx.build_graph(knn_k=args.graph_knn, degree=args.graph_degree,
+                        nprobe_build=args.graph_nprobe_build)
+        torch.cuda.synchronize()
+        out["graph"] = run_maturity_graph(args, idx, batches, nb)
+        out["graph"].update(build_s=time.perf_counter() - t0, knn_k=args.graph_knn,
+                            degree=args.graph_degree, search_width=GRAPH_W, n_entries=GRAPH_E)
     if rank == 0:
         print(json.dumps(out))
     idx.free()

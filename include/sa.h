@@ -192,7 +192,9 @@ sa_status sa_search_mature(const sa_index* idx, const void* queries, sa_dtype qd
  * n*(knn_k*4 + degree*12)).
  * sa_search_graph (R27): beam search per query over a list of search_range (L) entries,
  * expanding the search_width (w) best unexpanded entries per iteration, at most max_iters
- * iterations (also capped so the visited set fits: iterations <= (6144 - E) / (w*degree));
+ * iterations (the visited table is 8192 slots per query; when it would pass 3/4 load it is
+ * cleared down to the list's rows -- the list evolves exactly as with an unbounded visited
+ * set, forgotten rows may be scored again);
  * entry points = the first stored row (lowest id) of each of the n_entries (E) best IVF
  * lists of the query.  queries DEVICE [nq, d] of qdtype; out_ids DEVICE int64 [nq, k],
  * out_scores DEVICE fp32 [nq, k] (score desc, id asc; padded -1 / -INF), out_expanded
@@ -227,8 +229,10 @@ sa_status sa_index_import_graph(sa_index* idx, int32_t degree, const int64_t* ho
  *   - EMA_1 = RQ_1, EMA_t = a*RQ_t + (1-a)*EMA_{t-1}, a = 2/(opts->window+1), fp64;
  *   - after every opts->check_every steps the query stops if EMA_t >= opts->tau and
  *     *opts->engine_ready is nonzero (read by the device at that moment; NULL = always);
- *     otherwise it runs until no entry is left to expand or max_iters (capped as in
- *     sa_search_graph);
+ *     otherwise it runs until no entry is left to expand or max_iters;
+ *   - after a visited-table reset (see sa_search_graph) a re-scored forgotten row counts in
+ *     s_t; it lies below the list's last entry, so it can change s_t only in a step whose
+ *     genuinely new rows are all below that entry too (RQ_t > 1 either way);
  *   - the result is the list's first k entries at that point (R19).
  * One launch; each query's CTA decides on its own.  out_steps DEVICE int32 [nq] (iterations
  * run; may be NULL); out_rq / out_ema DEVICE fp64 [nq, trace_cols] per-step signal for steps
@@ -241,6 +245,32 @@ sa_status sa_search_graph_mature(const sa_index* idx, const void* queries, sa_dt
                                  const sa_maturity_opts* opts, int64_t* out_ids,
                                  float* out_scores, int32_t* out_steps, double* out_rq,
                                  double* out_ema, int32_t trace_cols, void* stream);
+
+/* ---- fp8 flat scan with bf16 re-rank (readings R30-R33) ----
+ * Not in the paper: a compressed variant of the exact mode (ENN).  The
+ * corpus scan reads an e4m3 copy of the rows (half the bytes, twice the bf16 tensor rate) to
+ * pick candidates; the candidates are re-scored on the bf16 rows, so returned scores and order
+ * are the bf16 data's, and the result is the exact top-k whenever the true top-k lie among the
+ * candidates.
+ *   R30 corpus: X8 = e4m3_rne_satfinite(x * 2^e), e = the largest integer with
+ *       max|x| * 2^e <= 448 over the whole corpus (every rank: the global maximum);
+ *   R31 queries: the same per query row with the row's own maximum;
+ *   R32 candidates: the n_cand best stored rows by the fp32 sum of the e4m3 products (score
+ *       desc, stored position asc); re-scored as the fp32 dot product of the bf16 query and row;
+ *   R33 result: the k best re-scored candidates (score desc, global id asc), padded (-1, -INF).
+ * sa_index_build_fp8: builds the copy (n_local * ceil(d/128)*128 bytes kept).  Synchronous;
+ * collective on a sharded index (every rank must call).
+ * sa_search_fp8: queries DEVICE [nq, d] of qdtype; out_ids DEVICE int64 [nq, k], out_scores
+ * DEVICE fp32 [nq, k]; 1 <= k <= n_cand <= 256.  Stream-ordered, asynchronous; sharded indexes
+ * as sa_search (every rank calls, every rank receives the global result).  SA_ERR_STATE
+ * without sa_index_build_fp8.
+ * sa_index_export_fp8: *scale_exp = e; host_out (may be NULL) HOST uint8 [n_local, d] e4m3
+ * bytes, row = global id - row_offset. */
+sa_status sa_index_build_fp8(sa_index* idx, void* stream);
+sa_status sa_search_fp8(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
+                        int32_t k, int32_t n_cand, int64_t* out_ids, float* out_scores,
+                        void* stream);
+sa_status sa_index_export_fp8(const sa_index* idx, uint8_t* host_out, int32_t* scale_exp);
 
 /* ---- agent loop support (Alg. 1, App. A.1) ---- */
 

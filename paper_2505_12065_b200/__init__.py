@@ -106,6 +106,9 @@ def lib() -> ctypes.CDLL:
         "sa_search_graph": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, i32, i32, P, P, P, P]),
         "sa_index_export_graph": (st, [P, ctypes.POINTER(i32), ctypes.POINTER(i32), P, P]),
         "sa_index_import_graph": (st, [P, i32, P]),
+        "sa_index_build_fp8": (st, [P, P]),
+        "sa_search_fp8": (st, [P, P, ctypes.c_int, i64, i32, i32, P, P, P]),
+        "sa_index_export_fp8": (st, [P, P, ctypes.POINTER(i32)]),
         "sa_search_graph_mature": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, i32, i32,
                                         ctypes.POINTER(_MaturityOpts), P, P, P, P, P, i32, P]),
         "sa_retriever_create": (st, [P, i32, i32, i32, i32, ctypes.POINTER(P)]),
@@ -368,6 +371,34 @@ class Index:
                                             _ptr(ema) if ema is not None else None,
                                             trace_cols, _stream_ptr(stream)))
         return (ids, scores, steps, rq, ema) if trace_cols > 0 else (ids, scores, steps)
+
+    # sa_index_build_fp8 / sa_search_fp8 / sa_index_export_fp8 (e4m3 scan + bf16 re-rank)
+    def build_fp8(self, stream=None):
+        _check(lib().sa_index_build_fp8(self.handle, _stream_ptr(stream)))
+        return self
+
+    def search_fp8(self, queries: torch.Tensor, k: int, n_cand: int = 64, out=None, stream=None):
+        if not queries.is_cuda or queries.dim() != 2 or not queries.is_contiguous():
+            raise ValueError("queries must be a contiguous 2-D CUDA tensor")
+        if queries.shape[1] != self.d:
+            raise SAError(SA_ERR_INVALID_ARG, f"queries have d={queries.shape[1]}, index d={self.d}")
+        nq = queries.shape[0]
+        if out is None:
+            ids = torch.empty(nq, k, dtype=torch.int64, device=queries.device)
+            scores = torch.empty(nq, k, dtype=torch.float32, device=queries.device)
+        else:
+            ids, scores = out
+        _check(lib().sa_search_fp8(self.handle, _ptr(queries), _dtype_code(queries), nq, k, n_cand,
+                                   _ptr(ids), _ptr(scores), _stream_ptr(stream)))
+        return ids, scores
+
+    def export_fp8(self):
+        """(uint8 [n_local, d] e4m3 bytes by local id, scale exponent e)."""
+        e = ctypes.c_int32()
+        out = np.empty((self.info()["n_local"], self.d), dtype=np.uint8)
+        _check(lib().sa_index_export_fp8(self.handle, out.ctypes.data_as(ctypes.c_void_p),
+                                         ctypes.byref(e)))
+        return out, e.value
 
     def import_graph(self, nbr: np.ndarray):
         """sa_index_import_graph: nbr int64 [n_local, degree] of global ids (-1 padded)."""

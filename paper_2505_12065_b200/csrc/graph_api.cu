@@ -158,7 +158,7 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
         (out_rq && trace_cols < 1))
       return set_error(SA_ERR_INVALID_ARG, "out_rq / out_ema: both NULL or both [nq, trace_cols >= 1]");
   }
-  const int T = std::min(max_iters, (GR_VISIT_CAP - E) / (w * R));
+  const int T = max_iters;   // the visited table forgets (graph.cu), so no capacity cap
   cudaStream_t s = (cudaStream_t)stream;
   // queries in chunks: the probe's dense score buffer is chunk x nlist fp32
   const int64_t C = 4096;

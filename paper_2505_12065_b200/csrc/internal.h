@@ -65,6 +65,12 @@ struct sa_index {
   int32_t graph_R = 0, graph_K = 0;
   int32_t* graph = nullptr;
   int32_t* graph_knn = nullptr;  // kept kNN lists [n_local, graph_K] (build flag bit 0)
+  // e4m3 copy of the stored rows for the fp8 flat scan (fp8_api.cu; sa_index_build_fp8)
+  uint8_t* X8 = nullptr;       // [n_local, d8_pad], stored order, scaled by 2^x8_exp
+  int32_t d8_pad = 0;          // multiple of 128 (one 128-byte K-block)
+  int32_t x8_exp = 0;
+  CUtensorMap tmap_x8;         // as 16-bit pairs [n_local, d8_pad / 2], box 128 rows
+  CUtensorMap tmap_x8_2;       // box 64 rows (cta_group 2)
   // captured progressive (maturity-exit) searches, guarded by graph_mu (mature.cu)
   std::vector<std::unique_ptr<sa::MaturePlan, void (*)(sa::MaturePlan*)>> mature_plans;
 };
@@ -80,6 +86,9 @@ sa_status make_tmap_bf16(CUtensorMap* m, const void* base, int64_t rows, int32_t
 
 // NCCL: every rank r contributes bytes [off[r], off[r]+len[r]) of buf; all ranks end with all.
 sa_status comm_broadcast_parts(const sa_comm* c, void* buf, const int64_t* off, const int64_t* len,
+                               cudaStream_t s);
+// NCCL all-gather of `bytes` per rank: recv holds world * bytes, rank-major
+sa_status comm_allgather_bytes(const sa_comm* c, const void* send, void* recv, size_t bytes,
                                cudaStream_t s);
 // balanced contiguous split
 inline void shard_range(int64_t n, int world, int rank, int64_t* off, int64_t* len) {
@@ -119,7 +128,13 @@ struct CorpusView {
   int32_t d_pad;
   const int32_t* row_ids;    // stored row -> global id, or nullptr (id = id_base + row)
   uint32_t id_base;
+  bool fp8 = false;          // e4m3 corpus and queries; d_pad counts 16-bit pairs (bytes / 2)
 };
+
+// a9 for sharded indexes: rank-local sorted [nq, k] keys -> ncclAllGather -> k-way merge
+// into (out_ids, out_scores) (sa_api.cu)
+sa_status gather_merge_keys(const sa_index* idx, const uint64_t* keys_local, int64_t nq, int32_t k,
+                            int64_t* out_ids, float* out_scores, cudaStream_t s);
 
 // exact scan of `cv` for nq staged queries (bf16 [>= nq, d_pad]) + intra-GPU merge (sa_api.cu)
 sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,

@@ -56,13 +56,14 @@ constexpr int kLockstepLag = 8;
 constexpr int kTailRows = FS_TAIL_ROWS;
 constexpr int kItemQ = 4;                // depth of the dynamic work-item queue  // box rows of the tail tensor map (IVF list tails)  // tiles a unit may run ahead of units sharing its slice  // K-blocks (64 wide) per ring stage: 8 MMAs per barrier round trip
 
-template <int CG>
+template <int CG, bool F8 = false>
 struct Cfg {
   static constexpr int kRowsPerCta = kBN / CG;              // corpus rows staged per CTA per tile
   static constexpr int kBoxBytes = kRowsPerCta * kBK * 2;  // one TMA box: rows x 64 bf16
   static constexpr int kStageBytes = kBoxBytes * kKbPerStage;
   static constexpr int kStages = CG == 1 ? 4 : 7;          // 128 / 112 KB of corpus in flight
-  static constexpr uint32_t kIdesc = ptx::umma_idesc_bf16(kBM * CG, kBN);
+  static constexpr uint32_t kIdesc =
+      F8 ? ptx::umma_idesc_e4m3(kBM * CG, kBN) : ptx::umma_idesc_bf16(kBM * CG, kBN);
 };
 
 template <int CG>
@@ -166,12 +167,12 @@ __device__ __forceinline__ WorkItem uniform_item(const WorkItem& w) {
 
 }  // namespace
 
-template <int CG>
+template <int CG, bool F8>
 __global__ void __launch_bounds__(FS_THREADS, 1)
 flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
                       const __grid_constant__ CUtensorMap tmap_tail,
                       const __grid_constant__ CUtensorMap tmap_q, const FlatScanArgs a) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, F8>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -376,15 +377,25 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (kb < kb_t) {
                   const uint32_t a_tmem = tmem + a_col + (uint32_t)(kb * (kBK / 2));
 #pragma unroll
-                  for (int kk = 0; kk < kBK / 16; ++kk)
-                    ptx::mma_bf16_elect<CG, true>(d_tmem, a_tmem + kk * 8, bdesc + kk * 2,
-                                                  C::kIdesc, (kb | kk) ? 1u : 0u);
+                  for (int kk = 0; kk < kBK / 16; ++kk) {
+                    if constexpr (F8)
+                      ptx::mma_e4m3_elect<CG, true>(d_tmem, a_tmem + kk * 8, bdesc + kk * 2,
+                                                    C::kIdesc, (kb | kk) ? 1u : 0u);
+                    else
+                      ptx::mma_bf16_elect<CG, true>(d_tmem, a_tmem + kk * 8, bdesc + kk * 2,
+                                                    C::kIdesc, (kb | kk) ? 1u : 0u);
+                  }
                 } else {
                   const uint64_t adesc = adesc0 + (uint64_t)(((kb - kb_t) * kASmemKb) >> 4);
 #pragma unroll
-                  for (int kk = 0; kk < kBK / 16; ++kk)
-                    ptx::mma_bf16_elect<CG, false>(d_tmem, adesc + kk * 2, bdesc + kk * 2,
-                                                   C::kIdesc, 1u);
+                  for (int kk = 0; kk < kBK / 16; ++kk) {
+                    if constexpr (F8)
+                      ptx::mma_e4m3_elect<CG, false>(d_tmem, adesc + kk * 2, bdesc + kk * 2,
+                                                     C::kIdesc, 1u);
+                    else
+                      ptx::mma_bf16_elect<CG, false>(d_tmem, adesc + kk * 2, bdesc + kk * 2,
+                                                     C::kIdesc, 1u);
+                  }
                 }
               }
             }
@@ -682,24 +693,23 @@ cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_ta
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cta_group == 2) {
-    static bool set2 = false;
-    if (!set2) {
-      cudaError_t e = cudaFuncSetAttribute(flat_scan_topk_kernel<2>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto go = [&](auto kern, bool& set) -> cudaError_t {
+    if (!set) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
       if (e != cudaSuccess) return e;
-      set2 = true;
+      set = true;
     }
-    return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<2>, tmap, tmap_tail, tmap_q, a);
+    return cudaLaunchKernelEx(&cfg, kern, tmap, tmap_tail, tmap_q, a);
+  };
+  static bool set[4] = {false, false, false, false};
+  if (a.fp8) {
+    if (a.mode == FS_MODE_IVF) return cudaErrorInvalidValue;  // fp8 runs the flat modes only
+    return cta_group == 2 ? go(flat_scan_topk_kernel<2, true>, set[2])
+                          : go(flat_scan_topk_kernel<1, true>, set[3]);
   }
-  static bool set1 = false;
-  if (!set1) {
-    cudaError_t e = cudaFuncSetAttribute(flat_scan_topk_kernel<1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set1 = true;
-  }
-  return cudaLaunchKernelEx(&cfg, flat_scan_topk_kernel<1>, tmap, tmap_tail, tmap_q, a);
+  return cta_group == 2 ? go(flat_scan_topk_kernel<2, false>, set[0])
+                        : go(flat_scan_topk_kernel<1, false>, set[1]);
 }
 
 }  // namespace sa

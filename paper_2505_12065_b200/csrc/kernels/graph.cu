@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
   __syncthreads();
   int expanded = 0;
   int scored = n_new;
+  int visited = n_new;   // entries in the visited table
   double ema = 0.0;  // thread 0 (maturity exit)
   int steps = 0;     // iterations run (maturity exit)
   for (int it = 0;; ++it) {
@@ -450,6 +451,18 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
     const int nc = sm.n_chosen;
     if (nc == 0) break;
     expanded += nc;
+    // ---- forgettable visited set: when the table would pass 3/4 load, clear it and keep only
+    // the list's rows.  The list evolves exactly as with the full visited set: a forgotten row
+    // is not in the list, so it was scored below the list's L-th key (or dropped below it), the
+    // L-th key only rises, and a re-scored copy is dropped by the floor test again -- only work
+    // is repeated, never a list entry.
+    if (visited + nc * a.R > GR_VISIT_CAP) {
+      for (int i = threadIdx.x; i < GR_HASH; i += kSThreads) sm.hash[i] = 0u;
+      __syncthreads();
+      for (int i = threadIdx.x; i < cnt; i += kSThreads) visit(sm.hash, sm.pos[cur][i]);
+      __syncthreads();
+      visited = cnt;
+    }
     // ---- neighbours not yet visited
     for (int t = threadIdx.x; t < nc * a.R; t += kSThreads) {
       const int32_t c = a.nbr[(int64_t)sm.chosen[t / a.R] * a.R + (t % a.R)];
@@ -458,6 +471,7 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
     __syncthreads();
     n_new = sm.n_new;
     scored += n_new;
+    visited += n_new;
     score_rows<kSThreads, kRowsPerWarp, kMature>(a, sm, n_new, nchunk,
                                         cnt == a.L ? sm.key[cur][a.L - 1] : 0ull);
     __syncthreads();

@@ -282,6 +282,39 @@ __device__ __forceinline__ void mma_bf16_elect(uint32_t d_tmem, uint64_t a, uint
           : "memory");
   }
 }
+// kind::f8f6f4 (e4m3 x e4m3 -> fp32): K = 32 per instruction, i.e. the same 32 bytes of each
+// operand row as kind::f16's K = 16, so descriptors and TMEM columns advance identically.
+template <int CG, bool A_TMEM>
+__device__ __forceinline__ void mma_e4m3_elect(uint32_t d_tmem, uint64_t a, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  if constexpr (A_TMEM) {
+    if constexpr (CG == 2)
+      asm volatile(
+          "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+          "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "r"((uint32_t)a), "l"(b_desc), "r"(idesc), "r"(accumulate)
+          : "memory");
+    else
+      asm volatile(
+          "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+          "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "r"((uint32_t)a), "l"(b_desc), "r"(idesc), "r"(accumulate)
+          : "memory");
+  } else {
+    if constexpr (CG == 2)
+      asm volatile(
+          "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+          "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "l"(a), "l"(b_desc), "r"(idesc), "r"(accumulate)
+          : "memory");
+    else
+      asm volatile(
+          "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+          "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+          "l"(a), "l"(b_desc), "r"(idesc), "r"(accumulate)
+          : "memory");
+  }
+}
 template <int CG>
 __device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
   if constexpr (CG == 2)
@@ -317,6 +350,15 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N) {
   return (1u << 4)          // c_format = F32
          | (1u << 7)        // a_format = BF16
          | (1u << 10)       // b_format = BF16
+         | ((N >> 3) << 17) // n_dim
+         | ((M >> 4) << 24);// m_dim
+}
+
+// Instruction descriptor, kind::f8f6f4: D fp32, A/B e4m3 (format code 0), both K-major.
+__host__ __device__ constexpr uint32_t umma_idesc_e4m3(uint32_t M, uint32_t N) {
+  return (1u << 4)          // c_format = F32
+         | (0u << 7)        // a_format = E4M3
+         | (0u << 10)       // b_format = E4M3
          | ((N >> 3) << 17) // n_dim
          | ((M >> 4) << 24);// m_dim
 }

@@ -197,6 +197,7 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   a.part = part;
   a.heap_g = heap;
   a.mode = FS_MODE_TOPK;
+  a.fp8 = cv.fp8 ? 1 : 0;
   {
     static const int experiment = [] {
       const char* e = getenv("SA_EXPERIMENT");
@@ -254,6 +255,7 @@ sa_status flat_scores_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   a.k = 1;
   a.dbg = out;
   a.mode = FS_MODE_DEBUG;
+  a.fp8 = cv.fp8 ? 1 : 0;
   CUtensorMap tmap_q;
   sa_status st = make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM);
   if (st != SA_OK) return st;
@@ -333,6 +335,12 @@ sa_status comm_broadcast_parts(const sa_comm* c, void* buf, const int64_t* off, 
   }
   sa_status st2 = nccl_status(nccl().GroupEnd(), "ncclGroupEnd");
   return st != SA_OK ? st : st2;
+}
+sa_status comm_allgather_bytes(const sa_comm* c, const void* send, void* recv, size_t bytes,
+                               cudaStream_t s) {
+  if (!nccl().ok) return set_error(SA_ERR_NCCL, "libnccl.so.2 not found");
+  return nccl_status(nccl().AllGather(send, recv, bytes, ncclUint8, (ncclComm_t)c->nccl, s),
+                     "ncclAllGather");
 }
 }  // namespace sa
 
@@ -425,6 +433,7 @@ sa_status sa_index_free(sa_index* idx) {
   cudaFree(idx->list_off);
   cudaFree(idx->graph);
   cudaFree(idx->graph_knn);
+  cudaFree(idx->X8);
   delete idx;
   return SA_OK;
 }
@@ -563,24 +572,37 @@ sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype
     return search_local(idx, queries, qdtype, nq, k, nprobe, out, s);
   }
   // a9: rank-local sorted [nq, k] keys (global ids) -> ncclAllGather -> k-way merge.
-  const int w = idx->comm->world;
-  uint64_t *keys_local = nullptr, *keys_all = nullptr;
+  uint64_t* keys_local = nullptr;
   st = dalloc(&keys_local, (size_t)nq * k, s, "alloc local keys");
-  if (st == SA_OK) st = dalloc(&keys_all, (size_t)nq * k * w, s, "alloc gathered keys");
   if (st == SA_OK) {
     SearchOut out;
     out.keys = keys_local;
     st = search_local(idx, queries, qdtype, nq, k, nprobe, out, s);
   }
+  if (st == SA_OK) st = gather_merge_keys(idx, keys_local, nq, k, out_ids, out_scores, s);
+  if (keys_local) cudaFreeAsync(keys_local, s);
+  return st;
+}
+
+}  // extern "C"
+
+namespace sa {
+sa_status gather_merge_keys(const sa_index* idx, const uint64_t* keys_local, int64_t nq, int32_t k,
+                            int64_t* out_ids, float* out_scores, cudaStream_t s) {
+  const int w = idx->comm->world;
+  uint64_t* keys_all = nullptr;
+  sa_status st = dalloc(&keys_all, (size_t)nq * k * w, s, "alloc gathered keys");
   if (st == SA_OK)
     st = nccl_status(nccl().AllGather(keys_local, keys_all, (size_t)nq * k, ncclUint64,
                                       (ncclComm_t)idx->comm->nccl, s),
                      "ncclAllGather");
   if (st == SA_OK) st = merge_keys(keys_all, w, nq, k, out_ids, out_scores, s);
-  if (keys_local) cudaFreeAsync(keys_local, s);
   if (keys_all) cudaFreeAsync(keys_all, s);
   return st;
 }
+}  // namespace sa
+
+extern "C" {
 
 sa_status sa_search_keys(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
                          int32_t k, int32_t nprobe, uint64_t* out_keys, void* stream) {

@@ -172,3 +172,29 @@ def test_batch_invariance_and_chunking(sa, small):
         for row in (q, q + 48 * 86):           # first chunk and second chunk (row >= 4096)
             assert torch.equal(gi[row], si[0]) and torch.equal(gs[row], ss[0])
             assert int(gx[row]) == int(sx[0]) and int(gsc[row]) == int(ssc[0])
+
+
+def test_forgettable_visited_table_keeps_the_list(sa):
+    """R27b: long searches clear the 8192-slot visited table (8 x 32 new rows per iteration
+    pass 3/4 load after ~23 iterations); the list evolves exactly as with the oracle's unbounded
+    visited set, so results and expansion counts match the oracle, and no iteration cap
+    applies (the search runs until no entry is left to expand)."""
+    mx = make_mixture(d=128, C=16, r=16, s_n=0.7)
+    X = draw_rows(mx, 60_000, row_seed=73)
+    Q = draw_rows(mx, 24, row_seed=74)
+    Xb, Qb = to_bf16_bits(X), to_bf16_bits(Q)
+    idx = sa.Index.build(bits_to_tensor(Xb).cuda(), 64, kmeans_iters=8)
+    idx.build_graph(knn_k=32, degree=32, nprobe_build=4)
+    nbr = idx.export_graph()
+    ent = entries_of(idx, Qb, 4)
+    gi, gs, gx, gsc = idx.search_graph(bits_to_tensor(Qb).cuda(), 10, 256, search_width=8,
+                                       n_entries=4, expanded=True)
+    gi, gx, gsc = gi.cpu().numpy(), gx.cpu().numpy(), gsc.cpu().numpy()
+    same = 0
+    for q in range(len(Qb)):
+        o = graph.search(Xb, nbr, Qb[q], 10, L=256, w=8, entries=ent[q], T=10_000)
+        assert o["iterations"] * 8 * 32 > 6144          # the table was reset at least once
+        same += np.array_equal(gi[q], o["ids"]) and gx[q] == o["expanded"]
+    assert same >= 0.9 * len(Qb), same
+    assert np.all(gsc >= gx)
+    idx.free()
