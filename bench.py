@@ -198,6 +198,8 @@ def main():
     ap.add_argument("--d", type=int, default=None, help="override dimension (experiments)")
     ap.add_argument("--n", type=int, default=None, help="override corpus rows (experiments)")
     ap.add_argument("--no-graph", action="store_true", help="skip the proximity-graph mode")
+    ap.add_argument("--no-fp8", action="store_true", help="skip the fp8 scan + re-rank leg")
+    ap.add_argument("--fp8-cand", type=int, default=16, help="fp8 candidates re-ranked per query")
     ap.add_argument("--graph-knn", type=int, default=64)
     ap.add_argument("--graph-degree", type=int, default=48)
     ap.add_argument("--graph-nprobe-build", type=int, default=8)
@@ -320,6 +322,8 @@ def main():
         return float(t.item())
 
     def run_search(i, nprobe):
+        if isinstance(nprobe, tuple) and nprobe[0] == "fp8":   # ("fp8", n_cand)
+            return idx.search_fp8(batches[i], k, nprobe[1], out=(ids, scores))
         if isinstance(nprobe, tuple):          # ("graph", L)
             return gidx.search_graph(gbatches[i], k, nprobe[1], search_width=GRAPH_W,
                                      n_entries=GRAPH_E)
@@ -394,6 +398,40 @@ def main():
                          "frac_of_sustained": achieved / pk["bf16_sus"] if pk["bf16_sus"] else None,
                          "kernel_ms": per_launch, "kernel_share_of_step": fs_ms / ms_e,
                          "traffic": traffic_from_profiles("flat_scan", args.config, nq)},
+        }
+    # ---- fp8 flat scan + bf16 re-rank, beside the exact mode
+    result_fp8 = None
+    if mode in ("auto", "exact") and not args.no_fp8:
+        t0 = time.perf_counter()
+        idx.build_fp8()
+        torch.cuda.synchronize()
+        fp8_build_s = time.perf_counter() - t0
+        egt = gt if gt else {i: idx.search(batches[i], k, 0)[0].clone()
+                             for i in range(args.warmup, nb)}
+        ms_8, kern_8, clk_8 = timed(("fp8", args.fp8_cand))
+        rec, exact_q = [], []
+        for i in range(args.warmup, nb):
+            fi = idx.search_fp8(batches[i], k, args.fp8_cand)[0]
+            rec.append(recall_at_k(fi, egt[i]))
+            exact_q.append((fi == egt[i]).all(dim=1).float().mean().item())
+        fs_ms, fs_n = kern_8["flat_scan"]
+        per_launch = fs_ms / max(fs_n, 1)
+        achieved = 2.0 * nq * n_local * d / (per_launch / 1e3) / 1e12
+        peak8 = 2.0 * pk["bf16"]   # measured bf16 peak x the guide's nominal fp8/bf16 ratio (2)
+        result_fp8 = {
+            "value": args.steps * nq / (ms_8 / 1e3), "unit": "queries/s",
+            "recall": float(np.mean(rec)), "n_cand": args.fp8_cand,
+            "exact_match_frac": float(np.mean(exact_q)),   # queries whose ids equal exact's
+            "ms_per_step": ms_8 / args.steps, "clocks": clk_8, "build_s": fp8_build_s,
+            "kernel_ms": {kk: v[0] for kk, v in kern_8.items()},
+            "kernel_launches": {kk: v[1] for kk, v in kern_8.items()},
+            "roofline": {"kernel": "flat_scan_topk_kernel<fp8>", "bound": "tensor",
+                         "achieved": achieved, "peak": peak8, "unit": "TFLOP/s",
+                         "frac": achieved / peak8,
+                         "peak_kind": f"e4m3 dense = 2 x bf16 {pk['src']} burst "
+                                      "(MEASURED_PEAKS.json x the guide's nominal ratio 4.5/2.25)",
+                         "kernel_ms": per_launch, "kernel_share_of_step": fs_ms / ms_8,
+                         "traffic": traffic_from_profiles("flat_scan_fp8", args.config, nq)},
         }
     result_ivf = None
     if use_ivf and mode != "graph":
@@ -541,7 +579,7 @@ def main():
         "gpu_launches": int(sum(v for v in head["kernel_launches"].values())),
         "kernel_ms": head["kernel_ms"], "kernel_launches": head["kernel_launches"],
         "clocks": head["clocks"],
-        "exact": result_exact, "ivf": result_ivf, "graph": result_graph,
+        "exact": result_exact, "exact_fp8": result_fp8, "ivf": result_ivf, "graph": result_graph,
         "build_s": build_s, "graph_build_s": graph_build_s, "gen_s": gen_s,
     }
     # ---- agent-step batches (BASELINE config 5 shape): p50/p99 latency of one sa_search_host

@@ -418,9 +418,14 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const int k = a.k;
     // Heaps live in smem for k <= FS_KSMEM (insertions are latency-critical: the epilogue
-    // must finish a tile within one MMA tile time), else in global scratch.
-    uint64_t* heap = (k <= FS_KSMEM) ? (heap_s + et)
-                                     : (a.heap_g + (size_t)blockIdx.x * k * kEpiT + et);
+    // must finish a tile within one MMA tile time), for k <= FS_KSMEM_BIG when the whole A
+    // operand sits in TMEM (the heaps then start at the unused smem A region, which directly
+    // precedes heap_s: 64 + 32 KB = 48 x 256 keys), else in global scratch.
+    static_assert(FS_KB_SMEM * kASmemKb + FS_KSMEM * kEpiT * 8 == FS_KSMEM_BIG * kEpiT * 8,
+                  "smem A region + heap region must hold FS_KSMEM_BIG heaps");
+    const bool heap_smem = k <= (kb_s == 0 ? FS_KSMEM_BIG : FS_KSMEM);
+    uint64_t* heap = heap_smem ? ((kb_s == 0 ? reinterpret_cast<uint64_t*>(a_smem) : heap_s) + et)
+                               : (a.heap_g + (size_t)blockIdx.x * k * kEpiT + et);
     if (a.mode != FS_MODE_DEBUG)
       for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
     float thr = heap_threshold(0ull);

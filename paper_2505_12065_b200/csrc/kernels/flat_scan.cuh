@@ -18,8 +18,15 @@ constexpr int FS_MAX_DPAD = 768; // queries: up to 8 K-blocks in TMEM + 4 in sme
 constexpr int FS_KB_TMEM = 8;    // K-blocks of the A operand held in TMEM (256 columns)
 constexpr int FS_KB_SMEM = 4;    // K-blocks of the A operand held in smem (64 KB)
 constexpr int FS_KSMEM = 16;     // running heaps in smem for k <= 16, else in global scratch
+constexpr int FS_KSMEM_BIG = 48; // ... or k <= 48 when the A operand fits TMEM (d_pad <= 512):
+                                 // the heaps then also take the unused 64 KB A region
 constexpr int FS_TAIL_ROWS = 32;  // box rows of the tail tensor map (IVF list tails)
 constexpr int FS_LISTS_PER_ITEM = 2;  // partial lists per (query, work item): one per column half
+
+// largest k whose running heaps stay in shared memory for this d_pad
+inline int fs_heap_smem_cap(int32_t d_pad) {
+  return d_pad <= FS_KB_TMEM * FS_BK ? FS_KSMEM_BIG : FS_KSMEM;
+}
 
 enum FlatScanMode : int32_t {
   FS_MODE_TOPK = 0,   // flat: work item = (query group, corpus slice)

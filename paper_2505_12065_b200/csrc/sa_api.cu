@@ -157,7 +157,7 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   uint64_t *part = nullptr, *heap = nullptr;
   sa_status st = dalloc(&part, (size_t)nq_pad * p.S * FS_LISTS_PER_ITEM * k, s, "alloc partials");
   if (st != SA_OK) return st;
-  if (k > FS_KSMEM) {
+  if (k > fs_heap_smem_cap(cv.d_pad)) {
     st = dalloc(&heap, (size_t)p.grid * k * FS_EPI_THREADS, s, "alloc heaps");
     if (st != SA_OK) { cudaFreeAsync(part, s); return st; }
   }
