@@ -336,12 +336,17 @@ def main():
         barrier()
         sa.profile_enable(True)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # NVTX range per timed region: `ncu --nvtx --nvtx-include "timed_graph/"` (or timed_ivf,
+        # timed_exact, timed_fp8) lists exactly the launches of one mode's timed steps
+        tag = nprobe[0] if isinstance(nprobe, tuple) else ("ivf" if nprobe else "exact")
         with ClockSampler(local) as clk:
             barrier()
+            torch.cuda.nvtx.range_push(f"timed_{tag}")
             ev0.record(stream)
             for i in range(args.steps):
                 run_search(args.warmup + i, nprobe)
             ev1.record(stream)
+            torch.cuda.nvtx.range_pop()
             barrier()
         ms = max_over_ranks(ev0.elapsed_time(ev1))
         kern = {kind: sa.profile_read(kind) for kind in sa.KERNEL_KINDS}
@@ -525,13 +530,9 @@ def main():
     sc_h = torch.empty(nq, k, dtype=torch.float32).pin_memory()
 
     def host_search(qhost):
-        if head_is_graph:   # public API: pinned host -> device, sa_search_graph, device -> host
-            gi, gs = gidx.search_graph(qhost.to("cuda", non_blocking=True), k,
-                                       head["search_range"], search_width=GRAPH_W,
-                                       n_entries=GRAPH_E)
-            ids_h.copy_(gi, non_blocking=True)
-            sc_h.copy_(gs, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+        if head_is_graph:   # C ABI with host buffers: H2D, sa_search_graph, D2H in the call
+            gidx.search_graph_host(qhost, k, head["search_range"], search_width=GRAPH_W,
+                                   n_entries=GRAPH_E, out=(ids_h, sc_h))
         else:
             idx.search_host(qhost, k, head_nprobe, out=(ids_h, sc_h))
 
@@ -613,11 +614,8 @@ def main():
             ts = []
             for i in range(105):
                 t_s = time.perf_counter()
-                gi, gs = gidx.search_graph(qb[i % 8].to("cuda", non_blocking=True), 5, Lg,
-                                          search_width=GRAPH_W, n_entries=GRAPH_E)
-                ih.copy_(gi, non_blocking=True)
-                sh.copy_(gs, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+                gidx.search_graph_host(qb[i % 8], 5, Lg, search_width=GRAPH_W, n_entries=GRAPH_E,
+                                       out=(ih, sh))
                 if i >= 5:
                     ts.append(time.perf_counter() - t_s)
             agent_g.append({"batch": b, "k": 5, "search_range": Lg,

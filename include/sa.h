@@ -212,6 +212,25 @@ sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdt
                           float* out_scores, int32_t* out_expanded, void* stream);
 sa_status sa_index_export_graph(const sa_index* idx, int32_t* degree, int32_t* knn_k,
                                 int64_t* host_nbr, int64_t* host_knn);
+/* sa_search_graph_ex: sa_search_graph with flags.  SA_GRAPH_FP8 (reading R34): the beam
+ * search scores rows on the index's e4m3 copy (sa_index_build_fp8; R30/R31 quantisation,
+ * scores = fp32 sums of e4m3 products) -- half the gathered bytes -- and the final list of
+ * search_range entries is re-scored on the bf16 rows (fp32 dot products), the k best returned
+ * (score desc, id asc).  SA_ERR_STATE without the e4m3 copy; other flags SA_ERR_INVALID_ARG. */
+#define SA_GRAPH_FP8 1
+sa_status sa_search_graph_ex(const sa_index* idx, const void* queries, sa_dtype qdtype,
+                             int64_t nq, int32_t k, int32_t search_range, int32_t search_width,
+                             int32_t n_entries, int32_t max_iters, int32_t flags,
+                             int64_t* out_ids, float* out_scores, int32_t* out_expanded,
+                             void* stream);
+/* sa_search_graph_host: sa_search_graph_ex (no iteration cap) with HOST buffers (queries HOST
+ * [nq, d] of qdtype, out_ids HOST int64 [nq, k], out_scores HOST fp32 [nq, k]); the
+ * host->device copy, the search and the device->host copy are enqueued on `stream` and the
+ * call returns when the results are in host memory (the end-to-end API of the graph mode). */
+sa_status sa_search_graph_host(const sa_index* idx, const void* queries_host, sa_dtype qdtype,
+                               int64_t nq, int32_t k, int32_t search_range, int32_t search_width,
+                               int32_t n_entries, int32_t flags, int64_t* out_ids_host,
+                               float* out_scores_host, void* stream);
 /* sa_index_import_graph: replace idx's graph by host_nbr HOST int64 [n_local, degree] in
  * sa_index_export_graph's layout (row = global id - row_offset, entries global ids of this
  * index, -1 padded); the inverse of export (a saved graph, or a hand-built one in tests).

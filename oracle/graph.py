@@ -23,6 +23,9 @@ best-first beam search over a candidate list of size L (the search range).  Read
        list entries (stop if there are none), mark them expanded, collect their neighbours
        not yet visited (mark visited), score them and keep the top-L of list + new ones.
        Result: the first k list entries, padded (-1, -inf).
+  R34  search_fp8: R27 with every score taken on the e4m3 values of oracle/fp8.py (R30
+       corpus, R31 query), then the final list's L entries re-scored on the bf16 values; the
+       k best (score desc, id asc), padded.
 
 Scores are fp64 dot products of the stored bf16 values (numpy matmul as a library step).
 Graph-building steps R23-R26 are integer logic on the kNN lists.
@@ -108,7 +111,8 @@ def build(X_bits: np.ndarray, K: int, R: int, candidates=None):
 
 
 def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: int, w: int,
-           entries, T: int, tau=None, window: int = 1, g: int = 1, ready=True):
+           entries, T: int, tau=None, window: int = 1, g: int = 1, ready=True, values=None,
+           qv=None):
     """R27 for one query.  Returns dict(ids, scores, expanded, iterations[, rq, ema]).
 
     With tau set, the non-stall maturity exit of PAPER.md §3.3 (App. B.2) runs on
@@ -117,9 +121,10 @@ def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: i
     the rows scored in the step (none -> RQ = 1), RQ_t = (s_best - s_t)/(s_best - s_worst)
     over the list's first / last entries (1 if equal), EMA as R17 (alpha = 2/(window+1),
     seeded with RQ_1); after every g-th step the search stops if EMA >= tau and the engine is
-    ready (ready(t) or a constant); the result is the list at that point (R19)."""
-    X = bf16_to_f64(X_bits)
-    q = bf16_to_f64(q_bits)
+    ready (ready(t) or a constant); the result is the list at that point (R19).
+    values / qv: fp64 rows / query to score with instead of the bf16 ones (R34)."""
+    X = bf16_to_f64(X_bits) if values is None else values
+    q = bf16_to_f64(q_bits) if qv is None else qv
     visited = set()
     ent = []
     for e in entries:
@@ -171,8 +176,28 @@ def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: i
     for j, e in enumerate(lst[:k]):
         out_ids[j] = e[1]
         out_sc[j] = e[0]
-    out = {"ids": out_ids, "scores": out_sc, "expanded": expanded, "iterations": it}
+    out = {"ids": out_ids, "scores": out_sc, "expanded": expanded, "iterations": it,
+           "list_ids": np.array([e[1] for e in lst], dtype=np.int64)}
     if tau is not None:
         out["rq"] = np.array(rqs)
         out["ema"] = np.array(emas)
     return out
+
+
+def search_fp8(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: int, w: int,
+               entries, T: int, X8=None):
+    """R34 for one query.  X8: oracle.fp8.quantize_corpus(X_bits)[0] (computed if None)."""
+    from . import fp8
+    if X8 is None:
+        X8 = fp8.quantize_corpus(X_bits)[0]
+    q8 = fp8.quantize_queries(np.asarray(q_bits)[None, :])[0][0]
+    r = search(X_bits, nbr, q_bits, L, L, w, entries, T, values=X8, qv=q8)
+    cand = r["list_ids"]
+    s = bf16_to_f64(X_bits[cand]) @ bf16_to_f64(q_bits) if cand.size else np.empty(0)
+    order = np.lexsort((cand, -s))[:k]
+    out_ids = np.full(k, -1, dtype=np.int64)
+    out_sc = np.full(k, -np.inf)
+    out_ids[:order.size] = cand[order]
+    out_sc[:order.size] = s[order]
+    return {"ids": out_ids, "scores": out_sc, "expanded": r["expanded"],
+            "iterations": r["iterations"], "list_ids": cand}

@@ -22,6 +22,7 @@ _SO = os.path.join(_PKG, "libsa.so")
 
 SA_OK, SA_ERR_INVALID_ARG, SA_ERR_STATE, SA_ERR_OOM, SA_ERR_CUDA, SA_ERR_NCCL, SA_ERR_UNSUPPORTED = range(7)
 SA_BF16, SA_F32 = 0, 1
+SA_GRAPH_FP8 = 1   # sa_search_graph_ex flag (include/sa.h)
 KERNEL_KINDS = ("flat_scan", "merge", "stage", "ivf_probe", "ivf_scan", "other", "graph_search")
 
 
@@ -106,6 +107,9 @@ def lib() -> ctypes.CDLL:
         "sa_search_graph": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, i32, i32, P, P, P, P]),
         "sa_index_export_graph": (st, [P, ctypes.POINTER(i32), ctypes.POINTER(i32), P, P]),
         "sa_index_import_graph": (st, [P, i32, P]),
+        "sa_search_graph_host": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, i32, i32, P, P, P]),
+        "sa_search_graph_ex": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, i32, i32, i32, P, P, P,
+                                    P]),
         "sa_index_build_fp8": (st, [P, P]),
         "sa_search_fp8": (st, [P, P, ctypes.c_int, i64, i32, i32, P, P, P]),
         "sa_index_export_fp8": (st, [P, P, ctypes.POINTER(i32)]),
@@ -330,19 +334,38 @@ class Index:
 
     def search_graph(self, queries: torch.Tensor, k: int, search_range: int, *,
                      search_width: int = 4, n_entries: int = 8, max_iters: int = 1 << 30,
-                     expanded: bool = False, stream=None):
+                     expanded: bool = False, fp8: bool = False, stream=None):
         if not queries.is_cuda or queries.dim() != 2 or not queries.is_contiguous():
             raise ValueError("queries must be a contiguous 2-D CUDA tensor")
         nq = queries.shape[0]
         ids = torch.empty(nq, k, dtype=torch.int64, device=queries.device)
         scores = torch.empty(nq, k, dtype=torch.float32, device=queries.device)
         ex = torch.empty(2, nq, dtype=torch.int32, device=queries.device) if expanded else None
-        _check(lib().sa_search_graph(self.handle, _ptr(queries), _dtype_code(queries), nq, k,
-                                     search_range, search_width, n_entries,
-                                     min(max_iters, 2**31 - 1), _ptr(ids), _ptr(scores),
-                                     _ptr(ex) if expanded else None, _stream_ptr(stream)))
+        _check(lib().sa_search_graph_ex(self.handle, _ptr(queries), _dtype_code(queries), nq, k,
+                                        search_range, search_width, n_entries,
+                                        min(max_iters, 2**31 - 1), SA_GRAPH_FP8 if fp8 else 0,
+                                        _ptr(ids), _ptr(scores), _ptr(ex) if expanded else None,
+                                        _stream_ptr(stream)))
         # expanded: (entries expanded [nq], rows scored [nq])
         return (ids, scores, ex[0], ex[1]) if expanded else (ids, scores)
+
+    def search_graph_host(self, queries: torch.Tensor, k: int, search_range: int, *,
+                          search_width: int = 4, n_entries: int = 8, fp8: bool = False, out=None,
+                          stream=None):
+        """sa_search_graph_host: queries a (pinned) CPU tensor; results in CPU tensors."""
+        if queries.is_cuda or queries.dim() != 2 or not queries.is_contiguous():
+            raise ValueError("queries must be a contiguous 2-D CPU tensor")
+        nq = queries.shape[0]
+        if out is None:
+            ids = torch.empty(nq, k, dtype=torch.int64).pin_memory()
+            scores = torch.empty(nq, k, dtype=torch.float32).pin_memory()
+        else:
+            ids, scores = out
+        _check(lib().sa_search_graph_host(self.handle, _ptr(queries), _dtype_code(queries), nq, k,
+                                          search_range, search_width, n_entries,
+                                          SA_GRAPH_FP8 if fp8 else 0, _ptr(ids), _ptr(scores),
+                                          _stream_ptr(stream)))
+        return ids, scores
 
     def search_graph_mature(self, queries: torch.Tensor, k: int, search_range: int, *,
                             tau: float, window: int, check_every: int = 1,

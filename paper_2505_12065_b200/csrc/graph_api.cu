@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "kernels/fp8.cuh"
 #include "kernels/graph.cuh"
 #include "kernels/merge.cuh"
 
@@ -131,12 +132,14 @@ sa_status sa_index_build_graph(sa_index* idx, int32_t knn_k, int32_t degree, int
 
 namespace {
 
-// sa_search_graph and sa_search_graph_mature: `mo` NULL = plain beam search (R27)
+// sa_search_graph(_ex) and sa_search_graph_mature: `mo` NULL = plain beam search (R27);
+// fp8 = navigation on the e4m3 copy + bf16 re-rank of the final list (R34)
 sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
                        int32_t k, int32_t search_range, int32_t search_width, int32_t n_entries,
                        int32_t max_iters, const sa_maturity_opts* mo, int64_t* out_ids,
                        float* out_scores, int32_t* out_expanded, int32_t* out_steps,
-                       double* out_rq, double* out_ema, int32_t trace_cols, void* stream) {
+                       double* out_rq, double* out_ema, int32_t trace_cols, void* stream,
+                       bool fp8 = false) {
   if (!idx || !queries || !out_ids || !out_scores)
     return set_error(SA_ERR_INVALID_ARG, "null pointer");
   if (!idx->graph) return set_error(SA_ERR_STATE, "no graph: call sa_index_build_graph");
@@ -150,6 +153,8 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
   if (E < 1 || E > std::min(idx->nlist, 256))
     return set_error(SA_ERR_INVALID_ARG, "need 1 <= n_entries <= min(nlist, 256)");
   if (max_iters < 0) return set_error(SA_ERR_INVALID_ARG, "max_iters must be >= 0");
+  if (fp8 && !idx->X8) return set_error(SA_ERR_STATE, "fp8 navigation: call sa_index_build_fp8");
+  if (fp8 && mo) return set_error(SA_ERR_UNSUPPORTED, "maturity exit with fp8 navigation");
   if (mo) {
     if (!(mo->tau == mo->tau)) return set_error(SA_ERR_INVALID_ARG, "tau is NaN");
     if (mo->window < 1 || mo->check_every < 1)
@@ -170,7 +175,13 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
     __nv_bfloat16* Qs = nullptr;
     float* psc = nullptr;
     uint64_t* pkeys = nullptr;
-    st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "graph search");
+    uint8_t* Q8 = nullptr;
+    uint64_t* cand = nullptr;
+    if (fp8) {
+      st = dalloc(&Q8, (size_t)nq_pad * idx->d8_pad, s, "graph search");
+      if (st == SA_OK) st = dalloc(&cand, (size_t)nc * L, s, "graph search");
+    }
+    if (st == SA_OK) st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "graph search");
     if (st == SA_OK) st = dalloc(&psc, (size_t)nc * idx->nlist, s, "graph search");
     if (st == SA_OK) st = dalloc(&pkeys, (size_t)nc * E, s, "graph search");
     if (st == SA_OK) {
@@ -179,6 +190,10 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
                                        qdtype == SA_F32, nc, idx->d, Qs, nq_pad, idx->d_pad,
                                        idx->num_sms, s),
                        "stage queries");
+      if (st == SA_OK && fp8)
+        st = cuda_status(launch_quant_e4m3(Qs, nq_pad, idx->d_pad, nullptr, Q8, idx->d8_pad,
+                                           nullptr, idx->num_sms, s),
+                         "stage fp8 queries");
       prof_end(SA_KERNEL_STAGE, s);
       prof_count(SA_KERNEL_STAGE);
     }
@@ -229,14 +244,40 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
         m.out_rq = out_rq ? out_rq + q0 * trace_cols : nullptr;
         m.out_ema = out_rq ? out_ema + q0 * trace_cols : nullptr;
       }
+      if (fp8) {
+        a.X8 = idx->X8;
+        a.Q8 = Q8;
+        a.d8_pad = idx->d8_pad;
+        a.out_keys = cand;
+      }
       prof_begin(SA_KERNEL_GRAPH_SEARCH, s);
-      st = cuda_status(launch_graph_search(a, mo ? &m : nullptr, nc, s), "graph search");
+      st = cuda_status(launch_graph_search(a, mo ? &m : nullptr, nc, s, fp8), "graph search");
       prof_end(SA_KERNEL_GRAPH_SEARCH, s);
       prof_count(SA_KERNEL_GRAPH_SEARCH);
+    }
+    if (st == SA_OK && fp8) {
+      // R34: the final list re-scored on the bf16 rows, the k best
+      RerankArgs r{};
+      r.X = idx->X;
+      r.d_pad = idx->d_pad;
+      r.row_ids = idx->row_ids;
+      r.row_offset = idx->row_offset;
+      r.Qs = Qs;
+      r.cand = cand;
+      r.n_cand = L;
+      r.k = k;
+      r.out_ids = out_ids + q0 * k;
+      r.out_scores = out_scores + q0 * k;
+      prof_begin(SA_KERNEL_MERGE, s);
+      st = cuda_status(launch_rerank(r, nc, s), "graph re-rank");
+      prof_end(SA_KERNEL_MERGE, s);
+      prof_count(SA_KERNEL_MERGE);
     }
     if (Qs) cudaFreeAsync(Qs, s);
     if (psc) cudaFreeAsync(psc, s);
     if (pkeys) cudaFreeAsync(pkeys, s);
+    if (Q8) cudaFreeAsync(Q8, s);
+    if (cand) cudaFreeAsync(cand, s);
   }
   return st;
 }
@@ -252,6 +293,54 @@ sa_status sa_search_graph(const sa_index* idx, const void* queries, sa_dtype qdt
   return graph_search(idx, queries, qdtype, nq, k, search_range, search_width, n_entries,
                       max_iters, nullptr, out_ids, out_scores, out_expanded, nullptr, nullptr,
                       nullptr, 0, stream);
+}
+
+sa_status sa_search_graph_ex(const sa_index* idx, const void* queries, sa_dtype qdtype,
+                             int64_t nq, int32_t k, int32_t search_range, int32_t search_width,
+                             int32_t n_entries, int32_t max_iters, int32_t flags,
+                             int64_t* out_ids, float* out_scores, int32_t* out_expanded,
+                             void* stream) {
+  if (flags & ~SA_GRAPH_FP8) return set_error(SA_ERR_INVALID_ARG, "unknown flags");
+  return graph_search(idx, queries, qdtype, nq, k, search_range, search_width, n_entries,
+                      max_iters, nullptr, out_ids, out_scores, out_expanded, nullptr, nullptr,
+                      nullptr, 0, stream, (flags & SA_GRAPH_FP8) != 0);
+}
+
+sa_status sa_search_graph_host(const sa_index* idx, const void* queries_host, sa_dtype qdtype,
+                               int64_t nq, int32_t k, int32_t search_range, int32_t search_width,
+                               int32_t n_entries, int32_t flags, int64_t* out_ids_host,
+                               float* out_scores_host, void* stream) {
+  if (flags & ~SA_GRAPH_FP8) return set_error(SA_ERR_INVALID_ARG, "unknown flags");
+  if (!idx || !queries_host || !out_ids_host || !out_scores_host)
+    return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
+  if (nq < 1 || nq > (1ll << 31) - 1) return set_error(SA_ERR_INVALID_ARG, "bad nq");
+  if (k < 1 || k > 256) return set_error(SA_ERR_INVALID_ARG, "k must be in [1, 256]");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t qbytes = (size_t)nq * idx->d * (qdtype == SA_F32 ? 4 : 2);
+  void* dq = nullptr;
+  int64_t* dids = nullptr;
+  float* dsc = nullptr;
+  sa_status st = cuda_status(cudaMallocAsync(&dq, qbytes, s), "alloc queries");
+  if (st == SA_OK) st = dalloc(&dids, (size_t)nq * k, s, "alloc ids");
+  if (st == SA_OK) st = dalloc(&dsc, (size_t)nq * k, s, "alloc scores");
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(dq, queries_host, qbytes, cudaMemcpyHostToDevice, s), "H2D");
+  if (st == SA_OK)
+    st = graph_search(idx, dq, qdtype, nq, k, search_range, search_width, n_entries, 1 << 30,
+                      nullptr, dids, dsc, nullptr, nullptr, nullptr, nullptr, 0, stream,
+                      (flags & SA_GRAPH_FP8) != 0);
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(out_ids_host, dids, (size_t)nq * k * 8,
+                                     cudaMemcpyDeviceToHost, s), "D2H ids");
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(out_scores_host, dsc, (size_t)nq * k * 4,
+                                     cudaMemcpyDeviceToHost, s), "D2H scores");
+  if (dq) cudaFreeAsync(dq, s);
+  if (dids) cudaFreeAsync(dids, s);
+  if (dsc) cudaFreeAsync(dsc, s);
+  sa_status st2 = cuda_status(cudaStreamSynchronize(s), "search sync");
+  return st != SA_OK ? st : st2;
 }
 
 sa_status sa_search_graph_mature(const sa_index* idx, const void* queries, sa_dtype qdtype,

@@ -12,6 +12,8 @@
 // survivors are merged into the sorted list by rank counting.  Memory-latency bound: a query's
 // iterations are dependent gathers, so several CTAs per SM hide each other's latency.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include "graph.cuh"
 #include "keys.cuh"
@@ -325,6 +327,70 @@ __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, in
   }
 }
 
+// 16 e4m3 values (one uint4) . 16 fp32 query values
+__device__ __forceinline__ float e4m3x16_dot(const uint4 v, const float* q) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const __half2_raw r =
+          __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[i] >> (16 * h)), __NV_E4M3);
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&r));
+      acc = fmaf(f.x, q[4 * i + 2 * h], acc);
+      acc = fmaf(f.y, q[4 * i + 2 * h + 1], acc);
+    }
+  }
+  return acc;
+}
+
+constexpr int kF8RowsPerWarp = 4;  // 4 x 2 uint4 in flight per lane: 0 spills at 64 registers
+
+// score_rows on the e4m3 copy (R34): a row is d8_pad bytes = nch 16-byte chunks, lane l holds
+// chunks l and l + 32; twice the rows in flight of the bf16 path for the same registers.
+template <int kSThreads, int kRowsPerWarp>
+__device__ void score_rows_f8(const GraphSearchArgs& a, SearchSmem& sm, int cnt,
+                              unsigned long long floor) {
+  constexpr int kSWarps = kSThreads / 32;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nch = a.d8_pad / 16;
+  const uint4* X4 = reinterpret_cast<const uint4*>(a.X8);
+  for (int j0 = warp * kRowsPerWarp; j0 < cnt; j0 += kSWarps * kRowsPerWarp) {
+    uint4 v[kRowsPerWarp][2];
+    int32_t p[kRowsPerWarp];
+    uint32_t gid[kRowsPerWarp];
+#pragma unroll
+    for (int u = 0; u < kRowsPerWarp; ++u) {
+      p[u] = j0 + u < cnt ? sm.npos[j0 + u] : -1;
+      gid[u] = (lane == 0 && p[u] >= 0) ? (uint32_t)__ldg(a.row_ids + p[u]) : 0u;
+#pragma unroll
+      for (int rd = 0; rd < 2; ++rd) {
+        const int c = rd * 32 + lane;
+        v[u][rd] = (p[u] >= 0 && c < nch) ? __ldg(X4 + (int64_t)p[u] * nch + c)
+                                          : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kRowsPerWarp; ++u) {
+      float acc = 0.f;
+#pragma unroll
+      for (int rd = 0; rd < 2; ++rd)
+        if (rd * 32 + lane < nch) acc += e4m3x16_dot(v[u][rd], sm.q + (rd * 32 + lane) * 16);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0 && p[u] >= 0) {
+        const unsigned long long key = make_key(acc, gid[u]);
+        if (key > floor) {
+          const int t = atomicAdd(&sm.n_ins, 1);
+          sm.nkey[t] = key;
+          sm.ipos[t] = p[u];
+        }
+      }
+    }
+  }
+}
+
 // number of entries of the descending array a[0, n) that are > x
 __device__ __forceinline__ int count_greater(const unsigned long long* a, int n,
                                              unsigned long long x) {
@@ -337,7 +403,7 @@ __device__ __forceinline__ int count_greater(const unsigned long long* a, int n,
   return lo;
 }
 
-template <int kSThreads, int kRowsPerWarp, bool kMature>
+template <int kSThreads, int kRowsPerWarp, bool kMature, bool kF8>
 __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
     graph_search_kernel(const GraphSearchArgs a, const GraphMatureArgs m) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -346,8 +412,15 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
   const int lane = threadIdx.x % 32;
   const int nchunk = a.d_pad / 8;
   for (int i = threadIdx.x; i < GR_HASH; i += kSThreads) sm.hash[i] = 0u;
-  for (int i = threadIdx.x; i < a.d_pad; i += kSThreads)
-    sm.q[i] = __bfloat162float(a.Q[(int64_t)q * a.d_pad + i]);
+  if constexpr (kF8) {
+    for (int i = threadIdx.x; i < a.d8_pad; i += kSThreads) {
+      const __half_raw r = __nv_cvt_fp8_to_halfraw(a.Q8[(int64_t)q * a.d8_pad + i], __NV_E4M3);
+      sm.q[i] = __half2float(*reinterpret_cast<const __half*>(&r));
+    }
+  } else {
+    for (int i = threadIdx.x; i < a.d_pad; i += kSThreads)
+      sm.q[i] = __bfloat162float(a.Q[(int64_t)q * a.d_pad + i]);
+  }
   if (threadIdx.x == 0) {
     sm.n_new = 0;
     sm.n_ins = 0;
@@ -366,7 +439,8 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
   int cur = 0;
   int n_new = sm.n_new;
   int cnt = 0;
-  score_rows<kSThreads, kRowsPerWarp, false>(a, sm, n_new, nchunk, 0ull);
+  if constexpr (kF8) score_rows_f8<kSThreads, kF8RowsPerWarp>(a, sm, n_new, 0ull);
+  else score_rows<kSThreads, kRowsPerWarp, false>(a, sm, n_new, nchunk, 0ull);
   __syncthreads();
   int expanded = 0;
   int scored = n_new;
@@ -472,14 +546,25 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
     n_new = sm.n_new;
     scored += n_new;
     visited += n_new;
-    score_rows<kSThreads, kRowsPerWarp, kMature>(a, sm, n_new, nchunk,
-                                        cnt == a.L ? sm.key[cur][a.L - 1] : 0ull);
+    if constexpr (kF8)
+      score_rows_f8<kSThreads, kF8RowsPerWarp>(a, sm, n_new,
+                                                 cnt == a.L ? sm.key[cur][a.L - 1] : 0ull);
+    else
+      score_rows<kSThreads, kRowsPerWarp, kMature>(a, sm, n_new, nchunk,
+                                                   cnt == a.L ? sm.key[cur][a.L - 1] : 0ull);
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < a.k; i += kSThreads) {
-    const unsigned long long key = i < cnt ? sm.key[cur][i] : 0ull;
-    a.out_ids[(int64_t)q * a.k + i] = key == 0ull ? -1 : (int64_t)key_id(key);
-    a.out_scores[(int64_t)q * a.k + i] = key == 0ull ? -INFINITY : key_score(key);
+  if constexpr (kF8) {
+    // the whole list, re-keyed with stored positions, for the bf16 re-rank
+    for (int i = threadIdx.x; i < a.L; i += kSThreads)
+      a.out_keys[(int64_t)q * a.L + i] =
+          i < cnt ? make_key(key_score(sm.key[cur][i]), (uint32_t)sm.pos[cur][i]) : 0ull;
+  } else {
+    for (int i = threadIdx.x; i < a.k; i += kSThreads) {
+      const unsigned long long key = i < cnt ? sm.key[cur][i] : 0ull;
+      a.out_ids[(int64_t)q * a.k + i] = key == 0ull ? -1 : (int64_t)key_id(key);
+      a.out_scores[(int64_t)q * a.k + i] = key == 0ull ? -INFINITY : key_score(key);
+    }
   }
   if (a.out_expanded && threadIdx.x == 0) {
     a.out_expanded[q] = expanded;
@@ -534,38 +619,40 @@ cudaError_t launch_graph_merge(const int32_t* fwd, const uint64_t* rev, int64_t 
 
 size_t graph_search_smem(int) { return sizeof(SearchSmem); }
 
-template <int TH, int RW, bool M>
+template <int TH, int RW, bool M, bool F8>
 cudaError_t launch_shape(const GraphSearchArgs& a, const GraphMatureArgs& m, int64_t nq,
                          cudaStream_t s) {
   const size_t smem = sizeof(SearchSmem);
   static bool set = false;
   if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(graph_search_kernel<TH, RW, M>,
+    cudaError_t e = cudaFuncSetAttribute(graph_search_kernel<TH, RW, M, F8>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     set = true;
   }
-  graph_search_kernel<TH, RW, M><<<(unsigned)nq, TH, smem, s>>>(a, m);
+  graph_search_kernel<TH, RW, M, F8><<<(unsigned)nq, TH, smem, s>>>(a, m);
   return cudaGetLastError();
 }
 
-template <bool M>
+template <bool M, bool F8>
 cudaError_t launch_shapes(const GraphSearchArgs& a, const GraphMatureArgs& m, int64_t nq,
                           cudaStream_t s) {
-  if (nq <= 148) return launch_shape<1024, 3, M>(a, m, nq, s);
-  if (nq <= 296) return launch_shape<512, 3, M>(a, m, nq, s);
-  return launch_shape<256, 3, M>(a, m, nq, s);
+  if (nq <= 148) return launch_shape<1024, 3, M, F8>(a, m, nq, s);
+  if (nq <= 296) return launch_shape<512, 3, M, F8>(a, m, nq, s);
+  return launch_shape<256, 3, M, F8>(a, m, nq, s);
 }
 
 cudaError_t launch_graph_search(const GraphSearchArgs& a, const GraphMatureArgs* m, int64_t nq,
-                                cudaStream_t s) {
+                                cudaStream_t s, bool fp8) {
   // Throughput shape: 256 threads x 3 rows in flight per warp at 4 CTAs/SM (64 registers,
   // ~45 KB smem), every query of a 512 batch resident at once.  Measured alternatives (C3,
   // L=160): 128 threads x 6 rows 0.84x, 128 x 8 (spills) 0.6x, 256 x 4 (spills) slower.
   // Latency shapes for small batches (agent steps): 1024 threads when at most one query per
   // SM (an iteration's ~100-200 new rows all in flight at once), 512 threads for two.
   // (C3, L=104: batch 1 0.32 ms, 64 0.40 ms, 148 0.43 ms vs 0.65 ms with the 256 shape.)
-  return m ? launch_shapes<true>(a, *m, nq, s) : launch_shapes<false>(a, GraphMatureArgs{}, nq, s);
+  if (fp8) return m ? cudaErrorInvalidValue : launch_shapes<false, true>(a, GraphMatureArgs{}, nq, s);
+  return m ? launch_shapes<true, false>(a, *m, nq, s)
+           : launch_shapes<false, false>(a, GraphMatureArgs{}, nq, s);
 }
 
 }  // namespace sa

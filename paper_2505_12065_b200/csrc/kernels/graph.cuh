@@ -47,6 +47,13 @@ struct GraphSearchArgs {
   float* out_scores;        // [nq, k]
   int32_t* out_expanded;    // optional [2, nq]: entries expanded, rows scored
   int32_t nq;
+  // fp8 navigation (reading R34): rows scored on the e4m3 copy X8 [n, d8_pad] against the
+  // staged e4m3 queries Q8 [nq, d8_pad]; the final list (L entries, keys with STORED
+  // positions, 0-padded) goes to out_keys [nq, L] for the bf16 re-rank (fp8.cu)
+  const uint8_t* X8;
+  const uint8_t* Q8;
+  int32_t d8_pad;
+  uint64_t* out_keys;
 };
 // non-stall maturity exit on the beam search (§3.3; readings R28-R29): a step is one
 // iteration; RQ_t / EMA_t in fp64; after every g-th step the query stops if EMA_t >= tau and
@@ -61,8 +68,8 @@ struct GraphMatureArgs {
   double* out_ema;
 };
 size_t graph_search_smem(int L);
-// m == nullptr: plain beam search
+// m == nullptr: plain beam search; fp8: navigation on the e4m3 copy (no maturity exit)
 cudaError_t launch_graph_search(const GraphSearchArgs& a, const GraphMatureArgs* m, int64_t nq,
-                                cudaStream_t s);
+                                cudaStream_t s, bool fp8 = false);
 
 }  // namespace sa

@@ -198,3 +198,59 @@ def test_forgettable_visited_table_keeps_the_list(sa):
     assert same >= 0.9 * len(Qb), same
     assert np.all(gsc >= gx)
     idx.free()
+
+
+def test_host_buffer_call_equals_device_call(sa, small):
+    """sa_search_graph_host (H2D + search + D2H inside the call) == sa_search_graph."""
+    idx, Xb, Qb, nbr, kn = small
+    Qd = bits_to_tensor(Qb).cuda()
+    gi, gs = idx.search_graph(Qd, 10, 64, search_width=2, n_entries=4)
+    for q in (Qd.cpu().pin_memory(), Qd.float().cpu()):     # bf16 pinned, fp32 pageable
+        hi, hs = idx.search_graph_host(q, 10, 64, search_width=2, n_entries=4)
+        assert torch.equal(hi, gi.cpu()) and torch.equal(hs, gs.cpu())
+
+
+def test_fp8_navigation_matches_oracle(sa, small):
+    """R34: the beam search on the e4m3 copy + bf16 re-rank of the final list reproduces
+    oracle/graph.search_fp8 on the same graph and entries (identical ids for almost all
+    queries; fp32 vs fp64 sums of the same e4m3 products can reorder near-ties), returned
+    scores = the bf16 scores within the band."""
+    from oracle import fp8 as ofp8
+    idx, Xb, Qb, nbr, kn = small
+    idx.build_fp8()
+    X8 = ofp8.quantize_corpus(Xb)[0]
+    ent = entries_of(idx, Qb, 4)
+    Qd = bits_to_tensor(Qb).cuda()
+    same, rec = 0, []
+    for L, w in ((32, 2), (96, 4)):
+        gi, gs, gx, _ = idx.search_graph(Qd, 10, L, search_width=w, n_entries=4, expanded=True,
+                                         fp8=True)
+        gi, gs, gx = gi.cpu().numpy(), gs.cpu().numpy(), gx.cpu().numpy()
+        for q in range(len(Qb)):
+            o = graph.search_fp8(Xb, nbr, Qb[q], 10, L=L, w=w, entries=ent[q], T=10_000, X8=X8)
+            same += np.array_equal(gi[q], o["ids"]) and gx[q] == o["expanded"]
+            rec.append(len(set(gi[q]) & set(o["ids"])) / 10)
+            ps = oracle.pair_scores(Xb, Qb[q:q + 1], np.zeros(10, int), gi[q])
+            assert np.all(np.abs(ps - gs[q]) <= 1e-3 * np.maximum(np.abs(ps), 1e-3))
+            assert np.all(np.diff(gs[q]) <= 0) and len(set(gi[q].tolist())) == 10
+    assert same >= 0.9 * 2 * len(Qb), same
+    assert np.mean(rec) >= 0.99
+    hi, hs = idx.search_graph_host(Qd.cpu().pin_memory(), 10, 96, search_width=4, n_entries=4,
+                                   fp8=True)
+    assert np.array_equal(hi.numpy(), gi) and np.array_equal(hs.numpy(), gs)
+
+
+def test_fp8_navigation_golden_path_graph(sa):
+    """GR6 on the GPU: on the e4m3 grid the fp8 search is the bf16 search, bit for bit."""
+    from test_graph_oracle import path_graph
+    X, nbr, q = path_graph()
+    idx = sa.Index.build(bits_to_tensor(X).cuda(), 1,
+                         centroids=torch.ones(1, X.shape[1], dtype=torch.float32).cuda())
+    idx.import_graph(nbr).build_fp8()
+    gi, gs = idx.search_graph(bits_to_tensor(q).cuda(), 2, 2, search_width=1, n_entries=1,
+                              fp8=True)
+    assert gi.cpu().tolist()[0] == [3, 2] and gs.cpu().tolist()[0] == [0.5, 0.375]
+    with pytest.raises(sa.SAError):
+        sa.Index.build(bits_to_tensor(X).cuda(), 1).import_graph(nbr).search_graph(
+            bits_to_tensor(q).cuda(), 2, 2, fp8=True)      # no e4m3 copy -> SA_ERR_STATE
+    idx.free()

@@ -118,3 +118,38 @@ def test_gr5_maturity_on_beam_search_by_hand():
     assert r["iterations"] == 4 and r["ids"].tolist() == [3, 2]
     r = graph.search(X, nbr, q[0], 2, L=2, w=1, entries=[0], T=100, tau=0.0, window=3, g=3)
     assert r["iterations"] == 3 and r["ids"].tolist() == [3, 2]
+
+
+def test_gr6_fp8_navigation_exact_on_e4m3_grid():
+    """R34 on the GR2 path graph: every value is on the e4m3 grid after the power-of-two
+    scaling (0.125..0.5 -> 64..256), so the fp8 scores are the bf16 scores times 2^17 and the
+    fp8-navigated search equals the bf16 one, ids and (re-ranked) scores."""
+    X, nbr, q = path_graph()
+    a = graph.search(X, nbr, q[0], 2, L=2, w=1, entries=[0], T=100)
+    b = graph.search_fp8(X, nbr, q[0], 2, L=2, w=1, entries=[0], T=100)
+    assert b["ids"].tolist() == a["ids"].tolist() == [3, 2]
+    assert b["scores"].tolist() == [0.5, 0.375] and b["iterations"] == a["iterations"]
+
+
+def test_gr7_fp8_exhaustive_is_bf16_brute_force_over_reachable():
+    """L >= n keeps every reachable node in the list whatever the (fp8) scores, so the bf16
+    re-rank returns the exact bf16 top-k of the reachable set (oracle.c)."""
+    Xb = mixture()
+    nbr, _ = graph.build(Xb, 16, 8)
+    g = np.random.default_rng(3)
+    Q = g.standard_normal((6, 32))
+    Q /= np.linalg.norm(Q, axis=1, keepdims=True)
+    Qb = bits(Q)
+    seen, todo = {0}, [0]
+    while todo:
+        u = todo.pop()
+        for v in nbr[u]:
+            if v >= 0 and int(v) not in seen:
+                seen.add(int(v))
+                todo.append(int(v))
+    reach = np.array(sorted(seen))
+    ids, sc = oracle.flat_topk(Xb[reach], Qb, 10)
+    for i in range(6):
+        r = graph.search_fp8(Xb, nbr, Qb[i], 10, L=300, w=4, entries=[0], T=10_000)
+        assert r["ids"].tolist() == reach[ids[i]].tolist()
+        assert np.allclose(r["scores"], sc[i], rtol=0, atol=1e-12)
