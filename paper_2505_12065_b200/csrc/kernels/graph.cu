@@ -12,8 +12,6 @@
 // survivors are merged into the sorted list by rank counting.  Memory-latency bound: a query's
 // iterations are dependent gathers, so several CTAs per SM hide each other's latency.
 #include <cuda_bf16.h>
-#include <cuda_fp16.h>
-#include <cuda_fp8.h>
 
 #include "graph.cuh"
 #include "keys.cuh"
@@ -233,7 +231,7 @@ __global__ void __launch_bounds__(256) graph_merge_kernel(const int32_t* __restr
 
 struct SearchSmem {
   uint32_t hash[GR_HASH];
-  float q[768];
+  __align__(16) float q[768];   // float4 slots, swizzled (q_slot_bf16 / q_slot_e4m3)
   unsigned long long key[2][GR_MAX_L];
   int32_t pos[2][GR_MAX_L];
   uint8_t flag[2][GR_MAX_L];
@@ -263,9 +261,17 @@ __device__ __forceinline__ bool visit(uint32_t* hash, int32_t pos) {
   }
 }
 
-__device__ __forceinline__ float bf16x8_dot(const uint4 v, const float* q) {
-  const float4 qa = *reinterpret_cast<const float4*>(q);
-  const float4 qb = *reinterpret_cast<const float4*>(q + 4);
+// The query sits in smem as float4 slots, swizzled so that the 8 lanes of one LDS.128 phase
+// (consecutive chunks) hit 8 different 16-byte bank groups: bf16 chunk c (8 values) owns slots
+// 2c, 2c+1 with its two halves swapped when bit 2 of c is set; e4m3 chunk c (16 values) owns
+// slots 4c..4c+3 rotated by c >> 1.  (Unswizzled, the lanes' 32 / 64-byte strides gave 2- and
+// 4-way conflicts: short-scoreboard stalls on the FMAs.)
+__device__ __forceinline__ int q_slot_bf16(int c, int g) { return 2 * c + (g ^ ((c >> 2) & 1)); }
+__device__ __forceinline__ int q_slot_e4m3(int c, int g) { return 4 * c + ((g + (c >> 1)) & 3); }
+
+__device__ __forceinline__ float bf16x8_dot(const uint4 v, const float4* q4, int c) {
+  const float4 qa = q4[q_slot_bf16(c, 0)];
+  const float4 qb = q4[q_slot_bf16(c, 1)];
   const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
   const float2 f0 = __bfloat1622float2(b[0]), f1 = __bfloat1622float2(b[1]);
   const float2 f2 = __bfloat1622float2(b[2]), f3 = __bfloat1622float2(b[3]);
@@ -311,7 +317,8 @@ __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, in
       float acc = 0.f;
 #pragma unroll
       for (int rd = 0; rd < 3; ++rd)
-        if (rd * 32 + lane < nchunk) acc += bf16x8_dot(v[u][rd], sm.q + (rd * 32 + lane) * 8);
+        if (rd * 32 + lane < nchunk)
+          acc += bf16x8_dot(v[u][rd], reinterpret_cast<const float4*>(sm.q), rd * 32 + lane);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0 && p[u] >= 0) {
@@ -327,22 +334,29 @@ __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, in
   }
 }
 
-// 16 e4m3 values (one uint4) . 16 fp32 query values
-__device__ __forceinline__ float e4m3x16_dot(const uint4 v, const float* q) {
+// e4m3 byte at bits 31..24 of t -> fp32 bits of (value * 2^-120): the sign moves as is and
+// the 7 exponent/mantissa bits land in the low exponent bits (eeee) and the top mantissa bits
+// (mmm), i.e. the e4m3 exponent bias 7 becomes fp32's 127 (subnormals map to fp32 subnormals,
+// exactly).  Three integer ops instead of the conversion-unit cvt path.
+__device__ __forceinline__ float e4m3_top_to_f32(uint32_t t) {
+  return __uint_as_float((t & 0x80000000u) | ((t >> 4) & 0x07F00000u));
+}
+constexpr int kF8QueryShift = 112;  // query values are pre-scaled by 2^112: products = x*q*2^-8
+
+// 16 e4m3 values (one uint4) . 16 fp32 query values (pre-scaled by 2^kF8QueryShift)
+__device__ __forceinline__ float e4m3x16_dot(const uint4 v, const float4* q4, int c) {
+  // four independent 4-long FMA chains (one per 32-bit word), summed pairwise
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  float acc = 0.f;
+  float acc[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const __half2_raw r =
-          __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[i] >> (16 * h)), __NV_E4M3);
-      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&r));
-      acc = fmaf(f.x, q[4 * i + 2 * h], acc);
-      acc = fmaf(f.y, q[4 * i + 2 * h + 1], acc);
-    }
+    const float4 q = q4[q_slot_e4m3(c, i)];
+    acc[i] = e4m3_top_to_f32(w[i] << 24) * q.x;
+    acc[i] = fmaf(e4m3_top_to_f32(w[i] << 16), q.y, acc[i]);
+    acc[i] = fmaf(e4m3_top_to_f32(w[i] << 8), q.z, acc[i]);
+    acc[i] = fmaf(e4m3_top_to_f32(w[i]), q.w, acc[i]);
   }
-  return acc;
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
 constexpr int kF8RowsPerWarp = 4;  // 4 x 2 uint4 in flight per lane: 0 spills at 64 registers
@@ -376,7 +390,8 @@ __device__ void score_rows_f8(const GraphSearchArgs& a, SearchSmem& sm, int cnt,
       float acc = 0.f;
 #pragma unroll
       for (int rd = 0; rd < 2; ++rd)
-        if (rd * 32 + lane < nch) acc += e4m3x16_dot(v[u][rd], sm.q + (rd * 32 + lane) * 16);
+        if (rd * 32 + lane < nch)
+          acc += e4m3x16_dot(v[u][rd], reinterpret_cast<const float4*>(sm.q), rd * 32 + lane);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0 && p[u] >= 0) {
@@ -413,13 +428,14 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
   const int nchunk = a.d_pad / 8;
   for (int i = threadIdx.x; i < GR_HASH; i += kSThreads) sm.hash[i] = 0u;
   if constexpr (kF8) {
-    for (int i = threadIdx.x; i < a.d8_pad; i += kSThreads) {
-      const __half_raw r = __nv_cvt_fp8_to_halfraw(a.Q8[(int64_t)q * a.d8_pad + i], __NV_E4M3);
-      sm.q[i] = __half2float(*reinterpret_cast<const __half*>(&r));
-    }
+    for (int i = threadIdx.x; i < a.d8_pad; i += kSThreads)
+      sm.q[q_slot_e4m3(i >> 4, (i >> 2) & 3) * 4 + (i & 3)] =
+          ldexpf(e4m3_top_to_f32((uint32_t)a.Q8[(int64_t)q * a.d8_pad + i] << 24),
+                 120 + kF8QueryShift);
   } else {
     for (int i = threadIdx.x; i < a.d_pad; i += kSThreads)
-      sm.q[i] = __bfloat162float(a.Q[(int64_t)q * a.d_pad + i]);
+      sm.q[q_slot_bf16(i >> 3, (i >> 2) & 1) * 4 + (i & 3)] =
+          __bfloat162float(a.Q[(int64_t)q * a.d_pad + i]);
   }
   if (threadIdx.x == 0) {
     sm.n_new = 0;

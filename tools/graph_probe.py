@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--widths", default="1,2,4")
     ap.add_argument("--entries", default="8")
     ap.add_argument("--latency", action="store_true", help="also time agent-step batches")
+    ap.add_argument("--fp8", default="0", help="comma list of 0/1: bf16 and/or fp8 navigation")
     args = ap.parse_args()
     cfg = dict(CONFIGS["c3"])
     n, d = args.n, cfg["d"]
@@ -49,6 +50,9 @@ def main():
     idx.build_graph(knn_k=args.knn, degree=args.degree, nprobe_build=args.nprobe_build)
     torch.cuda.synchronize()
     graph_s = time.perf_counter() - t0
+    fp8s = [int(x) for x in args.fp8.split(",")]
+    if any(fp8s):
+        idx.build_fp8()
     Q = torch.empty(4 * args.nq, d, dtype=torch.bfloat16, device="cuda")
     draw_rows_into(mix, Q, QUERY_SEED, 0)
     qs = [Q[i * args.nq:(i + 1) * args.nq] for i in range(4)]
@@ -57,13 +61,15 @@ def main():
            "nprobe_build": args.nprobe_build, "ivf_build_s": ivf_s, "graph_build_s": graph_s,
            "nq": args.nq, "rows": []}
     stream = torch.cuda.current_stream()
-    for E, w, L in [(E, w, L) for E in [int(x) for x in args.entries.split(",")]
-                    for w in [int(x) for x in args.widths.split(",")]
-                    for L in [int(x) for x in args.ranges.split(",")]]:
+    for f8, E, w, L in [(f8, E, w, L) for f8 in fp8s
+                        for E in [int(x) for x in args.entries.split(",")]
+                        for w in [int(x) for x in args.widths.split(",")]
+                        for L in [int(x) for x in args.ranges.split(",")]]:
         if True:
             rec, exp = [], []
             for q, t in zip(qs, gt):
-                gi, _, ex, sc_rows = idx.search_graph(q, 10, L, search_width=w, n_entries=E, expanded=True)
+                gi, _, ex, sc_rows = idx.search_graph(q, 10, L, search_width=w, n_entries=E,
+                                                      expanded=True, fp8=bool(f8))
                 gi = gi.cpu().numpy()
                 rec.append(np.mean([len(set(gi[i]) & set(t[i])) / 10 for i in range(len(t))]))
                 exp.append(ex.float().mean().item())
@@ -73,14 +79,20 @@ def main():
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 for i in range(8):
-                    idx.search_graph(qs[i % 4], 10, L, search_width=w, n_entries=E)
+                    idx.search_graph(qs[i % 4], 10, L, search_width=w, n_entries=E, fp8=bool(f8))
                 e1.record(stream)
                 torch.cuda.synchronize()
                 reps.append(e0.elapsed_time(e1) / 8)
             ms = float(np.median(reps))
-            out["rows"].append({"L": L, "w": w, "E": E, "recall": float(np.mean(rec)),
+            sa.profile_enable(True)
+            for i in range(8):
+                idx.search_graph(qs[i % 4], 10, L, search_width=w, n_entries=E, fp8=bool(f8))
+            torch.cuda.synchronize()
+            kern = {kd: round(sa.profile_read(kd)[0] / 8, 4) for kd in sa.KERNEL_KINDS}
+            sa.profile_enable(False)
+            out["rows"].append({"fp8": f8, "L": L, "w": w, "E": E, "recall": float(np.mean(rec)),
                                 "expanded": float(np.mean(exp)), "ms_per_batch": ms,
-                                "qps": args.nq / (ms / 1e3)})
+                                "qps": args.nq / (ms / 1e3), "kernel_ms": kern})
             print(json.dumps(out["rows"][-1]), file=sys.stderr, flush=True)
     if args.latency:
         # agent-step batches: device time per call (stage + probe + search), median of 50
