@@ -167,7 +167,7 @@ __device__ __forceinline__ WorkItem uniform_item(const WorkItem& w) {
 
 }  // namespace
 
-template <int CG, bool F8>
+template <int CG, bool F8, bool DUMP>
 __global__ void __launch_bounds__(FS_THREADS, 1)
 flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
                       const __grid_constant__ CUtensorMap tmap_tail,
@@ -426,7 +426,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     const bool heap_smem = k <= (kb_s == 0 ? FS_KSMEM_BIG : FS_KSMEM);
     uint64_t* heap = heap_smem ? ((kb_s == 0 ? reinterpret_cast<uint64_t*>(a_smem) : heap_s) + et)
                                : (a.heap_g + (size_t)blockIdx.x * k * kEpiT + et);
-    if (a.mode != FS_MODE_DEBUG)
+    if constexpr (!DUMP)
       for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
     float thr = heap_threshold(0ull);
     int acc = 0;
@@ -596,19 +596,35 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           nx_ready = true;
           if (nx.qkey < 0 || nx.qkey != wi.qkey) stage_a(nx, ns);
         }
-        if (!valid || a.experiment != 0) continue;
-
         const int32_t row0 = wi.row_base + t * kBN + half * 64;
-        if (a.mode == FS_MODE_DEBUG) {
-          // debug: materialise the score tile (tests only)
-          float* dst = a.dbg + (size_t)q * a.n_rows;
+        if constexpr (DUMP) {
+          // Score dump (IVF probe, graph entry points, tests): the warp's 32 queries x 64
+          // columns go through a 4 KB smem tile per 32 columns (XOR-swizzled, conflict-free)
+          // so every store instruction writes one query's 32 consecutive scores (128 B)
+          // instead of 32 scattered words.  Flat work items: the lanes hold consecutive
+          // queries.  heap_s is free in this mode (no heaps).
+          if (a.experiment == 0 && __any_sync(0xffffffffu, valid)) {
+            float* tb = reinterpret_cast<float*>(heap_s) + ew * 1024;
+            const int64_t qbase = q - lane;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (row0 + j < a.n_rows) dst[row0 + j] = __uint_as_float(r0[j]);
-            if (row0 + 32 + j < a.n_rows) dst[row0 + 32 + j] = __uint_as_float(r1[j]);
+            for (int j = 0; j < 32; ++j) tb[lane * 32 + (j ^ lane)] = __uint_as_float(r0[j]);
+            __syncwarp();
+            for (int rr = 0; rr < 32; ++rr)
+              if (qbase + rr < a.nq && row0 + lane < a.n_rows)
+                a.dbg[(qbase + rr) * a.n_rows + row0 + lane] = tb[rr * 32 + (lane ^ rr)];
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tb[lane * 32 + (j ^ lane)] = __uint_as_float(r1[j]);
+            __syncwarp();
+            for (int rr = 0; rr < 32; ++rr)
+              if (qbase + rr < a.nq && row0 + 32 + lane < a.n_rows)
+                a.dbg[(qbase + rr) * a.n_rows + row0 + 32 + lane] = tb[rr * 32 + (lane ^ rr)];
+            __syncwarp();
           }
           continue;
         }
+        if (!valid || a.experiment != 0) continue;
+
         float m0 = fmaxf(__uint_as_float(r0[0]), __uint_as_float(r0[1]));
         float m1 = fmaxf(__uint_as_float(r1[0]), __uint_as_float(r1[1]));
 #pragma unroll
@@ -639,7 +655,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           }
         }
       }
-      if (a.mode != FS_MODE_DEBUG) {
+      if constexpr (!DUMP) {
         // flush this work item's partial list and reset the heap
         if (valid) {
           const size_t slot = ivf ? (size_t)(a.q_slot[(size_t)q * a.nprobe + probe_j] + wi.chunk)
@@ -707,14 +723,20 @@ cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_ta
     }
     return cudaLaunchKernelEx(&cfg, kern, tmap, tmap_tail, tmap_q, a);
   };
-  static bool set[4] = {false, false, false, false};
+  // instantiations: (CG, F8, DUMP); the score dump (FS_MODE_DEBUG) has its own, heap-free one
+  static bool set[6] = {false, false, false, false, false, false};
+  if (a.mode == FS_MODE_DEBUG) {
+    if (a.fp8) return cudaErrorInvalidValue;
+    return cta_group == 2 ? go(flat_scan_topk_kernel<2, false, true>, set[4])
+                          : go(flat_scan_topk_kernel<1, false, true>, set[5]);
+  }
   if (a.fp8) {
     if (a.mode == FS_MODE_IVF) return cudaErrorInvalidValue;  // fp8 runs the flat modes only
-    return cta_group == 2 ? go(flat_scan_topk_kernel<2, true>, set[2])
-                          : go(flat_scan_topk_kernel<1, true>, set[3]);
+    return cta_group == 2 ? go(flat_scan_topk_kernel<2, true, false>, set[2])
+                          : go(flat_scan_topk_kernel<1, true, false>, set[3]);
   }
-  return cta_group == 2 ? go(flat_scan_topk_kernel<2, false>, set[0])
-                        : go(flat_scan_topk_kernel<1, false>, set[1]);
+  return cta_group == 2 ? go(flat_scan_topk_kernel<2, false, false>, set[0])
+                        : go(flat_scan_topk_kernel<1, false, false>, set[1]);
 }
 
 }  // namespace sa
