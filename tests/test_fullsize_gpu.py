@@ -94,3 +94,41 @@ def test_c3_ivf_full_size(sa, c3):
     assert np.array_equal(ei.cpu().numpy(), c3["ids"]) and np.array_equal(es.cpu().numpy(), c3["sc"])
     del Xl
     idx.free()
+
+
+def test_c3_graph_and_fp8_full_size(sa, c3):
+    """The headline graph mode (degree 48, L = 104, w = 4, 16 entry lists: bench.py's
+    calibrated point) and the fp8 scan + re-rank at full size: recall against the exact result
+    over all 512 queries, returned scores = the fp64 oracle's scores of the returned ids (band
+    rule) on the sampled queries, strict order, batch invariance of the graph search."""
+    X, Q = c3["X"], c3["Q"]
+    idx = sa.Index.build(X, 16384)
+    idx.build_graph(knn_k=64, degree=48, nprobe_build=8)
+    idx.build_fp8()
+    Qb_all = _bits(Q)
+    exact = c3["ids"]
+
+    def scores_ok(ids, sc, q):
+        rows = _bits(X[torch.as_tensor(ids, device="cuda")])
+        ps = oracle.pair_scores(rows, Qb_all[q:q + 1], np.zeros(len(ids), int), np.arange(len(ids)))
+        return np.all(np.abs(ps - sc) <= 1e-3 * np.maximum(np.abs(ps), 1e-3))
+
+    gi, gs = idx.search_graph(Q, 10, 104, search_width=4, n_entries=16)
+    gi, gs = gi.cpu().numpy(), gs.cpu().numpy()
+    rec = np.mean([len(set(gi[q]) & set(exact[q])) / 10 for q in range(len(gi))])
+    assert rec >= 0.95, rec
+    for q in SAMPLE_Q:
+        assert scores_ok(gi[q], gs[q], q), q
+        assert len(set(gi[q].tolist())) == 10
+        for j in range(9):
+            assert gs[q, j] > gs[q, j + 1] or (gs[q, j] == gs[q, j + 1] and gi[q, j] < gi[q, j + 1])
+    for q in (0, 300):   # alone (1024-thread shape) == inside the 512 batch (256-thread shape)
+        si, ss = idx.search_graph(Q[q:q + 1].contiguous(), 10, 104, search_width=4, n_entries=16)
+        assert np.array_equal(si.cpu().numpy()[0], gi[q]) and np.array_equal(ss.cpu().numpy()[0], gs[q])
+    fi, fs = idx.search_fp8(Q, 10, 16)
+    fi, fs = fi.cpu().numpy(), fs.cpu().numpy()
+    same = np.mean([np.array_equal(fi[q], exact[q]) for q in range(len(fi))])
+    assert same >= 0.99, same
+    for q in SAMPLE_Q:
+        assert scores_ok(fi[q], fs[q], q), q
+    idx.free()
