@@ -328,6 +328,14 @@ sa_status sa_retriever_create(const sa_index* idx, int32_t streams, int32_t slot
 sa_status sa_retriever_submit(sa_retriever* r, const float* queries_host, int32_t nq, int32_t k,
                               int32_t nprobe_max, int32_t mature, const sa_maturity_opts* opts,
                               int64_t* task_id);
+/* The same task over the proximity graph (the paper's own retriever family): mature = 0 ->
+ * sa_search_graph, mature = 1 -> sa_search_graph_mature with *opts and the retriever's flag.
+ * result's per-query count is the beam-search iterations run (maturity exit) or -1 (plain).
+ * Errors as sa_retriever_submit and sa_search_graph. */
+sa_status sa_retriever_submit_graph(sa_retriever* r, const float* queries_host, int32_t nq,
+                                    int32_t k, int32_t search_range, int32_t search_width,
+                                    int32_t n_entries, int32_t mature,
+                                    const sa_maturity_opts* opts, int64_t* task_id);
 sa_status sa_retriever_poll(sa_retriever* r, int64_t task_id, int32_t* done);
 sa_status sa_retriever_result(sa_retriever* r, int64_t task_id, int64_t* ids_host,
                               float* scores_host, int32_t* lists_host);

@@ -118,6 +118,8 @@ def lib() -> ctypes.CDLL:
         "sa_retriever_create": (st, [P, i32, i32, i32, i32, ctypes.POINTER(P)]),
         "sa_retriever_submit": (st, [P, P, i32, i32, i32, i32, ctypes.POINTER(_MaturityOpts),
                                      ctypes.POINTER(i64)]),
+        "sa_retriever_submit_graph": (st, [P, P, i32, i32, i32, i32, i32, i32,
+                                           ctypes.POINTER(_MaturityOpts), ctypes.POINTER(i64)]),
         "sa_retriever_poll": (st, [P, i64, ctypes.POINTER(i32)]),
         "sa_retriever_result": (st, [P, i64, P, P, P]),
         "sa_retriever_set_engine_ready": (st, [P, i32]),
@@ -552,6 +554,20 @@ class Retriever:
         _check(lib().sa_retriever_submit(self.handle, q.ctypes.data_as(ctypes.c_void_p),
                                          q.shape[0], k, nprobe_max, int(mature), ctypes.byref(o),
                                          ctypes.byref(t)))
+        self._shape[t.value] = (q.shape[0], k)
+        return t.value
+
+    def submit_graph(self, queries: np.ndarray, k: int, search_range: int, *,
+                     search_width: int = 4, n_entries: int = 16, mature: bool = False,
+                     tau: float = 0.0, window: int = 1, check_every: int = 1) -> int:
+        q = np.ascontiguousarray(queries, dtype=np.float32)
+        o = _MaturityOpts()
+        o.tau, o.window, o.check_every = float(tau), int(window), int(check_every)
+        t = ctypes.c_int64()
+        _check(lib().sa_retriever_submit_graph(self.handle, q.ctypes.data_as(ctypes.c_void_p),
+                                               q.shape[0], k, search_range, search_width,
+                                               n_entries, int(mature), ctypes.byref(o),
+                                               ctypes.byref(t)))
         self._shape[t.value] = (q.shape[0], k)
         return t.value
 

@@ -107,14 +107,21 @@ sa_status sa_retriever_create(const sa_index* idx, int32_t streams, int32_t slot
   return SA_OK;
 }
 
-sa_status sa_retriever_submit(sa_retriever* r, const float* queries_host, int32_t nq, int32_t k,
-                              int32_t nprobe_max, int32_t mature, const sa_maturity_opts* opts,
-                              int64_t* task_id) {
+}  // extern "C"
+
+namespace {
+
+// Alg. 1 LaunchAsyncRetrievalTask: stage the queries in a free slot's pinned buffer, enqueue
+// H2D -> `search(d_q, d_ids, d_sc, d_lists, stream)` -> D2H on the next stream, record the
+// slot's event and return the task id.  `lists_fill` >= 0: the per-query count reported
+// instead of a device-written one.
+template <typename Search>
+sa_status submit_task(sa_retriever* r, const float* queries_host, int32_t nq, int32_t k,
+                      bool device_lists, int32_t lists_fill, int32_t nprobe, int32_t mature,
+                      int64_t* task_id, Search search) {
   if (!r || !queries_host || !task_id) return set_error(SA_ERR_INVALID_ARG, "null pointer");
   if (nq < 1 || nq > r->max_nq || k < 1 || k > r->max_k)
     return set_error(SA_ERR_INVALID_ARG, "nq / k outside the retriever's limits");
-  if (mature && (!opts || nprobe_max < 1))
-    return set_error(SA_ERR_INVALID_ARG, "maturity exit needs opts and nprobe_max >= 1");
   std::lock_guard<std::mutex> lock(r->mu);
   sa_retriever::Slot* s = nullptr;
   for (auto& c : r->slots)
@@ -130,36 +137,72 @@ sa_status sa_retriever_submit(sa_retriever* r, const float* queries_host, int32_
                                              cudaMemcpyHostToDevice, st),
                              "retrieval H2D");
   if (rc != SA_OK) return rc;
-  if (mature) {
-    sa_maturity_opts o = *opts;
-    o.engine_ready = r->flag;
-    rc = sa_search_mature(r->idx, s->d_q, SA_F32, nq, k, nprobe_max, &o, s->d_ids, s->d_sc,
-                          s->d_lists, nullptr, nullptr, st);
-  } else {
-    rc = sa_search_ex(r->idx, s->d_q, SA_F32, nq, k, nprobe_max, s->d_ids, s->d_sc, st);
-  }
+  rc = search(s->d_q, s->d_ids, s->d_sc, s->d_lists, st);
   if (rc != SA_OK) return rc;
   const size_t nk = (size_t)nq * k;
   rc = cuda_status(cudaMemcpyAsync(s->h_ids, s->d_ids, nk * 8, cudaMemcpyDeviceToHost, st), "D2H");
   if (rc == SA_OK)
     rc = cuda_status(cudaMemcpyAsync(s->h_sc, s->d_sc, nk * 4, cudaMemcpyDeviceToHost, st), "D2H");
-  if (rc == SA_OK && mature)
+  if (rc == SA_OK && device_lists)
     rc = cuda_status(cudaMemcpyAsync(s->h_lists, s->d_lists, (size_t)nq * 4,
                                      cudaMemcpyDeviceToHost, st),
                      "D2H");
   if (rc == SA_OK) rc = cuda_status(cudaEventRecord(s->done, st), "event");
   if (rc != SA_OK) return rc;
-  if (!mature)
-    for (int i = 0; i < nq; ++i) s->h_lists[i] = nprobe_max;
+  if (!device_lists)
+    for (int i = 0; i < nq; ++i) s->h_lists[i] = lists_fill;
   s->busy = true;
   s->task = r->next_task++;
   s->nq = nq;
   s->k = k;
-  s->nprobe = nprobe_max;
+  s->nprobe = nprobe;
   s->mature = mature;
   r->next_stream = (r->next_stream + 1) % r->streams.size();
   *task_id = s->task;
   return SA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sa_status sa_retriever_submit(sa_retriever* r, const float* queries_host, int32_t nq, int32_t k,
+                              int32_t nprobe_max, int32_t mature, const sa_maturity_opts* opts,
+                              int64_t* task_id) {
+  if (mature && (!opts || nprobe_max < 1))
+    return set_error(SA_ERR_INVALID_ARG, "maturity exit needs opts and nprobe_max >= 1");
+  if (!r) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  return submit_task(r, queries_host, nq, k, mature != 0, nprobe_max, nprobe_max, mature, task_id,
+                     [&](float* dq, int64_t* dids, float* dsc, int32_t* dlists, cudaStream_t st) {
+                       if (mature) {
+                         sa_maturity_opts o = *opts;
+                         o.engine_ready = r->flag;
+                         return sa_search_mature(r->idx, dq, SA_F32, nq, k, nprobe_max, &o, dids,
+                                                 dsc, dlists, nullptr, nullptr, st);
+                       }
+                       return sa_search_ex(r->idx, dq, SA_F32, nq, k, nprobe_max, dids, dsc, st);
+                     });
+}
+
+sa_status sa_retriever_submit_graph(sa_retriever* r, const float* queries_host, int32_t nq,
+                                    int32_t k, int32_t search_range, int32_t search_width,
+                                    int32_t n_entries, int32_t mature,
+                                    const sa_maturity_opts* opts, int64_t* task_id) {
+  if (mature && !opts) return set_error(SA_ERR_INVALID_ARG, "maturity exit needs opts");
+  if (!r) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  return submit_task(r, queries_host, nq, k, mature != 0, -1, 0, mature, task_id,
+                     [&](float* dq, int64_t* dids, float* dsc, int32_t* dsteps, cudaStream_t st) {
+                       if (mature) {
+                         sa_maturity_opts o = *opts;
+                         o.engine_ready = r->flag;
+                         return sa_search_graph_mature(r->idx, dq, SA_F32, nq, k, search_range,
+                                                       search_width, n_entries, 1 << 30, &o, dids,
+                                                       dsc, dsteps, nullptr, nullptr, 0, st);
+                       }
+                       return sa_search_graph(r->idx, dq, SA_F32, nq, k, search_range,
+                                              search_width, n_entries, 1 << 30, dids, dsc,
+                                              nullptr, st);
+                     });
 }
 
 sa_status sa_retriever_poll(sa_retriever* r, int64_t task_id, int32_t* done) {

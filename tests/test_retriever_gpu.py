@@ -87,3 +87,32 @@ def test_engine_ready_stops_running_maturity_search(sa, setup):
     _, _, lists = wait(r, t)
     assert np.all((lists >= 1) & (lists < 64)), lists
     r.free()
+
+
+def test_graph_tasks_match_synchronous_calls(sa, setup):
+    """Alg. 1 over the proximity graph (the paper's own retriever): plain and maturity-exit
+    graph tasks equal the synchronous calls bit for bit; the engine flag (never raised) keeps
+    the maturity search running to its natural stop, which equals the plain search."""
+    idx, Q = setup
+    idx.build_graph(knn_k=24, degree=16, nprobe_build=4)
+    r = sa.Retriever(idx, streams=2, slots=4, max_nq=16, max_k=10)
+    Qd = torch.from_numpy(Q).cuda()
+    r.set_engine_ready(True)
+    t_g = r.submit_graph(Q[:8], 10, 64, search_width=2, n_entries=4)
+    t_m = r.submit_graph(Q[8:], 10, 64, search_width=2, n_entries=4, mature=True, tau=0.9,
+                         window=4, check_every=1)
+    ids, sc, it = wait(r, t_g)
+    gi, gs = idx.search_graph(Qd[:8].contiguous(), 10, 64, search_width=2, n_entries=4)
+    assert np.array_equal(ids, gi.cpu().numpy()) and np.array_equal(sc, gs.cpu().numpy())
+    assert np.all(it == -1)
+    ids, sc, it = wait(r, t_m)
+    mi, ms, mt = idx.search_graph_mature(Qd[8:].contiguous(), 10, 64, tau=0.9, window=4,
+                                         check_every=1, search_width=2, n_entries=4)
+    assert np.array_equal(ids, mi.cpu().numpy()) and np.array_equal(it, mt.cpu().numpy())
+    r.set_engine_ready(False)
+    t_n = r.submit_graph(Q[8:], 10, 64, search_width=2, n_entries=4, mature=True, tau=0.0,
+                         window=4, check_every=1)
+    ids, sc, it = wait(r, t_n)
+    pi, ps = idx.search_graph(Qd[8:].contiguous(), 10, 64, search_width=2, n_entries=4)
+    assert np.array_equal(ids, pi.cpu().numpy()) and np.array_equal(sc, ps.cpu().numpy())
+    r.free()

@@ -42,7 +42,11 @@ def main():
     ap.add_argument("--k", type=int, default=5)
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--modes", default="fixed,mature",
-                    help="comma list of: exact, fixed, mature (maturity exit + engine flag)")
+                    help="comma list of: exact, fixed, mature (maturity exit + engine flag), "
+                         "graph (fixed search range), graph_mature (the paper's own setting: "
+                         "maturity exit on the graph beam search + engine flag)")
+    ap.add_argument("--search-range", type=int, default=104)
+    ap.add_argument("--graph-tau", type=float, default=0.9, help="the paper's tau (P:387)")
     args = ap.parse_args()
     cfg = dict(CONFIGS["c3"])
     n = args.n or cfg["n"]
@@ -53,6 +57,8 @@ def main():
     idx = sa.Index.build(X, 16384 if n > 1_000_000 else 1024)
     del X
     torch.cuda.empty_cache()
+    if any(m.startswith("graph") for m in args.modes.split(",")):
+        idx.build_graph(knn_k=64, degree=48, nprobe_build=8)
     g = np.random.default_rng(2505)
     # request traces: 1-5 retrievals (P:236-238 report ~2.3-3.3 per request), 20-60 steps each
     traces = []
@@ -79,7 +85,7 @@ def main():
         while len(e2e) < len(traces):
             now = time.perf_counter() - t0
             waiting = [i for i, s in enumerate(st) if s["state"] == "waiting"]
-            if mode == "mature":         # Alg. 1 lines 10-11: engine has waiting requests
+            if mode in ("mature", "graph_mature"):   # Alg. 1 lines 10-11: engine has waiting
                 r.set_engine_ready(bool(waiting) and bool(active))
             for task, i in list(active.items()):          # step 3: completed searches
                 if r.poll(task):
@@ -131,6 +137,11 @@ def main():
                     task = r.submit(q, args.k, 0)
                 elif mode == "fixed":
                     task = r.submit(q, args.k, args.nprobe)
+                elif mode == "graph":
+                    task = r.submit_graph(q, args.k, args.search_range)
+                elif mode == "graph_mature":
+                    task = r.submit_graph(q, args.k, 256, mature=True, tau=args.graph_tau,
+                                          window=4, check_every=1)
                 else:
                     task = r.submit(q, args.k, 128, mature=True, tau=3.0, window=32,
                                     check_every=8)
