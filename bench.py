@@ -157,8 +157,12 @@ def run_reference(args, cfg, name):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times) * cfg["n"] / rows,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": workload_name(cfg, name, args.nprobe),
-                                        "n": cfg["n"], "d": cfg["d"], "nq": cfg["nq"], "k": cfg["k"]},
+        "data": "synthetic (seeded low-rank Gaussian mixture, unit-norm; DESIGN.md §3)",
+        "config": {"workload": f"{name}: top-{cfg['k']}, {cfg['n']}x{cfg['d']} bf16 corpus, batch "
+                               f"{cfg['nq']} (the same workload as the GPU arm; the CPU oracle "
+                               "searches exactly, recall@k 1.0)",
+                   "n": cfg["n"], "d": cfg["d"], "nq": cfg["nq"], "k": cfg["k"],
+                   "recall_at_k": 1.0, "parallelism": f"{cores} host threads"},
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
