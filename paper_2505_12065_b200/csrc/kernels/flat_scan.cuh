@@ -65,6 +65,7 @@ struct FlatScanArgs {
                            // mode with one work item per unit and QP > 1)
   int32_t experiment;      // timing experiments only (env SA_EXPERIMENT): 1 = skip score
                            // processing, 2 = also skip the TMEM loads.  0 in production.
+  int32_t lockstep_lag;    // tiles a unit may run ahead of the units sharing its slice (0 = 4)
   int32_t fp8;             // 1: Q and the corpus are e4m3 bytes (kind::f8f6f4 MMAs), passed
                            // as 16-bit pairs -- d_pad counts PAIRS of e4m3 values (bytes / 2),
                            // so TMA boxes, swizzle, descriptors and TMEM columns are the bf16

@@ -204,6 +204,11 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
       return e ? atoi(e) : 0;
     }();
     a.experiment = experiment;
+    static const int lag = [] {   // SA_LOCKSTEP_LAG: tuning experiments only
+      const char* e = getenv("SA_LOCKSTEP_LAG");
+      return e ? atoi(e) : 0;
+    }();
+    a.lockstep_lag = lag;
   }
   CUtensorMap tmap_q;
   st = make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM);
