@@ -312,17 +312,27 @@ __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, in
                                              : make_uint4(0, 0, 0, 0);
       }
     }
+    // the query chunk is loaded from smem once per rd and reused by every row in flight
+    // (rows outer would reload it per row: LDS latency exposed on the FMAs); per row the sum
+    // order is unchanged (rd = 0, 1, 2)
+    float acc[kRowsPerWarp];
+#pragma unroll
+    for (int u = 0; u < kRowsPerWarp; ++u) acc[u] = 0.f;
+#pragma unroll
+    for (int rd = 0; rd < 3; ++rd)
+      if (rd * 32 + lane < nchunk) {
+#pragma unroll
+        for (int u = 0; u < kRowsPerWarp; ++u)
+          acc[u] += bf16x8_dot(v[u][rd], reinterpret_cast<const float4*>(sm.q), rd * 32 + lane);
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < kRowsPerWarp; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
 #pragma unroll
     for (int u = 0; u < kRowsPerWarp; ++u) {
-      float acc = 0.f;
-#pragma unroll
-      for (int rd = 0; rd < 3; ++rd)
-        if (rd * 32 + lane < nchunk)
-          acc += bf16x8_dot(v[u][rd], reinterpret_cast<const float4*>(sm.q), rd * 32 + lane);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0 && p[u] >= 0) {
-        const unsigned long long key = make_key(acc, gid[u]);
+        const unsigned long long key = make_key(acc[u], gid[u]);
         if (kMature) atomicMax(&sm.smax, key);
         if (key > floor) {
           const int t = atomicAdd(&sm.n_ins, 1);
