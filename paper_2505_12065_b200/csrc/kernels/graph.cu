@@ -395,17 +395,38 @@ __device__ void score_rows_f8(const GraphSearchArgs& a, SearchSmem& sm, int cnt,
                                           : make_uint4(0, 0, 0, 0);
       }
     }
+    // each float4 of the query is loaded once and used by every row in flight (one FMA chain
+    // per row; the rows give the ILP)
+    float acc[kRowsPerWarp];
+#pragma unroll
+    for (int u = 0; u < kRowsPerWarp; ++u) acc[u] = 0.f;
+    const float4* q4 = reinterpret_cast<const float4*>(sm.q);
+#pragma unroll
+    for (int rd = 0; rd < 2; ++rd)
+      if (rd * 32 + lane < nch) {
+        const int c = rd * 32 + lane;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 q = q4[q_slot_e4m3(c, i)];
+#pragma unroll
+          for (int u = 0; u < kRowsPerWarp; ++u) {
+            const uint32_t w = i == 0 ? v[u][rd].x : i == 1 ? v[u][rd].y : i == 2 ? v[u][rd].z
+                                                                              : v[u][rd].w;
+            acc[u] = fmaf(e4m3_top_to_f32(w << 24), q.x, acc[u]);
+            acc[u] = fmaf(e4m3_top_to_f32(w << 16), q.y, acc[u]);
+            acc[u] = fmaf(e4m3_top_to_f32(w << 8), q.z, acc[u]);
+            acc[u] = fmaf(e4m3_top_to_f32(w), q.w, acc[u]);
+          }
+        }
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < kRowsPerWarp; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
 #pragma unroll
     for (int u = 0; u < kRowsPerWarp; ++u) {
-      float acc = 0.f;
-#pragma unroll
-      for (int rd = 0; rd < 2; ++rd)
-        if (rd * 32 + lane < nch)
-          acc += e4m3x16_dot(v[u][rd], reinterpret_cast<const float4*>(sm.q), rd * 32 + lane);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0 && p[u] >= 0) {
-        const unsigned long long key = make_key(acc, gid[u]);
+        const unsigned long long key = make_key(acc[u], gid[u]);
         if (key > floor) {
           const int t = atomicAdd(&sm.n_ins, 1);
           sm.nkey[t] = key;
