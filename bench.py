@@ -173,7 +173,7 @@ def run_reference(args, cfg, name):
 
 # ------------------------------------------------------------------ GPU arm
 NPROBE_LADDER = (8, 16, 24, 32, 36, 40, 44, 48, 52, 56, 64, 80, 96, 128, 192, 256)
-GRAPH_L = (64, 80, 96, 104, 112, 120, 128, 144, 160, 192, 256)   # search range ladder
+GRAPH_L = (64, 80, 88, 96, 100, 104, 108, 112, 120, 128, 144, 160, 192, 256)   # search ranges
 GRAPH_W, GRAPH_E = 4, 16                                     # search width, entry lists
 RECALL_TARGET = 0.95
 CALIBRATION_MARGIN = 0.005   # calibrate at >= 0.955 so the timed batches' mean stays >= 0.95
