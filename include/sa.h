@@ -8,10 +8,18 @@
  * knowledge base (§2.1: queries "encoded into dense vector
  * representations"; top-k documents concatenated into the context, P:44,
  * P:216).  Similarity is the inner product (maximum inner-product
- * search, BASELINE.json north_star; reading R1).  Two modes:
+ * search, BASELINE.json north_star; reading R1).  Modes:
  *   - exact flat scan ("exact nearest neighbor (ENN) search");
  *   - IVF approximate search whose nprobe knob plays the role of the HNSW
- *     "search range": more effort, higher recall.
+ *     "search range": more effort, higher recall;
+ *   - proximity-graph beam search (the paper's own ANN family, HNSW-like; its
+ *     search range is the paper's knob), optionally with the non-stall
+ *     maturity exit of §3.3 (sa_search_graph*, below);
+ *   - fp8 (e4m3) flat scan with bf16 re-rank (a compressed exact mode;
+ *     sa_search_fp8, below).
+ * Plus the agent-side support of Alg. 1: the maturity exit on IVF list order
+ * (sa_search_mature), the priority scheduler (sa_priority_order) and an
+ * asynchronous retrieval executor (sa_retriever_*).
  *
  * Conventions (all entry points):
  *   - Every call returns sa_status; nothing else crosses the boundary.  On
