@@ -288,15 +288,18 @@ sa_status sa_search_graph_mature(const sa_index* idx, const void* queries, sa_dt
  * sa_index_build_fp8: builds the copy (n_local * ceil(d/128)*128 bytes kept).  Synchronous;
  * collective on a sharded index (every rank must call).
  * sa_search_fp8: queries DEVICE [nq, d] of qdtype; out_ids DEVICE int64 [nq, k], out_scores
- * DEVICE fp32 [nq, k]; 1 <= k <= n_cand <= 256.  Stream-ordered, asynchronous; sharded indexes
+ * DEVICE fp32 [nq, k]; 1 <= k <= n_cand <= 256.  nprobe = 0: the candidates come from every
+ * row (exact mode, compressed); 1 <= nprobe <= nlist: from the rows of the nprobe best IVF
+ * lists (probed with the bf16 query exactly as sa_search, R11), the list scan on the e4m3 copy
+ * (IVF mode, compressed: half the list bytes).  Stream-ordered, asynchronous; sharded indexes
  * as sa_search (every rank calls, every rank receives the global result).  SA_ERR_STATE
- * without sa_index_build_fp8.
+ * without sa_index_build_fp8 or with nprobe > 0 on a flat-only index.
  * sa_index_export_fp8: *scale_exp = e; host_out (may be NULL) HOST uint8 [n_local, d] e4m3
  * bytes, row = global id - row_offset. */
 sa_status sa_index_build_fp8(sa_index* idx, void* stream);
 sa_status sa_search_fp8(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
-                        int32_t k, int32_t n_cand, int64_t* out_ids, float* out_scores,
-                        void* stream);
+                        int32_t k, int32_t nprobe, int32_t n_cand, int64_t* out_ids,
+                        float* out_scores, void* stream);
 sa_status sa_index_export_fp8(const sa_index* idx, uint8_t* host_out, int32_t* scale_exp);
 
 /* ---- agent loop support (Alg. 1, App. A.1) ---- */

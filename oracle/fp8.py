@@ -11,6 +11,8 @@ a compressed variant of the exact mode (ENN).  Readings (D
   R32  candidates: the n_cand best rows by <q8, x8> (score desc, row asc);
   R33  re-rank: the candidates re-scored on the bf16 values, the k best (score desc, id asc),
        padded (-1, -inf).
+  R35  IVF: with nprobe > 0 the candidates of R32 are taken among the rows of the query's
+       nprobe best lists (probed on the bf16 query, R11) -- `candidates` over that row subset.
 
 Values are fp64; every e4m3 value times a power of two is exactly a bf16 value (3 <= 7 mantissa
 bits, exponents in range), so the fp8 scores of R32 are the C oracle's exact fp64 scan over

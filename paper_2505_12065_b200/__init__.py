@@ -111,7 +111,7 @@ def lib() -> ctypes.CDLL:
         "sa_search_graph_ex": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, i32, i32, i32, P, P, P,
                                     P]),
         "sa_index_build_fp8": (st, [P, P]),
-        "sa_search_fp8": (st, [P, P, ctypes.c_int, i64, i32, i32, P, P, P]),
+        "sa_search_fp8": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, P, P, P]),
         "sa_index_export_fp8": (st, [P, P, ctypes.POINTER(i32)]),
         "sa_search_graph_mature": (st, [P, P, ctypes.c_int, i64, i32, i32, i32, i32, i32,
                                         ctypes.POINTER(_MaturityOpts), P, P, P, P, P, i32, P]),
@@ -402,7 +402,8 @@ class Index:
         _check(lib().sa_index_build_fp8(self.handle, _stream_ptr(stream)))
         return self
 
-    def search_fp8(self, queries: torch.Tensor, k: int, n_cand: int = 64, out=None, stream=None):
+    def search_fp8(self, queries: torch.Tensor, k: int, n_cand: int = 16, nprobe: int = 0,
+                   out=None, stream=None):
         if not queries.is_cuda or queries.dim() != 2 or not queries.is_contiguous():
             raise ValueError("queries must be a contiguous 2-D CUDA tensor")
         if queries.shape[1] != self.d:
@@ -413,8 +414,8 @@ class Index:
             scores = torch.empty(nq, k, dtype=torch.float32, device=queries.device)
         else:
             ids, scores = out
-        _check(lib().sa_search_fp8(self.handle, _ptr(queries), _dtype_code(queries), nq, k, n_cand,
-                                   _ptr(ids), _ptr(scores), _stream_ptr(stream)))
+        _check(lib().sa_search_fp8(self.handle, _ptr(queries), _dtype_code(queries), nq, k, nprobe,
+                                   n_cand, _ptr(ids), _ptr(scores), _stream_ptr(stream)))
         return ids, scores
 
     def export_fp8(self):

@@ -21,7 +21,8 @@ using namespace sa;
 namespace {
 
 sa_status fp8_search_local(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
-                           int32_t k, int32_t n_cand, const SearchOut& out, cudaStream_t s) {
+                           int32_t k, int32_t nprobe, int32_t n_cand, const SearchOut& out,
+                           cudaStream_t s) {
   const int64_t nq_pad = padded_nq(nq);
   __nv_bfloat16* Qs = nullptr;
   uint8_t* Q8 = nullptr;
@@ -42,13 +43,18 @@ sa_status fp8_search_local(const sa_index* idx, const void* queries, sa_dtype qd
     st = cuda_status(e, "stage queries");
   }
   if (st == SA_OK) {
-    // R32: the n_cand best stored rows by e4m3 score; keys carry stored positions
-    CorpusView cv{&idx->tmap_x8, &idx->tmap_x8_2, idx->n_local, idx->d8_pad / 2, nullptr, 0u,
-                  true};
+    // R32: the n_cand best stored rows by e4m3 score (all rows, or the rows of the nprobe
+    // best lists -- probed on the bf16 query, as the bf16 IVF mode); keys carry stored positions
     SearchOut c;
     c.keys = cand;
-    st = flat_search_view(cv, idx->num_sms, reinterpret_cast<const __nv_bfloat16*>(Q8), nq,
-                          n_cand, c, s);
+    if (nprobe > 0) {
+      st = ivf_search(idx, Qs, nq, nq_pad, n_cand, nprobe, c, s, Q8);
+    } else {
+      CorpusView cv{&idx->tmap_x8, &idx->tmap_x8_2, idx->n_local, idx->d8_pad / 2, nullptr, 0u,
+                    true};
+      st = flat_search_view(cv, idx->num_sms, reinterpret_cast<const __nv_bfloat16*>(Q8), nq,
+                            n_cand, c, s);
+    }
   }
   if (st == SA_OK) {
     RerankArgs r{};
@@ -120,9 +126,10 @@ sa_status sa_index_build_fp8(sa_index* idx, void* stream) {
     st = cuda_status(cudaMemcpyAsync(&e_host, e_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, s),
                      "copy");
   if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "fp8 build sync");
-  CUtensorMap t1, t2;
+  CUtensorMap t1, t2, t3;
   if (st == SA_OK) st = make_tmap_bf16(&t1, X8, n, d8_pad / 2, FS_BN);
   if (st == SA_OK) st = make_tmap_bf16(&t2, X8, n, d8_pad / 2, FS_BN / 2);
+  if (st == SA_OK) st = make_tmap_bf16(&t3, X8, n, d8_pad / 2, FS_TAIL_ROWS);
   cudaFree(amax);
   if (st != SA_OK) {
     cudaFree(X8);
@@ -134,12 +141,13 @@ sa_status sa_index_build_fp8(sa_index* idx, void* stream) {
   idx->x8_exp = e_host;
   idx->tmap_x8 = t1;
   idx->tmap_x8_2 = t2;
+  idx->tmap_x8t = t3;
   return SA_OK;
 }
 
 sa_status sa_search_fp8(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
-                        int32_t k, int32_t n_cand, int64_t* out_ids, float* out_scores,
-                        void* stream) {
+                        int32_t k, int32_t nprobe, int32_t n_cand, int64_t* out_ids,
+                        float* out_scores, void* stream) {
   if (!idx || !queries || !out_ids || !out_scores)
     return set_error(SA_ERR_INVALID_ARG, "null pointer");
   if (!idx->X8) return set_error(SA_ERR_STATE, "no fp8 copy: call sa_index_build_fp8");
@@ -147,20 +155,23 @@ sa_status sa_search_fp8(const sa_index* idx, const void* queries, sa_dtype qdtyp
   if (nq < 1 || nq > (1ll << 31) / 2) return set_error(SA_ERR_INVALID_ARG, "bad nq");
   if (k < 1 || n_cand < k || n_cand > F8_MAX_CAND)
     return set_error(SA_ERR_INVALID_ARG, "need 1 <= k <= n_cand <= 256");
+  if (nprobe < 0 || nprobe > idx->nlist)
+    return set_error(nprobe > 0 && idx->nlist == 0 ? SA_ERR_STATE : SA_ERR_INVALID_ARG,
+                     "need 0 <= nprobe <= nlist");
   cudaStream_t s = (cudaStream_t)stream;
   const bool sharded = idx->comm && idx->comm->world > 1;
   if (!sharded) {
     SearchOut out;
     out.ids = out_ids;
     out.scores = out_scores;
-    return fp8_search_local(idx, queries, qdtype, nq, k, n_cand, out, s);
+    return fp8_search_local(idx, queries, qdtype, nq, k, nprobe, n_cand, out, s);
   }
   uint64_t* keys_local = nullptr;
   sa_status st = dalloc(&keys_local, (size_t)nq * k, s, "alloc local keys");
   if (st == SA_OK) {
     SearchOut out;
     out.keys = keys_local;
-    st = fp8_search_local(idx, queries, qdtype, nq, k, n_cand, out, s);
+    st = fp8_search_local(idx, queries, qdtype, nq, k, nprobe, n_cand, out, s);
   }
   if (st == SA_OK) st = gather_merge_keys(idx, keys_local, nq, k, out_ids, out_scores, s);
   if (keys_local) cudaFreeAsync(keys_local, s);

@@ -71,6 +71,7 @@ struct sa_index {
   int32_t x8_exp = 0;
   CUtensorMap tmap_x8;         // as 16-bit pairs [n_local, d8_pad / 2], box 128 rows
   CUtensorMap tmap_x8_2;       // box 64 rows (cta_group 2)
+  CUtensorMap tmap_x8t;        // box 32 rows (IVF list tails)
   // captured progressive (maturity-exit) searches, guarded by graph_mu (mature.cu)
   std::vector<std::unique_ptr<sa::MaturePlan, void (*)(sa::MaturePlan*)>> mature_plans;
 };
@@ -154,8 +155,12 @@ sa_status dalloc(T** p, size_t count, cudaStream_t s, const char* what) {
 
 // IVF (ivf.cu)
 sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s);
+// Q8: optional staged e4m3 queries [nq, d8_pad] -> the list scan runs on the e4m3 copy and
+// `out.keys` receive keys with STORED positions (for the bf16 re-rank, fp8_api.cu); the probe
+// still uses the bf16 queries Qs
 sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
-                     int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s);
+                     int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s,
+                     const uint8_t* Q8 = nullptr);
 sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
                     int32_t nprobe, int32_t* out_lists, cudaStream_t s);
 

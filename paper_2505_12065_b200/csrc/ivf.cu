@@ -294,7 +294,8 @@ sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, in
 }
 
 sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
-                     int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s) {
+                     int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s,
+                     const uint8_t* Q8) {
   (void)nq_pad;
   const int nlist = idx->nlist;
   const int sms = idx->num_sms;
@@ -323,10 +324,11 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   want = (want + FS_BN - 1) / FS_BN * FS_BN;
   const int chunk_rows = (int)std::min<int64_t>(kChunkRows, std::max<int64_t>(kChunkRowsSmall, want));
   const int64_t max_chunks = std::max<int64_t>(1, (idx->max_list + chunk_rows - 1) / chunk_rows);
-  static const bool legacy = [] {
+  static const bool legacy_env = [] {
     const char* e = getenv("SA_IVF_LEGACY");
     return e && e[0] == '1';
   }();
+  const bool legacy = legacy_env && Q8 == nullptr;
   const int qblock = legacy ? FS_BM : IVS_NQ;
   const int parts = legacy ? FS_LISTS_PER_ITEM : IVS_PARTS;
   IvfSearchScratch w{};
@@ -378,10 +380,11 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   cudaError_t e;
   if (!legacy) {
     IvfScanArgs v{};
-    v.Q = Qs;
-    v.d_pad = idx->d_pad;
+    v.Q = Q8 ? reinterpret_cast<const __nv_bfloat16*>(Q8) : Qs;
+    v.d_pad = Q8 ? idx->d8_pad / 2 : idx->d_pad;
+    v.fp8 = Q8 ? 1 : 0;
     v.k = k;
-    v.row_ids = idx->row_ids;
+    v.row_ids = Q8 ? nullptr : idx->row_ids;
     v.part = part;
     v.heap_g = heap;
     v.items = w.items;
@@ -394,7 +397,8 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
     v.q_hint = hint;
     v.item_counter = reinterpret_cast<int32_t*>(hint + nq);
     prof_begin(SA_KERNEL_IVF_SCAN, s);
-    e = launch_ivf_scan(idx->tmap_x, idx->tmap_xt, v, sms, s);
+    e = Q8 ? launch_ivf_scan(idx->tmap_x8, idx->tmap_x8t, v, sms, s)
+           : launch_ivf_scan(idx->tmap_x, idx->tmap_xt, v, sms, s);
     prof_end(SA_KERNEL_IVF_SCAN, s);
     prof_count(SA_KERNEL_IVF_SCAN);
     SA_CUDA(e, "ivf scan");

@@ -120,6 +120,7 @@ __device__ __noinline__ float heap_push(uint64_t* h, int k, uint64_t key) {
 
 }  // namespace
 
+template <bool F8>
 __global__ void __launch_bounds__(kThreads, 1)
 ivf_scan_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const __grid_constant__ CUtensorMap tmap_tail, const IvfScanArgs a) {
@@ -249,7 +250,8 @@ ivf_scan_kernel(const __grid_constant__ CUtensorMap tmap_x,
       const int w = take_item(i);
       if (w < 0) break;
       const Item it = uniform(decode(w, a));
-      const uint32_t idesc = ptx::umma_idesc_bf16(kBM, it.cnt <= 16 ? 16 : 32);
+      const uint32_t idesc = F8 ? ptx::umma_idesc_e4m3(kBM, it.cnt <= 16 ? 16 : 32)
+                                : ptx::umma_idesc_bf16(kBM, it.cnt <= 16 ? 16 : 32);
       const int buf = i & 1;
       ptx::mbar_wait(ptx::smem_u32(&tail->b_full[buf]), (uint32_t)((i >> 1) & 1));
       ptx::tc_fence_after();
@@ -269,9 +271,14 @@ ivf_scan_kernel(const __grid_constant__ CUtensorMap tmap_x,
               const uint64_t ad = sdesc + (uint64_t)((j * kBoxBytes) >> 4);
               const uint64_t bd = bdesc_buf + (uint64_t)((kb * kBKbBytes) >> 4);
 #pragma unroll
-              for (int kk = 0; kk < kBK / 16; ++kk)
-                ptx::mma_bf16_elect<1, false>(d_tmem, ad + kk * 2, bd + kk * 2, idesc,
-                                              (kb | kk) ? 1u : 0u);
+              for (int kk = 0; kk < kBK / 16; ++kk) {
+                if constexpr (F8)
+                  ptx::mma_e4m3_elect<1, false>(d_tmem, ad + kk * 2, bd + kk * 2, idesc,
+                                                (kb | kk) ? 1u : 0u);
+                else
+                  ptx::mma_bf16_elect<1, false>(d_tmem, ad + kk * 2, bd + kk * 2, idesc,
+                                                (kb | kk) ? 1u : 0u);
+              }
             }
           }
           ptx::tc_commit_elect<1>(empty0 + stage * 8);
@@ -387,7 +394,7 @@ ivf_scan_kernel(const __grid_constant__ CUtensorMap tmap_x,
           uint32_t m = __ballot_sync(0xffffffffu, pass);
           if (m) {
             if (pass && !have_id) {
-              id = (uint32_t)__ldg(a.row_ids + row);
+              id = a.row_ids ? (uint32_t)__ldg(a.row_ids + row) : (uint32_t)row;
               have_id = true;
             }
             const uint64_t key = pass ? make_key(s, id) : 0ull;
@@ -437,15 +444,18 @@ size_t ivf_scan_smem_bytes() {
 cudaError_t launch_ivf_scan(const CUtensorMap& tmap_x, const CUtensorMap& tmap_tail,
                             const IvfScanArgs& a, int grid, cudaStream_t stream) {
   const size_t smem = ivf_scan_smem_bytes();
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(ivf_scan_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
-  ivf_scan_kernel<<<grid, kThreads, smem, stream>>>(tmap_x, tmap_tail, a);
-  return cudaGetLastError();
+  static bool set[2] = {false, false};
+  auto go = [&](auto kern, bool& done) -> cudaError_t {
+    if (!done) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      done = true;
+    }
+    kern<<<grid, kThreads, smem, stream>>>(tmap_x, tmap_tail, a);
+    return cudaGetLastError();
+  };
+  return a.fp8 ? go(ivf_scan_kernel<true>, set[1]) : go(ivf_scan_kernel<false>, set[0]);
 }
 
 }  // namespace sa

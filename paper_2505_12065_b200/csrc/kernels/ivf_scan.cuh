@@ -18,7 +18,7 @@ struct IvfScanArgs {
   const __nv_bfloat16* Q;  // staged queries [nq, d_pad] bf16
   int32_t d_pad;           // multiple of 64, <= 768
   int32_t k;               // 1..256
-  const int32_t* row_ids;  // stored row -> global id
+  const int32_t* row_ids;  // stored row -> global id (nullptr: the stored position)
   uint64_t* part;          // out: [slot][IVS_PARTS][k] packed keys (unordered, 0 = empty)
   uint64_t* heap_g;        // scratch [grid][k][IVS_HEAPS] when k > IVS_KSMEM
   const int4* items;       // [*n_items] {list, first prober in lq_ent, chunk, prober count <= 32}
@@ -31,6 +31,9 @@ struct IvfScanArgs {
   uint32_t* q_hint;        // [nq] ordered-fp32 lower bound of each query's k-th score (zeroed);
                            // nullptr: no shared bound (every partial list is its exact top-k)
   int32_t* item_counter;   // zeroed global counter: dynamic item scheduling
+  int32_t fp8;             // 1: e4m3 rows and queries (kind::f8f6f4) passed as 16-bit pairs:
+                           // Q [nq, d_pad pairs], tensor maps over the e4m3 copy; row_ids may
+                           // then be nullptr (keys carry stored positions for the re-rank)
 };
 
 size_t ivf_scan_smem_bytes();

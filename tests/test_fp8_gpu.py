@@ -129,3 +129,51 @@ def test_errors(sa, data):
     with pytest.raises(sa.SAError):
         idx.search_fp8(Qd, 33, 32)
     idx.free()
+
+
+def test_ivf_fp8_candidates_and_rerank(sa, data):
+    """R35: with nprobe > 0 the e4m3 candidates come from the rows of the nprobe best lists
+    (probed on the bf16 query, as sa_search): the GPU's candidate set = the oracle's e4m3
+    top-n_cand over exactly those rows (band rule on fp8 scores), the result = the exact
+    top-k over the GPU's candidates, and nprobe = nlist gives the flat fp8 candidates."""
+    Xb, Qb = data
+    idx = sa.Index.build(bits_to_tensor(Xb).cuda(), 32, kmeans_iters=4).build_fp8()
+    Qd = bits_to_tensor(Qb).cuda()
+    off, gid = idx.export_lists()
+    X8, _ = fp8.quantize_corpus(Xb)
+    Q8, _ = fp8.quantize_queries(Qb)
+    Xc, Qc = fp8._as_bf16_bits(X8), fp8._as_bf16_bits(Q8)
+    n_cand, nprobe = 16, 6
+    P = idx.probes(Qd, nprobe).cpu().numpy()
+    ci, cs = idx.search_fp8(Qd, n_cand, n_cand, nprobe=nprobe)
+    ci = ci.cpu().numpy()
+    gi, gs = idx.search_fp8(Qd, 10, n_cand, nprobe=nprobe)
+    gi, gs = gi.cpu().numpy(), gs.cpu().numpy()
+    assert np.array_equal(gi, ci[:, :10])
+    for q in range(0, len(Qb), 3):
+        rows = np.sort(np.concatenate([gid[off[l]:off[l + 1]] for l in P[q]]))
+        oi, osc = oracle.flat_topk(Xc[rows], Qc[q:q + 1], min(n_cand + 8, rows.size))
+        navail = min(n_cand, rows.size)
+        sk = osc[0][navail - 1]
+        t = tol_of(sk, 1e-3)
+        must = set(rows[oi[0][(oi[0] >= 0) & (osc[0] > sk + t)]].tolist())
+        got = set(ci[q][:navail].tolist())
+        assert must <= got and len(got) == navail and got <= set(rows.tolist()), q
+        s_g = oracle.pair_scores(Xc, Qc[q:q + 1], np.zeros(navail, int), ci[q][:navail])
+        assert np.all(s_g >= sk - t), q
+        # re-rank: exact top-10 over the GPU's candidates
+        cr = np.sort(ci[q][:navail])
+        ei, es = oracle.flat_topk(Xb[cr], Qb[q:q + 1], 10)
+        ei = np.where(ei >= 0, cr[np.maximum(ei, 0)], -1)
+        r = check(gi[q:q + 1], gs[q:q + 1], ei, es,
+                  lambda _q, ids_: oracle.pair_scores(Xb, Qb[q:q + 1], np.zeros(len(ids_), int),
+                                                      ids_), 10)
+        assert r["ok"], (q, r)
+    # nprobe = nlist: every row is probed -> the flat fp8 candidates
+    fi, fsc = idx.search_fp8(Qd, n_cand, n_cand)
+    ai, asc = idx.search_fp8(Qd, n_cand, n_cand, nprobe=32)
+    same = np.mean([set(fi[q].tolist()) == set(ai[q].tolist()) for q in range(len(Qb))])
+    assert same >= 0.97, same     # differ only where fp32 sums reorder the n_cand boundary
+    with pytest.raises(sa.SAError):
+        idx.search_fp8(Qd, 10, 16, nprobe=33)
+    idx.free()
