@@ -177,3 +177,19 @@ def test_ivf_fp8_candidates_and_rerank(sa, data):
     with pytest.raises(sa.SAError):
         idx.search_fp8(Qd, 10, 16, nprobe=33)
     idx.free()
+
+
+def test_power_of_two_scaling_is_exact(sa, data):
+    """P8-ii for the fp8 modes: scaling a query by 2^j leaves its e4m3 codes unchanged (R31's
+    per-row exponent absorbs it), so the candidates are identical and the re-ranked scores are
+    the originals times 2^j exactly (flat and IVF)."""
+    Xb, Qb = data
+    idx = sa.Index.build(bits_to_tensor(Xb).cuda(), 32, kmeans_iters=4).build_fp8()
+    Qd = bits_to_tensor(Qb).cuda()
+    for nprobe in (0, 6):
+        gi, gs = idx.search_fp8(Qd, 10, 16, nprobe=nprobe)
+        for j in (-2, 3):
+            qj = (Qd.float() * 2.0 ** j).to(torch.bfloat16)
+            si, ss = idx.search_fp8(qj, 10, 16, nprobe=nprobe)
+            assert torch.equal(si, gi) and torch.equal(ss, gs * 2.0 ** j), (nprobe, j)
+    idx.free()

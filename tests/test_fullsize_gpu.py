@@ -131,4 +131,11 @@ def test_c3_graph_and_fp8_full_size(sa, c3):
     assert same >= 0.99, same
     for q in SAMPLE_Q:
         assert scores_ok(fi[q], fs[q], q), q
+    # IVF on the e4m3 copy (R35) at bench.py's point: recall vs exact, returned scores
+    vi, vs = idx.search_fp8(Q, 10, 16, nprobe=48)
+    vi, vs = vi.cpu().numpy(), vs.cpu().numpy()
+    rec8 = np.mean([len(set(vi[q]) & set(exact[q])) / 10 for q in range(len(vi))])
+    assert rec8 >= 0.95, rec8
+    for q in SAMPLE_Q:
+        assert scores_ok(vi[q], vs[q], q), q
     idx.free()

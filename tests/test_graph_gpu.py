@@ -254,3 +254,22 @@ def test_fp8_navigation_golden_path_graph(sa):
         sa.Index.build(bits_to_tensor(X).cuda(), 1).import_graph(nbr).search_graph(
             bits_to_tensor(q).cuda(), 2, 2, fp8=True)      # no e4m3 copy -> SA_ERR_STATE
     idx.free()
+
+
+def test_power_of_two_scaling_is_exact(sa, small):
+    """P8-ii for the graph modes: q * 2^j is exact in bf16 and every fp32 sum scales exactly,
+    so ids are identical and scores are multiplied by 2^j bit for bit (bf16 navigation); with
+    fp8 navigation the query's e4m3 codes are unchanged (R31 rescales per row) and the bf16
+    re-rank scales exactly too."""
+    idx, Xb, Qb, nbr, kn = small
+    Qd = bits_to_tensor(Qb).cuda()
+    gi, gs = idx.search_graph(Qd, 10, 64, search_width=2, n_entries=4)
+    for j in (-3, 2):
+        qj = (Qd.float() * 2.0 ** j).to(torch.bfloat16)
+        si, ss = idx.search_graph(qj, 10, 64, search_width=2, n_entries=4)
+        assert torch.equal(si, gi) and torch.equal(ss, gs * 2.0 ** j)
+    idx.build_fp8()
+    fi, fs = idx.search_graph(Qd, 10, 64, search_width=2, n_entries=4, fp8=True)
+    qj = (Qd.float() * 8.0).to(torch.bfloat16)
+    si, ss = idx.search_graph(qj, 10, 64, search_width=2, n_entries=4, fp8=True)
+    assert torch.equal(si, fi) and torch.equal(ss, fs * 8.0)
