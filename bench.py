@@ -728,6 +728,36 @@ def run_sweep(args, sa, idx, batches, gt, k, nq, d, nlist, n, world, rank, barri
             out["rows"].append({"batch": batch, "nprobe": p, "recall": rec,
                                 "qps": args.steps * batch / (ms / 1e3),
                                 "ms_per_batch": ms / args.steps})
+    # the other modes on the same batches: IVF on the e4m3 copy (nprobe ladder, n_cand 16) and
+    # the proximity graph (search-range ladder, width 4, 16 entry lists; built here)
+    if world == 1 and nlist > 0:
+        idx.build_fp8()          # (the graph was built before the sweep, as for the default run)
+        out["rows_ivf_fp8"], out["rows_graph"] = [], []
+        for batch in (nq, 64):
+            qs = [b[:batch].contiguous() for b in batches]
+            runs = [("ivf_fp8", p, lambda q, p=p: idx.search_fp8(q, k, args.fp8_cand, nprobe=p))
+                    for p in (8, 16, 32, 48, 64, 96, 128) if p <= nlist]
+            if not args.no_graph:
+                runs += [("graph", L, lambda q, L=L: idx.search_graph(q, k, L, search_width=GRAPH_W,
+                                                                      n_entries=GRAPH_E))
+                         for L in (32, 64, 96, 104, 128, 160, 256)]
+            for name, knob, fn in runs:
+                for i in range(args.warmup):
+                    fn(qs[i])
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for i in range(args.warmup, nb):
+                    fn(qs[i])
+                e1.record(stream)
+                barrier()
+                ms = max_over_ranks(e0.elapsed_time(e1))
+                rec = float(np.mean([recall_at_k(fn(qs[i])[0], gt[i][:batch])
+                                     for i in range(args.warmup, min(nb, args.warmup + 4))]))
+                out["rows_" + name].append({"batch": batch,
+                                            ("nprobe" if name == "ivf_fp8" else "search_range"): knob,
+                                            "recall": rec, "qps": args.steps * batch / (ms / 1e3),
+                                            "ms_per_batch": ms / args.steps})
     for p in (48, 0):
         for b in (1, 2, 4, 8, 16, 32, 64):
             qh = [batches[(args.warmup + i) % nb][:b].float().cpu().pin_memory() for i in range(8)]

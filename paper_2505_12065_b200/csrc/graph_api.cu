@@ -201,18 +201,10 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
       // entry points: the E best IVF lists (tensor-core centroid scores + exact select)
       prof_begin(SA_KERNEL_IVF_PROBE, s);
       const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, idx->nlist, idx->d_pad, nullptr, 0u};
-      static const bool fused = [] {
-        const char* e = getenv("SA_GRAPH_ENTRY_FUSED");
-        return e && e[0] == '1';
-      }();
-      if (fused) {
-        SearchOut eo;
-        eo.keys = pkeys;
-        st = flat_search_view(cvc, idx->num_sms, Qs, nc, E, eo, s);
-      } else {
-        st = flat_scores_view(cvc, idx->num_sms, Qs, nc, psc, s);
-      }
-      if (st == SA_OK && !fused) {
+      // score dump + exact select (a fused top-E scan was measured slower: 0.19 vs 0.07 ms at
+      // nq = 512, the per-unit query staging dominates a 16384-row scan)
+      st = flat_scores_view(cvc, idx->num_sms, Qs, nc, psc, s);
+      if (st == SA_OK) {
         MergeArgs m{};
         m.cand_scores = psc;
         m.m_flat = idx->nlist;
