@@ -138,8 +138,12 @@ sa_status gather_merge_keys(const sa_index* idx, const uint64_t* keys_local, int
                             int64_t* out_ids, float* out_scores, cudaStream_t s);
 
 // exact scan of `cv` for nq staged queries (bf16 [>= nq, d_pad]) + intra-GPU merge (sa_api.cu)
+// prepass: seed the shared pruning bound with the k-th best score of a sub-scan (exact: a lower
+// bound of the final k-th score)
 sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
-                           int32_t k, const SearchOut& out, cudaStream_t s);
+                           int32_t k, const SearchOut& out, cudaStream_t s, bool prepass = true);
+// while set, flat_search_view's launches are profiled as SA_KERNEL_OTHER (sub-scans)
+void set_prof_kind_other(bool on);
 // raw fp32 score matrix out[q, row] = <Q_q, X_row> for q < nq (tensor cores, no selection)
 sa_status flat_scores_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
                            float* out, cudaStream_t s);

@@ -560,14 +560,13 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         if (h != 0u) hint = float_from_ordered(h);
       }
       thr = fmaxf(thr, hint);
+      uint32_t h_next = 0u;   // the bound, loaded one tile before it is used (L2 latency hidden)
       for (int32_t t = wi.t0; t < wi.t1; ++t) {
-        if (valid && a.q_hint && ((t - wi.t0) & 3) == 3) {
-          const uint32_t h = __ldcg(a.q_hint + q);
-          if (h != 0u) {
-            hint = fmaxf(hint, float_from_ordered(h));
-            thr = fmaxf(thr, hint);
-          }
+        if (valid && a.q_hint && ((t - wi.t0) & 3) == 3 && h_next != 0u) {
+          hint = fmaxf(hint, float_from_ordered(h_next));
+          thr = fmaxf(thr, hint);
         }
+        if (valid && a.q_hint && ((t - wi.t0) & 3) == 2) h_next = __ldcg(a.q_hint + q);
         ptx::mbar_wait(ptx::smem_u32(&tail->tmem_full[acc]), acc_phase);
         ptx::tc_fence_after();
         uint32_t r0[32], r1[32];
@@ -624,7 +623,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           }
           continue;
         }
-        if (!valid || a.experiment != 0) continue;
+        if (!valid || (a.experiment != 0 && a.experiment != 3)) continue;
 
         float m0 = fmaxf(__uint_as_float(r0[0]), __uint_as_float(r0[1]));
         float m1 = fmaxf(__uint_as_float(r1[0]), __uint_as_float(r1[1]));
@@ -632,6 +631,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         for (int j = 2; j < 32; j += 2) {
           m0 = fmaxf(m0, fmaxf(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1])));
           m1 = fmaxf(m1, fmaxf(__uint_as_float(r1[j]), __uint_as_float(r1[j + 1])));
+        }
+        if (a.experiment == 3) {   // timing experiment: the 64-way max only, no insertion
+          if (fmaxf(m0, m1) == 1234.5f) a.part[0] = 0ull;
+          continue;
         }
         if (fmaxf(m0, m1) >= thr) {
 #pragma unroll

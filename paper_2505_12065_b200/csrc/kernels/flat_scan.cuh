@@ -64,7 +64,8 @@ struct FlatScanArgs {
   int32_t* progress;       // optional [units] tile progress for soft lockstep (zeroed; flat
                            // mode with one work item per unit and QP > 1)
   int32_t experiment;      // timing experiments only (env SA_EXPERIMENT): 1 = skip score
-                           // processing, 2 = also skip the TMEM loads.  0 in production.
+                           // processing, 2 = also skip the TMEM loads, 3 = the 64-way max
+                           // only (no insertion).  0 in production.
   int32_t lockstep_lag;    // tiles a unit may run ahead of the units sharing its slice (0 = 4)
   int32_t fp8;             // 1: Q and the corpus are e4m3 bytes (kind::f8f6f4 MMAs), passed
                            // as 16-bit pairs -- d_pad counts PAIRS of e4m3 values (bytes / 2),

@@ -85,20 +85,29 @@ struct Prof {
 Prof g_prof;
 thread_local cudaEvent_t t_open[SA_KERNEL_KINDS];
 thread_local bool t_capturing = false;  // inside a graph capture: no events, no counting
+thread_local int t_other = 0;   // sub-scan depth: flat-scan / merge launches count as OTHER
+int remap(int kind) {
+  return t_other > 0 && (kind == SA_KERNEL_FLAT_SCAN || kind == SA_KERNEL_MERGE) ? SA_KERNEL_OTHER
+                                                                                : kind;
+}
 }  // namespace
 
 void set_capturing(bool on) { t_capturing = on; }
+void set_prof_kind_other(bool on) { t_other += on ? 1 : -1; }
 
 void prof_count(int kind) {
+  kind = remap(kind);
   if (t_capturing) return;
   std::lock_guard<std::mutex> l(g_prof.mu);
   g_prof.launches[kind]++;
 }
 void prof_count_n(int kind, int64_t n) {
+  kind = remap(kind);
   std::lock_guard<std::mutex> l(g_prof.mu);
   g_prof.launches[kind] += n;
 }
 void prof_begin(int kind, cudaStream_t s) {
+  kind = remap(kind);
   if (t_capturing) return;
   std::lock_guard<std::mutex> l(g_prof.mu);
   if (!g_prof.on) return;
@@ -106,6 +115,7 @@ void prof_begin(int kind, cudaStream_t s) {
   cudaEventRecord(t_open[kind], s);
 }
 void prof_end(int kind, cudaStream_t s) {
+  kind = remap(kind);
   if (t_capturing) return;
   std::lock_guard<std::mutex> l(g_prof.mu);
   if (!g_prof.on || !t_open[kind]) return;
@@ -150,8 +160,18 @@ static FlatPlan plan_flat(int64_t n_rows, int num_sms, int64_t nq_pad) {
   return p;
 }
 
+namespace {
+// hint[q] = ordered score of the k-th key of query q's sorted list (0 when fewer than k)
+__global__ void hint_from_keys_kernel(const uint64_t* __restrict__ keys, int64_t nq, int k,
+                                      uint32_t* __restrict__ hint) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x)
+    hint[q] = (uint32_t)(keys[q * k + k - 1] >> 32);
+}
+}  // namespace
+
 sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
-                           int32_t k, const SearchOut& out, cudaStream_t s) {
+                           int32_t k, const SearchOut& out, cudaStream_t s, bool prepass) {
   const int64_t nq_pad = padded_nq(nq);
   const FlatPlan p = plan_flat(cv.n_rows, num_sms, nq_pad);
   uint64_t *part = nullptr, *heap = nullptr;
@@ -166,7 +186,47 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   if (p.S > 1) {
     st = dalloc(&hint, (size_t)nq, s, "alloc hints");
     if (st == SA_OK) st = cuda_status(cudaMemsetAsync(hint, 0, nq * sizeof(uint32_t), s), "memset");
+    // Seed the bound before the scan: the k-th best score over the first m rows (a
+    // sub-scan, ~1/32 of the corpus up to 2^18 rows) is a lower bound of the final k-th
+    // score, so the running heaps start pruning at once instead of each filling its own k
+    // entries first (that warm-up dominated the insert work: ~40% of the e4m3 scan).
+    static const int64_t seed_rows = [] {   // SA_SEED_ROWS: tuning experiments only
+      const char* e = getenv("SA_SEED_ROWS");
+      return e ? atoll(e) : (int64_t)(1 << 18);
+    }();
+    static const bool seed_recurse = [] {
+      const char* e = getenv("SA_SEED_RECURSE");
+      return !(e && e[0] == '0');
+    }();
+    const int64_t m = std::min<int64_t>(cv.n_rows / 32, seed_rows) / FS_BN * FS_BN;
+    static const bool no_seed = [] {   // SA_NO_SEED=1: timing experiments only
+      const char* e = getenv("SA_NO_SEED");
+      return e && e[0] == '1';
+    }();
+    if (st == SA_OK && prepass && !no_seed && m >= 8 * FS_BN) {
+      CorpusView pv = cv;
+      pv.n_rows = m;
+      uint64_t* pk = nullptr;
+      st = dalloc(&pk, (size_t)nq * k, s, "alloc hint keys");
+      if (st == SA_OK) {
+        SearchOut po;
+        po.keys = pk;
+        set_prof_kind_other(true);
+        // the sub-scan seeds its own bound the same way (m / 32 rows, ...): without it its
+        // heaps would pay the whole warm-up themselves
+        st = flat_search_view(pv, num_sms, Qs, nq, k, po, s, seed_recurse);
+        set_prof_kind_other(false);
+      }
+      if (st == SA_OK) {
+        hint_from_keys_kernel<<<(unsigned)std::min<int64_t>((nq + 255) / 256, 1024), 256, 0, s>>>(
+            pk, nq, k, hint);
+        st = cuda_status(cudaGetLastError(), "hint seed");
+        prof_count(SA_KERNEL_OTHER);
+      }
+      if (pk) cudaFreeAsync(pk, s);
+    }
     if (st != SA_OK) {
+      if (hint) cudaFreeAsync(hint, s);
       if (heap) cudaFreeAsync(heap, s);
       cudaFreeAsync(part, s);
       return st;
