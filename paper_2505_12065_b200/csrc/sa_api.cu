@@ -190,10 +190,12 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
     // sub-scan, ~1/32 of the corpus up to 2^18 rows) is a lower bound of the final k-th
     // score, so the running heaps start pruning at once instead of each filling its own k
     // entries first (that warm-up dominated the insert work: ~40% of the e4m3 scan).
-    static const int64_t seed_rows = [] {   // SA_SEED_ROWS: tuning experiments only
+    // 2^18 rows (bf16) / 2^19 (e4m3, whose scan is cheaper): measured best of 2^16..2^20
+    static const int64_t seed_env = [] {   // SA_SEED_ROWS: tuning experiments only
       const char* e = getenv("SA_SEED_ROWS");
-      return e ? atoll(e) : (int64_t)(1 << 18);
+      return e ? atoll(e) : (int64_t)0;
     }();
+    const int64_t seed_rows = seed_env > 0 ? seed_env : (int64_t)(cv.fp8 ? 1 << 19 : 1 << 18);
     static const bool seed_recurse = [] {
       const char* e = getenv("SA_SEED_RECURSE");
       return !(e && e[0] == '0');
