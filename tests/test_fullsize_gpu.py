@@ -139,3 +139,23 @@ def test_c3_graph_and_fp8_full_size(sa, c3):
     for q in SAMPLE_Q:
         assert scores_ok(vi[q], vs[q], q), q
     idx.free()
+
+
+def test_c3_agent_step_shapes(sa, c3):
+    """BASELINE config 5 shapes at full size (batches of 1 and 64, top-5): the exact and IVF
+    results of a small batch equal the first 5 entries of the same queries' batch-512 top-10
+    bit for bit (P8-i: each query's scores do not depend on the batch it is in)."""
+    X, Q = c3["X"], c3["Q"]
+    flat = sa.Index.build(X)
+    for b in (1, 64):
+        qi, qs = flat.search(Q[:b].contiguous(), 5)
+        assert np.array_equal(qi.cpu().numpy(), c3["ids"][:b, :5])
+        assert np.array_equal(qs.cpu().numpy(), c3["sc"][:b, :5])
+    flat.free()
+    idx = sa.Index.build(X, 16384)
+    bi, bs = idx.search(Q, 10, nprobe=48)
+    for b in (1, 64):
+        qi, qs = idx.search(Q[:b].contiguous(), 5, nprobe=48)
+        assert np.array_equal(qi.cpu().numpy(), bi.cpu().numpy()[:b, :5])
+        assert np.array_equal(qs.cpu().numpy(), bs.cpu().numpy()[:b, :5])
+    idx.free()
