@@ -31,15 +31,13 @@ sa_status fp8_search_local(const sa_index* idx, const void* queries, sa_dtype qd
   if (st == SA_OK) st = dalloc(&Q8, (size_t)nq_pad * idx->d8_pad, s, "alloc fp8 queries");
   if (st == SA_OK) st = dalloc(&cand, (size_t)nq * n_cand, s, "alloc candidates");
   if (st == SA_OK) {
-    prof_begin(SA_KERNEL_STAGE, s);
+    ProfRegion prof_region(SA_KERNEL_STAGE, s);
     cudaError_t e = launch_cast_pad(queries, qdtype == SA_F32, nq, idx->d, Qs, nq_pad, idx->d_pad,
                                     idx->num_sms, s);
     // R31: each query row on its own power-of-two scale (rows >= nq are zero -> stay zero)
     if (e == cudaSuccess)
       e = launch_quant_e4m3(Qs, nq_pad, idx->d_pad, nullptr, Q8, idx->d8_pad, nullptr,
                             idx->num_sms, s);
-    prof_end(SA_KERNEL_STAGE, s);
-    prof_count_n(SA_KERNEL_STAGE, 2);
     st = cuda_status(e, "stage queries");
   }
   if (st == SA_OK) {
@@ -69,10 +67,8 @@ sa_status fp8_search_local(const sa_index* idx, const void* queries, sa_dtype qd
     r.out_keys = out.keys;
     r.out_ids = out.ids;
     r.out_scores = out.scores;
-    prof_begin(SA_KERNEL_MERGE, s);
+    ProfRegion prof_region(SA_KERNEL_MERGE, s);
     st = cuda_status(launch_rerank(r, nq, s), "re-rank");
-    prof_end(SA_KERNEL_MERGE, s);
-    prof_count(SA_KERNEL_MERGE);
   }
   if (Qs) cudaFreeAsync(Qs, s);
   if (Q8) cudaFreeAsync(Q8, s);

@@ -185,7 +185,7 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
     if (st == SA_OK) st = dalloc(&psc, (size_t)nc * idx->nlist, s, "graph search");
     if (st == SA_OK) st = dalloc(&pkeys, (size_t)nc * E, s, "graph search");
     if (st == SA_OK) {
-      prof_begin(SA_KERNEL_STAGE, s);
+      ProfRegion prof_region(SA_KERNEL_STAGE, s);
       st = cuda_status(launch_cast_pad(static_cast<const uint8_t*>(queries) + q0 * qsize,
                                        qdtype == SA_F32, nc, idx->d, Qs, nq_pad, idx->d_pad,
                                        idx->num_sms, s),
@@ -194,12 +194,10 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
         st = cuda_status(launch_quant_e4m3(Qs, nq_pad, idx->d_pad, nullptr, Q8, idx->d8_pad,
                                            nullptr, idx->num_sms, s),
                          "stage fp8 queries");
-      prof_end(SA_KERNEL_STAGE, s);
-      prof_count(SA_KERNEL_STAGE);
     }
     if (st == SA_OK) {
       // entry points: the E best IVF lists (tensor-core centroid scores + exact select)
-      prof_begin(SA_KERNEL_IVF_PROBE, s);
+      ProfRegion prof_region(SA_KERNEL_IVF_PROBE, s);
       const CorpusView cvc{&idx->tmap_c, &idx->tmap_c2, idx->nlist, idx->d_pad, nullptr, 0u};
       // score dump + exact select (a fused top-E scan was measured slower: 0.19 vs 0.07 ms at
       // nq = 512, the per-unit query staging dominates a 16384-row scan)
@@ -212,9 +210,7 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
         m.k = E;
         m.out_keys = pkeys;
         st = cuda_status(launch_merge(m, nc, s), "entry select");
-        prof_count(SA_KERNEL_MERGE);
       }
-      prof_end(SA_KERNEL_IVF_PROBE, s);
     }
     if (st == SA_OK) {
       GraphSearchArgs a{};
@@ -252,10 +248,8 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
         a.d8_pad = idx->d8_pad;
         a.out_keys = cand;
       }
-      prof_begin(SA_KERNEL_GRAPH_SEARCH, s);
+      ProfRegion prof_region(SA_KERNEL_GRAPH_SEARCH, s);
       st = cuda_status(launch_graph_search(a, mo ? &m : nullptr, nc, s, fp8), "graph search");
-      prof_end(SA_KERNEL_GRAPH_SEARCH, s);
-      prof_count(SA_KERNEL_GRAPH_SEARCH);
     }
     if (st == SA_OK && fp8) {
       // R34: the final list re-scored on the bf16 rows, the k best
@@ -270,10 +264,8 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
       r.k = k;
       r.out_ids = out_ids + q0 * k;
       r.out_scores = out_scores + q0 * k;
-      prof_begin(SA_KERNEL_MERGE, s);
+      ProfRegion prof_region(SA_KERNEL_MERGE, s);
       st = cuda_status(launch_rerank(r, nc, s), "graph re-rank");
-      prof_end(SA_KERNEL_MERGE, s);
-      prof_count(SA_KERNEL_MERGE);
     }
     if (Qs) cudaFreeAsync(Qs, s);
     if (psc) cudaFreeAsync(psc, s);

@@ -29,8 +29,12 @@ struct sa_graph_entry {
   void* d_q = nullptr;
   int64_t* d_ids = nullptr;
   float* d_sc = nullptr;
-  int64_t kernels = 0;
+  int64_t launches[SA_KERNEL_KINDS] = {};   // per-kind kernel launches of one replay
+  uint64_t last_use = 0;                    // LRU stamp (sa_index::use_clock)
 };
+// Bound on the captured-graph caches of one index (sa_search_host shapes, maturity plans):
+// an agent loop whose batch size changes every step must not grow memory without limit.
+constexpr size_t kMaxCapturedSearches = 32;
 
 namespace sa {
 struct MaturePlan;
@@ -61,6 +65,7 @@ struct sa_index {
   // captured small-batch searches (host-buffer path), guarded by graph_mu
   std::mutex graph_mu;
   std::vector<sa_graph_entry> graphs;
+  uint64_t use_clock = 0;   // LRU clock of both caches
   // proximity graph (graph_api.cu): neighbour lists in stored positions [n_local, graph_R]
   int32_t graph_R = 0, graph_K = 0;
   int32_t* graph = nullptr;
@@ -98,12 +103,26 @@ inline void shard_range(int64_t n, int world, int rank, int64_t* off, int64_t* l
   *len = base + (rank < rem ? 1 : 0);
 }
 
-// profiler hooks (no events and no counting while a graph is being captured)
+// Kernel accounting (sa_api.cu).  A region attributes every launch made while it is the
+// calling thread's outermost open region (note_launch(), kernels/launch.cuh) to `kind`, and
+// times itself with CUDA events on `s` when profiling is on.  Inner regions are absorbed.
+class ProfRegion {
+ public:
+  ProfRegion(int kind, cudaStream_t s);
+  ~ProfRegion();
+  ProfRegion(const ProfRegion&) = delete;
+  ProfRegion& operator=(const ProfRegion&) = delete;
+
+ private:
+  bool owner_;
+  cudaStream_t s_;
+  cudaEvent_t begin_ = nullptr;
+};
+// While a graph is captured no events are recorded and launches go to a per-kind tally
+// (capture_tally); a replay adds the tally back with prof_add_launches.
 void set_capturing(bool on);
-void prof_count_n(int kind, int64_t n);
-void prof_count(int kind);
-void prof_begin(int kind, cudaStream_t s);
-void prof_end(int kind, cudaStream_t s);
+void capture_tally(int64_t out[SA_KERNEL_KINDS]);
+void prof_add_launches(const int64_t counts[SA_KERNEL_KINDS]);
 
 // Query padding / kernel variant: cta_group 2 (M=256 pairs) when more than one
 // 128-query block is searched, else cta_group 1.
@@ -142,8 +161,6 @@ sa_status gather_merge_keys(const sa_index* idx, const uint64_t* keys_local, int
 // bound of the final k-th score)
 sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
                            int32_t k, const SearchOut& out, cudaStream_t s, bool prepass = true);
-// while set, flat_search_view's launches are profiled as SA_KERNEL_OTHER (sub-scans)
-void set_prof_kind_other(bool on);
 // raw fp32 score matrix out[q, row] = <Q_q, X_row> for q < nq (tensor cores, no selection)
 sa_status flat_scores_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
                            float* out, cudaStream_t s);

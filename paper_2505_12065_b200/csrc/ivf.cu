@@ -81,7 +81,6 @@ sa_status sort_by_list(const int64_t* ids, int64_t n, int nlist, int num_sms, in
   SA_CUDA(cudaMemsetAsync(hist, 0, sizeof(int64_t) * nlist, s), "memset");
   SA_CUDA(launch_histogram(keys, n, hist, num_sms, s), "histogram");
   SA_CUDA(exclusive_scan_i64(hist, nlist, off, scratch, s), "scan");
-  for (int i = 0; i < 9; ++i) prof_count(SA_KERNEL_OTHER);
   return SA_OK;
 }
 
@@ -133,7 +132,6 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
     SA_CUDA(launch_gather_rows(idx->X, dp, nullptr, n_total, idx->row_offset, toff[me], n_train,
                                toff[me + 1] - toff[me], sample + (size_t)toff[me] * dp, sms, s),
             "gather sample");
-    prof_count(SA_KERNEL_OTHER);
     if (comm) {
       for (int r = 0; r < world; ++r) {
         boff[r] = toff[r] * dp * (int64_t)sizeof(__nv_bfloat16);
@@ -142,7 +140,6 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
       SA_TRY(comm_broadcast_parts(comm, sample, boff.data(), blen.data(), s));
     }
     SA_CUDA(launch_init_centroids(sample, dp, nlist, n_train, o.seed, idx->centroids, s), "init");
-    prof_count(SA_KERNEL_OTHER);
   } else {
     // caller-provided quantiser: fp32 [nlist, d] -> [nlist, d_pad], zero padded
     SA_CUDA(cudaMemsetAsync(idx->centroids, 0, (size_t)nlist * dp * sizeof(float), s), "memset");
@@ -178,7 +175,6 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   for (int it = 0; train && it < o.kmeans_iters; ++it) {
     SA_CUDA(launch_f32_to_bf16(idx->centroids, (int64_t)nlist * dp, idx->centroids_bf16, sms, s),
             "centroids->bf16");
-    prof_count(SA_KERNEL_OTHER);
     SearchOut so;
     so.ids = ids;
     so.scores = scores;
@@ -188,7 +184,6 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
     SA_CUDA(launch_centroid_update(sample, dp, perm, off, nlist, idx->centroids, empty_flag, n_empty,
                                    s),
             "centroid update");
-    prof_count(SA_KERNEL_OTHER);
     int32_t h_empty = 0;
     SA_CUDA(cudaMemcpyAsync(&h_empty, n_empty, sizeof(int32_t), cudaMemcpyDeviceToHost, s), "D2H");
     SA_CUDA(cudaStreamSynchronize(s), "sync");
@@ -206,12 +201,10 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
       SA_CUDA(launch_merge(m, 1, s), "repair select");
       SA_CUDA(launch_repair_apply(sample, dp, nlist, empty_flag, rsel, idx->centroids, s),
               "repair apply");
-      for (int i = 0; i < 3; ++i) prof_count(SA_KERNEL_OTHER);
     }
   }
   SA_CUDA(launch_f32_to_bf16(idx->centroids, (int64_t)nlist * dp, idx->centroids_bf16, sms, s),
           "centroids->bf16");
-  prof_count(SA_KERNEL_OTHER);
 
   // ---- a3: assign every local row, sort list-major, permute
   int64_t* ids_all;
@@ -241,8 +234,6 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
     cudaFree(Xp);
     return cuda_status(e, "permute corpus");
   }
-  prof_count(SA_KERNEL_OTHER);
-  prof_count(SA_KERNEL_OTHER);
   cudaFree(idx->X);
   idx->X = Xp;
   SA_TRY(make_tmap_bf16(&idx->tmap_x, idx->X, n, dp, FS_BN));
@@ -276,7 +267,6 @@ static sa_status probe_keys(const sa_index* idx, const __nv_bfloat16* Qs, int64_
   m.k = nprobe;
   m.out_keys = pkeys;
   SA_CUDA(launch_merge(m, nq, s), "probe select");
-  prof_count(SA_KERNEL_MERGE);
   return SA_OK;
 }
 
@@ -289,7 +279,6 @@ sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, in
   f.add(pkeys);
   SA_TRY(probe_keys(idx, Qs, nq, nprobe, pkeys, s));
   SA_CUDA(launch_keys_to_lists(pkeys, nq * nprobe, nullptr, out_lists, idx->num_sms, s), "lists");
-  prof_count(SA_KERNEL_OTHER);
   return SA_OK;
 }
 
@@ -309,13 +298,11 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   SA_TRY(dalloc(&probes, np, s, "alloc probes"));
   f.add(probes);
   {
-    prof_begin(SA_KERNEL_IVF_PROBE, s);
+    ProfRegion prof_region(SA_KERNEL_IVF_PROBE, s);
     sa_status st = probe_keys(idx, Qs, nq, nprobe, pkeys, s);
-    prof_end(SA_KERNEL_IVF_PROBE, s);
     if (st != SA_OK) return st;
   }
   SA_CUDA(launch_keys_to_lists(pkeys, np, probes, nullptr, sms, s), "probe lists");
-  prof_count(SA_KERNEL_OTHER);
 
   // ---- invert: lists -> probing queries, output slots, work items
   // aim for ~4 work items per SM: rows probed ~= np * mean list length
@@ -357,11 +344,9 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   if (np <= kInvertSmallMax) {
     SA_CUDA(launch_invert_small(probes, (int)nq, nprobe, idx->list_off, chunk_rows, qblock, w, s),
             "probe inversion");
-    prof_count(SA_KERNEL_OTHER);
   } else {
     SA_CUDA(launch_probe_invert(probes, nq, nprobe, nlist, idx->list_off, chunk_rows, qblock, w, sms, s),
             "probe inversion");
-    for (int i = 0; i < 10; ++i) prof_count(SA_KERNEL_OTHER);
   }
 
   // ---- a8: list-major scan on the tensor cores
@@ -396,11 +381,9 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
     v.chunk_rows = chunk_rows;
     v.q_hint = hint;
     v.item_counter = reinterpret_cast<int32_t*>(hint + nq);
-    prof_begin(SA_KERNEL_IVF_SCAN, s);
+    ProfRegion prof_region(SA_KERNEL_IVF_SCAN, s);
     e = Q8 ? launch_ivf_scan(idx->tmap_x8, idx->tmap_x8t, v, sms, s)
            : launch_ivf_scan(idx->tmap_x, idx->tmap_xt, v, sms, s);
-    prof_end(SA_KERNEL_IVF_SCAN, s);
-    prof_count(SA_KERNEL_IVF_SCAN);
     SA_CUDA(e, "ivf scan");
   } else {
   CUtensorMap tmap_q;
@@ -426,10 +409,8 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   a.chunk_rows = chunk_rows;
   a.q_hint = hint;
   a.item_counter = reinterpret_cast<int32_t*>(hint + nq);
-  prof_begin(SA_KERNEL_IVF_SCAN, s);
+  ProfRegion prof_region(SA_KERNEL_IVF_SCAN, s);
   e = launch_flat_scan(idx->tmap_x, idx->tmap_xt, tmap_q, a, 1, sms, s);
-  prof_end(SA_KERNEL_IVF_SCAN, s);
-  prof_count(SA_KERNEL_IVF_SCAN);
   SA_CUDA(e, "ivf scan");
   }
 
@@ -442,10 +423,8 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   m.out_keys = out.keys;
   m.out_ids = out.ids;
   m.out_scores = out.scores;
-  prof_begin(SA_KERNEL_MERGE, s);
+  ProfRegion prof_region(SA_KERNEL_MERGE, s);
   e = launch_merge(m, nq, s);
-  prof_end(SA_KERNEL_MERGE, s);
-  prof_count(SA_KERNEL_MERGE);
   return cuda_status(e, "ivf merge");
 }
 

@@ -38,6 +38,7 @@
 
 #include "flat_scan.cuh"
 #include "keys.cuh"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace sa {
@@ -52,9 +53,12 @@ constexpr uint32_t kTmemCols = 512;
 constexpr int kASmemKb = FS_BM * FS_BK * 2;  // one 128-row x 64-col K-block of A in smem: 16 KB
 
 constexpr int kKbPerStage = 2;
-constexpr int kLockstepLag = 4;  // tiles ahead (C3: DRAM reads 51 -> 33 GB per batch vs 8; 2 gives 32.3 GB but no faster)
-constexpr int kTailRows = FS_TAIL_ROWS;
-constexpr int kItemQ = 4;                // depth of the dynamic work-item queue  // box rows of the tail tensor map (IVF list tails)  // tiles a unit may run ahead of units sharing its slice  // K-blocks (64 wide) per ring stage: 8 MMAs per barrier round trip
+// tiles a unit may run ahead of units sharing its slice (C3: DRAM reads 51 -> 33 GB per batch
+// vs 8; 2 gives 32.3 GB but no faster)
+constexpr int kLockstepLag = 4;
+constexpr int kLockstepSpinCap = 1 << 14;   // sleeps of one lockstep wait before pacing stops
+constexpr int kTailRows = FS_TAIL_ROWS;     // box rows of the tail tensor map (IVF list tails)
+constexpr int kItemQ = 4;                   // depth of the dynamic work-item queue
 
 template <int CG, bool F8 = false>
 struct Cfg {
@@ -267,7 +271,12 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       // and none runs more than kLockstepLag tiles ahead of another, so the slice is read
       // from HBM once and served from L2 to the other groups (37 slices x lag x 192 KB
       // stays well inside the 126 MB L2).  Only the pair leader's producer paces.
-      const bool lockstep = a.progress != nullptr && leader;
+      // Pacing is only an L2 optimisation, and nothing guarantees the peer units are resident
+      // (a plain cluster launch; other streams may hold SMs): a wait that lasts longer than
+      // kLockstepSpinCap sleeps (>= ~4 ms, tiles take ~µs) turns pacing off for this unit,
+      // so a unit never waits on a peer that has not been scheduled.
+      bool lockstep = a.progress != nullptr && leader;
+      const bool publish = lockstep;
       const int lag = a.lockstep_lag > 0 ? a.lockstep_lag : kLockstepLag;
       int fetched = 0;
       auto next_w = [&](int w_prev) -> int {
@@ -284,14 +293,21 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       for (int w = next_w(-1); w >= 0 && w < n_work; w = next_w(w)) {
         const WorkItem wi = work_item(w, a, T);
         for (int32_t t = wi.t0; t < wi.t1; ++t) {
-          if (lockstep) {
+          if (publish) {
             const int32_t done = t - wi.t0;
             if ((done & 3) == 0) {
-              ptx::st_release_gpu(a.progress + unit, done);
-              for (int g = 0; g < a.QP; ++g) {
+              ptx::st_release_gpu(a.progress + unit, done);   // published even if not pacing
+              for (int g = 0; g < a.QP && lockstep; ++g) {
                 const int p = g * S + wi.s;
                 if (p == unit) continue;
-                while (ptx::ld_acquire_gpu(a.progress + p) < done - lag) __nanosleep(256);
+                int spins = 0;
+                while (ptx::ld_acquire_gpu(a.progress + p) < done - lag) {
+                  if (++spins > kLockstepSpinCap) {
+                    lockstep = false;
+                    break;
+                  }
+                  __nanosleep(256);
+                }
               }
             }
           }
@@ -718,29 +734,26 @@ cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_ta
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto go = [&](auto kern, bool& set) -> cudaError_t {
-    if (!set) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      set = true;
-    }
-    return cudaLaunchKernelEx(&cfg, kern, tmap, tmap_tail, tmap_q, a);
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = ensure_max_smem(reinterpret_cast<const void*>(kern), smem);
+    if (e != cudaSuccess) return e;
+    e = cudaLaunchKernelEx(&cfg, kern, tmap, tmap_tail, tmap_q, a);
+    note_launch();
+    return e;
   };
   // instantiations: (CG, F8, DUMP); the score dump (FS_MODE_DEBUG) has its own, heap-free one
-  static bool set[6] = {false, false, false, false, false, false};
   if (a.mode == FS_MODE_DEBUG) {
     if (a.fp8) return cudaErrorInvalidValue;
-    return cta_group == 2 ? go(flat_scan_topk_kernel<2, false, true>, set[4])
-                          : go(flat_scan_topk_kernel<1, false, true>, set[5]);
+    return cta_group == 2 ? go(flat_scan_topk_kernel<2, false, true>)
+                          : go(flat_scan_topk_kernel<1, false, true>);
   }
   if (a.fp8) {
     if (a.mode == FS_MODE_IVF) return cudaErrorInvalidValue;  // fp8 runs the flat modes only
-    return cta_group == 2 ? go(flat_scan_topk_kernel<2, true, false>, set[2])
-                          : go(flat_scan_topk_kernel<1, true, false>, set[3]);
+    return cta_group == 2 ? go(flat_scan_topk_kernel<2, true, false>)
+                          : go(flat_scan_topk_kernel<1, true, false>);
   }
-  return cta_group == 2 ? go(flat_scan_topk_kernel<2, false, false>, set[0])
-                        : go(flat_scan_topk_kernel<1, false, false>, set[1]);
+  return cta_group == 2 ? go(flat_scan_topk_kernel<2, false, false>)
+                        : go(flat_scan_topk_kernel<1, false, false>);
 }
 
 }  // namespace sa

@@ -10,6 +10,7 @@
 
 #include "fp8.cuh"
 #include "keys.cuh"
+#include "launch.cuh"
 
 namespace sa {
 
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(kRrThreads) rerank_kernel(const RerankArgs a) 
 cudaError_t launch_absmax_bf16(const __nv_bfloat16* X, int64_t n, int32_t d_pad,
                                uint32_t* out_bits, int num_sms, cudaStream_t s) {
   absmax_kernel<<<grid_for(n * d_pad / 8, 256, num_sms), 256, 0, s>>>(X, n * d_pad, out_bits);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -200,12 +202,14 @@ cudaError_t launch_quant_e4m3(const __nv_bfloat16* X, int64_t n, int32_t d_pad,
                               int32_t* exp_out, int num_sms, cudaStream_t s) {
   quant_e4m3_kernel<<<grid_for(n, 8, num_sms), 256, 0, s>>>(X, n, d_pad, absmax_bits, X8, d8_pad,
                                                             exp_out);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_rerank(const RerankArgs& a, int64_t nq, cudaStream_t s) {
   if (a.n_cand > F8_MAX_CAND || a.k > a.n_cand || a.d_pad > 768) return cudaErrorInvalidValue;
   rerank_kernel<<<(unsigned)nq, kRrThreads, 0, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -15,6 +15,7 @@
 
 #include "graph.cuh"
 #include "keys.cuh"
+#include "launch.cuh"
 
 namespace sa {
 
@@ -551,6 +552,7 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
         const int i = base + lane;
         const bool un = i < cnt && sm.flag[cur][i] == 0;
         unsigned m = __ballot_sync(0xffffffffu, un);
+        __syncwarp();   // every lane's flag read precedes lane 0's writes below
         while (m && taken < a.w) {
           const int b = __ffs(m) - 1;
           m &= m - 1;
@@ -564,7 +566,9 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
       if (lane == 0) {
         sm.n_chosen = taken;
         sm.n_new = 0;
-        sm.n_ins = 0;
+        // every thread read n_ins at the top of this iteration; when it was nonzero the merge's
+        // barrier orders those reads before this write, when zero there is nothing to reset
+        if (n_ins != 0) sm.n_ins = 0;
         if constexpr (kMature) sm.smax = 0ull;
       }
     }
@@ -632,6 +636,7 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
 cudaError_t launch_inverse_ids(const int32_t* row_ids, int64_t n, int64_t row_offset,
                                int32_t* pos_of, cudaStream_t s) {
   inverse_ids_kernel<<<grid_for(n, 256), 256, 0, s>>>(row_ids, n, row_offset, pos_of);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -640,12 +645,14 @@ cudaError_t launch_knn_to_pos(const int64_t* ids, int64_t nb, int kk, int64_t p0
                               cudaStream_t s) {
   knn_to_pos_kernel<<<grid_for(nb, 128), 128, 0, s>>>(ids, nb, kk, p0, pos_of, row_offset, K,
                                                       knn);
+  note_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_graph_prune(const int32_t* knn, int64_t n, int K, int R, int32_t* fwd,
                                cudaStream_t s) {
   graph_prune_kernel<<<grid_for(n, 8), 256, 0, s>>>(knn, n, K, R, fwd);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -653,6 +660,7 @@ cudaError_t launch_graph_reverse(const int32_t* fwd, int64_t n, int R, const int
                                  uint64_t* rev, cudaStream_t s) {
   graph_reverse_kernel<<<grid_for(n * R, 256), 256, 0, s>>>(
       fwd, n, R, row_ids, reinterpret_cast<unsigned long long*>(rev));
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -661,6 +669,7 @@ cudaError_t launch_graph_merge(const int32_t* fwd, const uint64_t* rev, int64_t 
                                cudaStream_t s) {
   graph_merge_kernel<<<grid_for(n, 8), 256, 0, s>>>(
       fwd, reinterpret_cast<const unsigned long long*>(rev), n, R, pos_of, row_offset, nbr);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -670,14 +679,11 @@ template <int TH, int RW, bool M, bool F8>
 cudaError_t launch_shape(const GraphSearchArgs& a, const GraphMatureArgs& m, int64_t nq,
                          cudaStream_t s) {
   const size_t smem = sizeof(SearchSmem);
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(graph_search_kernel<TH, RW, M, F8>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e =
+      ensure_max_smem(reinterpret_cast<const void*>(graph_search_kernel<TH, RW, M, F8>), smem);
+  if (e != cudaSuccess) return e;
   graph_search_kernel<TH, RW, M, F8><<<(unsigned)nq, TH, smem, s>>>(a, m);
+  note_launch();
   return cudaGetLastError();
 }
 

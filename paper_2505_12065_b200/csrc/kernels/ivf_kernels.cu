@@ -11,6 +11,7 @@
 
 #include "ivf_kernels.cuh"
 #include "keys.cuh"
+#include "launch.cuh"
 
 namespace sa {
 
@@ -54,6 +55,7 @@ cudaError_t launch_gather_rows(const __nv_bfloat16* X, int d_pad, const int32_t*
   if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
   gather_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, d_pad, idx, n_total, row_offset, t0,
                                                       n_train, n_out, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -72,6 +74,7 @@ cudaError_t launch_init_centroids(const __nv_bfloat16* sample, int d_pad, int nl
   const int64_t stride = n_train / nlist;
   const int64_t o = (int64_t)(host_splitmix64(seed) % (uint64_t)stride);
   init_centroids_kernel<<<nlist, 256, 0, s>>>(sample, d_pad, nlist, stride, o, cent);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -88,6 +91,7 @@ cudaError_t launch_f32_to_bf16(const float* in, int64_t n, __nv_bfloat16* out, i
   if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
   if (blocks < 1) return cudaSuccess;
   f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, n, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -130,9 +134,16 @@ __global__ void scan_add_kernel(int64_t* __restrict__ out, int64_t n,
 cudaError_t exclusive_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t* scratch,
                                cudaStream_t s) {
   const int64_t nb = (n + kScanBlock - 1) / kScanBlock;
-  if (n > 0) scan_block_kernel<<<(unsigned)nb, kScanBlock, 0, s>>>(in, n, out, scratch);
+  if (n > 0) {
+    scan_block_kernel<<<(unsigned)nb, kScanBlock, 0, s>>>(in, n, out, scratch);
+    note_launch();
+  }
   scan_sums_kernel<<<1, 32, 0, s>>>(scratch, nb, out + n);
-  if (n > 0) scan_add_kernel<<<(unsigned)nb, kScanBlock, 0, s>>>(out, n, scratch);
+  note_launch();
+  if (n > 0) {
+    scan_add_kernel<<<(unsigned)nb, kScanBlock, 0, s>>>(out, n, scratch);
+    note_launch();
+  }
   return cudaGetLastError();
 }
 
@@ -197,14 +208,18 @@ cudaError_t stable_sort_by_key16(const int32_t* keys, int64_t n, int32_t* keys_t
   const int64_t nb = (n + kSortTile - 1) / kSortTile;
   // pass 1: low byte, values = positions
   radix_count_kernel<<<(unsigned)nb, 256, 0, s>>>(keys, n, 0, nb, counts);
+  note_launch();
   exclusive_scan_i64(counts, 256 * nb, offs, scratch, s);
   radix_scatter_kernel<<<(unsigned)nb, 32, 0, s>>>(keys, nullptr, n, 0, nb, offs, keys_tmp,
                                                    vals_tmp);
+  note_launch();
   // pass 2: high byte
   radix_count_kernel<<<(unsigned)nb, 256, 0, s>>>(keys_tmp, n, 8, nb, counts);
+  note_launch();
   exclusive_scan_i64(counts, 256 * nb, offs, scratch, s);
   radix_scatter_kernel<<<(unsigned)nb, 32, 0, s>>>(keys_tmp, vals_tmp, n, 8, nb, offs, keys_out,
                                                    vals_out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -221,6 +236,7 @@ cudaError_t launch_histogram(const int32_t* keys, int64_t n, int64_t* hist, int 
   if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
   if (blocks < 1) return cudaSuccess;
   histogram_kernel<<<(unsigned)blocks, 256, 0, s>>>(keys, n, hist);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -237,6 +253,7 @@ cudaError_t launch_i64_to_i32(const int64_t* in, int64_t n, int32_t* out, int nu
   if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
   if (blocks < 1) return cudaSuccess;
   i64_to_i32_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, n, out);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -295,6 +312,7 @@ cudaError_t launch_centroid_update(const __nv_bfloat16* sample, int d_pad, const
                                    int32_t* empty_flag, int32_t* n_empty, cudaStream_t s) {
   centroid_update_kernel<<<nlist, 256, 0, s>>>(sample, d_pad, rows, off, cent, empty_flag,
                                                 n_empty);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -310,6 +328,7 @@ cudaError_t launch_repair_keys(const float* scores, int64_t n, uint64_t* keys, i
   int64_t blocks = (n + 255) / 256;
   if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
   repair_keys_kernel<<<(unsigned)blocks, 256, 0, s>>>(scores, n, keys);
+  note_launch();
   return cudaGetLastError();
 }
 // The i-th empty list (ascending id) takes sample row key_id(sel[i]).
@@ -335,6 +354,7 @@ cudaError_t launch_repair_apply(const __nv_bfloat16* sample, int d_pad, int nlis
                                 const int32_t* empty_flag, const uint64_t* sel, float* cent,
                                 cudaStream_t s) {
   repair_apply_kernel<<<1, 256, 0, s>>>(sample, d_pad, nlist, empty_flag, sel, cent);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -538,6 +558,7 @@ cudaError_t launch_invert_small(const int64_t* probes, int nq, int nprobe, const
   invert_small_kernel<<<1, 1024, P2 * sizeof(uint64_t), s>>>(probes, nq, nprobe, list_off,
                                                               chunk_rows, qblock, w.lq_ent, w.q_slot,
                                                               w.items, w.n_items, StageSrc{});
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -549,6 +570,7 @@ cudaError_t launch_invert_stage(int64_t* stage_probes, int nq, int g, const Stag
   invert_small_kernel<<<1, 1024, P2 * sizeof(uint64_t), s>>>(stage_probes, nq, g, list_off,
                                                               chunk_rows, qblock, w.lq_ent, w.q_slot,
                                                               w.items, w.n_items, src);
+  note_launch();
   return cudaGetLastError();
 }
 __global__ void i32_to_i64_kernel(const int32_t* __restrict__ in, int64_t n,
@@ -569,15 +591,21 @@ cudaError_t launch_probe_invert(const int64_t* probes, int64_t nq, int nprobe, i
   cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * nlist, s);
   cudaMemsetAsync(w.cursor, 0, sizeof(int32_t) * nlist, s);
   probe_count_kernel<<<b, 256, 0, s>>>(probes, n, w.cnt);
+  note_launch();
   i32_to_i64_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, w.tmp64);
+  note_launch();
   exclusive_scan_i64(w.tmp64, nlist, w.lq_off64, w.scratch, s);
   probe_fill_kernel<<<b, 256, 0, s>>>(probes, nq, nprobe, w.lq_off64, w.cursor, w.lq_ent);
+  note_launch();
   probe_slots_kernel<<<b, 256, 0, s>>>(probes, n, list_off, chunk_rows, w.tmp64b);
+  note_launch();
   exclusive_scan_i64(w.tmp64b, n, w.q_slot, w.scratch, s);
   list_items_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, list_off, chunk_rows, qblock, w.tmp64);
+  note_launch();
   exclusive_scan_i64(w.tmp64, nlist, w.item_off, w.scratch, s);
   items_fill_kernel<<<bl, 256, 0, s>>>(w.cnt, nlist, list_off, chunk_rows, qblock, w.lq_off64, w.item_off,
                                        w.items, w.n_items);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -598,6 +626,7 @@ cudaError_t launch_keys_to_lists(const uint64_t* keys, int64_t n, int64_t* lists
   if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
   if (blocks < 1) return cudaSuccess;
   keys_to_lists_kernel<<<(unsigned)blocks, 256, 0, s>>>(keys, n, lists, lists32);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -614,6 +643,7 @@ cudaError_t launch_perm_ids(const int32_t* perm, int64_t n, int64_t row_offset, 
   if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
   if (blocks < 1) return cudaSuccess;
   perm_ids_kernel<<<(unsigned)blocks, 256, 0, s>>>(perm, n, row_offset, ids);
+  note_launch();
   return cudaGetLastError();
 }
 

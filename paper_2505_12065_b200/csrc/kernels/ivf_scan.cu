@@ -23,6 +23,7 @@
 
 #include "ivf_scan.cuh"
 #include "keys.cuh"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace sa {
@@ -444,18 +445,14 @@ size_t ivf_scan_smem_bytes() {
 cudaError_t launch_ivf_scan(const CUtensorMap& tmap_x, const CUtensorMap& tmap_tail,
                             const IvfScanArgs& a, int grid, cudaStream_t stream) {
   const size_t smem = ivf_scan_smem_bytes();
-  static bool set[2] = {false, false};
-  auto go = [&](auto kern, bool& done) -> cudaError_t {
-    if (!done) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      done = true;
-    }
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = ensure_max_smem(reinterpret_cast<const void*>(kern), smem);
+    if (e != cudaSuccess) return e;
     kern<<<grid, kThreads, smem, stream>>>(tmap_x, tmap_tail, a);
+    note_launch();
     return cudaGetLastError();
   };
-  return a.fp8 ? go(ivf_scan_kernel<true>, set[1]) : go(ivf_scan_kernel<false>, set[0]);
+  return a.fp8 ? go(ivf_scan_kernel<true>) : go(ivf_scan_kernel<false>);
 }
 
 }  // namespace sa

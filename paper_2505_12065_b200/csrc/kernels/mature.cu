@@ -17,6 +17,7 @@
 #include <cmath>
 
 #include "keys.cuh"
+#include "launch.cuh"
 #include "mature.cuh"
 
 namespace sa {
@@ -207,6 +208,7 @@ unsigned blocks_for(int64_t n) {
 cudaError_t launch_mature_init(const MatureArgs& a, cudaStream_t s) {
   const int64_t n = (int64_t)a.nq * (a.k > a.nprobe_max ? a.k : a.nprobe_max);
   mature_init_kernel<<<blocks_for(n), 256, 0, s>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -215,14 +217,10 @@ cudaError_t launch_mature_update(const MatureArgs& a, cudaGraphConditionalHandle
   int n2 = 1;
   while (n2 < a.k + kCandBlock) n2 <<= 1;
   const size_t smem = (size_t)n2 * sizeof(uint64_t);
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(mature_update_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e = ensure_max_smem(reinterpret_cast<const void*>(mature_update_kernel), 64 * 1024);
+  if (e != cudaSuccess) return e;
   mature_update_kernel<<<a.nq, kUpdThreads, smem, s>>>(a, h);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -230,6 +228,7 @@ cudaError_t launch_mature_final(const MatureArgs& a, int64_t* out_ids, float* ou
                                 int32_t* out_t, cudaStream_t s) {
   mature_final_kernel<<<blocks_for((int64_t)a.nq * a.k), 256, 0, s>>>(a, out_ids, out_scores,
                                                                        out_t);
+  note_launch();
   return cudaGetLastError();
 }
 

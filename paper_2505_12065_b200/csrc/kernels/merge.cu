@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 
 #include "keys.cuh"
+#include "launch.cuh"
 #include "merge.cuh"
 
 namespace sa {
@@ -366,23 +367,21 @@ cudaError_t launch_merge(const MergeArgs& a, int64_t nq, cudaStream_t stream) {
   if (nq <= 0) return cudaSuccess;
   if (a.cand_scores) {
     const size_t smem = (size_t)a.m_flat * sizeof(uint32_t);
-    static int cur = 0;
-    if ((int)smem > cur) {
-      cudaError_t e = cudaFuncSetAttribute(select_dense_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      cur = (int)smem;
-    }
+    cudaError_t e = ensure_max_smem(reinterpret_cast<const void*>(select_dense_kernel), smem);
+    if (e != cudaSuccess) return e;
     select_dense_kernel<<<(unsigned)nq, kThreads, smem, stream>>>(a);
+    note_launch();
     return cudaGetLastError();
   }
   if (a.k == 1 && !a.slot_off && a.m_flat <= 0 && a.groups <= 64) {
     int64_t blocks = (nq + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     merge_top1_kernel<<<(unsigned)blocks, 256, 0, stream>>>(a, nq);
+    note_launch();
     return cudaGetLastError();
   }
   merge_topk_kernel<<<(unsigned)nq, kThreads, 0, stream>>>(a);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -439,6 +438,7 @@ cudaError_t launch_cast_pad(const void* src, bool src_f32, int64_t rows, int d, 
   else
     cast_pad_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, stream>>>(
         static_cast<const __nv_bfloat16*>(src), rows, d, dst, rows_pad, d_pad);
+  note_launch();
   return cudaGetLastError();
 }
 

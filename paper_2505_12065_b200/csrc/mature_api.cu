@@ -52,6 +52,10 @@ struct MaturePlan {
   int32_t* out_t = nullptr;
   cudaGraphExec_t exec = nullptr;
   std::vector<void*> allocs;
+  // launches of one replay per kernel kind (the WHILE body counted once: the number of
+  // stages is decided on the device); LRU stamp
+  int64_t launches[SA_KERNEL_KINDS] = {};
+  uint64_t last_use = 0;
 };
 
 void free_mature_plan(MaturePlan* p) {
@@ -259,6 +263,7 @@ sa_status make_plan(const sa_index* idx, MaturePlan& p) {
     SA_TRY(cuda_status(e, "end capture (epilogue)"));
   }
   SA_TRY(cuda_status(cudaGraphInstantiate(&p.exec, graph, 0), "instantiate"));
+  capture_tally(p.launches);
   return SA_OK;
 }
 
@@ -301,6 +306,16 @@ extern "C" sa_status sa_search_mature(const sa_index* idx, const void* queries, 
         e->qdtype == (int32_t)qdtype && e->trace == trace && e->stream == s)
       p = e.get();
   if (!p) {
+    if (mi->mature_plans.size() >= kMaxCapturedSearches) {
+      // bounded cache: drop the least recently used plan once its last replay has finished
+      auto lru = std::min_element(mi->mature_plans.begin(), mi->mature_plans.end(),
+                                  [](const auto& a, const auto& b) {
+                                    return a->last_use < b->last_use;
+                                  });
+      cudaError_t e = cudaStreamSynchronize((*lru)->stream);
+      if (e != cudaSuccess) return cuda_status(e, "evict maturity plan");
+      mi->mature_plans.erase(lru);
+    }
     std::unique_ptr<MaturePlan, void (*)(MaturePlan*)> np(new MaturePlan, free_mature_plan);
     np->nq = nq;
     np->k = k;
@@ -317,6 +332,7 @@ extern "C" sa_status sa_search_mature(const sa_index* idx, const void* queries, 
     p = np.get();
     mi->mature_plans.push_back(std::move(np));
   }
+  p->last_use = ++mi->use_clock;
   const size_t qbytes = (size_t)nq * idx->d * (qdtype == SA_F32 ? 4 : 2);
   sa_status st = cuda_status(cudaMemcpyAsync(p->d_q, queries, qbytes, cudaMemcpyDefault, s),
                              "queries in");
@@ -338,6 +354,6 @@ extern "C" sa_status sa_search_mature(const sa_index* idx, const void* queries, 
       st = cuda_status(cudaMemcpyAsync(out_ema, p->trace_ema, nt, cudaMemcpyDefault, s),
                        "trace out");
   }
-  prof_count_n(SA_KERNEL_OTHER, 7);
+  if (st == SA_OK) prof_add_launches(p->launches);
   return st;
 }

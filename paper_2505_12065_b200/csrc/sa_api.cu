@@ -64,6 +64,10 @@ sa_status make_tmap_bf16(CUtensorMap* m, const void* base, int64_t rows, int32_t
 }
 
 // ====================================================================== profiler
+// Kernel accounting: every launch site calls note_launch() (kernels/launch.cuh); the launch is
+// counted under the kind of the calling thread's OUTERMOST open ProfRegion (OTHER outside any
+// region), and each outermost region is timed with a pair of CUDA events on its stream.  So a
+// kind's launches and its time always cover the same kernels (inner regions are absorbed).
 namespace {
 struct Prof {
   std::mutex mu;
@@ -83,46 +87,72 @@ struct Prof {
   }
 };
 Prof g_prof;
-thread_local cudaEvent_t t_open[SA_KERNEL_KINDS];
-thread_local bool t_capturing = false;  // inside a graph capture: no events, no counting
-thread_local int t_other = 0;   // sub-scan depth: flat-scan / merge launches count as OTHER
-int remap(int kind) {
-  return t_other > 0 && (kind == SA_KERNEL_FLAT_SCAN || kind == SA_KERNEL_MERGE) ? SA_KERNEL_OTHER
-                                                                                : kind;
-}
+thread_local int t_depth = 0;            // open regions on this thread
+thread_local int t_kind = SA_KERNEL_OTHER;   // kind of the outermost one
+thread_local bool t_capturing = false;   // inside a graph capture: no events; tally launches
+thread_local int64_t t_tally[SA_KERNEL_KINDS];
 }  // namespace
 
-void set_capturing(bool on) { t_capturing = on; }
-void set_prof_kind_other(bool on) { t_other += on ? 1 : -1; }
+void set_capturing(bool on) {
+  t_capturing = on;
+  if (on)
+    for (int i = 0; i < SA_KERNEL_KINDS; ++i) t_tally[i] = 0;
+}
+void capture_tally(int64_t out[SA_KERNEL_KINDS]) {
+  for (int i = 0; i < SA_KERNEL_KINDS; ++i) out[i] = t_tally[i];
+}
+void prof_add_launches(const int64_t counts[SA_KERNEL_KINDS]) {
+  std::lock_guard<std::mutex> l(g_prof.mu);
+  for (int i = 0; i < SA_KERNEL_KINDS; ++i) g_prof.launches[i] += counts[i];
+}
 
-void prof_count(int kind) {
-  kind = remap(kind);
-  if (t_capturing) return;
+void note_launch() {
+  const int kind = t_depth > 0 ? t_kind : SA_KERNEL_OTHER;
+  if (t_capturing) {
+    ++t_tally[kind];
+    return;
+  }
   std::lock_guard<std::mutex> l(g_prof.mu);
   g_prof.launches[kind]++;
 }
-void prof_count_n(int kind, int64_t n) {
-  kind = remap(kind);
-  std::lock_guard<std::mutex> l(g_prof.mu);
-  g_prof.launches[kind] += n;
-}
-void prof_begin(int kind, cudaStream_t s) {
-  kind = remap(kind);
+
+ProfRegion::ProfRegion(int kind, cudaStream_t s) : owner_(t_depth++ == 0), s_(s) {
+  if (!owner_) return;
+  t_kind = kind;
   if (t_capturing) return;
   std::lock_guard<std::mutex> l(g_prof.mu);
   if (!g_prof.on) return;
-  t_open[kind] = g_prof.get();
-  cudaEventRecord(t_open[kind], s);
+  begin_ = g_prof.get();
+  cudaEventRecord(begin_, s);
 }
-void prof_end(int kind, cudaStream_t s) {
-  kind = remap(kind);
-  if (t_capturing) return;
+
+ProfRegion::~ProfRegion() {
+  --t_depth;
+  if (!owner_ || !begin_) return;
   std::lock_guard<std::mutex> l(g_prof.mu);
-  if (!g_prof.on || !t_open[kind]) return;
   cudaEvent_t e = g_prof.get();
-  cudaEventRecord(e, s);
-  g_prof.ev[kind].push_back({t_open[kind], e});
-  t_open[kind] = nullptr;
+  cudaEventRecord(e, s_);
+  g_prof.ev[t_kind].push_back({begin_, e});
+}
+
+// Raise a kernel's dynamic shared-memory limit once per (device, kernel); thread-safe.
+cudaError_t ensure_max_smem(const void* func, size_t bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, const void*>, size_t>> done;
+  std::lock_guard<std::mutex> l(mu);
+  for (auto& d : done)
+    if (d.first.first == dev && d.first.second == func) {
+      if (d.second >= bytes) return cudaSuccess;
+      e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e == cudaSuccess) d.second = bytes;
+      return e;
+    }
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) done.push_back({{dev, func}, bytes});
+  return e;
 }
 
 // ====================================================================== helpers
@@ -214,20 +244,19 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
       pv.n_rows = m;
       uint64_t* pk = nullptr;
       st = dalloc(&pk, (size_t)nq * k, s, "alloc hint keys");
+      ProfRegion region(SA_KERNEL_OTHER, s);   // the seed sub-scans count as OTHER
       if (st == SA_OK) {
         SearchOut po;
         po.keys = pk;
-        set_prof_kind_other(true);
         // the sub-scan seeds its own bound the same way (m / 32 rows, ...): without it its
         // heaps would pay the whole warm-up themselves
         st = flat_search_view(pv, num_sms, Qs, nq, k, po, s, seed_recurse);
-        set_prof_kind_other(false);
       }
       if (st == SA_OK) {
         hint_from_keys_kernel<<<(unsigned)std::min<int64_t>((nq + 255) / 256, 1024), 256, 0, s>>>(
             pk, nq, k, hint);
+        note_launch();
         st = cuda_status(cudaGetLastError(), "hint seed");
-        prof_count(SA_KERNEL_OTHER);
       }
       if (pk) cudaFreeAsync(pk, s);
     }
@@ -245,7 +274,13 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
     st = dalloc(&progress, (size_t)units, s, "alloc progress");
     if (st == SA_OK)
       st = cuda_status(cudaMemsetAsync(progress, 0, units * sizeof(int32_t), s), "memset");
-    if (st != SA_OK) return st;
+    if (st != SA_OK) {
+      if (progress) cudaFreeAsync(progress, s);
+      if (hint) cudaFreeAsync(hint, s);
+      if (heap) cudaFreeAsync(heap, s);
+      cudaFreeAsync(part, s);
+      return st;
+    }
   }
   FlatScanArgs a{};
   a.progress = progress;
@@ -279,15 +314,18 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   CUtensorMap tmap_q;
   st = make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM);
   if (st != SA_OK) {
+    if (progress) cudaFreeAsync(progress, s);
+    if (hint) cudaFreeAsync(hint, s);
     if (heap) cudaFreeAsync(heap, s);
     cudaFreeAsync(part, s);
     return st;
   }
-  prof_begin(SA_KERNEL_FLAT_SCAN, s);
   const CUtensorMap& tm = p.cg == 2 ? *cv.tmap2 : *cv.tmap1;
-  cudaError_t e = launch_flat_scan(tm, tm, tmap_q, a, p.cg, p.grid, s);
-  prof_end(SA_KERNEL_FLAT_SCAN, s);
-  prof_count(SA_KERNEL_FLAT_SCAN);
+  cudaError_t e;
+  {
+    ProfRegion region(SA_KERNEL_FLAT_SCAN, s);
+    e = launch_flat_scan(tm, tm, tmap_q, a, p.cg, p.grid, s);
+  }
   if (e == cudaSuccess) {
     MergeArgs m{};
     m.cand = part;
@@ -299,10 +337,8 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
     m.out_ids = out.ids;
     m.out_scores = out.scores;
     m.id_offset = 0;
-    prof_begin(SA_KERNEL_MERGE, s);
+    ProfRegion region(SA_KERNEL_MERGE, s);
     e = launch_merge(m, nq, s);
-    prof_end(SA_KERNEL_MERGE, s);
-    prof_count(SA_KERNEL_MERGE);
   }
   if (heap) cudaFreeAsync(heap, s);
   if (hint) cudaFreeAsync(hint, s);
@@ -332,7 +368,6 @@ sa_status flat_scores_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   if (st != SA_OK) return st;
   const CUtensorMap& tm = p.cg == 2 ? *cv.tmap2 : *cv.tmap1;
   cudaError_t e = launch_flat_scan(tm, tm, tmap_q, a, p.cg, p.grid, s);
-  prof_count(SA_KERNEL_FLAT_SCAN);
   return cuda_status(e, "score scan");
 }
 
@@ -557,9 +592,9 @@ sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nl
   idx->comm = opts->comm;
   st = cuda_status(cudaMalloc(&idx->X, (size_t)n * d_pad * sizeof(__nv_bfloat16)), "alloc corpus");
   if (st == SA_OK) {
+    ProfRegion region(SA_KERNEL_STAGE, s);
     st = cuda_status(launch_cast_pad(corpus, opts->dtype == SA_F32, n, d, idx->X, n, d_pad, sms, s),
                      "cast/pad corpus");
-    prof_count(SA_KERNEL_STAGE);
   }
   if (st == SA_OK) st = make_tmap_bf16(&idx->tmap_x, idx->X, n, d_pad, FS_BN);
   if (st == SA_OK) st = make_tmap_bf16(&idx->tmap_x2, idx->X, n, d_pad, FS_BN / 2);
@@ -596,11 +631,12 @@ static sa_status search_local(const sa_index* idx, const void* queries, sa_dtype
   __nv_bfloat16* Qs = nullptr;
   sa_status st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "alloc staged queries");
   if (st != SA_OK) return st;
-  prof_begin(SA_KERNEL_STAGE, s);
-  cudaError_t e = launch_cast_pad(queries, qdtype == SA_F32, nq, idx->d, Qs, nq_pad, idx->d_pad,
-                                  idx->num_sms, s);
-  prof_end(SA_KERNEL_STAGE, s);
-  prof_count(SA_KERNEL_STAGE);
+  cudaError_t e;
+  {
+    ProfRegion region(SA_KERNEL_STAGE, s);
+    e = launch_cast_pad(queries, qdtype == SA_F32, nq, idx->d, Qs, nq_pad, idx->d_pad,
+                        idx->num_sms, s);
+  }
   if (e != cudaSuccess) {
     cudaFreeAsync(Qs, s);
     return cuda_status(e, "stage queries");
@@ -621,11 +657,8 @@ static sa_status merge_keys(const uint64_t* keys, int32_t w, int64_t nq, int32_t
   m.gstride = nq * k;
   m.out_ids = out_ids;
   m.out_scores = out_scores;
-  prof_begin(SA_KERNEL_MERGE, s);
-  sa_status st = cuda_status(launch_merge(m, nq, s), "final merge");
-  prof_end(SA_KERNEL_MERGE, s);
-  prof_count(SA_KERNEL_MERGE);
-  return st;
+  ProfRegion region(SA_KERNEL_MERGE, s);
+  return cuda_status(launch_merge(m, nq, s), "final merge");
 }
 
 sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
@@ -726,7 +759,7 @@ static sa_status capture_search(const sa_index* idx, sa_graph_entry& g) {
   cudaGraph_t graph = nullptr;
   st = cuda_status(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
   if (st == SA_OK) {
-    t_capturing = true;
+    set_capturing(true);
     sa_status s1 = cuda_status(cudaMemcpyAsync(g.d_q, g.h_q, qbytes, cudaMemcpyHostToDevice, cs),
                                "H2D");
     SearchOut out;
@@ -738,21 +771,12 @@ static sa_status capture_search(const sa_index* idx, sa_graph_entry& g) {
       s1 = cuda_status(cudaMemcpyAsync(g.h_ids, g.d_ids, nk * 8, cudaMemcpyDeviceToHost, cs), "D2H");
     if (s1 == SA_OK)
       s1 = cuda_status(cudaMemcpyAsync(g.h_sc, g.d_sc, nk * 4, cudaMemcpyDeviceToHost, cs), "D2H");
-    t_capturing = false;
+    capture_tally(g.launches);
+    set_capturing(false);
     cudaError_t e = cudaStreamEndCapture(cs, &graph);
     st = s1 != SA_OK ? s1 : cuda_status(e, "end capture");
   }
   if (st == SA_OK) st = cuda_status(cudaGraphInstantiate(&g.exec, graph, 0), "instantiate");
-  if (st == SA_OK) {
-    size_t nn = 0;
-    cudaGraphGetNodes(graph, nullptr, &nn);
-    std::vector<cudaGraphNode_t> nodes(nn);
-    cudaGraphGetNodes(graph, nodes.data(), &nn);
-    for (auto nd : nodes) {
-      cudaGraphNodeType t;
-      if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++g.kernels;
-    }
-  }
   if (graph) cudaGraphDestroy(graph);
   cudaStreamDestroy(cs);
   return st;
@@ -783,6 +807,16 @@ sa_status sa_search_host(const sa_index* idx, const void* queries_host, sa_dtype
     for (auto& e : mi->graphs)
       if (e.nq == nq && e.k == k && e.nprobe == nprobe && e.qdtype == (int32_t)qdtype) g = &e;
     if (!g) {
+      // bounded cache: evict the least recently used shape (no graph of this index is in
+      // flight -- every replay below completes under graph_mu)
+      if (mi->graphs.size() >= kMaxCapturedSearches) {
+        auto lru = std::min_element(mi->graphs.begin(), mi->graphs.end(),
+                                    [](const sa_graph_entry& a, const sa_graph_entry& b) {
+                                      return a.last_use < b.last_use;
+                                    });
+        free_graph_entry(*lru);
+        mi->graphs.erase(lru);
+      }
       sa_graph_entry e;
       e.nq = nq;
       e.k = k;
@@ -796,13 +830,14 @@ sa_status sa_search_host(const sa_index* idx, const void* queries_host, sa_dtype
       mi->graphs.push_back(e);
       g = &mi->graphs.back();
     }
+    g->last_use = ++mi->use_clock;
     std::memcpy(g->h_q, queries_host, qbytes);
     st = cuda_status(cudaGraphLaunch(g->exec, s), "graph launch");
     if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "search sync");
     if (st != SA_OK) return st;
     std::memcpy(out_ids_host, g->h_ids, (size_t)nq * k * 8);
     std::memcpy(out_scores_host, g->h_sc, (size_t)nq * k * 4);
-    prof_count_n(SA_KERNEL_OTHER, g->kernels);
+    prof_add_launches(g->launches);
     return SA_OK;
   }
   void* dq = nullptr;

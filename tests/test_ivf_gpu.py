@@ -147,8 +147,6 @@ def test_p11_result_is_exact_over_probed_lists(sa, mixture_index, nprobe, k):
     gi, gs = gi.cpu().numpy(), gs.cpu().numpy()
     for qi in range(len(Qb)):
         rows = np.sort(np.concatenate([glists[j] for j in P[qi]]))
-        rep = check_against_rows(gi[qi:qi + 1], gs[qi:qi + 1], Xb[rows], Qb[qi:qi + 1], k) \
-            if False else None
         oi, osc = oracle.flat_topk(Xb[rows], Qb[qi:qi + 1], k + 8)
         oi = np.where(oi >= 0, rows[np.maximum(oi, 0)], -1)
         r = check(gi[qi:qi + 1], gs[qi:qi + 1], oi, osc,
