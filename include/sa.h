@@ -59,7 +59,7 @@ typedef enum {
 typedef enum { SA_BF16 = 0, SA_F32 = 1 } sa_dtype;
 
 typedef struct sa_index sa_index; /* opaque; owns all device memory of one rank's shard */
-typedef struct sa_comm sa_comm;   /* opaque; wraps an NCCL communicator */
+typedef struct sa_comm sa_comm;   /* opaque; an NCCL communicator or an in-process rank */
 
 typedef struct {
   sa_dtype dtype;          /* dtype of `corpus` (default SA_BF16) */
@@ -140,6 +140,41 @@ sa_status sa_comm_unique_id(void* out_128_bytes);
 sa_status sa_comm_init(const void* nccl_unique_id, int32_t rank, int32_t world, int32_t cuda_device,
                        sa_comm** out);
 sa_status sa_comm_free(sa_comm* c);
+
+/*
+ * In-process communicator group: `world` ranks that live in
+ * ONE process, each driven by its own host thread, on one or several GPUs.  The library's
+ * sharded code paths run unchanged on top of it -- the row-sharded search (a9: per-rank keys
+ * -> all-gather -> merge), the sharded IVF build (the training sample assembled from every
+ * rank's part), the fp8 build (global scale).  Collectives are stream-synchronous
+ * device-to-device copies between the ranks' buffers under a group barrier, so every rank of
+ * the group must make the same sequence of sharded calls concurrently (from its own thread);
+ * a rank missing for 300 s makes the waiting ranks fail with SA_ERR_STATE instead of hanging.
+ * (NCCL refuses two ranks on one device; this transport is how one GPU exercises the sharded
+ * branch, and it serves single-process multi-GPU drivers.)
+ *   sa_comm_group_create: world in [1, 1024].  The group outlives its communicators:
+ *                         sa_comm_group_free returns SA_ERR_STATE while any is alive.
+ *   sa_comm_init_local:   the communicator of `rank` in group `g` on CUDA device
+ *                         `cuda_device`; owned by the caller (sa_comm_free).
+ */
+typedef struct sa_comm_group sa_comm_group;
+sa_status sa_comm_group_create(int32_t world, sa_comm_group** out);
+sa_status sa_comm_group_free(sa_comm_group* g);
+sa_status sa_comm_init_local(sa_comm_group* g, int32_t rank, int32_t cuda_device, sa_comm** out);
+
+/*
+ * Cross-rank argument check (SURVEY.md §8(b) "Errors").  When on, every sharded sa_search /
+ * sa_search_ex / sa_search_host / sa_search_fp8 first all-gathers a fixed-size header of its
+ * arguments (nq, k, nprobe, qdtype, n_cand) and its local validation status; if any rank
+ * failed validation or passed different arguments, EVERY rank returns SA_ERR_INVALID_ARG
+ * (outputs untouched) instead of some ranks waiting in a collective the others never enter.
+ * Costs one small all-gather and a host synchronisation per call; off by default.
+ * All ranks must set the same value.
+ */
+sa_status sa_comm_set_checks(sa_comm* c, int32_t on);
+/* rank / world of this communicator; nccl_nranks = ncclCommCount for an NCCL communicator
+ * (world for the in-process transport).  Any output pointer may be NULL. */
+sa_status sa_comm_info(const sa_comm* c, int32_t* rank, int32_t* world, int32_t* nccl_nranks);
 
 const char* sa_status_string(sa_status s);
 const char* sa_last_error(void);

@@ -95,6 +95,11 @@ def lib() -> ctypes.CDLL:
         "sa_comm_unique_id": (st, [P]),
         "sa_comm_init": (st, [P, i32, i32, i32, ctypes.POINTER(P)]),
         "sa_comm_free": (st, [P]),
+        "sa_comm_group_create": (st, [i32, ctypes.POINTER(P)]),
+        "sa_comm_group_free": (st, [P]),
+        "sa_comm_init_local": (st, [P, i32, i32, ctypes.POINTER(P)]),
+        "sa_comm_set_checks": (st, [P, i32]),
+        "sa_comm_info": (st, [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]),
         "sa_status_string": (ctypes.c_char_p, [ctypes.c_int]),
         "sa_last_error": (ctypes.c_char_p, []),
         "sa_index_info": (st, [P, ctypes.POINTER(i64), ctypes.POINTER(i32), ctypes.POINTER(i32),
@@ -180,10 +185,37 @@ def _dtype_code(t: torch.Tensor) -> int:
 
 # ----------------------------------------------------------------- comm
 class Comm:
-    """NCCL communicator for a row-sharded index; unique id exchanged via torch.distributed."""
+    """Communicator of a row-sharded index: NCCL (one process per GPU; unique id exchanged
+    via torch.distributed) or a rank of an in-process group (local_group)."""
 
-    def __init__(self, handle, rank, world):
+    def __init__(self, handle, rank, world, group=None):
         self.handle, self.rank, self.world = handle, rank, world
+        self._group = group
+
+    @classmethod
+    def local_group(cls, world: int, devices=None):
+        """sa_comm_group_create + sa_comm_init_local: `world` in-process ranks (each must be
+        driven from its own thread) on `devices` (default: the current device for all)."""
+        g = ctypes.c_void_p()
+        _check(lib().sa_comm_group_create(world, ctypes.byref(g)))
+        grp = _LocalGroup(g, world)
+        comms = []
+        for r in range(world):
+            dev = torch.cuda.current_device() if devices is None else devices[r]
+            h = ctypes.c_void_p()
+            _check(lib().sa_comm_init_local(g, r, dev, ctypes.byref(h)))
+            comms.append(cls(h, r, world, grp))
+        return comms
+
+    def set_checks(self, on: bool = True):
+        """sa_comm_set_checks: cross-rank argument check before every sharded search."""
+        _check(lib().sa_comm_set_checks(self.handle, 1 if on else 0))
+        return self
+
+    def info(self):
+        r, w, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().sa_comm_info(self.handle, ctypes.byref(r), ctypes.byref(w), ctypes.byref(n)))
+        return dict(rank=r.value, world=w.value, nccl_nranks=n.value)
 
     @staticmethod
     def exchange_unique_id() -> bytes:
@@ -213,6 +245,21 @@ class Comm:
     def free(self):
         if self.handle:
             lib().sa_comm_free(self.handle)
+            self.handle = None
+            if self._group is not None:
+                self._group.release()
+
+
+class _LocalGroup:
+    """sa_comm_group handle, freed with its last communicator."""
+
+    def __init__(self, handle, members):
+        self.handle, self.members = handle, members
+
+    def release(self):
+        self.members -= 1
+        if self.members == 0 and self.handle:
+            _check(lib().sa_comm_group_free(self.handle))
             self.handle = None
 
 

@@ -144,18 +144,28 @@ sa_status sa_index_build_fp8(sa_index* idx, void* stream) {
 sa_status sa_search_fp8(const sa_index* idx, const void* queries, sa_dtype qdtype, int64_t nq,
                         int32_t k, int32_t nprobe, int32_t n_cand, int64_t* out_ids,
                         float* out_scores, void* stream) {
-  if (!idx || !queries || !out_ids || !out_scores)
-    return set_error(SA_ERR_INVALID_ARG, "null pointer");
-  if (!idx->X8) return set_error(SA_ERR_STATE, "no fp8 copy: call sa_index_build_fp8");
-  if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
-  if (nq < 1 || nq > (1ll << 31) / 2) return set_error(SA_ERR_INVALID_ARG, "bad nq");
-  if (k < 1 || n_cand < k || n_cand > F8_MAX_CAND)
-    return set_error(SA_ERR_INVALID_ARG, "need 1 <= k <= n_cand <= 256");
-  if (nprobe < 0 || nprobe > idx->nlist)
-    return set_error(nprobe > 0 && idx->nlist == 0 ? SA_ERR_STATE : SA_ERR_INVALID_ARG,
-                     "need 0 <= nprobe <= nlist");
+  if (!idx) return set_error(SA_ERR_INVALID_ARG, "null index");
+  sa_status st = SA_OK;
+  if (!queries || !out_ids || !out_scores)
+    st = set_error(SA_ERR_INVALID_ARG, "null pointer");
+  else if (!idx->X8)
+    st = set_error(SA_ERR_STATE, "no fp8 copy: call sa_index_build_fp8");
+  else if (qdtype != SA_BF16 && qdtype != SA_F32)
+    st = set_error(SA_ERR_INVALID_ARG, "bad qdtype");
+  else if (nq < 1 || nq > (1ll << 31) / 2)
+    st = set_error(SA_ERR_INVALID_ARG, "bad nq");
+  else if (k < 1 || n_cand < k || n_cand > F8_MAX_CAND)
+    st = set_error(SA_ERR_INVALID_ARG, "need 1 <= k <= n_cand <= 256");
+  else if (nprobe < 0 || nprobe > idx->nlist)
+    st = set_error(nprobe > 0 && idx->nlist == 0 ? SA_ERR_STATE : SA_ERR_INVALID_ARG,
+                   "need 0 <= nprobe <= nlist");
   cudaStream_t s = (cudaStream_t)stream;
   const bool sharded = idx->comm && idx->comm->world > 1;
+  if (sharded) {
+    const int64_t args[kCommArgs] = {0x5a58, nq, k, nprobe, (int64_t)qdtype, n_cand};
+    st = comm_check_args(idx->comm, args, st, s);
+  }
+  if (st != SA_OK) return st;
   if (!sharded) {
     SearchOut out;
     out.ids = out_ids;
@@ -163,7 +173,7 @@ sa_status sa_search_fp8(const sa_index* idx, const void* queries, sa_dtype qdtyp
     return fp8_search_local(idx, queries, qdtype, nq, k, nprobe, n_cand, out, s);
   }
   uint64_t* keys_local = nullptr;
-  sa_status st = dalloc(&keys_local, (size_t)nq * k, s, "alloc local keys");
+  st = dalloc(&keys_local, (size_t)nq * k, s, "alloc local keys");
   if (st == SA_OK) {
     SearchOut out;
     out.keys = keys_local;

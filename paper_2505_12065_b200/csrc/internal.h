@@ -12,9 +12,12 @@
 
 #include "../../include/sa.h"
 
+struct sa_comm_group;   // in-process rank group (comm.cu)
 struct sa_comm {
-  void* nccl = nullptr;  // ncclComm_t
+  void* nccl = nullptr;            // ncclComm_t (NCCL transport)
+  sa_comm_group* group = nullptr;  // in-process transport (sa_comm_init_local)
   int32_t rank = 0, world = 1, device = 0;
+  bool check_args = false;         // sa_comm_set_checks: cross-rank argument check
 };
 
 // One captured search (sa_search_host fast path): H2D from a pinned staging buffer, the whole
@@ -84,18 +87,26 @@ struct sa_index {
 namespace sa {
 
 sa_status set_error(sa_status s, const std::string& msg);
+// getenv for timing-experiment switches; always NULL unless built with -DSA_TUNING_BUILD
+const char* tuning_env(const char* name);
 sa_status cuda_status(cudaError_t e, const char* what);
 
 // TMA descriptor for a row-major bf16 [rows, cols] matrix with box [box_rows, 64 cols], SW128.
 sa_status make_tmap_bf16(CUtensorMap* m, const void* base, int64_t rows, int32_t cols,
                          int32_t box_rows);
 
-// NCCL: every rank r contributes bytes [off[r], off[r]+len[r]) of buf; all ranks end with all.
+// Collectives (comm.cu; NCCL or the in-process group): every rank r contributes bytes [off[r], off[r]+len[r]) of buf; all ranks end with all.
 sa_status comm_broadcast_parts(const sa_comm* c, void* buf, const int64_t* off, const int64_t* len,
                                cudaStream_t s);
-// NCCL all-gather of `bytes` per rank: recv holds world * bytes, rank-major
+// all-gather of `bytes` per rank: recv holds world * bytes, rank-major
 sa_status comm_allgather_bytes(const sa_comm* c, const void* send, void* recv, size_t bytes,
                                cudaStream_t s);
+// Cross-rank argument check before a sharded call (sa_comm_set_checks; a no-op when off):
+// every rank all-gathers its kCommArgs arguments and its local validation status; any failure
+// or mismatch -> SA_ERR_INVALID_ARG on every rank (no rank left waiting in a collective).
+constexpr int kCommArgs = 6;
+sa_status comm_check_args(const sa_comm* c, const int64_t (&args)[kCommArgs], sa_status local,
+                          cudaStream_t s);
 // balanced contiguous split
 inline void shard_range(int64_t n, int world, int rank, int64_t* off, int64_t* len) {
   const int64_t base = n / world, rem = n % world;

@@ -8,8 +8,7 @@
 //     corpus = the bf16 centroids, k = 1 (ties -> lowest list id, R8);
 //   * the probe (a7): queries x centroids, k = nprobe (ties -> lowest id, R11);
 //   * the list scan (a8): ivf_scan.cu (list rows on the MMA M side, the probing
-//     queries of a list on N); SA_IVF_LEGACY=1 selects the flat kernel's older
-//     list-major mode (queries on M) for comparison.
+//     queries of a list on N).
 // The rest (sample gather, stable sort by list, deterministic centroid update,
 // empty-list repair, probe inversion) is SIMT glue in ivf_kernels.cu.
 #include <algorithm>
@@ -311,13 +310,6 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   want = (want + FS_BN - 1) / FS_BN * FS_BN;
   const int chunk_rows = (int)std::min<int64_t>(kChunkRows, std::max<int64_t>(kChunkRowsSmall, want));
   const int64_t max_chunks = std::max<int64_t>(1, (idx->max_list + chunk_rows - 1) / chunk_rows);
-  static const bool legacy_env = [] {
-    const char* e = getenv("SA_IVF_LEGACY");
-    return e && e[0] == '1';
-  }();
-  const bool legacy = legacy_env && Q8 == nullptr;
-  const int qblock = legacy ? FS_BM : IVS_NQ;
-  const int parts = legacy ? FS_LISTS_PER_ITEM : IVS_PARTS;
   IvfSearchScratch w{};
   SA_TRY(dalloc(&w.cnt, nlist, s, "ivf scratch"));
   f.add(w.cnt);
@@ -342,28 +334,27 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   SA_TRY(dalloc(&w.scratch, std::max<int64_t>(nlist, np) / 1024 + 4, s, "ivf scratch"));
   f.add(w.scratch);
   if (np <= kInvertSmallMax) {
-    SA_CUDA(launch_invert_small(probes, (int)nq, nprobe, idx->list_off, chunk_rows, qblock, w, s),
+    SA_CUDA(launch_invert_small(probes, (int)nq, nprobe, idx->list_off, chunk_rows, IVS_NQ, w, s),
             "probe inversion");
   } else {
-    SA_CUDA(launch_probe_invert(probes, nq, nprobe, nlist, idx->list_off, chunk_rows, qblock, w, sms, s),
+    SA_CUDA(launch_probe_invert(probes, nq, nprobe, nlist, idx->list_off, chunk_rows, IVS_NQ, w, sms, s),
             "probe inversion");
   }
 
   // ---- a8: list-major scan on the tensor cores
   const size_t max_slots = (size_t)np * max_chunks;
   uint64_t *part, *heap = nullptr;
-  SA_TRY(dalloc(&part, max_slots * parts * k, s, "ivf partials"));
+  SA_TRY(dalloc(&part, max_slots * IVS_PARTS * k, s, "ivf partials"));
   f.add(part);
-  if (k > (legacy ? FS_KSMEM : IVS_KSMEM)) {
-    SA_TRY(dalloc(&heap, (size_t)sms * k * (legacy ? FS_EPI_THREADS : IVS_HEAPS), s, "ivf heaps"));
+  if (k > IVS_KSMEM) {
+    SA_TRY(dalloc(&heap, (size_t)sms * k * IVS_HEAPS, s, "ivf heaps"));
     f.add(heap);
   }
   uint32_t* hint;   // [nq] pruning bounds + [1] dynamic item counter
   SA_TRY(dalloc(&hint, nq + 1, s, "ivf hints"));
   f.add(hint);
   SA_CUDA(cudaMemsetAsync(hint, 0, sizeof(uint32_t) * (nq + 1), s), "memset hints");
-  cudaError_t e;
-  if (!legacy) {
+  {
     IvfScanArgs v{};
     v.Q = Q8 ? reinterpret_cast<const __nv_bfloat16*>(Q8) : Qs;
     v.d_pad = Q8 ? idx->d8_pad / 2 : idx->d_pad;
@@ -382,36 +373,9 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
     v.q_hint = hint;
     v.item_counter = reinterpret_cast<int32_t*>(hint + nq);
     ProfRegion prof_region(SA_KERNEL_IVF_SCAN, s);
-    e = Q8 ? launch_ivf_scan(idx->tmap_x8, idx->tmap_x8t, v, sms, s)
-           : launch_ivf_scan(idx->tmap_x, idx->tmap_xt, v, sms, s);
-    SA_CUDA(e, "ivf scan");
-  } else {
-  CUtensorMap tmap_q;
-  SA_TRY(make_tmap_bf16(&tmap_q, Qs, nq, idx->d_pad, FS_BM));
-  FlatScanArgs a{};
-  a.Q = Qs;
-  a.nq = nq;
-  a.nq_pad = nq;
-  a.d_pad = idx->d_pad;
-  a.n_rows = idx->n_local;
-  a.k = k;
-  a.row_ids = idx->row_ids;
-  a.id_base = 0;
-  a.part = part;
-  a.heap_g = heap;
-  a.mode = FS_MODE_IVF;
-  a.items = w.items;
-  a.n_items = w.n_items;
-  a.list_off = idx->list_off;
-  a.lq_ent = w.lq_ent;
-  a.q_slot = w.q_slot;
-  a.nprobe = nprobe;
-  a.chunk_rows = chunk_rows;
-  a.q_hint = hint;
-  a.item_counter = reinterpret_cast<int32_t*>(hint + nq);
-  ProfRegion prof_region(SA_KERNEL_IVF_SCAN, s);
-  e = launch_flat_scan(idx->tmap_x, idx->tmap_xt, tmap_q, a, 1, sms, s);
-  SA_CUDA(e, "ivf scan");
+    SA_CUDA(Q8 ? launch_ivf_scan(idx->tmap_x8, idx->tmap_x8t, v, sms, s)
+               : launch_ivf_scan(idx->tmap_x, idx->tmap_xt, v, sms, s),
+            "ivf scan");
   }
 
   MergeArgs m{};
@@ -419,13 +383,12 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   m.k = k;
   m.slot_off = w.q_slot;
   m.slot_stride = nprobe;
-  m.slot_keys = parts * k;
+  m.slot_keys = IVS_PARTS * k;
   m.out_keys = out.keys;
   m.out_ids = out.ids;
   m.out_scores = out.scores;
   ProfRegion prof_region(SA_KERNEL_MERGE, s);
-  e = launch_merge(m, nq, s);
-  return cuda_status(e, "ivf merge");
+  return cuda_status(launch_merge(m, nq, s), "ivf merge");
 }
 
 }  // namespace sa

@@ -28,12 +28,7 @@
 //     warp 9: TMEM alloc + MMA issuer (leader CTA).
 //   * persistent grid: work item = (query group, corpus slice); partial
 //     lists go to part[q][slice][half][k] and are merged by merge.cu.
-//   * FS_MODE_IVF (list-major IVF scan, §8(a) a8): work item = (inverted
-//     list, block of <= 128 queries that probe it, row chunk).  The query
-//     rows are gathered into the A operand per item, the list's rows stream
-//     through the same TMA ring, and each (query, item) writes its partial
-//     list to the query's own output slot -- one read of a list serves every
-//     query that probes it.
+//   (The IVF list scan, §8(a) a8, has its own kernel: ivf_scan.cu.)
 #include <cuda_bf16.h>
 
 #include "flat_scan.cuh"
@@ -57,8 +52,6 @@ constexpr int kKbPerStage = 2;
 // vs 8; 2 gives 32.3 GB but no faster)
 constexpr int kLockstepLag = 4;
 constexpr int kLockstepSpinCap = 1 << 14;   // sleeps of one lockstep wait before pacing stops
-constexpr int kTailRows = FS_TAIL_ROWS;     // box rows of the tail tensor map (IVF list tails)
-constexpr int kItemQ = 4;                   // depth of the dynamic work-item queue
 
 template <int CG, bool F8 = false>
 struct Cfg {
@@ -78,9 +71,6 @@ struct __align__(8) SmemTail {
   uint64_t tmem_empty[2];
   uint64_t a_full;
   uint64_t a_tma;
-  uint64_t iq_full[kItemQ];   // dynamic work queue (IVF): producer -> MMA + epilogue warps
-  uint64_t iq_empty[kItemQ];
-  int32_t iq_w[kItemQ];
   uint32_t tmem_base;
 };
 
@@ -112,61 +102,21 @@ __device__ __noinline__ float heap_offer(uint64_t* h, int k, uint64_t key) {
   return heap_threshold(h[0]);
 }
 
-// One unit of work for all three roles (producer, MMA, epilogue decode it identically).
+// One unit of work (query group, corpus slice); producer, MMA and epilogue decode it
+// identically.  Pure arithmetic on the item index, so it is warp-uniform by construction.
 struct WorkItem {
-  int qkey;          // query-block identity (flat: query group); -1 = always reload (ivf)
-  int s;             // flat: corpus slice
+  int qkey;          // query group
+  int s;             // corpus slice
   int32_t t0, t1;    // tile range
-  int32_t row_base;  // first corpus row of tile 0 (rows < 2^31: n_local limit)
-  int32_t row_end;   // rows >= row_end are masked (list end / corpus end)
-  int chunk;         // ivf: chunk index within the list
-  int e0, cnt;       // ivf: probing queries lq_ent[e0, e0 + cnt)
 };
 
 __device__ __forceinline__ WorkItem work_item(int w, const FlatScanArgs& a, int32_t T) {
   WorkItem wi;
-  if (a.mode == FS_MODE_IVF) {
-    const int4 it = a.items[w];
-    const int32_t lo = (int32_t)a.list_off[it.x], hi = (int32_t)a.list_off[it.x + 1];
-    const int32_t r0 = lo + it.z * a.chunk_rows;
-    const int32_t r1 = hi < r0 + a.chunk_rows ? hi : r0 + a.chunk_rows;
-    wi.qkey = -1;
-    wi.s = 0;
-    wi.t0 = 0;
-    wi.t1 = (r1 - r0 + FS_BN - 1) / FS_BN;
-    wi.row_base = r0;
-    wi.row_end = r1;
-    wi.chunk = it.z;
-    wi.e0 = it.y;   // probers of this item: lq_ent[e0, e0 + cnt), cnt <= FS_BM
-    wi.cnt = it.w;
-  } else {
-    wi.qkey = w / a.S;
-    wi.s = w % a.S;
-    wi.t0 = (int32_t)((int64_t)wi.s * T / a.S);
-    wi.t1 = (int32_t)((int64_t)(wi.s + 1) * T / a.S);
-    wi.row_base = 0;
-    wi.row_end = (int32_t)a.n_rows;
-    wi.chunk = 0;
-    wi.e0 = 0;
-    wi.cnt = 0;
-  }
+  wi.qkey = w / a.S;
+  wi.s = w % a.S;
+  wi.t0 = (int32_t)((int64_t)wi.s * T / a.S);
+  wi.t1 = (int32_t)((int64_t)(wi.s + 1) * T / a.S);
   return wi;
-}
-
-// Warp-uniform copy of a work item (whole warp must call): values loaded from memory
-// (IVF items) are broadcast from lane 0 so the MMA loop stays provably uniform.
-__device__ __forceinline__ WorkItem uniform_item(const WorkItem& w) {
-  WorkItem u;
-  u.qkey = __shfl_sync(0xffffffffu, w.qkey, 0);
-  u.s = __shfl_sync(0xffffffffu, w.s, 0);
-  u.t0 = __shfl_sync(0xffffffffu, w.t0, 0);
-  u.t1 = __shfl_sync(0xffffffffu, w.t1, 0);
-  u.row_base = __shfl_sync(0xffffffffu, w.row_base, 0);
-  u.row_end = __shfl_sync(0xffffffffu, w.row_end, 0);
-  u.chunk = __shfl_sync(0xffffffffu, w.chunk, 0);
-  u.e0 = __shfl_sync(0xffffffffu, w.e0, 0);
-  u.cnt = __shfl_sync(0xffffffffu, w.cnt, 0);
-  return u;
 }
 
 }  // namespace
@@ -174,7 +124,6 @@ __device__ __forceinline__ WorkItem uniform_item(const WorkItem& w) {
 template <int CG, bool F8, bool DUMP>
 __global__ void __launch_bounds__(FS_THREADS, 1)
 flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
-                      const __grid_constant__ CUtensorMap tmap_tail,
                       const __grid_constant__ CUtensorMap tmap_q, const FlatScanArgs a) {
   using C = Cfg<CG, F8>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -201,21 +150,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
   const int unit = blockIdx.x / CG;        // CTA (CG=1) or CTA pair (CG=2)
   const int n_units = gridDim.x / CG;
   const int S = a.S;
-  const bool ivf = a.mode == FS_MODE_IVF;
-  const int n_work = ivf ? *a.n_items : a.QP * S;
-  // IVF items differ in size (list lengths): hand them out dynamically from a global counter
-  // (the producer fetches, the MMA warp and the epilogue warps follow through a small smem
-  // queue) instead of a static round robin whose slowest CTA sets the kernel time.
-  const bool dyn = ivf && CG == 1 && a.item_counter != nullptr;
-  // consumer side of the queue: item #i of this CTA (-1 = no more work)
-  auto take_item = [&](int i, bool arrive_lane) __attribute__((always_inline)) -> int {
-    const int slot = i % kItemQ;
-    ptx::mbar_wait(ptx::smem_u32(&tail->iq_full[slot]), (uint32_t)((i / kItemQ) & 1));
-    const int w = *reinterpret_cast<volatile int32_t*>(&tail->iq_w[slot]);
-    __syncwarp();
-    if (arrive_lane) ptx::mbar_arrive(ptx::smem_u32(&tail->iq_empty[slot]));
-    return w;
-  };
+  const int n_work = a.QP * S;
   const int32_t T = (int32_t)((a.n_rows + kBN - 1) / kBN);
   const int num_kb = a.d_pad / kBK;
   const int nacc = 2;
@@ -234,10 +169,6 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     }
     ptx::mbar_init(ptx::smem_u32(&tail->a_full), FS_EPI_WARPS * CG);
     ptx::mbar_init(ptx::smem_u32(&tail->a_tma), 1);
-    for (int i = 0; i < kItemQ; ++i) {
-      ptx::mbar_init(ptx::smem_u32(&tail->iq_full[i]), 1);
-      ptx::mbar_init(ptx::smem_u32(&tail->iq_empty[i]), 1 + FS_EPI_WARPS);
-    }
     ptx::fence_mbar_init();
     ptx::fence_proxy_async_smem();
   }
@@ -278,19 +209,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       bool lockstep = a.progress != nullptr && leader;
       const bool publish = lockstep;
       const int lag = a.lockstep_lag > 0 ? a.lockstep_lag : kLockstepLag;
-      int fetched = 0;
-      auto next_w = [&](int w_prev) -> int {
-        if (!dyn) return w_prev < 0 ? unit : w_prev + n_units;
-        const int slot = fetched % kItemQ;
-        ptx::mbar_wait(ptx::smem_u32(&tail->iq_empty[slot]), (uint32_t)(((fetched / kItemQ) & 1) ^ 1));
-        int w = atomicAdd(a.item_counter, 1);
-        if (w >= n_work) w = -1;
-        *reinterpret_cast<volatile int32_t*>(&tail->iq_w[slot]) = w;
-        ptx::mbar_arrive(ptx::smem_u32(&tail->iq_full[slot]));
-        ++fetched;
-        return w;
-      };
-      for (int w = next_w(-1); w >= 0 && w < n_work; w = next_w(w)) {
+      for (int w = unit; w < n_work; w += n_units) {
         const WorkItem wi = work_item(w, a, T);
         for (int32_t t = wi.t0; t < wi.t1; ++t) {
           if (publish) {
@@ -311,7 +230,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
               }
             }
           }
-          const int32_t row = wi.row_base + t * kBN + (int32_t)rank * C::kRowsPerCta;
+          const int32_t row = t * kBN + (int32_t)rank * C::kRowsPerCta;
           for (int sl = 0; sl < n_sl; ++sl) {
             const int kb0 = sl * kKbPerStage;
             const int nkb = num_kb - kb0 < kKbPerStage ? num_kb - kb0 : kKbPerStage;
@@ -319,22 +238,9 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const uint32_t dst = ptx::smem_u32(stage_base + stage * C::kStageBytes);
             const uint32_t fb = full0 + stage * 8;
             if (CG == 1) {
-              const int32_t left = wi.row_end - row;
-              if (ivf && left < kBN) {
-                // last tile of an IVF chunk: fetch only ceil(left/32) 32-row boxes instead of
-                // the full 128 rows (the rest of the stage is stale and masked by row_end);
-                // a list's tail otherwise drags in up to 127 rows of the next list
-                const int nbox = (left + kTailRows - 1) / kTailRows;
-                ptx::mbar_arrive_expect_tx(fb, nkb * nbox * kTailRows * kBK * 2);
-                for (int j = 0; j < nkb; ++j)
-                  for (int bx = 0; bx < nbox; ++bx)
-                    ptx::tma_load_2d(dst + j * C::kBoxBytes + bx * kTailRows * kBK * 2, &tmap_tail,
-                                     fb, (kb0 + j) * kBK, row + bx * kTailRows);
-              } else {
-                ptx::mbar_arrive_expect_tx(fb, nkb * C::kBoxBytes);
-                for (int j = 0; j < nkb; ++j)
-                  ptx::tma_load_2d(dst + j * C::kBoxBytes, &tmap_x, fb, (kb0 + j) * kBK, row);
-              }
+              ptx::mbar_arrive_expect_tx(fb, nkb * C::kBoxBytes);
+              for (int j = 0; j < nkb; ++j)
+                ptx::tma_load_2d(dst + j * C::kBoxBytes, &tmap_x, fb, (kb0 + j) * kBK, row);
             } else {
               if (leader) ptx::mbar_arrive_expect_tx(fb, 2 * nkb * C::kBoxBytes);
               const uint32_t fbl = ptx::mapa(fb, 0);
@@ -367,12 +273,9 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       const uint64_t adesc0 = ptx::umma_desc_sw128(ptx::smem_u32(a_smem));
       const uint32_t full0 = ptx::smem_u32(&tail->full[0]);
       const uint32_t empty0 = ptx::smem_u32(&tail->empty[0]);
-      int taken = 0;
-      int w = dyn ? __shfl_sync(0xffffffffu, take_item(taken++, lane == 0), 0) : unit;
-      for (; w >= 0 && w < n_work_u;
-           w = dyn ? __shfl_sync(0xffffffffu, take_item(taken++, lane == 0), 0) : w + n_units) {
-        const WorkItem wi = uniform_item(work_item(w, a, T));
-        if (wi.qkey < 0 || wi.qkey != cur_qp) {
+      for (int w = unit; w < n_work_u; w += n_units) {
+        const WorkItem wi = work_item(w, a, T);
+        if (wi.qkey != cur_qp) {
           ptx::mbar_wait(ptx::smem_u32(&tail->a_full), a_phase);
           a_phase ^= 1;
           cur_qp = wi.qkey;
@@ -448,78 +351,41 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     float thr = heap_threshold(0ull);
     int acc = 0;
     uint32_t acc_phase = 0;
-    int cur_qp = -1;
     uint32_t a_tma_phase = 0;
     const uint32_t a_full_leader = CG == 2 ? ptx::mapa(ptx::smem_u32(&tail->a_full), 0)
                                            : ptx::smem_u32(&tail->a_full);
     const uint32_t tmem_empty0 = CG == 2 ? ptx::mapa(ptx::smem_u32(&tail->tmem_empty[0]), 0)
                                          : ptx::smem_u32(&tail->tmem_empty[0]);
-    // This thread's query in a work item: flat -> row of the staged batch; ivf -> gathered
-    // prober (query id, probe rank).
-    struct QSel {
-      int64_t q;
-      int j;
-      bool valid;
-    };
-    auto qsel = [&](const WorkItem& wi) __attribute__((always_inline)) -> QSel {
-      QSel r{0, 0, false};
-      if (ivf) {
-        // Prober i of the item sits on TMEM lane (i % 4) * 32 + i / 4: an item usually has
-        // only a few probers, and this spreads them over the four lane quadrants, i.e. over
-        // four different warps / SM sub-partitions, instead of piling them onto one warp.
-        const int i = lane * 4 + quad;
-        r.valid = i < wi.cnt;
-        if (r.valid) {
-          const int2 e = a.lq_ent[wi.e0 + i];
-          r.q = e.x;
-          r.j = e.y;
-        }
-      } else {
-        r.q = ((int64_t)wi.qkey * CG + rank) * kBM + rib;
-        r.valid = r.q < a.nq;
-      }
-      return r;
-    };
-    // Stage item wi's query block into the A operand (TMEM K-blocks + smem K-blocks) and
+    // Stage query group `qkey`'s block into the A operand (TMEM K-blocks + smem K-blocks) and
     // arrive on a_full.  Callers guarantee every MMA that read the previous block has
     // completed (they consumed that block's last tmem_full).
-    auto stage_a = [&](const WorkItem& wi, const QSel& qs) __attribute__((always_inline)) {
-      const bool tma_thread = (!ivf && ew == 0 && lane == 0 && kb_s > 0);
+    auto stage_a = [&](int qkey) __attribute__((always_inline)) {
+      const int64_t q_row = ((int64_t)qkey * CG + rank) * kBM + rib;
+      const bool q_ok = q_row < a.nq;
+      const bool tma_thread = ew == 0 && lane == 0 && kb_s > 0;
       if (tma_thread) {
         // K-blocks [kb_t, num_kb) of this CTA's 128 query rows -> smem (SS operand)
         const uint32_t bar = ptx::smem_u32(&tail->a_tma);
         ptx::mbar_arrive_expect_tx(bar, (uint32_t)(kb_s * kASmemKb));
-        const int32_t qrow0 = (int32_t)(((int64_t)wi.qkey * CG + rank) * kBM);
+        const int32_t qrow0 = (int32_t)(((int64_t)qkey * CG + rank) * kBM);
         for (int j = 0; j < kb_s; ++j)
           ptx::tma_load_2d(ptx::smem_u32(a_smem + j * kASmemKb), &tmap_q, bar,
                            (kb_t + j) * kBK, qrow0);
       }
       // Rows of absent queries are left as they are: MMA output rows are independent and the
       // epilogue never reads the rows of invalid lanes, so a warp with no valid lane skips.
-      if (half == 0 && __any_sync(0xffffffffu, qs.valid)) {
-        const uint4* src = reinterpret_cast<const uint4*>(a.Q + (size_t)qs.q * a.d_pad);
+      if (half == 0 && __any_sync(0xffffffffu, q_ok)) {
+        const uint4* src = reinterpret_cast<const uint4*>(a.Q + (size_t)q_row * a.d_pad);
         for (int c = 0; c < kb_t; ++c) {
           uint32_t r[32];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            uint4 v = qs.valid ? __ldg(src + c * 8 + i) : make_uint4(0, 0, 0, 0);
+            uint4 v = q_ok ? __ldg(src + c * 8 + i) : make_uint4(0, 0, 0, 0);
             r[4 * i + 0] = v.x; r[4 * i + 1] = v.y; r[4 * i + 2] = v.z; r[4 * i + 3] = v.w;
           }
           ptx::tmem_st32(tmem + lane_addr + a_col + c * 32, r);
         }
         ptx::tmem_wait_st();
-        if (ivf && qs.valid) {
-          // smem K-blocks of a gathered row, written in the 128-byte-swizzled K-major
-          // layout the UMMA descriptor expects (16-byte chunk c of row r at c ^ (r & 7)).
-          for (int j = 0; j < kb_s; ++j) {
-            uint8_t* blk = a_smem + j * kASmemKb + (rib >> 3) * 1024 + (rib & 7) * 128;
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              *reinterpret_cast<uint4*>(blk + ((c ^ (rib & 7)) << 4)) =
-                  __ldg(src + (kb_t + j) * 8 + c);
-          }
-          ptx::fence_proxy_async_smem();
-        }
       }
       if (tma_thread) {
         ptx::mbar_wait(ptx::smem_u32(&tail->a_tma), a_tma_phase);
@@ -531,44 +397,26 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         if (CG == 2 && !leader) ptx::mbar_arrive_cluster(a_full_leader);
         else ptx::mbar_arrive(ptx::smem_u32(&tail->a_full));
       }
-      cur_qp = wi.qkey;
     };
 
-    int taken = 0;
-    int w = dyn ? take_item(taken++, lane == 0) : unit;
-    WorkItem wi{};
-    QSel cs{};
-    if (w >= 0 && w < n_work) {
-      wi = work_item(w, a, T);
-      cs = qsel(wi);
-      stage_a(wi, cs);
-    }
-    while (w >= 0 && w < n_work) {
-      // next item: static -> known now; dynamic -> taken at this item's last tile, when the
-      // producer (which runs ahead) has certainly fetched it
-      int wn = dyn ? -2 : w + n_units;
-      if (dyn && wi.t1 <= wi.t0) wn = take_item(taken++, lane == 0);
-      bool has_next = wn >= 0 && wn < n_work;
-      // The next item is decoded only when needed (at this item's last tile) to keep its
-      // state out of the registers of the tile loop.
-      WorkItem nx{};
-      QSel ns{};
-      bool nx_ready = false;
+    if (unit < n_work) stage_a(work_item(unit, a, T).qkey);
+    for (int w = unit; w < n_work; w += n_units) {
+      const WorkItem wi = work_item(w, a, T);
+      const int wn = w + n_units;
+      const bool has_next = wn < n_work;
+      // the next item's query group (decoded lazily, at this item's last tile)
+      const int64_t q = ((int64_t)wi.qkey * CG + rank) * kBM + rib;
+      const bool valid = q < a.nq;
       if (wi.t1 <= wi.t0 && has_next) {
-        nx = work_item(wn, a, T);
-        ns = qsel(nx);
-        nx_ready = true;
-        if (nx.qkey < 0 || nx.qkey != wi.qkey) stage_a(nx, ns);
+        const int nq_key = work_item(wn, a, T).qkey;
+        if (nq_key != wi.qkey) stage_a(nq_key);
       }
-      const int64_t q = cs.q;
-      const int probe_j = cs.j;
-      const bool valid = cs.valid;
-      // Exact pruning bound shared by all heaps of a query (all corpus slices / IVF items /
-      // column halves): q_hint[q] = max over published heap roots.  Each root is the k-th
-      // best score of a subset of q's candidates, so q's final k-th score is >= q_hint[q]
-      // and smaller scores can never be returned (ties pass: s >= thr).  Roots are
-      // published as they rise and the bound is re-read every 4 tiles, so every heap prunes
-      // with the best threshold any heap of the query has reached.
+      // Exact pruning bound shared by all heaps of a query (all corpus slices / column
+      // halves): q_hint[q] = max over published heap roots.  Each root is the k-th best score
+      // of a subset of q's candidates, so q's final k-th score is >= q_hint[q] and smaller
+      // scores can never be returned (ties pass: s >= thr).  Roots are published as they rise
+      // and the bound is re-read every 4 tiles, so every heap prunes with the best threshold
+      // any heap of the query has reached.
       float hint = heap_threshold(0ull);
       uint32_t published = 0u;
       if (valid && a.q_hint) {
@@ -602,23 +450,17 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         // The last accumulator of this item is in registers, so every MMA that read this
         // item's A operand has completed: stage the next item's queries now, before the
         // score processing, so the tensor core restarts as early as possible.
-        if (t == wi.t1 - 1 && wn == -2) {
-          wn = take_item(taken++, lane == 0);
-          has_next = wn >= 0 && wn < n_work;
-        }
         if (t == wi.t1 - 1 && has_next) {
-          nx = work_item(wn, a, T);
-          ns = qsel(nx);
-          nx_ready = true;
-          if (nx.qkey < 0 || nx.qkey != wi.qkey) stage_a(nx, ns);
+          const int nq_key = work_item(wn, a, T).qkey;
+          if (nq_key != wi.qkey) stage_a(nq_key);
         }
-        const int32_t row0 = wi.row_base + t * kBN + half * 64;
+        const int32_t row0 = t * kBN + half * 64;
         if constexpr (DUMP) {
           // Score dump (IVF probe, graph entry points, tests): the warp's 32 queries x 64
           // columns go through a 4 KB smem tile per 32 columns (XOR-swizzled, conflict-free)
           // so every store instruction writes one query's 32 consecutive scores (128 B)
-          // instead of 32 scattered words.  Flat work items: the lanes hold consecutive
-          // queries.  heap_s is free in this mode (no heaps).
+          // instead of 32 scattered words.  The lanes hold consecutive queries.  heap_s is
+          // free in this mode (no heaps).
           if (a.experiment == 0 && __any_sync(0xffffffffu, valid)) {
             float* tb = reinterpret_cast<float*>(heap_s) + ew * 1024;
             const int64_t qbase = q - lane;
@@ -658,7 +500,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const float s = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
             if (s >= thr) {
               const int32_t row = row0 + j;
-              if (row < wi.row_end) {
+              if (row < a.n_rows) {
                 const uint32_t id =
                     a.id_base + (a.row_ids ? (uint32_t)a.row_ids[row] : (uint32_t)row);
                 thr = fmaxf(heap_offer(heap, k, make_key(s, id)), hint);
@@ -678,9 +520,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       if constexpr (!DUMP) {
         // flush this work item's partial list and reset the heap
         if (valid) {
-          const size_t slot = ivf ? (size_t)(a.q_slot[(size_t)q * a.nprobe + probe_j] + wi.chunk)
-                                  : (size_t)q * S + wi.s;
-          uint64_t* dst = a.part + (slot * FS_LISTS_PER_ITEM + half) * k;
+          uint64_t* dst = a.part + (((size_t)q * S + wi.s) * FS_LISTS_PER_ITEM + half) * k;
           for (int i = 0; i < k; ++i) dst[i] = heap[(size_t)i * kEpiT];
           const uint64_t root = heap[0];
           if (a.q_hint && root != 0ull) atomicMax(a.q_hint + q, (uint32_t)(root >> 32));
@@ -688,17 +528,6 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
         thr = heap_threshold(0ull);
       }
-      if (wn == -2) {
-        wn = take_item(taken++, lane == 0);
-        has_next = wn >= 0 && wn < n_work;
-      }
-      if (has_next && !nx_ready) {
-        nx = work_item(wn, a, T);
-        ns = qsel(nx);
-      }
-      w = wn;
-      wi = nx;
-      cs = ns;
     }
   }
 
@@ -718,8 +547,7 @@ size_t flat_scan_smem_bytes(int cta_group) {
   return 1024 + (size_t)Cfg<1>::kStages * Cfg<1>::kStageBytes + fixed + sizeof(SmemTail<1>);
 }
 
-cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_tail,
-                             const CUtensorMap& tmap_q, const FlatScanArgs& a, int cta_group,
+cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_q, const FlatScanArgs& a, int cta_group,
                              int grid, cudaStream_t stream) {
   const size_t smem = flat_scan_smem_bytes(cta_group);
   cudaLaunchConfig_t cfg{};
@@ -737,7 +565,7 @@ cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_ta
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = ensure_max_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    e = cudaLaunchKernelEx(&cfg, kern, tmap, tmap_tail, tmap_q, a);
+    e = cudaLaunchKernelEx(&cfg, kern, tmap, tmap_q, a);
     note_launch();
     return e;
   };
@@ -748,7 +576,6 @@ cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_ta
                           : go(flat_scan_topk_kernel<1, false, true>);
   }
   if (a.fp8) {
-    if (a.mode == FS_MODE_IVF) return cudaErrorInvalidValue;  // fp8 runs the flat modes only
     return cta_group == 2 ? go(flat_scan_topk_kernel<2, true, false>)
                           : go(flat_scan_topk_kernel<1, true, false>);
   }

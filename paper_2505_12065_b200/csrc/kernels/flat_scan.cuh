@@ -20,7 +20,8 @@ constexpr int FS_KB_SMEM = 4;    // K-blocks of the A operand held in smem (64 K
 constexpr int FS_KSMEM = 16;     // running heaps in smem for k <= 16, else in global scratch
 constexpr int FS_KSMEM_BIG = 48; // ... or k <= 48 when the A operand fits TMEM (d_pad <= 512):
                                  // the heaps then also take the unused 64 KB A region
-constexpr int FS_TAIL_ROWS = 32;  // box rows of the tail tensor map (IVF list tails)
+constexpr int FS_TAIL_ROWS = 32;  // box rows of the index's tail tensor map (IVF list tails,
+                                  // ivf_scan.cu)
 constexpr int FS_LISTS_PER_ITEM = 2;  // partial lists per (query, work item): one per column half
 
 // largest k whose running heaps stay in shared memory for this d_pad
@@ -29,9 +30,8 @@ inline int fs_heap_smem_cap(int32_t d_pad) {
 }
 
 enum FlatScanMode : int32_t {
-  FS_MODE_TOPK = 0,   // flat: work item = (query group, corpus slice)
-  FS_MODE_DEBUG = 1,  // flat, raw score dump (tests)
-  FS_MODE_IVF = 2,    // grouped: work item = (inverted list, block of <=128 probing queries, chunk)
+  FS_MODE_TOPK = 0,   // work item = (query group, corpus slice), running top-k
+  FS_MODE_DEBUG = 1,  // raw score dump (IVF probe, graph entry points, tests)
 };
 
 struct FlatScanArgs {
@@ -45,32 +45,22 @@ struct FlatScanArgs {
   int32_t k;               // 1..256
   const int32_t* row_ids;  // optional row -> id map (nullptr: id = row)
   uint32_t id_base;        // added to the id stored in each key
-  uint64_t* part;          // flat out: [nq_pad][S][FS_LISTS_PER_ITEM][k] packed keys (unordered)
-                           // ivf out:  [slot][FS_LISTS_PER_ITEM][k]
+  uint64_t* part;          // out: [nq_pad][S][FS_LISTS_PER_ITEM][k] packed keys (unordered)
   uint64_t* heap_g;        // scratch [grid][k][FS_EPI_THREADS] when k > FS_KSMEM
   float* dbg;              // debug: [nq_pad][n_rows] raw scores
   int32_t mode;            // FlatScanMode
-  // ---- FS_MODE_IVF (cta_group 1 only)
-  const int4* items;       // [*n_items] {list, first prober in lq_ent, chunk, prober count}
-  const int32_t* n_items;  // device scalar
-  const int64_t* list_off; // [nlist + 1] stored-row range of each list
-  const int2* lq_ent;      // (query, probe rank) pairs grouped by list
-  const int64_t* q_slot;   // [nq * nprobe] first output slot of (query, probe rank)
-  int32_t nprobe;
-  int32_t chunk_rows;      // rows per IVF work item (multiple of FS_BN)
   uint32_t* q_hint;        // optional [nq] ordered-fp32 lower bound of each query's k-th score
                            // (zero-initialised by the caller; 0 = none)
-  int32_t* item_counter;   // IVF: zeroed global counter -> dynamic item scheduling (or nullptr)
-  int32_t* progress;       // optional [units] tile progress for soft lockstep (zeroed; flat
-                           // mode with one work item per unit and QP > 1)
-  int32_t experiment;      // timing experiments only (env SA_EXPERIMENT): 1 = skip score
+  int32_t* progress;       // optional [units] tile progress for soft lockstep (zeroed; one
+                           // work item per unit and QP > 1)
+  int32_t experiment;      // timing experiments only (tuning builds, SA_EXPERIMENT): 1 = skip score
                            // processing, 2 = also skip the TMEM loads, 3 = the 64-way max
                            // only (no insertion).  0 in production.
   int32_t lockstep_lag;    // tiles a unit may run ahead of the units sharing its slice (0 = 4)
   int32_t fp8;             // 1: Q and the corpus are e4m3 bytes (kind::f8f6f4 MMAs), passed
                            // as 16-bit pairs -- d_pad counts PAIRS of e4m3 values (bytes / 2),
                            // so TMA boxes, swizzle, descriptors and TMEM columns are the bf16
-                           // ones byte for byte.  Flat modes only.
+                           // ones byte for byte.
 };
 
 // cta_group = 1: one CTA per query block of 128 (M=128, box 128 rows).
@@ -78,9 +68,7 @@ struct FlatScanArgs {
 size_t flat_scan_smem_bytes(int cta_group);
 // tmap: corpus rows (box 128 rows for cta_group 1, 64 for 2); tmap_q: the staged queries
 // (box 128 rows, rows = nq), used for the K-blocks of the A operand that live in smem.
-// tmap_tail: the corpus with FS_TAIL_ROWS-row boxes (IVF tails, cta_group 1; else unused).
-cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_tail,
-                             const CUtensorMap& tmap_q, const FlatScanArgs& a, int cta_group,
-                             int grid, cudaStream_t stream);
+cudaError_t launch_flat_scan(const CUtensorMap& tmap, const CUtensorMap& tmap_q,
+                             const FlatScanArgs& a, int cta_group, int grid, cudaStream_t stream);
 
 }  // namespace sa

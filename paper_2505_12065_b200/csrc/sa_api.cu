@@ -3,7 +3,6 @@
 // library's kernels; there is no host or library fallback.
 #include <cudaTypedefs.h>
 #include <dlfcn.h>
-#include <nccl.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -155,6 +154,20 @@ cudaError_t ensure_max_smem(const void* func, size_t bytes) {
   return e;
 }
 
+// ====================================================================== tuning switches
+// Timing experiments (SA_EXPERIMENT skips score processing -- invalid results; SA_NO_SEED,
+// SA_SEED_ROWS, SA_SEED_RECURSE, SA_LOCKSTEP_LAG change the schedule) are read only by a
+// library built with -DSA_TUNING_BUILD (build.py --tuning, written to libsa_tuning.so); the
+// product library ignores them, so no environment can change what it computes.
+const char* tuning_env(const char* name) {
+#ifdef SA_TUNING_BUILD
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 // ====================================================================== helpers
 static sa_status check_device(int* dev_out, int* sms_out) {
   int dev = 0;
@@ -222,17 +235,17 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
     // entries first (that warm-up dominated the insert work: ~40% of the e4m3 scan).
     // 2^18 rows (bf16) / 2^19 (e4m3, whose scan is cheaper): measured best of 2^16..2^20
     static const int64_t seed_env = [] {   // SA_SEED_ROWS: tuning experiments only
-      const char* e = getenv("SA_SEED_ROWS");
+      const char* e = tuning_env("SA_SEED_ROWS");
       return e ? atoll(e) : (int64_t)0;
     }();
     const int64_t seed_rows = seed_env > 0 ? seed_env : (int64_t)(cv.fp8 ? 1 << 19 : 1 << 18);
     static const bool seed_recurse = [] {
-      const char* e = getenv("SA_SEED_RECURSE");
+      const char* e = tuning_env("SA_SEED_RECURSE");
       return !(e && e[0] == '0');
     }();
     const int64_t m = std::min<int64_t>(cv.n_rows / 32, seed_rows) / FS_BN * FS_BN;
     static const bool no_seed = [] {   // SA_NO_SEED=1: timing experiments only
-      const char* e = getenv("SA_NO_SEED");
+      const char* e = tuning_env("SA_NO_SEED");
       return e && e[0] == '1';
     }();
     // worth it only for long scans: the sub-scans cost ~0.3-0.5 ms whatever the corpus and
@@ -301,12 +314,12 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   a.fp8 = cv.fp8 ? 1 : 0;
   {
     static const int experiment = [] {
-      const char* e = getenv("SA_EXPERIMENT");
+      const char* e = tuning_env("SA_EXPERIMENT");   // results invalid: timing only
       return e ? atoi(e) : 0;
     }();
     a.experiment = experiment;
     static const int lag = [] {   // SA_LOCKSTEP_LAG: tuning experiments only
-      const char* e = getenv("SA_LOCKSTEP_LAG");
+      const char* e = tuning_env("SA_LOCKSTEP_LAG");
       return e ? atoi(e) : 0;
     }();
     a.lockstep_lag = lag;
@@ -324,7 +337,7 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   cudaError_t e;
   {
     ProfRegion region(SA_KERNEL_FLAT_SCAN, s);
-    e = launch_flat_scan(tm, tm, tmap_q, a, p.cg, p.grid, s);
+    e = launch_flat_scan(tm, tmap_q, a, p.cg, p.grid, s);
   }
   if (e == cudaSuccess) {
     MergeArgs m{};
@@ -367,7 +380,7 @@ sa_status flat_scores_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   sa_status st = make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM);
   if (st != SA_OK) return st;
   const CUtensorMap& tm = p.cg == 2 ? *cv.tmap2 : *cv.tmap1;
-  cudaError_t e = launch_flat_scan(tm, tm, tmap_q, a, p.cg, p.grid, s);
+  cudaError_t e = launch_flat_scan(tm, tmap_q, a, p.cg, p.grid, s);
   return cuda_status(e, "score scan");
 }
 
@@ -382,73 +395,6 @@ sa_status flat_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, 
 }  // namespace sa
 
 using namespace sa;
-
-// ====================================================================== NCCL (dlopen)
-namespace {
-struct NcclApi {
-  bool ok = false;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*GroupStart)() = nullptr;
-  ncclResult_t (*GroupEnd)() = nullptr;
-};
-NcclApi& nccl() {
-  static NcclApi api;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return;
-    api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
-    api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
-    api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
-    api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
-    api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-    api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
-    api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
-    api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
-    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather;
-  });
-  return api;
-}
-sa_status nccl_status(ncclResult_t r, const char* what) {
-  if (r == ncclSuccess) return SA_OK;
-  const char* m = nccl().GetErrorString ? nccl().GetErrorString(r) : "?";
-  return set_error(SA_ERR_NCCL, std::string(what) + ": " + m);
-}
-}  // namespace
-
-namespace sa {
-// Every rank r contributes bytes [off[r], off[r] + len[r]) of `buf`; afterwards every rank
-// holds all parts (one ncclBroadcast per root inside a group).
-sa_status comm_broadcast_parts(const sa_comm* c, void* buf, const int64_t* off, const int64_t* len,
-                               cudaStream_t s) {
-  if (!nccl().ok || !nccl().Broadcast || !nccl().GroupStart || !nccl().GroupEnd)
-    return set_error(SA_ERR_NCCL, "libnccl.so.2 not found");
-  sa_status st = nccl_status(nccl().GroupStart(), "ncclGroupStart");
-  for (int r = 0; st == SA_OK && r < c->world; ++r) {
-    if (len[r] == 0) continue;
-    char* p = static_cast<char*>(buf) + off[r];
-    st = nccl_status(nccl().Broadcast(p, p, (size_t)len[r], ncclUint8, r, (ncclComm_t)c->nccl, s),
-                     "ncclBroadcast");
-  }
-  sa_status st2 = nccl_status(nccl().GroupEnd(), "ncclGroupEnd");
-  return st != SA_OK ? st : st2;
-}
-sa_status comm_allgather_bytes(const sa_comm* c, const void* send, void* recv, size_t bytes,
-                               cudaStream_t s) {
-  if (!nccl().ok) return set_error(SA_ERR_NCCL, "libnccl.so.2 not found");
-  return nccl_status(nccl().AllGather(send, recv, bytes, ncclUint8, (ncclComm_t)c->nccl, s),
-                     "ncclAllGather");
-}
-}  // namespace sa
 
 extern "C" {
 
@@ -479,44 +425,6 @@ void sa_build_opts_default(sa_build_opts* o) {
   o->comm = nullptr;
   o->stream = nullptr;
   o->centroids = nullptr;
-}
-
-sa_status sa_comm_unique_id(void* out) {
-  if (!out) return set_error(SA_ERR_INVALID_ARG, "out is NULL");
-  if (!nccl().ok) return set_error(SA_ERR_NCCL, "libnccl.so.2 not found");
-  ncclUniqueId id;
-  sa_status st = nccl_status(nccl().GetUniqueId(&id), "ncclGetUniqueId");
-  if (st != SA_OK) return st;
-  std::memcpy(out, &id, sizeof(id));
-  return SA_OK;
-}
-
-sa_status sa_comm_init(const void* uid, int32_t rank, int32_t world, int32_t device,
-                       sa_comm** out) {
-  if (!uid || !out) return set_error(SA_ERR_INVALID_ARG, "null pointer");
-  if (world < 1 || rank < 0 || rank >= world) return set_error(SA_ERR_INVALID_ARG, "bad rank/world");
-  if (!nccl().ok) return set_error(SA_ERR_NCCL, "libnccl.so.2 not found");
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
-  ncclUniqueId id;
-  std::memcpy(&id, uid, sizeof(id));
-  ncclComm_t c;
-  sa_status st = nccl_status(nccl().CommInitRank(&c, world, id, rank), "ncclCommInitRank");
-  if (st != SA_OK) return st;
-  sa_comm* sc = new sa_comm;
-  sc->nccl = c;
-  sc->rank = rank;
-  sc->world = world;
-  sc->device = device;
-  *out = sc;
-  return SA_OK;
-}
-
-sa_status sa_comm_free(sa_comm* c) {
-  if (!c) return SA_OK;
-  if (c->nccl && nccl().ok) nccl().CommDestroy((ncclComm_t)c->nccl);
-  delete c;
-  return SA_OK;
 }
 
 sa_status sa_index_build(const void* corpus, int64_t n, int32_t d, int32_t nlist, sa_index** out) {
@@ -665,10 +573,15 @@ sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype
                        int32_t k, int32_t nprobe, int64_t* out_ids, float* out_scores,
                        void* stream) {
   sa_status st = validate_search(idx, queries, nq, k, nprobe, out_ids, out_scores);
-  if (st != SA_OK) return st;
-  if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
+  if (st == SA_OK && qdtype != SA_BF16 && qdtype != SA_F32)
+    st = set_error(SA_ERR_INVALID_ARG, "bad qdtype");
   cudaStream_t s = (cudaStream_t)stream;
-  const bool sharded = idx->comm && idx->comm->world > 1;
+  const bool sharded = idx && idx->comm && idx->comm->world > 1;
+  if (sharded) {
+    const int64_t args[kCommArgs] = {0x5a5e, nq, k, nprobe, (int64_t)qdtype, 0};
+    st = comm_check_args(idx->comm, args, st, s);
+  }
+  if (st != SA_OK) return st;
   if (!sharded) {
     SearchOut out;
     out.ids = out_ids;
@@ -697,9 +610,7 @@ sa_status gather_merge_keys(const sa_index* idx, const uint64_t* keys_local, int
   uint64_t* keys_all = nullptr;
   sa_status st = dalloc(&keys_all, (size_t)nq * k * w, s, "alloc gathered keys");
   if (st == SA_OK)
-    st = nccl_status(nccl().AllGather(keys_local, keys_all, (size_t)nq * k, ncclUint64,
-                                      (ncclComm_t)idx->comm->nccl, s),
-                     "ncclAllGather");
+    st = comm_allgather_bytes(idx->comm, keys_local, keys_all, (size_t)nq * k * sizeof(uint64_t), s);
   if (st == SA_OK) st = merge_keys(keys_all, w, nq, k, out_ids, out_scores, s);
   if (keys_all) cudaFreeAsync(keys_all, s);
   return st;
