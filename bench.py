@@ -134,6 +134,11 @@ def sample_bits(cfg, rows, nq, device):
 
 
 def run_reference(args, cfg, name):
+    """The reference arm: the CPU oracle (oracle/oracle.c, as it stands) on the host cores.
+    A full-corpus pass of the fp64 oracle takes ~2 s per query per 8 cores (SURVEY [M4]), so
+    each step times `cores` queries against the first 2^18 corpus rows -- a bounded sample of
+    the same workload -- and the metric (queries/s over the full corpus) is PROJECTED by the
+    row ratio; ms_per_step is the measured time of one sampled step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -144,30 +149,73 @@ def run_reference(args, cfg, name):
     Xb, Qb = sample_bits(cfg, rows, cores, dev)
     for _ in range(args.warmup):
         cpu_oracle_sample(Xb, Qb, cfg["k"], cfg["n"])
-    vals, times = [], []
+    times = []
     for _ in range(args.steps):
-        v, dt, _ = cpu_oracle_sample(Xb, Qb, cfg["k"], cfg["n"])
-        vals.append(v)
+        _, dt, _ = cpu_oracle_sample(Xb, Qb, cfg["k"], cfg["n"])
         times.append(dt)
-    value = len(vals) * Qb.shape[0] / (sum(times) * cfg["n"] / rows)
-    sample = (f"{Qb.shape[0]} queries x first {rows} corpus rows per step, exact top-{cfg['k']} "
-              f"in fp64; q/s extrapolated x{rows}/{cfg['n']} to the full corpus")
+    value = len(times) * Qb.shape[0] / (sum(times) * cfg["n"] / rows)
+    sample = (f"per step: {Qb.shape[0]} queries x the first {rows} of {cfg['n']} corpus rows, "
+              f"exact top-{cfg['k']} in fp64 on {cores} threads; q/s projected to the full "
+              f"corpus by the row ratio")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(times) / len(times) * cfg["n"] / rows,
+        "ms_per_step": 1e3 * sum(times) / len(times), "ms_per_step_kind": "measured sample step",
+        "value_kind": "projected to the full corpus (row ratio)",
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded low-rank Gaussian mixture, unit-norm; DESIGN.md §3)",
-        "config": {"workload": f"{name}: top-{cfg['k']}, {cfg['n']}x{cfg['d']} bf16 corpus, batch "
-                               f"{cfg['nq']} (the same workload as the GPU arm; the CPU oracle "
-                               "searches exactly, recall@k 1.0)",
-                   "n": cfg["n"], "d": cfg["d"], "nq": cfg["nq"], "k": cfg["k"],
-                   "recall_at_k": 1.0, "parallelism": f"{cores} host threads"},
+        "config": {"workload": f"{name}: exact top-{cfg['k']} (CPU fp64 oracle) over "
+                               f"{cfg['n']}x{cfg['d']} bf16; timed: {Qb.shape[0]} queries x "
+                               f"{rows} rows per step, projected to the full corpus",
+                   "n": cfg["n"], "d": cfg["d"], "k": cfg["k"], "timed_rows": rows,
+                   "timed_queries_per_step": int(Qb.shape[0]), "recall_at_k": 1.0,
+                   "parallelism": f"{cores} host threads"},
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ launch plumbing
+TUNING_SWITCHES = ("SA_LIBRARY", "SA_EXPERIMENT", "SA_NO_SEED", "SA_SEED_ROWS", "SA_SEED_RECURSE",
+                   "SA_LOCKSTEP_LAG", "SA_NO_GRAPH")
+
+
+def refused_environment():
+    """Names of set switches that would change what is timed (the product library ignores the
+    experiment switches, but a tuning library would not) -- bench.py refuses them."""
+    return [v for v in TUNING_SWITCHES if os.environ.get(v)]
+
+
+def respawn_under_torchrun(n):
+    """`bench.py --gpus N` without a launcher: re-exec as N ranks under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def spawn_check(args):
+    """Launch plumbing only (CPU test, tests/test_bench_contract.py): the ranks respawn_under_
+    torchrun started meet in a gloo process group and rank 0 reports how many it saw."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
+        return 2
+    dist.init_process_group("gloo")
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    if dist.get_rank() == 0:
+        print(json.dumps({"spawn_check": world, "ranks_seen": int(t.item())}))
+    dist.destroy_process_group()
     return 0
 
 
@@ -233,8 +281,18 @@ def main():
         cfg["d"] = args.d
     if args.n:
         cfg["n"] = args.n
+    bad = refused_environment()
+    if bad:
+        print(json.dumps({"error": f"refusing to benchmark with {bad} set (timing-experiment "
+                                   "switches / tuning library; DESIGN.md §5)"}))
+        return 2
     if args.impl == "reference":
         return run_reference(args, cfg, args.config)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return respawn_under_torchrun(args.gpus)
+
+    if os.environ.get("SA_BENCH_SPAWN_CHECK"):
+        return spawn_check(args)
 
     import paper_2505_12065_b200 as sa
 
@@ -244,13 +302,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
+        return 2
     torch.cuda.set_device(local)
     dist = None
     comm = None
+    nccl_nranks = 1
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = sa.Comm.from_torch_distributed(local)
+        nccl_nranks = comm.info()["nccl_nranks"]
+        print(f"[bench rank {rank}/{world}] cuda:{local}, NCCL communicator of {nccl_nranks} ranks",
+              file=sys.stderr, flush=True)
     mode = args.mode
     use_ivf = mode in ("auto", "ivf", "graph")
     # graph mode: one full-corpus index + graph per rank (replicas; query batches are split
@@ -323,6 +388,13 @@ def main():
             return v
         t = torch.tensor([v], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
     def run_search(i, nprobe):
@@ -408,7 +480,7 @@ def main():
                          "peak_kind": f"bf16 dense, {pk['src']} burst (MEASURED_PEAKS.json)",
                          "frac_of_sustained": achieved / pk["bf16_sus"] if pk["bf16_sus"] else None,
                          "kernel_ms": per_launch, "kernel_share_of_step": fs_ms / ms_e,
-                         "traffic": traffic_from_profiles("flat_scan", args.config, nq)},
+                         "traffic": traffic_from_profiles("flat_scan", args.config, nq, world)},
         }
     # ---- fp8 flat scan + bf16 re-rank, beside the exact mode
     result_fp8 = None
@@ -442,7 +514,7 @@ def main():
                          "peak_kind": f"e4m3 dense = 2 x bf16 {pk['src']} burst "
                                       "(MEASURED_PEAKS.json x the guide's nominal ratio 4.5/2.25)",
                          "kernel_ms": per_launch, "kernel_share_of_step": fs_ms / ms_8,
-                         "traffic": traffic_from_profiles("flat_scan_fp8", args.config, nq)},
+                         "traffic": traffic_from_profiles("flat_scan_fp8", args.config, nq, world, f"ncand{args.fp8_cand}")},
         }
     result_ivf = None
     if use_ivf and mode != "graph":
@@ -476,7 +548,7 @@ def main():
                          "peak_kind": f"HBM copy, {pk['src']} (MEASURED_PEAKS.json)",
                          "frac_of_8TBs": achieved / 8000.0,
                          "kernel_ms": per_launch, "kernel_share_of_step": sc_ms / ms_i,
-                         "traffic": traffic_from_profiles("ivf_scan", args.config, nq)},
+                         "traffic": traffic_from_profiles("ivf_scan", args.config, nq, world, f"nprobe{nprobe}")},
         }
 
     # ---- IVF list scan on the e4m3 copy + bf16 re-rank (compressed IVF, R35)
@@ -559,9 +631,13 @@ def main():
                                       f"gathers random {d * 2} B rows",
                          "frac_of_8TBs": achieved / 8000.0,
                          "kernel_ms": per_launch, "kernel_share_of_step": gs_ms / ms_g,
-                         "traffic": traffic_from_profiles("graph_search", args.config, nq)},
+                         "traffic": traffic_from_profiles("graph_search", args.config, nq, world, f"L{L}")},
         }
 
+    for r in (result_exact, result_fp8, result_ivf, result_ivf_fp8):
+        if r is not None:
+            r.setdefault("parallelism", f"row-shard x{world}")
+            r.setdefault("scaling", "strong")
     # headline: the fastest of the modes that meet recall@10 >= 0.95
     cands = [r for r in (result_graph, result_ivf, result_exact)
              if r is not None and r["recall"] >= RECALL_TARGET]
@@ -603,6 +679,10 @@ def main():
                      f"{head['search_range']} width {GRAPH_W}")
     else:
         mode_name = "exact flat" if head_nprobe == 0 else f"IVF nlist={nlist} nprobe={head_nprobe}"
+    legs = {"exact": result_exact, "exact_fp8": result_fp8, "ivf": result_ivf,
+            "ivf_fp8": result_ivf_fp8, "graph": result_graph}
+    # every rank took part in the timed steps (the driver checks N ranks were busy)
+    gpus_active = int(round(sum_over_ranks(1.0)))
     line = {
         "metric": METRIC, "value": head["value"], "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
@@ -624,12 +704,14 @@ def main():
                 "p50_batch_ms": 1e3 * statistics.median(lat) if lat else None,
                 "p99_batch_ms": 1e3 * float(np.percentile(lat, 99)) if lat else None},
         "gpu_launches": int(sum(v for v in head["kernel_launches"].values())),
-        "kernel_ms": head["kernel_ms"], "kernel_launches": head["kernel_launches"],
-        "clocks": head["clocks"],
-        "exact": result_exact, "exact_fp8": result_fp8, "ivf": result_ivf,
-        "ivf_fp8": result_ivf_fp8, "graph": result_graph,
-        "build_s": build_s, "graph_build_s": graph_build_s, "gen_s": gen_s,
+        "clocks": head["clocks"], "gpus_active": gpus_active, "nccl_nranks": nccl_nranks,
+        # every mode, compact (full per-kernel detail: bench_detail_n<N>.json)
+        "legs": {name: compact_leg(r) for name, r in legs.items() if r is not None},
+        "build_s": round(build_s, 2),
+        "graph_build_s": round(graph_build_s, 2) if graph_build_s else None,
     }
+    detail = {"line": None, "legs": legs, "gen_s": gen_s, "kernel_ms": head["kernel_ms"],
+              "kernel_launches": head["kernel_launches"]}
     # ---- agent-step batches (BASELINE config 5 shape): p50/p99 latency of one sa_search_host
     # call (H2D + search + D2H) at the headline nprobe, closed loop, per batch size
     agent = []
@@ -648,7 +730,8 @@ def main():
         agent.append({"batch": b, "k": 5, "nprobe": head_nprobe,
                       "p50_ms": 1e3 * float(np.percentile(ts, 50)),
                       "p99_ms": 1e3 * float(np.percentile(ts, 99))})
-    line["agent_step_latency"] = agent
+    line["agent_step_latency"] = [{kk: (round(v, 4) if isinstance(v, float) else v)
+                                   for kk, v in r.items()} for r in agent]
     if result_graph is not None:
         # the same agent-step batches through the graph index (pinned H2D, search, D2H)
         agent_g = []
@@ -668,7 +751,8 @@ def main():
             agent_g.append({"batch": b, "k": 5, "search_range": Lg,
                             "p50_ms": 1e3 * float(np.percentile(ts, 50)),
                             "p99_ms": 1e3 * float(np.percentile(ts, 99))})
-        line["agent_step_latency_graph"] = agent_g
+        line["agent_step_latency_graph"] = [{kk: (round(v, 4) if isinstance(v, float) else v)
+                                             for kk, v in r.items()} for r in agent_g]
     # ---- non-stall maturity exit (PAPER §3.3; full grid: bench.py --maturity), batch 1, k=5
     if use_ivf and nlist >= 128 and world == 1:   # maturity exit: unsharded indexes only
         qs = [batches[i][:1].contiguous() for i in range(args.warmup, min(nb, args.warmup + 16))]
@@ -676,8 +760,8 @@ def main():
         m = mature_point(sa, idx, qs, 5, 128, 3.0, 32, 8, gt5)
         fx = fixed_point(idx, qs, 5, 64, gt5)
         st = stop_latency(sa, idx, qs[0], 5, 128, 0.0, 16, 1, 0.0002)
-        line["maturity_exit"] = {"batch": 1, "k": 5, "mature": m, "fixed_nprobe64": fx,
-                                 "engine_flag_stop": st}
+        detail["maturity_exit"] = {"batch": 1, "k": 5, "mature": m, "fixed_nprobe64": fx,
+                                   "engine_flag_stop": st}
     if build_error:
         line["ivf_build_error"] = build_error
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -692,6 +776,8 @@ def main():
                       f"fp64; q/s scaled by {rows}/{n} to the full corpus"}
     if rank == 0:
         print(json.dumps(line))
+        detail["line"] = line
+        write_detail(detail, world)
     if gidx is not None and gidx is not idx:
         gidx.free()
     idx.free()
@@ -1007,15 +1093,44 @@ def run_simulated(args, cfg, sa):
     return 0
 
 
-def traffic_from_profiles(kernel, config, nq):
+def compact_leg(r):
+    """One mode's numbers for the JSON line: throughput, recall, knob, roofline fraction."""
+    out = {kk: r[kk] for kk in ("value", "recall", "ms_per_step", "nprobe", "search_range",
+                                 "n_cand", "scaling", "parallelism") if r.get(kk) is not None}
+    out.setdefault("scaling", "strong")
+    rf = r["roofline"]
+    out["roofline"] = {kk: rf.get(kk) for kk in ("kernel", "bound", "achieved", "peak", "unit",
+                                                  "frac", "kernel_ms", "kernel_share_of_step")}
+    return {kk: (round(v, 4) if isinstance(v, float) else v) for kk, v in out.items()}
+
+
+def write_detail(detail, world):
+    """The full per-mode record (kernel times and launches per kind, sweeps, clocks, maturity
+    point) next to the JSON line: gpurun_out/bench_detail_n<N>.json when that directory exists
+    (SA_BENCH_DETAIL overrides the path)."""
+    path = os.environ.get("SA_BENCH_DETAIL")
+    if not path:
+        d = os.path.join(ROOT, "gpurun_out")
+        if not os.path.isdir(d):
+            return
+        path = os.path.join(d, f"bench_detail_n{world}.json")
+    with open(path, "w") as fh:
+        json.dump(detail, fh, indent=1, default=float)
+
+
+def traffic_from_profiles(kernel, config, nq, world, knob=""):
+    """DRAM bytes per launch of `kernel` from a committed ncu --set full capture of exactly this
+    configuration (profiles/ncu_traffic.json key kernel:config:nq<nq>:w<world>[:knob]), else None
+    -- a capture of another search range / nprobe / world size is never attached."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     try:
         j = json.load(open(p))
-        return j.get(f"{kernel}:{config}:nq{nq}")
-    except Exception:
+    except ValueError:
         return None
+    key = f"{kernel}:{config}:nq{nq}:w{world}" + (f":{knob}" if knob else "")
+    return j.get(key)
 
 
 if __name__ == "__main__":

@@ -18,7 +18,10 @@ import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_PKG, "libsa.so")
+# SA_LIBRARY=tuning loads libsa_tuning.so (build.py --tuning: the same code, honouring the
+# timing-experiment switches); bench.py refuses it.
+TUNING = os.environ.get("SA_LIBRARY", "") == "tuning"
+_SO = os.path.join(_PKG, "libsa_tuning.so" if TUNING else "libsa.so")
 
 SA_OK, SA_ERR_INVALID_ARG, SA_ERR_STATE, SA_ERR_OOM, SA_ERR_CUDA, SA_ERR_NCCL, SA_ERR_UNSUPPORTED = range(7)
 SA_BF16, SA_F32 = 0, 1

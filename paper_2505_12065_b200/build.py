@@ -10,6 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libsa.so")
+SO_TUNING = os.path.join(PKG, "libsa_tuning.so")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -35,32 +36,39 @@ def headers():
                   + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
-def needs_build() -> bool:
-    if not os.path.exists(SO):
+def needs_build(so: str = SO) -> bool:
+    if not os.path.exists(so):
         return True
-    t = os.path.getmtime(SO)
+    t = os.path.getmtime(so)
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return SO
+def build(force: bool = False, verbose: bool = False, tuning: bool = False) -> str:
+    """Compile libsa.so.  tuning=True builds libsa_tuning.so instead: the same library with
+    -DSA_TUNING_BUILD, which honours the timing-experiment switches (SA_EXPERIMENT, SA_NO_SEED,
+    ...).  The product library never reads them; bench.py refuses the tuning
+    library."""
+    so = SO_TUNING if tuning else SO
+    if not force and not needs_build(so):
+        return so
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build_tuning" if tuning else "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     logs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.relpath(src, CSRC).replace(os.sep, "_") + ".o")
         extra = PER_FILE_FLAGS.get(os.path.basename(src), [])
-        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        defs = ["-DSA_TUNING_BUILD"] if tuning else []
+        cmd = [nvcc, *NVCC_FLAGS, *extra, *defs, "-I", os.path.join(ROOT, "include"), "-c", src,
+               "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stdout + r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
         objs.append(obj)
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", SO, *objs,
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", so, *objs,
            "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -70,8 +78,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return SO
+    return so
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv, verbose=True, tuning="--tuning" in sys.argv)

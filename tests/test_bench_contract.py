@@ -27,3 +27,41 @@ def test_reference_arm_json_line():
     assert j["cpu_baseline"]["kind"] == "oracle" and j["cpu_baseline"]["cores"] >= 1
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["value"] == j["value"]
     assert "workload" in j["config"]
+
+
+def test_bench_refuses_timing_experiment_switches():
+    """SA_EXPERIMENT (and the other tuning switches) never reach a timed run: bench.py exits 2
+    with an error line before loading anything."""
+    env = dict(os.environ, SA_EXPERIMENT="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 2
+    j = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert "SA_EXPERIMENT" in j["error"]
+
+
+def test_bench_checks_world_size_against_gpus():
+    """--gpus N under a launcher whose WORLD_SIZE differs is an error, never a silent 1-rank
+    run (VERDICT r1 weak #1)."""
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--steps", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT,
+                       env=env)
+    assert r.returncode == 2
+    j = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert "WORLD_SIZE" in j["error"]
+
+
+def test_bench_gpus_n_spawns_n_ranks():
+    """`bench.py --gpus 2` without a launcher re-execs itself as 2 ranks under
+    torch.distributed.run (127.0.0.1 rendezvous); checked here with a gloo group on CPU."""
+    env = dict(os.environ, SA_BENCH_SPAWN_CHECK="1")
+    for v in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(v, None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--steps", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT,
+                       env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0]) == {"spawn_check": 2, "ranks_seen": 2}
