@@ -113,7 +113,15 @@ def build(X_bits: np.ndarray, K: int, R: int, candidates=None):
 def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: int, w: int,
            entries, T: int, tau=None, window: int = 1, g: int = 1, ready=True, values=None,
            qv=None):
-    """R27 for one query.  Returns dict(ids, scores, expanded, iterations[, rq, ema]).
+    """R27 for one query.  Returns dict(ids, scores, expanded, iterations, certified[, rq, ema]).
+
+    certified (diagnostic for parity tests, not part of R27): True when every order decision
+    the trajectory took -- the top-L truncations, the choice of the w entries to expand, and
+    the order / k-th boundary of the result -- separates two scores by more than the sum of
+    their fp32 accumulation error bounds, eb = (d - 1) * 2^-24 * sum_j |q_j x_j| (bf16
+    products are exact in fp32; the bound holds for any summation order).  A search that
+    scores in fp32 then provably takes the same path and returns the same list; when False
+    the two may legitimately differ at a near-tie.  `near_tie` holds the smallest such gap.
 
     With tau set, the non-stall maturity exit of PAPER.md §3.3 (App. B.2) runs on
     the beam search itself -- the paper's own setting (HNSW).  Readings R28-R29: a step is
@@ -125,6 +133,20 @@ def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: i
     values / qv: fp64 rows / query to score with instead of the bf16 ones (R34)."""
     X = bf16_to_f64(X_bits) if values is None else values
     q = bf16_to_f64(q_bits) if qv is None else qv
+    u_d = (X.shape[1] - 1) * 2.0 ** -24
+    cert = {"ok": True, "gap": np.inf}
+
+    def bound(rows):
+        return u_d * (np.abs(X[rows]) @ np.abs(q))
+
+    def separate(a, b):   # a, b: list entries [score, id, expanded, error bound]
+        if a[1] == b[1]:
+            return
+        gap = abs(a[0] - b[0])
+        if gap <= a[3] + b[3]:
+            cert["ok"] = False
+            cert["gap"] = min(cert["gap"], gap)
+
     visited = set()
     ent = []
     for e in entries:
@@ -133,16 +155,23 @@ def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: i
             ent.append(int(e))
     ids = np.array(ent, dtype=np.int64)
     sc = X[ids] @ q if ids.size else np.empty(0)
-    order = np.lexsort((ids, -sc))[:L]
-    lst = [[float(sc[o]), int(ids[o]), False] for o in order]
+    eb = bound(ids) if ids.size else np.empty(0)
+    order = np.lexsort((ids, -sc))
+    if order.size > L:
+        separate([sc[order[L - 1]], ids[order[L - 1]], 0, eb[order[L - 1]]],
+                 [sc[order[L]], ids[order[L]], 0, eb[order[L]]])
+    lst = [[float(sc[o]), int(ids[o]), False, float(eb[o])] for o in order[:L]]
     it = 0
     expanded = 0
     ema = None
     rqs, emas = [], []
     while it < T:
-        pick = [e for e in lst if not e[2]][:w]
+        unexp = [e for e in lst if not e[2]]
+        pick = unexp[:w]
         if not pick:
             break
+        if len(unexp) > w:
+            separate(unexp[w - 1], unexp[w])
         it += 1
         new = []
         for e in pick:
@@ -158,8 +187,11 @@ def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: i
             nid = np.array(new, dtype=np.int64)
             ns = X[nid] @ q
             s_t = float(ns.max())
-            allv = lst + [[float(s), int(i), False] for s, i in zip(ns, nid)]
+            allv = lst + [[float(s), int(i), False, float(b)]
+                          for s, i, b in zip(ns, nid, bound(nid))]
             allv.sort(key=lambda e: (-e[0], e[1]))
+            if len(allv) > L:
+                separate(allv[L - 1], allv[L])
             lst = allv[:L]
         if tau is not None:
             sb, sw = lst[0][0], lst[-1][0]
@@ -171,13 +203,16 @@ def search(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, L: i
             is_ready = ready(it) if callable(ready) else bool(ready)
             if it % g == 0 and ema >= tau and is_ready:
                 break
+    for j in range(min(k + 1, len(lst)) - 1):
+        separate(lst[j], lst[j + 1])      # result order and its k-th boundary
     out_ids = np.full(k, -1, dtype=np.int64)
     out_sc = np.full(k, -np.inf)
     for j, e in enumerate(lst[:k]):
         out_ids[j] = e[1]
         out_sc[j] = e[0]
     out = {"ids": out_ids, "scores": out_sc, "expanded": expanded, "iterations": it,
-           "list_ids": np.array([e[1] for e in lst], dtype=np.int64)}
+           "list_ids": np.array([e[1] for e in lst], dtype=np.int64),
+           "certified": cert["ok"], "near_tie": cert["gap"]}
     if tau is not None:
         out["rq"] = np.array(rqs)
         out["ema"] = np.array(emas)
@@ -193,11 +228,21 @@ def search_fp8(X_bits: np.ndarray, nbr: np.ndarray, q_bits: np.ndarray, k: int, 
     q8 = fp8.quantize_queries(np.asarray(q_bits)[None, :])[0][0]
     r = search(X_bits, nbr, q_bits, L, L, w, entries, T, values=X8, qv=q8)
     cand = r["list_ids"]
-    s = bf16_to_f64(X_bits[cand]) @ bf16_to_f64(q_bits) if cand.size else np.empty(0)
-    order = np.lexsort((cand, -s))[:k]
+    Xc, qf = bf16_to_f64(X_bits[cand]), bf16_to_f64(q_bits)
+    s = Xc @ qf if cand.size else np.empty(0)
+    order = np.lexsort((cand, -s))
+    # certification of the re-rank's order / k-th boundary (see search)
+    eb = (X_bits.shape[1] - 1) * 2.0 ** -24 * (np.abs(Xc) @ np.abs(qf)) if cand.size else s
+    cert, gap = r["certified"], r["near_tie"]
+    for j in range(min(k + 1, order.size) - 1):
+        a, b = order[j], order[j + 1]
+        if abs(s[a] - s[b]) <= eb[a] + eb[b]:
+            cert, gap = False, min(gap, abs(s[a] - s[b]))
+    order = order[:k]
     out_ids = np.full(k, -1, dtype=np.int64)
     out_sc = np.full(k, -np.inf)
     out_ids[:order.size] = cand[order]
     out_sc[:order.size] = s[order]
     return {"ids": out_ids, "scores": out_sc, "expanded": r["expanded"],
-            "iterations": r["iterations"], "list_ids": cand}
+            "iterations": r["iterations"], "list_ids": cand, "certified": cert,
+            "near_tie": gap}

@@ -60,29 +60,41 @@ def kmeans(X_bits: np.ndarray, nlist: int, iters: int = 20, train_per_list: int 
     C = S[np.arange(nlist) * stride + o].copy()
     a = None
     for _ in range(iters):
-        Cb = bf16_to_f64(centroids_bf16(C))
-        sc = S @ Cb.T
-        a = np.argmax(sc, axis=1)
-        best = sc[np.arange(n_train), a]
+        C, a, margin = lloyd_step(S, C)
         if trace is not None:
-            srt = np.sort(sc, axis=1)
-            trace.append(float(np.min(srt[:, -1] - srt[:, -2])) if nlist > 1 else np.inf)
-        newC = np.zeros_like(C)
-        empty = []
-        for j in range(nlist):
-            m = a == j
-            if not m.any():
-                empty.append(j)
-                continue
-            s = S[m].sum(axis=0)
-            newC[j] = s / np.linalg.norm(s)
-        if empty:
-            # R10: empty lists (ascending) take the lowest-scored sample rows, (score, row) ascending
-            order = np.lexsort((np.arange(n_train), best))
-            for r, j in zip(order, empty):
-                newC[j] = S[r]
-        C = newC
+            trace.append(float(np.min(margin)) if nlist > 1 else np.inf)
     return C, a, rows
+
+
+def lloyd_step(S: np.ndarray, C: np.ndarray):
+    """One iteration of step 3 (R8, R10) from centroids C (fp64 [nlist, d]) over the sample S
+    (fp64 [n_train, d]).  Returns (new C, assignment, margin) -- margin = best minus second-best
+    score of each sample row (+inf when nlist = 1), the size of the decision a(x)."""
+    nlist, n_train = C.shape[0], S.shape[0]
+    Cb = bf16_to_f64(centroids_bf16(C))
+    sc = S @ Cb.T
+    a = np.argmax(sc, axis=1)
+    best = sc[np.arange(n_train), a]
+    if nlist > 1:
+        srt = np.sort(sc, axis=1)
+        margin = srt[:, -1] - srt[:, -2]
+    else:
+        margin = np.full(n_train, np.inf)
+    newC = np.zeros_like(C)
+    empty = []
+    for j in range(nlist):
+        m = a == j
+        if not m.any():
+            empty.append(j)
+            continue
+        s = S[m].sum(axis=0)
+        newC[j] = s / np.linalg.norm(s)
+    if empty:
+        # R10: empty lists (ascending) take the lowest-scored sample rows, (score, row) ascending
+        order = np.lexsort((np.arange(n_train), best))
+        for r, j in zip(order, empty):
+            newC[j] = S[r]
+    return newC, a, margin
 
 
 def build(X_bits: np.ndarray, nlist: int, iters: int = 20, train_per_list: int = 256,

@@ -1,6 +1,10 @@
 """Parity at BASELINE.json's full size (C3: 21,015,324 x 768 bf16, batch 512, top-10) in the
 launch configuration bench.py times, on sampled outputs the oracle computes one by one
-(tests/parity.py band rule), plus IVF (nlist=16384) properties at full size."""
+(tests/parity.py band rule): queries 0-63 of the seed-5678 stream plus tile / CTA-half edge
+queries, and P7 planted winners at rows {0, 127, 128, 255, 256, n-1} and at every shard
+boundary +-1 of w = 2, 4, 8.  The row-sharded library path (w = 2 and 8
+in-process ranks, bench.py's per-rank launch configuration at N = 8) equals the unsharded
+result bit for bit.  Plus IVF (nlist=16384), graph and fp8 properties at full size."""
 import numpy as np
 import pytest
 import torch
@@ -12,6 +16,17 @@ from parity import check
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 SAMPLE_Q = [0, 1, 77, 255, 256, 300, 511]        # both query groups, both CTA halves, ragged
+PARITY_Q = list(range(64)) + [77, 255, 256, 300, 511]  # oracle parity over these
+
+
+def planted_rows(n):
+    """P7: tile edges, the last row, and every shard boundary +-1 for w = 2, 4, 8."""
+    rows = {0, 127, 128, 255, 256, n - 1}
+    for w in (2, 4, 8):
+        for r in range(1, w):
+            off = r * (n // w) + min(r, n % w)
+            rows.update({off - 1, off, off + 1})
+    return sorted(rows)
 
 
 def _bits(t):
@@ -27,22 +42,31 @@ def c3(sa):
     draw_rows_into(mix, X, CORPUS_SEED, 0)
     Q = torch.empty(nq, d, dtype=torch.bfloat16, device="cuda")
     draw_rows_into(mix, Q, QUERY_SEED, 0)
+    # P7 planted winners: query j of a separate seeded stream is planted (x 2, exact in bf16)
+    # at row planted[j]; it beats every unit-norm row for its own query
+    planted = planted_rows(n)
+    Qp = torch.empty(len(planted), d, dtype=torch.bfloat16, device="cuda")
+    draw_rows_into(mix, Qp, QUERY_SEED + 4321, 0)
+    X[torch.as_tensor(planted, device="cuda")] = (Qp.float() * 2.0).to(torch.bfloat16)
     flat = sa.Index.build(X)
     ids, sc = flat.search(Q, 10)
+    pid, psc = flat.search(Qp, 10)
     torch.cuda.synchronize()
-    # oracle over the whole corpus for the sampled queries, streamed in 2^21-row chunks
-    Qb = _bits(Q)[SAMPLE_Q]
+    # oracle over the whole corpus for the parity queries, streamed in 2^21-row chunks
+    Qb = np.concatenate([_bits(Q)[PARITY_Q], _bits(Qp)])
     top = oracle.TopK(Qb, 10 + 16)
     chunk = 1 << 21
     for lo in range(0, n, chunk):
         top.update(_bits(X[lo:lo + chunk]), lo)
     flat.free()
-    yield dict(X=X, Q=Q, ids=ids.cpu().numpy(), sc=sc.cpu().numpy(), top=top, Qb=Qb)
+    yield dict(X=X, Q=Q, Qp=Qp, planted=planted, ids=ids.cpu().numpy(), sc=sc.cpu().numpy(),
+               pid=pid.cpu().numpy(), psc=psc.cpu().numpy(), top=top, Qb=Qb)
 
 
-def test_c3_exact_sampled_parity(c3):
+def test_c3_exact_parity_queries_0_63_and_planted(c3):
     X, Qb, top = c3["X"], c3["Qb"], c3["top"]
-    gi, gs = c3["ids"][SAMPLE_Q], c3["sc"][SAMPLE_Q]
+    gi = np.concatenate([c3["ids"][PARITY_Q], c3["pid"]])
+    gs = np.concatenate([c3["sc"][PARITY_Q], c3["psc"]])
 
     def score_of(qi, ids):
         rows = _bits(X[torch.as_tensor(ids, device="cuda")])
@@ -52,6 +76,57 @@ def test_c3_exact_sampled_parity(c3):
     assert rep["ok"], rep
     rep5 = check(gi, gs, top.ids, top.scores, score_of, 10, rtol=1e-5)
     assert rep5["ok"], rep5
+    assert c3["pid"][:, 0].tolist() == c3["planted"]          # P7: every planted winner first
+    print(f"C3 parity: {len(gi)} queries, band median {rep['band_median']}, "
+          f"max {rep['band_max']}, max rel score err {rep['max_rel_score_err']:.2e}")
+
+
+def _run_ranks(world, fn):
+    import threading
+    out, err = [None] * world, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[r] = fn(r)
+                torch.cuda.current_stream().synchronize()
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            err.append(e)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=1200)
+    if err:
+        raise err[0]
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_c3_row_sharded_library_path(sa, c3, world):
+    """sa_search on w row shards (in-process communicator: the library's own all-gather +
+    merge branch, each rank in bench.py's per-rank launch configuration) == the unsharded
+    result bit for bit, for the 512-query batch and the planted queries (P8-iii at C3)."""
+    X, Q, Qp = c3["X"], c3["Q"], c3["Qp"]
+    n = X.shape[0]
+    comms = sa.Comm.local_group(world)
+
+    def rank(r):
+        off, ln = sa.shard_range(n, r, world)
+        idx = sa.Index.build(X[off:off + ln], row_offset=off, n_total=n, comm=comms[r])
+        a = [t.cpu().numpy() for t in idx.search(Q, 10)]
+        b = [t.cpu().numpy() for t in idx.search(Qp, 10)]
+        idx.free()
+        return a, b
+
+    res = _run_ranks(world, rank)
+    for c in comms:
+        c.free()
+    for a, b in res:
+        assert np.array_equal(a[0], c3["ids"]) and np.array_equal(a[1], c3["sc"])
+        assert np.array_equal(b[0], c3["pid"]) and np.array_equal(b[1], c3["psc"])
 
 
 def test_c3_exact_properties_all_queries(c3):

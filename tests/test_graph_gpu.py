@@ -78,20 +78,23 @@ def entries_of(idx, Q, E):
 def test_beam_search_matches_oracle(sa, small):
     idx, Xb, Qb, nbr, kn = small
     ent = entries_of(idx, Qb, 4)
-    same, rec = 0, []
+    rec, uncertified = [], 0
     for L, w in ((32, 1), (64, 4), (128, 2)):
         gi, gs, gx, _ = idx.search_graph(bits_to_tensor(Qb).cuda(), 10, L, search_width=w,
                                       n_entries=4, expanded=True)
         gi, gs, gx = gi.cpu().numpy(), gs.cpu().numpy(), gx.cpu().numpy()
         for q in range(len(Qb)):
             o = graph.search(Xb, nbr, Qb[q], 10, L=L, w=w, entries=ent[q], T=10_000)
-            if np.array_equal(gi[q], o["ids"]) and gx[q] == o["expanded"]:
-                same += 1
+            same = np.array_equal(gi[q], o["ids"]) and gx[q] == o["expanded"]
+            # identical unless the oracle's path crossed a near-tie its fp32 error bound cannot
+            # separate (oracle/graph.py `certified`)
+            assert same or not o["certified"], (L, w, q, gi[q], o["ids"], gx[q], o["expanded"])
+            uncertified += not o["certified"]
             rec.append(len(set(gi[q]) & set(o["ids"])) / 10)
             ps = oracle.pair_scores(Xb, Qb[q:q + 1], np.zeros(10, int), gi[q])
             assert np.all(np.abs(ps - gs[q]) <= 1e-3 * np.maximum(np.abs(ps), 1e-3))
             assert np.all(np.diff(gs[q]) <= 0) and len(set(gi[q].tolist())) == 10
-    assert same >= 0.9 * 3 * len(Qb), same
+    print(f"beam search: {uncertified} of {3 * len(Qb)} query paths cross an uncertified near-tie")
     assert np.mean(rec) >= 0.99
 
 
@@ -190,12 +193,11 @@ def test_forgettable_visited_table_keeps_the_list(sa):
     gi, gs, gx, gsc = idx.search_graph(bits_to_tensor(Qb).cuda(), 10, 256, search_width=8,
                                        n_entries=4, expanded=True)
     gi, gx, gsc = gi.cpu().numpy(), gx.cpu().numpy(), gsc.cpu().numpy()
-    same = 0
     for q in range(len(Qb)):
         o = graph.search(Xb, nbr, Qb[q], 10, L=256, w=8, entries=ent[q], T=10_000)
         assert o["iterations"] * 8 * 32 > 6144          # the table was reset at least once
-        same += np.array_equal(gi[q], o["ids"]) and gx[q] == o["expanded"]
-    assert same >= 0.9 * len(Qb), same
+        same = np.array_equal(gi[q], o["ids"]) and gx[q] == o["expanded"]
+        assert same or not o["certified"], q
     assert np.all(gsc >= gx)
     idx.free()
 
@@ -221,19 +223,19 @@ def test_fp8_navigation_matches_oracle(sa, small):
     X8 = ofp8.quantize_corpus(Xb)[0]
     ent = entries_of(idx, Qb, 4)
     Qd = bits_to_tensor(Qb).cuda()
-    same, rec = 0, []
+    rec = []
     for L, w in ((32, 2), (96, 4)):
         gi, gs, gx, _ = idx.search_graph(Qd, 10, L, search_width=w, n_entries=4, expanded=True,
                                          fp8=True)
         gi, gs, gx = gi.cpu().numpy(), gs.cpu().numpy(), gx.cpu().numpy()
         for q in range(len(Qb)):
             o = graph.search_fp8(Xb, nbr, Qb[q], 10, L=L, w=w, entries=ent[q], T=10_000, X8=X8)
-            same += np.array_equal(gi[q], o["ids"]) and gx[q] == o["expanded"]
+            same = np.array_equal(gi[q], o["ids"]) and gx[q] == o["expanded"]
+            assert same or not o["certified"], (L, w, q)
             rec.append(len(set(gi[q]) & set(o["ids"])) / 10)
             ps = oracle.pair_scores(Xb, Qb[q:q + 1], np.zeros(10, int), gi[q])
             assert np.all(np.abs(ps - gs[q]) <= 1e-3 * np.maximum(np.abs(ps), 1e-3))
             assert np.all(np.diff(gs[q]) <= 0) and len(set(gi[q].tolist())) == 10
-    assert same >= 0.9 * 2 * len(Qb), same
     assert np.mean(rec) >= 0.99
     hi, hs = idx.search_graph_host(Qd.cpu().pin_memory(), 10, 96, search_width=4, n_entries=4,
                                    fp8=True)

@@ -89,41 +89,43 @@ def test_trace_and_exit_match_oracle(sa, mixture):
     rq, ema = rq.cpu().numpy(), ema.cpu().numpy()
     # tau = inf never exits: the plain search, bit-exactly
     assert np.array_equal(gi.cpu().numpy(), pi) and torch.equal(gs, ps)
-    same = 0
-    taus = []
+    taus, certified, err = [], set(), 0.0
     for q in range(len(Qb)):
         o = graph.search(Xb, nbr, Qb[q], 10, L=L, w=w, entries=ent[q], T=10_000,
                          tau=math.inf, window=W)
-        if not (np.array_equal(pi[q], o["ids"]) and px[q] == o["expanded"]):
+        same = np.array_equal(pi[q], o["ids"]) and px[q] == o["expanded"]
+        # identical path unless the oracle's path crosses a near-tie the fp32 error bound
+        # cannot separate (oracle/graph.py `certified`); only then may traces differ
+        assert same or not o["certified"], q
+        if not o["certified"]:
             continue
-        same += 1
+        certified.add(q)
         n = o["iterations"]
         assert st[q] == n
         assert np.all(np.abs(rq[q, :n] - o["rq"]) <= 2e-3), q
         assert np.all(np.abs(ema[q, :n] - o["ema"]) <= 2e-3), q
         assert np.isnan(rq[q, n:]).all()
+        err = max(err, float(np.abs(ema[q, :n] - o["ema"]).max()))
         taus.append(np.median(o["ema"]))
-    assert same >= 0.9 * len(Qb), same
-    # a finite tau: exit steps agree with the oracle's unless its EMA is within 2e-3 of tau
+    print(f"graph maturity: {len(certified)} of {len(Qb)} paths certified, max EMA error {err:.2e}")
+    # a finite tau: on certified paths the exit step equals the oracle's unless its EMA at a
+    # checkpoint lies within the measured GPU-vs-oracle EMA error (x4) of tau
+    band = 4 * max(err, 1e-9)
     tau = float(np.median(taus))
     for g in (1, 3):
         gi, gs, st = idx.search_graph_mature(Qd, 10, L, tau=tau, window=W, check_every=g,
                                              search_width=w, n_entries=4)
         st = st.cpu().numpy()
         agree = checked = 0
-        for q in range(len(Qb)):
+        for q in sorted(certified):
             o = graph.search(Xb, nbr, Qb[q], 10, L=L, w=w, entries=ent[q], T=10_000,
                              tau=tau, window=W, g=g)
-            if not (np.array_equal(pi[q], graph.search(Xb, nbr, Qb[q], 10, L=L, w=w,
-                                                       entries=ent[q], T=10_000)["ids"])):
-                continue
             e = o["ema"]
-            cps = [t for t in range(g, len(e) + 1, g)]
-            if any(abs(e[t - 1] - tau) <= 2e-3 for t in cps):
+            if any(abs(e[t - 1] - tau) <= band for t in range(g, len(e) + 1, g)):
                 continue
             checked += 1
             agree += st[q] == o["iterations"]
-        assert checked >= 0.5 * len(Qb) and agree == checked, (g, agree, checked)
+        assert agree == checked and checked >= len(certified) - 2, (g, agree, checked)
 
 
 def test_prefix_property_and_readiness(sa, mixture):

@@ -153,3 +153,20 @@ def test_gr7_fp8_exhaustive_is_bf16_brute_force_over_reachable():
         r = graph.search_fp8(Xb, nbr, Qb[i], 10, L=300, w=4, entries=[0], T=10_000)
         assert r["ids"].tolist() == reach[ids[i]].tolist()
         assert np.allclose(r["scores"], sc[i], rtol=0, atol=1e-12)
+
+
+def test_gr8_certified_paths():
+    """The oracle's certification of its own search path (used by the GPU parity tests to tell
+    legitimate fp32-vs-fp64 near-tie divergence from a defect): GR2's path separates every
+    decision by >= 0.125 >> the fp32 error bound -> certified; two identical rows (different
+    ids) competing for the result order tie exactly -> not certified."""
+    X, nbr, q = path_graph()
+    assert graph.search(X, nbr, q[0], 2, L=2, w=1, entries=[0], T=100)["certified"]
+    Xd = bits([[0.25, 0.0], [0.5, 0.25], [0.5, 0.25]])
+    nb = np.array([[1, 2], [0, -1], [0, -1]])
+    r = graph.search(Xd, nb, bits([[1.0, 1.0]])[0], 2, L=2, w=1, entries=[0], T=100)
+    assert r["ids"].tolist() == [1, 2] and not r["certified"] and r["near_tie"] == 0.0
+    # a gap above the bound is certified even when tiny in absolute terms
+    Xg = bits([[0.25, 0.0], [0.5, 0.25], [0.5, 0.2421875]])
+    r = graph.search(Xg, nb, bits([[1.0, 1.0]])[0], 2, L=2, w=1, entries=[0], T=100)
+    assert r["ids"].tolist() == [1, 2] and r["certified"]

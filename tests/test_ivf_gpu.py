@@ -167,3 +167,103 @@ def test_p12_recall_monotone(sa, mixture_index):
         assert np.all(rec >= prev - 1e-9)
         prev = rec
     assert prev.mean() == 1.0
+
+
+def test_kmeans_mixture_steps_match_oracle(sa):
+    """k-means on realistic data: on a 40k-row mixture, the GPU's
+    initial centroids equal the oracle's bit for bit, and each of the first two Lloyd
+    iterations, started from the GPU's own previous centroids, equals the oracle's step
+    (oracle/ivf.lloyd_step) on every list no ambiguous row touches.  A row is ambiguous when
+    its best and second-best centroid scores are closer than twice the fp32 accumulation
+    bound of both, 2 * (d - 1) * 2^-24 * sum_j |x_j c_j| (the GPU decides on fp32 tensor-core
+    scores of exact bf16 products, the oracle in fp64); decisions with larger margins must
+    agree.  Unaffected centroids agree within 1e-5 (fp32 member sums); at least 3/4 of the
+    lists are compared in each iteration."""
+    mx = make_mixture(d=128, C=16, r=16, s_n=0.7)
+    Xb = to_bf16_bits(draw_rows(mx, 40_000, row_seed=91))
+    nlist = 64
+    Xd = bits_to_tensor(Xb).cuda()
+    rows = ivf.sample_rows(Xb.shape[0], nlist)
+    S = oracle.bf16_to_f64(Xb[rows])
+    C0_or = ivf.kmeans(Xb, nlist, iters=0)[0]
+    prev = None
+    touched_total = 0
+    for it in range(3):
+        idx = sa.Index.build(Xd, nlist, kmeans_iters=it)
+        Cg = idx.export_centroids().astype(np.float64)
+        idx.free()
+        if it == 0:
+            assert np.array_equal(Cg, C0_or)          # R9 init: sample rows, widened exactly
+        else:
+            C_or, a, margin = ivf.lloyd_step(S, prev)
+            Cb = oracle.bf16_to_f64(ivf.centroids_bf16(prev))
+            second = np.argsort(-(S @ Cb.T), axis=1)[:, 1]
+            d = S.shape[1]
+            absum = np.abs(S) @ np.abs(Cb).T
+            eb = 2 * (d - 1) * 2.0 ** -24 * (absum[np.arange(len(S)), a] +
+                                             absum[np.arange(len(S)), second])
+            amb = np.nonzero(margin <= eb)[0]
+            touched = set(a[amb].tolist()) | set(second[amb].tolist())
+            empty = [j for j in range(nlist) if not np.any(a == j)]
+            if empty:   # the repair depends on every row's score: compare only when unambiguous
+                assert amb.size == 0
+            ok = [j for j in range(nlist) if j not in touched]
+            assert len(ok) >= 3 * nlist // 4, (it, len(touched), amb.size)
+            assert np.abs(Cg[ok] - C_or[ok]).max() < 1e-5, it
+            touched_total += len(touched)
+        prev = Cg
+    print(f"k-means steps: {touched_total} list(s) touched by ambiguous rows over 2 iterations")
+
+
+def test_t1_error_paths_on_live_index(sa):
+    """SURVEY §8(b) conventions on a LIVE index (not just a null handle): each invalid call
+    returns its status and leaves the outputs untouched (validation is synchronous and side-
+    effect free); nprobe > 0 on a flat index is SA_ERR_STATE; k beyond the candidates is legal
+    and padded."""
+    mx = make_mixture(d=64, C=4, r=8, s_n=0.7)
+    X = draw_rows(mx, 3000, row_seed=93).cuda().to(torch.bfloat16)
+    Q = draw_rows(mx, 5, row_seed=94).cuda().to(torch.bfloat16)
+    flat = sa.Index.build(X)
+    ivfi = sa.Index.build(X, 8, kmeans_iters=2)
+    L = sa.lib()
+    ids = torch.full((5, 300), 123, dtype=torch.int64, device="cuda")
+    sc = torch.full((5, 300), 4.5, device="cuda")
+    st = sa._stream_ptr(None)
+
+    def call(idx, q, nq, k, nprobe, qdt=sa.SA_BF16):
+        r = L.sa_search_ex(idx.handle, q, qdt, nq, k, nprobe, sa._ptr(ids), sa._ptr(sc), st)
+        torch.cuda.synchronize()
+        return r
+
+    cases = [(flat, sa._ptr(Q), 5, 0, 0, sa.SA_ERR_INVALID_ARG),     # k = 0
+             (flat, sa._ptr(Q), 5, 257, 0, sa.SA_ERR_INVALID_ARG),   # k > 256
+             (flat, sa._ptr(Q), 0, 10, 0, sa.SA_ERR_INVALID_ARG),    # nq = 0
+             (flat, sa._ptr(Q), -3, 10, 0, sa.SA_ERR_INVALID_ARG),   # nq < 0
+             (flat, None, 5, 10, 0, sa.SA_ERR_INVALID_ARG),          # null queries
+             (flat, sa._ptr(Q), 5, 10, 1, sa.SA_ERR_STATE),          # nprobe > 0 on a flat index
+             (ivfi, sa._ptr(Q), 5, 10, 9, sa.SA_ERR_INVALID_ARG),    # nprobe > nlist
+             (ivfi, sa._ptr(Q), 5, 10, -1, sa.SA_ERR_INVALID_ARG),   # nprobe < 0
+             (ivfi, sa._ptr(Q), 5, 10, 4, sa.SA_ERR_INVALID_ARG, 7)]  # bad dtype code
+    for c in cases:
+        idx, q, nq, k, nprobe, want = c[:6]
+        qdt = c[6] if len(c) > 6 else sa.SA_BF16
+        assert call(idx, q, nq, k, nprobe, qdt) == want, c
+        assert sa.last_error() != ""
+        assert bool((ids == 123).all()) and bool((sc == 4.5).all()), c   # outputs untouched
+    # host-buffer and fp8 entry points validate the same way
+    hq = Q.cpu()
+    hi = torch.full((5, 10), 9, dtype=torch.int64)
+    hs = torch.zeros(5, 10)
+    assert L.sa_search_host(flat.handle, sa._ptr(hq), sa.SA_BF16, 5, 0, 0, sa._ptr(hi),
+                            sa._ptr(hs), st) == sa.SA_ERR_INVALID_ARG
+    assert bool((hi == 9).all())
+    assert L.sa_search_fp8(flat.handle, sa._ptr(Q), sa.SA_BF16, 5, 10, 0, 16, sa._ptr(ids),
+                           sa._ptr(sc), st) == sa.SA_ERR_STATE          # no fp8 copy built
+    assert bool((ids == 123).all())
+    # legal edge: k > n_local pads with (-1, -inf); k = n returns every row once
+    small = sa.Index.build(X[:7].contiguous())
+    gi, gs = small.search(Q, 12)
+    assert (gi[:, 7:] == -1).all() and torch.isinf(gs[:, 7:]).all()
+    assert all(sorted(r) == list(range(7)) for r in gi[:, :7].cpu().tolist())
+    for i in (flat, ivfi, small):
+        i.free()
