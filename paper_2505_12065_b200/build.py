@@ -20,9 +20,9 @@ NVCC_FLAGS = [
 ]
 
 
-# flat_scan_topk_kernel runs 320 threads at 1 CTA/SM: 65536 / 320 = 204 registers are
+# flat_scan_topk_kernel runs 352 threads at 1 CTA/SM: 65536 / 352 = 186 registers are
 # available; let ptxas use them instead of spilling the epilogue's state.
-PER_FILE_FLAGS = {"flat_scan.cu": ["-maxrregcount=200"]}
+PER_FILE_FLAGS = {"flat_scan.cu": ["-maxrregcount=184"]}
 
 
 def sources():

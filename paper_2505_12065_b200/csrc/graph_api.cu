@@ -21,11 +21,6 @@ using namespace sa;
 
 namespace {
 
-#define SA_TRY(expr)              \
-  do {                            \
-    sa_status _st = (expr);       \
-    if (_st != SA_OK) return _st; \
-  } while (0)
 
 struct DevFree {
   std::vector<void*> p;

@@ -185,6 +185,37 @@ sa_status dalloc(T** p, size_t count, cudaStream_t s, const char* what) {
   return cuda_status(cudaMallocAsync(reinterpret_cast<void**>(p), count * sizeof(T), s), what);
 }
 
+// Stream-ordered scratch that is released (cudaFreeAsync on s) when the scope ends, on every
+// return path.
+struct StreamFreer {
+  cudaStream_t s;
+  std::vector<void*> ptrs;
+  StreamFreer(const StreamFreer&) = delete;
+  StreamFreer& operator=(const StreamFreer&) = delete;
+  ~StreamFreer() {
+    for (void* p : ptrs)
+      if (p) cudaFreeAsync(p, s);
+  }
+  template <typename T>
+  T* add(T* p) {
+    ptrs.push_back(p);
+    return p;
+  }
+  template <typename T>
+  sa_status alloc(T** p, size_t count, const char* what) {
+    sa_status st = dalloc(p, count, s, what);
+    if (st == SA_OK) ptrs.push_back(*p);
+    return st;
+  }
+};
+
+#define SA_TRY(expr)                   \
+  do {                                 \
+    sa_status _st = (expr);            \
+    if (_st != SA_OK) return _st;      \
+  } while (0)
+#define SA_CUDA(expr, what) SA_TRY(::sa::cuda_status((expr), (what)))
+
 // IVF (ivf.cu)
 sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s);
 // Q8: optional staged e4m3 queries [nq, d8_pad] -> the list scan runs on the e4m3 copy and
@@ -195,5 +226,10 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
                      const uint8_t* Q8 = nullptr);
 sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
                     int32_t nprobe, int32_t* out_lists, cudaStream_t s);
+// Agent-step batches (nq <= 8, k <= 32, nprobe <= 256): the one-launch IVF search straight
+// from the caller's bf16 / fp32 queries (kernels/ivf_small.cu)
+bool ivf_small_applies(const sa_index* idx, int64_t nq, int32_t k, int32_t nprobe);
+sa_status ivf_small_search(const sa_index* idx, const void* queries, bool q_f32, int64_t nq,
+                           int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s);
 
 }  // namespace sa

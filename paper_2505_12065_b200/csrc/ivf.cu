@@ -18,6 +18,7 @@
 #include "kernels/flat_scan.cuh"
 #include "kernels/ivf_kernels.cuh"
 #include "kernels/ivf_scan.cuh"
+#include "kernels/ivf_small.cuh"
 #include "kernels/merge.cuh"
 
 namespace sa {
@@ -29,32 +30,11 @@ namespace {
 constexpr int kChunkRows = 4096;
 constexpr int kChunkRowsSmall = 256;
 
-struct Freer {
-  cudaStream_t s;
-  std::vector<void*> ptrs;
-  ~Freer() {
-    for (void* p : ptrs)
-      if (p) cudaFreeAsync(p, s);
-  }
-  template <typename T>
-  T* add(T* p) {
-    ptrs.push_back(p);
-    return p;
-  }
-};
-
-#define SA_TRY(expr)                   \
-  do {                                 \
-    sa_status _st = (expr);            \
-    if (_st != SA_OK) return _st;      \
-  } while (0)
-#define SA_CUDA(expr, what) SA_TRY(cuda_status((expr), (what)))
-
 // Stable sort of rows by list id + CSR offsets: perm = rows in list-major order (ascending row
 // inside a list), off[nlist + 1].
 sa_status sort_by_list(const int64_t* ids, int64_t n, int nlist, int num_sms, int32_t* perm,
                        int64_t* off, cudaStream_t s) {
-  Freer f{s};
+  StreamFreer f{s};
   int32_t *keys, *ktmp, *vtmp, *kout;
   int64_t *counts, *offs, *scratch, *hist;
   const int64_t cs = sort_counts_size(n);
@@ -94,7 +74,7 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   const int64_t n_total = idx->n_total;
   const sa_comm* comm = (idx->comm && idx->comm->world > 1) ? idx->comm : nullptr;
   const int64_t n_train = std::min<int64_t>(n_total, (int64_t)o.train_per_list * nlist);
-  Freer f{s};
+  StreamFreer f{s};
 
   SA_CUDA(cudaMalloc(&idx->centroids, (size_t)nlist * dp * sizeof(float)), "alloc centroids");
   SA_CUDA(cudaMalloc(&idx->centroids_bf16, (size_t)nlist * dp * sizeof(__nv_bfloat16)),
@@ -253,7 +233,7 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
 // Sorted packed keys [nq, nprobe] (list id in the key).
 static sa_status probe_keys(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq,
                             int32_t nprobe, uint64_t* pkeys, cudaStream_t s) {
-  Freer f{s};
+  StreamFreer f{s};
   float* sc;
   SA_TRY(dalloc(&sc, (size_t)nq * idx->nlist, s, "alloc probe scores"));
   f.add(sc);
@@ -272,13 +252,47 @@ static sa_status probe_keys(const sa_index* idx, const __nv_bfloat16* Qs, int64_
 sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
                     int32_t nprobe, int32_t* out_lists, cudaStream_t s) {
   (void)nq_pad;
-  Freer f{s};
+  StreamFreer f{s};
   uint64_t* pkeys;
   SA_TRY(dalloc(&pkeys, (size_t)nq * nprobe, s, "alloc probe keys"));
   f.add(pkeys);
   SA_TRY(probe_keys(idx, Qs, nq, nprobe, pkeys, s));
   SA_CUDA(launch_keys_to_lists(pkeys, nq * nprobe, nullptr, out_lists, idx->num_sms, s), "lists");
   return SA_OK;
+}
+
+bool ivf_small_applies(const sa_index* idx, int64_t nq, int32_t k, int32_t nprobe) {
+  return idx->nlist > 0 && idx->row_ids && nq >= 1 && nq <= IVSM_MAX_NQ && k <= IVSM_MAX_K &&
+         nprobe >= 1 && nprobe <= IVSM_MAX_NPROBE && idx->num_sms >= nq;
+}
+
+// Agent-step batches: probe + list scan + merge in one cooperative launch (ivf_small.cu),
+// straight from the caller's queries (no staging kernel).
+sa_status ivf_small_search(const sa_index* idx, const void* queries, bool q_f32, int64_t nq,
+                           int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s) {
+  const int grid = idx->num_sms;
+  StreamFreer f{s};
+  IvfSmallArgs a{};
+  SA_TRY(f.alloc(&a.psc, (size_t)nq * idx->nlist, "ivf small scratch"));
+  SA_TRY(f.alloc(&a.probes, (size_t)nq * nprobe, "ivf small scratch"));
+  SA_TRY(f.alloc(&a.cand, (size_t)grid * nq * k, "ivf small scratch"));
+  a.Q = queries;
+  a.q_f32 = q_f32 ? 1 : 0;
+  a.nq = (int32_t)nq;
+  a.d = idx->d;
+  a.d_pad = idx->d_pad;
+  a.C = idx->centroids_bf16;
+  a.nlist = idx->nlist;
+  a.nprobe = nprobe;
+  a.X = idx->X;
+  a.list_off = idx->list_off;
+  a.row_ids = idx->row_ids;
+  a.k = k;
+  a.out_keys = out.keys;
+  a.out_ids = out.ids;
+  a.out_scores = out.scores;
+  ProfRegion prof_region(SA_KERNEL_IVF_SCAN, s);
+  return cuda_status(launch_ivf_small(a, grid, s), "ivf small-batch search");
 }
 
 sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, int64_t nq_pad,
@@ -288,7 +302,7 @@ sa_status ivf_search(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, i
   const int nlist = idx->nlist;
   const int sms = idx->num_sms;
   const int64_t np = nq * nprobe;
-  Freer f{s};
+  StreamFreer f{s};
   // ---- a7: probe = top-nprobe centroids per query on the tensor cores
   uint64_t* pkeys;
   int64_t* probes;

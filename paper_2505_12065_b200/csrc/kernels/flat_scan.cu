@@ -25,7 +25,14 @@
 //   * warps 0..7: epilogue -- thread = (query, column half),
 //     each with a size-k min-heap of packed keys; per tile the fast path is
 //     a 64-way max and one compare against the heap root; warp 8: TMA producer;
-//     warp 9: TMEM alloc + MMA issuer (leader CTA).
+//     warp 9: TMEM alloc + MMA issuer (leader CTA); warp 10: bound warp.
+//   * pruning bounds (exact: a candidate below a lower bound of the query's final
+//     k-th score can never be returned; ties pass): q_hint = max of the published
+//     heap roots, and the k-th largest of the heaps' BEST scores, computed by the
+//     bound warp -- the heaps of a query cover disjoint rows, so k heaps' maxima are
+//     k distinct candidates.  With ~100 heaps per query the latter tracks the k-th
+//     best of every row scanned so far, so the per-tile slow path (a heap insert)
+//     stays rare even while each heap is still filling.
 //   * persistent grid: work item = (query group, corpus slice); partial
 //     lists go to part[q][slice][half][k] and are merged by merge.cu.
 //   (The IVF list scan, §8(a) a8, has its own kernel: ivf_scan.cu.)
@@ -52,6 +59,7 @@ constexpr int kKbPerStage = 2;
 // vs 8; 2 gives 32.3 GB but no faster)
 constexpr int kLockstepLag = 4;
 constexpr int kLockstepSpinCap = 1 << 14;   // sleeps of one lockstep wait before pacing stops
+constexpr int kBoundMaxK = 16;              // the bound warp serves k <= 16 (smem heaps)
 
 template <int CG, bool F8 = false>
 struct Cfg {
@@ -71,6 +79,10 @@ struct __align__(8) SmemTail {
   uint64_t tmem_empty[2];
   uint64_t a_full;
   uint64_t a_tma;
+  // bound warp -> epilogue: (query group << 32 | ordered k-th-of-maxima) per CTA query row
+  uint64_t bound[FS_BM];
+  int32_t bw_qkey;     // query group the epilogue is on (-1 none yet, -2 finished)
+  int32_t tiles_done;  // tiles the epilogue (warp 0) has consumed
   uint32_t tmem_base;
 };
 
@@ -144,6 +156,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
   // slot over the two epilogue warps that share it.
   constexpr int kProducerWarp = FS_EPI_WARPS;
   constexpr int kMmaWarp = FS_EPI_WARPS + 1;
+  constexpr int kBoundWarp = FS_EPI_WARPS + 2;
   const int lane = threadIdx.x % 32;
   const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
   const bool leader = rank == 0;
@@ -169,9 +182,13 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     }
     ptx::mbar_init(ptx::smem_u32(&tail->a_full), FS_EPI_WARPS * CG);
     ptx::mbar_init(ptx::smem_u32(&tail->a_tma), 1);
+    tail->bw_qkey = -1;
+    tail->tiles_done = 0;
     ptx::fence_mbar_init();
     ptx::fence_proxy_async_smem();
   }
+  if (warp == kBoundWarp)
+    for (int i = lane; i < FS_BM; i += 32) tail->bound[i] = 0ull;
   if (warp == kProducerWarp && lane == 0) {
     ptx::prefetch_tmap(&tmap_x);
     if (kb_s > 0) ptx::prefetch_tmap(&tmap_q);
@@ -328,6 +345,74 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       }
     }
     __syncwarp();
+  } else if (warp == kBoundWarp) {
+    // ===================== bound warp: k-th largest of the heaps' best scores ================
+    // Lane i refreshes rows i, i+32, ... of the CTA's current query block: it reads the
+    // query's q_max row (the best score of each of its heaps, published by the epilogue) and
+    // keeps the k largest in a sorted register list; the k-th is a lower bound of the query's
+    // final k-th score (k distinct rows).  Rounds run after the epilogue has processed 1, 2,
+    // 4, 8, ... tiles of the current query block: the maxima move fast early and rarely
+    // later, and each round reads every query's row from L2 (which the corpus stream needs).
+    const int k = a.k;
+    if (!DUMP && a.q_max != nullptr && k <= kBoundMaxK) {
+      const int H = a.q_max_stride;
+      int cur = -1, next_at = 0;
+      while (true) {
+        const int qkey = *reinterpret_cast<volatile int32_t*>(&tail->bw_qkey);
+        if (qkey == -2) break;
+        const int done = *reinterpret_cast<volatile int32_t*>(&tail->tiles_done);
+        if (qkey != cur) {
+          cur = qkey;
+          next_at = done + 1;
+        }
+        if (qkey >= 0 && done >= next_at) {
+          next_at = done + (done > 1 ? done : 1);
+          for (int i = lane; i < FS_BM; i += 32) {
+            const int64_t q = ((int64_t)qkey * CG + rank) * kBM + i;
+            if (q >= a.nq) break;
+            // descending top-k list in registers (static indices only), kth = its k-th entry
+            uint32_t t[kBoundMaxK];
+#pragma unroll
+            for (int j = 0; j < kBoundMaxK; ++j) t[j] = 0u;
+            uint32_t kth = 0u;
+            // the row (stride a multiple of 4 words) in batches of 32 values: all 8 vector
+            // loads of a batch are issued before any is used (one L2 round trip per batch)
+            const uint4* row = reinterpret_cast<const uint4*>(a.q_max + q * H);
+            for (int h0 = 0; h0 < H / 4; h0 += 8) {
+              uint4 vb[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                vb[u] = h0 + u < H / 4 ? ptx::ld_relaxed_gpu_v4(row + h0 + u)
+                                       : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+              for (int u = 0; u < 32; ++u) {
+                const uint4& w4 = vb[u >> 2];
+                uint32_t v = (u & 3) == 0 ? w4.x : (u & 3) == 1 ? w4.y : (u & 3) == 2 ? w4.z : w4.w;
+                if (v <= kth) continue;
+#pragma unroll
+                for (int j = 0; j < kBoundMaxK; ++j) {   // insert into the descending list
+                  const uint32_t hi = v > t[j] ? v : t[j];
+                  v = v > t[j] ? t[j] : v;
+                  t[j] = hi;
+                }
+                // kth = t[k - 1] = the smallest of the first k entries (a min, not an index:
+                // t stays in registers)
+                kth = 0xFFFFFFFFu;
+#pragma unroll
+                for (int j = 0; j < kBoundMaxK; ++j)
+                  kth = min(kth, t[j] | (j < k ? 0u : 0xFFFFFFFFu));
+              }
+            }
+            if (kth != 0u)
+              *reinterpret_cast<volatile uint64_t*>(&tail->bound[i]) =
+                  ((uint64_t)(uint32_t)qkey << 32) | kth;
+            if (*reinterpret_cast<volatile int32_t*>(&tail->bw_qkey) != qkey) break;
+          }
+        }
+        __nanosleep(500);
+      }
+    }
+    __syncwarp();
   } else {
     // ===================== epilogue: 8 warps, thread = (query, column half) =====================
     const int ew = warp;                     // epilogue warp 0..7
@@ -360,6 +445,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // arrive on a_full.  Callers guarantee every MMA that read the previous block has
     // completed (they consumed that block's last tmem_full).
     auto stage_a = [&](int qkey) __attribute__((always_inline)) {
+      if (ew == 0 && lane == 0) *reinterpret_cast<volatile int32_t*>(&tail->bw_qkey) = qkey;
       const int64_t q_row = ((int64_t)qkey * CG + rank) * kBM + rib;
       const bool q_ok = q_row < a.nq;
       const bool tma_thread = ew == 0 && lane == 0 && kb_s > 0;
@@ -425,9 +511,16 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       }
       thr = fmaxf(thr, hint);
       uint32_t h_next = 0u;   // the bound, loaded one tile before it is used (L2 latency hidden)
+      // this heap's best score so far (ordered), published to q_max for the bound warp
+      uint32_t best_o = 0u;
+      uint32_t* const my_max =
+          a.q_max ? a.q_max + q * a.q_max_stride + wi.s * FS_LISTS_PER_ITEM + half : nullptr;
       for (int32_t t = wi.t0; t < wi.t1; ++t) {
-        if (valid && a.q_hint && ((t - wi.t0) & 3) == 3 && h_next != 0u) {
-          hint = fmaxf(hint, float_from_ordered(h_next));
+        if (valid && ((t - wi.t0) & 3) == 3) {
+          if (a.q_hint && h_next != 0u) hint = fmaxf(hint, float_from_ordered(h_next));
+          const uint64_t b = *reinterpret_cast<volatile uint64_t*>(&tail->bound[rib]);
+          if ((uint32_t)(b >> 32) == (uint32_t)wi.qkey && (uint32_t)b != 0u)
+            hint = fmaxf(hint, float_from_ordered((uint32_t)b));
           thr = fmaxf(thr, hint);
         }
         if (valid && a.q_hint && ((t - wi.t0) & 3) == 2) h_next = __ldcg(a.q_hint + q);
@@ -447,6 +540,10 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           else ptx::mbar_arrive(ptx::smem_u32(&tail->tmem_empty[acc]));
         }
         if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
+        if (ew == 0 && lane == 0) {
+          const int32_t td = *reinterpret_cast<volatile int32_t*>(&tail->tiles_done);
+          *reinterpret_cast<volatile int32_t*>(&tail->tiles_done) = td + 1;
+        }
         // The last accumulator of this item is in registers, so every MMA that read this
         // item's A operand has completed: stage the next item's queries now, before the
         // score processing, so the tensor core restarts as early as possible.
@@ -483,27 +580,45 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         }
         if (!valid || (a.experiment != 0 && a.experiment != 3)) continue;
 
-        float m0 = fmaxf(__uint_as_float(r0[0]), __uint_as_float(r0[1]));
-        float m1 = fmaxf(__uint_as_float(r1[0]), __uint_as_float(r1[1]));
+        // maxima of the 4 groups of 16 columns, then of the tile: a passing tile visits only
+        // the groups whose maximum passes (usually one), not all 64 columns
+        float gm[4];
 #pragma unroll
-        for (int j = 2; j < 32; j += 2) {
-          m0 = fmaxf(m0, fmaxf(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1])));
-          m1 = fmaxf(m1, fmaxf(__uint_as_float(r1[j]), __uint_as_float(r1[j + 1])));
+        for (int g = 0; g < 4; ++g) {
+          const uint32_t* r = g < 2 ? r0 : r1;
+          const int b = (g & 1) * 16;
+          float x = fmaxf(__uint_as_float(r[b]), __uint_as_float(r[b + 1]));
+#pragma unroll
+          for (int j = 2; j < 16; j += 2)
+            x = fmaxf(x, fmaxf(__uint_as_float(r[b + j]), __uint_as_float(r[b + j + 1])));
+          gm[g] = x;
         }
+        const float mt = fmaxf(fmaxf(gm[0], gm[1]), fmaxf(gm[2], gm[3]));
         if (a.experiment == 3) {   // timing experiment: the 64-way max only, no insertion
-          if (fmaxf(m0, m1) == 1234.5f) a.part[0] = 0ull;
+          if (mt == 1234.5f) a.part[0] = 0ull;
           continue;
         }
-        if (fmaxf(m0, m1) >= thr) {
+        if (mt >= thr) {
 #pragma unroll
-          for (int j = 0; j < 64; ++j) {
-            const float s = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
-            if (s >= thr) {
-              const int32_t row = row0 + j;
-              if (row < a.n_rows) {
-                const uint32_t id =
-                    a.id_base + (a.row_ids ? (uint32_t)a.row_ids[row] : (uint32_t)row);
-                thr = fmaxf(heap_offer(heap, k, make_key(s, id)), hint);
+          for (int g = 0; g < 4; ++g) {
+            if (gm[g] < thr) continue;
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int j = g * 16 + jj;
+              const float s = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
+              if (s >= thr) {
+                const int32_t row = row0 + j;
+                if (row < a.n_rows) {
+                  const uint32_t id =
+                      a.id_base + (a.row_ids ? (uint32_t)a.row_ids[row] : (uint32_t)row);
+                  const uint64_t key = make_key(s, id);
+                  thr = fmaxf(heap_offer(heap, k, key), hint);
+                  const uint32_t o = (uint32_t)(key >> 32);
+                  if (my_max && o > best_o) {
+                    best_o = o;
+                    ptx::st_relaxed_gpu_u32(my_max, o);
+                  }
+                }
               }
             }
           }
@@ -529,6 +644,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         thr = heap_threshold(0ull);
       }
     }
+    if (ew == 0 && lane == 0) *reinterpret_cast<volatile int32_t*>(&tail->bw_qkey) = -2;
   }
 
   ptx::tc_fence_before();

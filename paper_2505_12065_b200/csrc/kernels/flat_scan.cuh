@@ -12,7 +12,7 @@ constexpr int FS_BM = 128;       // query rows per CTA (TMEM lanes)
 constexpr int FS_BN = 128;       // corpus rows per tile (MMA N, accumulator columns)
 constexpr int FS_BK = 64;        // bf16 per 128-byte swizzle row (one TMA box column extent)
 constexpr int FS_EPI_WARPS = 8;  // two warps per TMEM lane quadrant, 64 columns each
-constexpr int FS_THREADS = 64 + 32 * FS_EPI_WARPS;  // 8 epilogue warps, TMA warp, MMA warp
+constexpr int FS_THREADS = 96 + 32 * FS_EPI_WARPS;  // 8 epilogue warps, TMA, MMA, bound warp
 constexpr int FS_EPI_THREADS = 32 * FS_EPI_WARPS;
 constexpr int FS_MAX_DPAD = 768; // queries: up to 8 K-blocks in TMEM + 4 in smem
 constexpr int FS_KB_TMEM = 8;    // K-blocks of the A operand held in TMEM (256 columns)
@@ -51,6 +51,10 @@ struct FlatScanArgs {
   int32_t mode;            // FlatScanMode
   uint32_t* q_hint;        // optional [nq] ordered-fp32 lower bound of each query's k-th score
                            // (zero-initialised by the caller; 0 = none)
+  uint32_t* q_max;         // optional [nq][q_max_stride] ordered-fp32 best score of each heap
+                           // of a query (heap index = slice * FS_LISTS_PER_ITEM + half; zeroed
+                           // by the caller): the bound warp's k-th-of-maxima bound (flat_scan.cu)
+  int32_t q_max_stride;    // >= S * FS_LISTS_PER_ITEM, a multiple of 4 (unused entries stay 0)
   int32_t* progress;       // optional [units] tile progress for soft lockstep (zeroed; one
                            // work item per unit and QP > 1)
   int32_t experiment;      // timing experiments only (tuning builds, SA_EXPERIMENT): 1 = skip score

@@ -77,11 +77,6 @@ sa_status palloc(MaturePlan& p, T** ptr, size_t count, const char* what) {
   return SA_OK;
 }
 
-#define SA_TRY(expr)              \
-  do {                            \
-    sa_status _st = (expr);       \
-    if (_st != SA_OK) return _st; \
-  } while (0)
 
 struct CaptureFlag {
   CaptureFlag() { set_capturing(true); }

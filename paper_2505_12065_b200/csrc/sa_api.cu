@@ -217,18 +217,23 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
                            int32_t k, const SearchOut& out, cudaStream_t s, bool prepass) {
   const int64_t nq_pad = padded_nq(nq);
   const FlatPlan p = plan_flat(cv.n_rows, num_sms, nq_pad);
-  uint64_t *part = nullptr, *heap = nullptr;
-  sa_status st = dalloc(&part, (size_t)nq_pad * p.S * FS_LISTS_PER_ITEM * k, s, "alloc partials");
-  if (st != SA_OK) return st;
-  if (k > fs_heap_smem_cap(cv.d_pad)) {
-    st = dalloc(&heap, (size_t)p.grid * k * FS_EPI_THREADS, s, "alloc heaps");
-    if (st != SA_OK) { cudaFreeAsync(part, s); return st; }
-  }
-  // shared per-query pruning bound, useful when a query's rows are split over slices
-  uint32_t* hint = nullptr;
+  StreamFreer f{s};
+  uint64_t *part, *heap = nullptr;
+  SA_TRY(f.alloc(&part, (size_t)nq_pad * p.S * FS_LISTS_PER_ITEM * k, "alloc partials"));
+  if (k > fs_heap_smem_cap(cv.d_pad))
+    SA_TRY(f.alloc(&heap, (size_t)p.grid * k * FS_EPI_THREADS, "alloc heaps"));
+  // Shared per-query pruning bounds, useful when a query's rows are split over slices:
+  // q_hint (max of the heap roots) and q_max (each heap's best score; the kernel's bound warp
+  // takes the k-th largest of them).
+  const int H = (p.S * FS_LISTS_PER_ITEM + 3) / 4 * 4;   // q_max row stride (16-byte rows)
+  uint32_t *hint = nullptr, *qmax = nullptr;
   if (p.S > 1) {
-    st = dalloc(&hint, (size_t)nq, s, "alloc hints");
-    if (st == SA_OK) st = cuda_status(cudaMemsetAsync(hint, 0, nq * sizeof(uint32_t), s), "memset");
+    SA_TRY(f.alloc(&hint, (size_t)nq, "alloc hints"));
+    SA_CUDA(cudaMemsetAsync(hint, 0, nq * sizeof(uint32_t), s), "memset");
+    if (k <= 16 && p.S * FS_LISTS_PER_ITEM >= k) {
+      SA_TRY(f.alloc(&qmax, (size_t)nq * H, "alloc heap maxima"));
+      SA_CUDA(cudaMemsetAsync(qmax, 0, (size_t)nq * H * sizeof(uint32_t), s), "memset");
+    }
     // Seed the bound before the scan: the k-th best score over the first m rows (a
     // sub-scan, ~1/32 of the corpus up to 2^18 rows) is a lower bound of the final k-th
     // score, so the running heaps start pruning at once instead of each filling its own k
@@ -251,53 +256,35 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
     // worth it only for long scans: the sub-scans cost ~0.3-0.5 ms whatever the corpus and
     // save ~7% (bf16) / ~11% (e4m3) of the scan (C3 one-GPU emulations of 2-8 shards)
     const int64_t min_rows = cv.fp8 ? (4ll << 20) : (8ll << 20);
-    if (st == SA_OK && prepass && !no_seed && m >= 8 * FS_BN &&
-        (cv.n_rows >= min_rows || seed_env > 0)) {
+    if (prepass && !no_seed && m >= 8 * FS_BN && (cv.n_rows >= min_rows || seed_env > 0)) {
       CorpusView pv = cv;
       pv.n_rows = m;
-      uint64_t* pk = nullptr;
-      st = dalloc(&pk, (size_t)nq * k, s, "alloc hint keys");
+      uint64_t* pk;
+      SA_TRY(f.alloc(&pk, (size_t)nq * k, "alloc hint keys"));
       ProfRegion region(SA_KERNEL_OTHER, s);   // the seed sub-scans count as OTHER
-      if (st == SA_OK) {
-        SearchOut po;
-        po.keys = pk;
-        // the sub-scan seeds its own bound the same way (m / 32 rows, ...): without it its
-        // heaps would pay the whole warm-up themselves
-        st = flat_search_view(pv, num_sms, Qs, nq, k, po, s, seed_recurse);
-      }
-      if (st == SA_OK) {
-        hint_from_keys_kernel<<<(unsigned)std::min<int64_t>((nq + 255) / 256, 1024), 256, 0, s>>>(
-            pk, nq, k, hint);
-        note_launch();
-        st = cuda_status(cudaGetLastError(), "hint seed");
-      }
-      if (pk) cudaFreeAsync(pk, s);
-    }
-    if (st != SA_OK) {
-      if (hint) cudaFreeAsync(hint, s);
-      if (heap) cudaFreeAsync(heap, s);
-      cudaFreeAsync(part, s);
-      return st;
+      SearchOut po;
+      po.keys = pk;
+      // the sub-scan seeds its own bound the same way (m / 32 rows, ...): without it its
+      // heaps would pay the whole warm-up themselves
+      SA_TRY(flat_search_view(pv, num_sms, Qs, nq, k, po, s, seed_recurse));
+      hint_from_keys_kernel<<<(unsigned)std::min<int64_t>((nq + 255) / 256, 1024), 256, 0, s>>>(
+          pk, nq, k, hint);
+      note_launch();
+      SA_CUDA(cudaGetLastError(), "hint seed");
     }
   }
   // soft lockstep of units sharing a corpus slice (see flat_scan.cu)
   int32_t* progress = nullptr;
   const int units = p.grid / p.cg;
   if (p.QP > 1 && p.S > 1 && (int64_t)p.QP * p.S <= units) {
-    st = dalloc(&progress, (size_t)units, s, "alloc progress");
-    if (st == SA_OK)
-      st = cuda_status(cudaMemsetAsync(progress, 0, units * sizeof(int32_t), s), "memset");
-    if (st != SA_OK) {
-      if (progress) cudaFreeAsync(progress, s);
-      if (hint) cudaFreeAsync(hint, s);
-      if (heap) cudaFreeAsync(heap, s);
-      cudaFreeAsync(part, s);
-      return st;
-    }
+    SA_TRY(f.alloc(&progress, (size_t)units, "alloc progress"));
+    SA_CUDA(cudaMemsetAsync(progress, 0, units * sizeof(int32_t), s), "memset");
   }
   FlatScanArgs a{};
   a.progress = progress;
   a.q_hint = hint;
+  a.q_max = qmax;
+  a.q_max_stride = H;
   a.Q = Qs;
   a.nq = nq;
   a.nq_pad = nq_pad;
@@ -325,39 +312,24 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
     a.lockstep_lag = lag;
   }
   CUtensorMap tmap_q;
-  st = make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM);
-  if (st != SA_OK) {
-    if (progress) cudaFreeAsync(progress, s);
-    if (hint) cudaFreeAsync(hint, s);
-    if (heap) cudaFreeAsync(heap, s);
-    cudaFreeAsync(part, s);
-    return st;
-  }
+  SA_TRY(make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM));
   const CUtensorMap& tm = p.cg == 2 ? *cv.tmap2 : *cv.tmap1;
-  cudaError_t e;
   {
     ProfRegion region(SA_KERNEL_FLAT_SCAN, s);
-    e = launch_flat_scan(tm, tmap_q, a, p.cg, p.grid, s);
+    SA_CUDA(launch_flat_scan(tm, tmap_q, a, p.cg, p.grid, s), "flat search launch");
   }
-  if (e == cudaSuccess) {
-    MergeArgs m{};
-    m.cand = part;
-    m.groups = p.S * FS_LISTS_PER_ITEM;
-    m.k = k;
-    m.qstride = (int64_t)p.S * FS_LISTS_PER_ITEM * k;
-    m.gstride = k;
-    m.out_keys = out.keys;
-    m.out_ids = out.ids;
-    m.out_scores = out.scores;
-    m.id_offset = 0;
-    ProfRegion region(SA_KERNEL_MERGE, s);
-    e = launch_merge(m, nq, s);
-  }
-  if (heap) cudaFreeAsync(heap, s);
-  if (hint) cudaFreeAsync(hint, s);
-  if (progress) cudaFreeAsync(progress, s);
-  cudaFreeAsync(part, s);
-  return cuda_status(e, "flat search launch");
+  MergeArgs mg{};
+  mg.cand = part;
+  mg.groups = p.S * FS_LISTS_PER_ITEM;
+  mg.k = k;
+  mg.qstride = (int64_t)p.S * FS_LISTS_PER_ITEM * k;
+  mg.gstride = k;
+  mg.out_keys = out.keys;
+  mg.out_ids = out.ids;
+  mg.out_scores = out.scores;
+  mg.id_offset = 0;
+  ProfRegion region(SA_KERNEL_MERGE, s);
+  return cuda_status(launch_merge(mg, nq, s), "flat search merge");
 }
 
 sa_status flat_scores_view(const CorpusView& cv, int num_sms, const __nv_bfloat16* Qs, int64_t nq,
@@ -535,6 +507,8 @@ static sa_status validate_search(const sa_index* idx, const void* q, int64_t nq,
 static sa_status search_local(const sa_index* idx, const void* queries, sa_dtype qdtype,
                               int64_t nq, int32_t k, int32_t nprobe, const SearchOut& out,
                               cudaStream_t s) {
+  if (nprobe > 0 && ivf_small_applies(idx, nq, k, nprobe))
+    return ivf_small_search(idx, queries, qdtype == SA_F32, nq, k, nprobe, out, s);
   const int64_t nq_pad = padded_nq(nq);
   __nv_bfloat16* Qs = nullptr;
   sa_status st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "alloc staged queries");
