@@ -403,6 +403,16 @@ sa_status sa_search_probes(const sa_index* idx, const void* queries, int64_t nq,
  * [nq, n_local], columns in stored-row order (tests of the tensor-core path only). */
 sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, float* out_scores,
                           void* stream);
+/* Debug: the one-launch agent-step IVF search (nq <= 8; DESIGN.md §4.2 "small batches") with
+ * per-CTA phase timestamps.  queries DEVICE bf16 [nq, d]; out_ids / out_scores DEVICE as in
+ * sa_search; host_ns HOST int64 [grid * 8] receives %globaltimer (ns) per CTA at: 0 start,
+ * 1 centroid keys done, 2 probe candidates appended, 3 probe sets known, 4 list scan done,
+ * 5 final merge done (last CTA only; 0 elsewhere), 6 first centroid piece scored, 7 first list
+ * piece arrived; *host_grid = grid (<= 1024).  Synchronous.
+ * SA_ERR_UNSUPPORTED when the one-launch path does not apply to (nq, k, nprobe). */
+sa_status sa_debug_small_phases(const sa_index* idx, const void* queries, int64_t nq, int32_t k,
+                                int32_t nprobe, int64_t* out_ids, float* out_scores,
+                                int64_t* host_ns, int32_t* host_grid, void* stream);
 
 /* ---- kernel accounting (bench.py) ----
  * When enabled, every kernel launch is counted per kind and the dominant

@@ -135,6 +135,7 @@ def lib() -> ctypes.CDLL:
         "sa_search_mature": (st, [P, P, ctypes.c_int, i64, i32, i32, ctypes.POINTER(_MaturityOpts),
                                   P, P, P, P, P, P]),
         "sa_debug_scores": (st, [P, P, i64, P, P]),
+        "sa_debug_small_phases": (st, [P, P, i64, i32, i32, P, P, P, P, P]),
         "sa_profile_enable": (st, [i32]),
         "sa_profile_read": (st, [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]),
     }
@@ -341,8 +342,8 @@ class Index:
             raise SAError(SA_ERR_INVALID_ARG, f"queries have d={queries.shape[1]}, index d={self.d}")
         nq = queries.shape[0]
         if out is None:
-            ids = torch.empty(nq, k, dtype=torch.int64).pin_memory()
-            scores = torch.empty(nq, k, dtype=torch.float32).pin_memory()
+            ids = torch.empty(nq, k, dtype=torch.int64)
+            scores = torch.empty(nq, k, dtype=torch.float32)
         else:
             ids, scores = out
         _check(lib().sa_search_host(self.handle, _ptr(queries), _dtype_code(queries), nq, k, nprobe,
@@ -409,8 +410,8 @@ class Index:
             raise ValueError("queries must be a contiguous 2-D CPU tensor")
         nq = queries.shape[0]
         if out is None:
-            ids = torch.empty(nq, k, dtype=torch.int64).pin_memory()
-            scores = torch.empty(nq, k, dtype=torch.float32).pin_memory()
+            ids = torch.empty(nq, k, dtype=torch.int64)
+            scores = torch.empty(nq, k, dtype=torch.float32)
         else:
             ids, scores = out
         _check(lib().sa_search_graph_host(self.handle, _ptr(queries), _dtype_code(queries), nq, k,
@@ -523,6 +524,18 @@ class Index:
         _check(lib().sa_search_probes(self.handle, _ptr(queries), queries.shape[0], nprobe,
                                       _ptr(out), _stream_ptr(stream)))
         return out
+
+    def debug_small_phases(self, queries: torch.Tensor, k: int, nprobe: int, stream=None):
+        """The one-launch agent-step search with per-CTA phase timestamps (ns, [grid, 8])."""
+        nq = queries.shape[0]
+        ids = torch.empty(nq, k, dtype=torch.int64, device=queries.device)
+        sc = torch.empty(nq, k, dtype=torch.float32, device=queries.device)
+        ns = np.zeros(1024 * 8, dtype=np.int64)
+        grid = ctypes.c_int32(0)
+        _check(lib().sa_debug_small_phases(self.handle, _ptr(queries), nq, k, nprobe, _ptr(ids),
+                                           _ptr(sc), ns.ctypes.data_as(ctypes.c_void_p),
+                                           ctypes.byref(grid), _stream_ptr(stream)))
+        return ids, sc, ns[:grid.value * 8].reshape(grid.value, 8)
 
     def debug_scores(self, queries: torch.Tensor, stream=None) -> torch.Tensor:
         n = self.info()["n_local"]

@@ -32,6 +32,9 @@ struct sa_graph_entry {
   void* d_q = nullptr;
   int64_t* d_ids = nullptr;
   float* d_sc = nullptr;
+  void* small_scratch = nullptr;            // agent-step path: persistent kernel scratch,
+  int32_t* h_done = nullptr;                // pinned completion flag the kernel stores,
+  int32_t seq = 0;                          // and the number of replays so far
   int64_t launches[SA_KERNEL_KINDS] = {};   // per-kind kernel launches of one replay
   uint64_t last_use = 0;                    // LRU stamp (sa_index::use_clock)
 };
@@ -229,7 +232,15 @@ sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, in
 // Agent-step batches (nq <= 8, k <= 32, nprobe <= 256): the one-launch IVF search straight
 // from the caller's bf16 / fp32 queries (kernels/ivf_small.cu)
 bool ivf_small_applies(const sa_index* idx, int64_t nq, int32_t k, int32_t nprobe);
+// scratch: nullptr = stream-ordered allocations per call, else a block from
+// ivf_small_scratch_alloc for this (nq, k, nprobe) (sa_search_host's captured graphs), which
+// may also pass done_host (pinned completion flag) and queries_host (pinned queries, read by
+// the kernel; `queries` is then the device buffer it stages them in).
 sa_status ivf_small_search(const sa_index* idx, const void* queries, bool q_f32, int64_t nq,
-                           int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s);
+                           int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s,
+                           int64_t* debug_ns = nullptr, void* scratch = nullptr,
+                           int32_t* done_host = nullptr, const void* queries_host = nullptr);
+sa_status ivf_small_scratch_alloc(const sa_index* idx, int64_t nq, int32_t k, int32_t nprobe,
+                                  void** scratch);
 
 }  // namespace sa

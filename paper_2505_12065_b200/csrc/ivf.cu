@@ -206,8 +206,10 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   __nv_bfloat16* Xp = nullptr;
   SA_CUDA(cudaMalloc(&Xp, (size_t)n * dp * sizeof(__nv_bfloat16)), "alloc list-major corpus");
   cudaError_t e = launch_gather_rows(idx->X, dp, perm_all, 0, 0, 0, 1, n, Xp, sms, s);
-  if (e == cudaSuccess) e = cudaMalloc(&idx->row_ids, (size_t)n * sizeof(int32_t));
+  // +4 entries: the agent-step kernel bulk-copies 16-byte-aligned id ranges (ivf_small.cu)
+  if (e == cudaSuccess) e = cudaMalloc(&idx->row_ids, ((size_t)n + 4) * sizeof(int32_t));
   if (e == cudaSuccess) e = launch_perm_ids(perm_all, n, idx->row_offset, idx->row_ids, sms, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(idx->row_ids + n, 0xff, 4 * sizeof(int32_t), s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
     cudaFree(Xp);
@@ -262,20 +264,52 @@ sa_status ivf_probe(const sa_index* idx, const __nv_bfloat16* Qs, int64_t nq, in
 }
 
 bool ivf_small_applies(const sa_index* idx, int64_t nq, int32_t k, int32_t nprobe) {
-  return idx->nlist > 0 && idx->row_ids && nq >= 1 && nq <= IVSM_MAX_NQ && k <= IVSM_MAX_K &&
-         nprobe >= 1 && nprobe <= IVSM_MAX_NPROBE && idx->num_sms >= nq;
+  const int G = idx->num_sms;
+  return idx->nlist > 0 && idx->row_ids && idx->n_local < (1ll << 31) && nq >= 1 &&
+         nq <= IVSM_MAX_NQ && k <= IVSM_MAX_K &&
+         nprobe >= 1 && nprobe <= IVSM_MAX_NPROBE && G >= nq && idx->d_pad <= 768 &&
+         nprobe <= idx->nlist && ivf_small_fits((int)nq, nprobe, idx->nlist, G);
+}
+
+// Scratch of one agent-step search: the sizes of its four arrays, in one block.
+static void small_scratch_layout(const sa_index* idx, int64_t nq, int32_t k, int32_t nprobe,
+                                 size_t off[5]) {
+  const int grid = idx->num_sms;
+  const size_t n_top = (size_t)nq * grid * (ivf_small_m(nprobe, grid) + IVSM_EXTRA);
+  const size_t n_pc = (size_t)nq * idx->nlist, n_cand = (size_t)grid * nq * k;
+  off[0] = 0;                                   // top   (u64)
+  off[1] = off[0] + n_top * 8;                  // pcand (u64)
+  off[2] = off[1] + n_pc * 8;                   // cand  (u64)
+  off[3] = off[2] + n_cand * 8;                 // counters (i32) [nq + 1], seq, q-ready
+  off[4] = off[3] + ((size_t)nq + 3) * 4;       // total
+}
+
+sa_status ivf_small_scratch_alloc(const sa_index* idx, int64_t nq, int32_t k, int32_t nprobe,
+                                  void** scratch) {
+  size_t off[5];
+  small_scratch_layout(idx, nq, k, nprobe, off);
+  sa_status st = cuda_status(cudaMalloc(scratch, off[4]), "ivf small scratch");
+  if (st == SA_OK) st = cuda_status(cudaMemset(*scratch, 0, off[4]), "ivf small scratch");
+  return st;
 }
 
 // Agent-step batches: probe + list scan + merge in one cooperative launch (ivf_small.cu),
 // straight from the caller's queries (no staging kernel).
 sa_status ivf_small_search(const sa_index* idx, const void* queries, bool q_f32, int64_t nq,
-                           int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s) {
+                           int32_t k, int32_t nprobe, const SearchOut& out, cudaStream_t s,
+                           int64_t* debug_ns, void* scratch, int32_t* done_host,
+                           const void* queries_host) {
   const int grid = idx->num_sms;
   StreamFreer f{s};
+  size_t off[5];
+  small_scratch_layout(idx, nq, k, nprobe, off);
+  uint8_t* base = static_cast<uint8_t*>(scratch);
+  if (!base) SA_TRY(f.alloc(&base, off[4], "ivf small scratch"));
   IvfSmallArgs a{};
-  SA_TRY(f.alloc(&a.psc, (size_t)nq * idx->nlist, "ivf small scratch"));
-  SA_TRY(f.alloc(&a.probes, (size_t)nq * nprobe, "ivf small scratch"));
-  SA_TRY(f.alloc(&a.cand, (size_t)grid * nq * k, "ivf small scratch"));
+  a.top = reinterpret_cast<uint64_t*>(base + off[0]);
+  a.pcand = reinterpret_cast<uint64_t*>(base + off[1]);
+  a.cand = reinterpret_cast<uint64_t*>(base + off[2]);
+  a.counters = reinterpret_cast<int32_t*>(base + off[3]);
   a.Q = queries;
   a.q_f32 = q_f32 ? 1 : 0;
   a.nq = (int32_t)nq;
@@ -288,6 +322,11 @@ sa_status ivf_small_search(const sa_index* idx, const void* queries, bool q_f32,
   a.list_off = idx->list_off;
   a.row_ids = idx->row_ids;
   a.k = k;
+  a.debug_ns = debug_ns;
+  a.seq = a.counters + nq + 1;
+  a.q_ready = a.counters + nq + 2;
+  a.done_host = done_host;
+  a.Q_host = queries_host;
   a.out_keys = out.keys;
   a.out_ids = out.ids;
   a.out_scores = out.scores;

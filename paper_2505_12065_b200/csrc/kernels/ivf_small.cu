@@ -6,24 +6,37 @@
 // is latency-bound.  The batch path (probe kernel + select + inversion + list scan + merge)
 // costs ~10 launches of fixed overhead for ~20 us of HBM work at batch 1.  Here the whole
 // search -- R11's probe and the exact scan of the probed lists with the R5 ordering -- is
-// one kernel of one CTA per SM, phases separated by grid-wide barriers:
-//   A  centroid scores: each CTA streams its 1/G of the bf16 centroids (the dominant read,
-//      25 MB at nlist = 16384, d = 768) and writes the fp32 scores <q, c> of every query;
-//   B  probe: CTA q selects query q's nprobe best lists from its nlist scores (exact MSB-first
-//      radix select on the ordered fp32 bits; ties at the threshold -> lowest list id, R11);
-//   C  scan: the probed lists are cut into 64-row chunks, every CTA takes an equal share;
-//      16 warps x 4 rows in flight, fp32 dot products against the query in shared memory,
-//      per-warp top-k lists, merged into one list per (CTA, query);
-//   D  merge: CTA q keeps the k best of the G per-CTA lists of query q (R5 order) and writes
-//      the result (packed keys for a cross-rank merge, or ids / scores padded -1 / -inf).
+// one kernel of one CTA per SM.  Every byte it streams (centroids, then list rows and their
+// ids) moves HBM -> smem by 1-D TMA bulk copies through a 3-stage ring of 32-row pieces
+// (48 KB at d = 768) fed by a dedicated copy warp (full / empty mbarriers), so each SM keeps
+// ~100-150 KB in flight while 16 warps score rows on the CUDA cores.
+//   A  centroid keys: CTA b scores its 1/G slice of the bf16 centroids against every query
+//      and keeps the keys (score, list id) in smem, plus its m best per query in global;
+//   -- grid barrier
+//   B  probe (exact top-nprobe keys, R11: ties -> lowest list id): every CTA reads the
+//      published keys, takes T' = the nprobe-th largest of the CTAs' first m keys (<= the
+//      nprobe-th largest key overall: it is the nprobe-th of a subset) and, when every CTA's
+//      last published key is below T', ranks the published keys >= T' (all keys >= T' were
+//      published); otherwise (slices correlated with the query) the CTAs append every key
+//      >= T' and, after a second grid barrier, rank them (a 64-bit radix select when many);
+//   C  scan: the probed lists are cut into 32-row pieces, CTA b takes an equal share (in
+//      (query, list) order); a warp scores rows w and w + 16 of each piece against the query
+//      held in registers and keeps a sorted top-k in registers (lane j = j-th best); the 16
+//      warp lists are merged into one list per (CTA, query);
+//   D  the last CTA to finish (a counter, no grid barrier) keeps the k best of the G per-CTA
+//      lists of each query (R5 order) and writes the result (packed keys for a cross-rank
+//      merge, or ids / scores padded -1 / -inf).
 // Scores are fp32 sums of exact bf16 products on the CUDA cores (the batch path uses the
 // tensor cores; the two agree up to fp32 rounding order, i.e. at near-ties, R36).
+// List rows are read with an L2 evict-first policy (streamed once per step); the centroids
+// with the default policy.
 #include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
 #include "ivf_small.cuh"
 #include "keys.cuh"
 #include "launch.cuh"
+#include "ptx.cuh"
 
 namespace sa {
 
@@ -31,22 +44,84 @@ namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int kThreads = IVSM_THREADS;
+constexpr int kCWarps = 16;                           // scoring warps
+constexpr int kCThreads = 32 * kCWarps;
+constexpr int kThreads = IVSM_THREADS;                // + the copy warp
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 64;           // rows per scan work item (16 warps x 4 rows)
-constexpr int kRowsPerWarp = 4;
+static_assert(kThreads == kCThreads + 32, "one copy warp");
+constexpr int kPiece = 32;                            // rows per bulk copy
+constexpr int kStages = 3;
 constexpr int kMaxDPad = 768;
+constexpr int kRowsBytes = kPiece * kMaxDPad * 2;     // 48 KB
+constexpr int kIdBytes = 256;                         // a piece's ids (16-byte aligned range)
+constexpr int kStageBytes = kRowsBytes + kIdBytes;
+constexpr int kRingBytes = kStages * kStageBytes;
+constexpr int kRingKeys = kRingBytes / 8;
 constexpr int kMaxNp = IVSM_MAX_NQ * IVSM_MAX_NPROBE;
+constexpr int kRankMax = 1024;   // fallback candidates ranked by counting; more -> radix select
+constexpr int kFastCap = 512;    // published candidates per query on the fast path
+constexpr int kSvCap = kCWarps * IVSM_MAX_K;          // survivors of a warp-list merge
+static_assert((IVSM_MAX_NLIST + IVSM_MAX_NPROBE) <= kRingKeys, "probe candidates fit the ring");
 
-struct SmallSmem {
-  float q[IVSM_MAX_NQ][kMaxDPad];            // the queries, bf16-rounded, widened to fp32
-  uint64_t wl[kWarps][IVSM_MAX_NQ][IVSM_MAX_K];  // per-warp top-k lists (descending)
-  int32_t pre[kMaxNp + 1];                   // exclusive prefix of chunks per probe entry
-  int32_t lst[kMaxNp];                       // probe entry -> list id
+struct PieceInfo {
+  int64_t row0;
+  int32_t rows, qi;
+};
+
+struct __align__(16) SmallSmem {
+  float4 qp[IVSM_MAX_NQ][3][2][32];           // the queries, bf16-rounded, widened to fp32,
+                                              // lane-planar: elements [8 ch + 4 h, +4) of
+                                              // chunk ch = lane + 32 u (conflict-free LDS.128)
+  uint64_t full[kStages], empty[kStages];
+  PieceInfo info[kStages];
+  uint64_t lk[IVSM_MAX_NQ][IVSM_MAX_LOCAL];   // this CTA's centroid keys per query
+  uint64_t wl[kCWarps][IVSM_MAX_K];           // warp lists at a flush
+  uint64_t sv[kSvCap];                        // survivors of a warp-list merge
+  uint64_t thr[IVSM_MAX_NQ];                  // probe thresholds T'
+  int32_t probe[kMaxNp];                      // probe entries (query-major, by descending
+                                              // key): the list's first stored row
+  int32_t lend[kMaxNp];                       // each probe entry's list end
+  int32_t pre[kMaxNp + 1];                    // exclusive prefix of pieces per probe entry
   uint32_t hist[256];
   uint64_t red[kWarps];
+  int32_t ccnt[IVSM_MAX_NQ], unpub[IVSM_MAX_NQ];
   int32_t s_int[4];
 };
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// 1-D bulk copy global -> this CTA's smem, completing `bytes` on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar, uint64_t policy, bool hint) {
+  if (hint)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ int64_t globaltimer() {
+  int64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Barrier of nth threads: the whole CTA, or the scoring warps alone (named barrier 1).
+__device__ __forceinline__ void bsync(int nth) {
+  if (nth == kThreads) __syncthreads();
+  else asm volatile("bar.sync 1, %0;" ::"r"(nth) : "memory");
+}
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   const int lane = threadIdx.x & 31;
@@ -58,19 +133,23 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
   return v;
 }
 
-// Block-wide max of one u64 per thread (result to every thread).
-__device__ __forceinline__ uint64_t block_max(uint64_t v, SmallSmem& sm) {
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const uint64_t x = __shfl_xor_sync(0xffffffffu, v, o);
     v = x > v ? x : v;
   }
-  __syncthreads();
+  return v;
+}
+
+// Max of one u64 per thread over the first nth threads (result to each of them).
+__device__ __forceinline__ uint64_t block_max(uint64_t v, SmallSmem& sm, int nth) {
+  v = warp_max_u64(v);
+  bsync(nth);
   if ((threadIdx.x & 31) == 0) sm.red[threadIdx.x >> 5] = v;
-  __syncthreads();
+  bsync(nth);
   uint64_t m = 0ull;
-#pragma unroll
-  for (int w = 0; w < kWarps; ++w) m = sm.red[w] > m ? sm.red[w] : m;
+  for (int w = 0; w < nth / 32; ++w) m = sm.red[w] > m ? sm.red[w] : m;
   return m;
 }
 
@@ -98,12 +177,12 @@ __device__ __forceinline__ void warp_sort64_desc(uint64_t& x0, uint64_t& x1) {
   }
 }
 
-// Descending bitonic sort of sv[0, P) in shared memory by the whole block (P a power of two).
-__device__ void block_sort_desc(uint64_t* sv, int P) {
+// Descending bitonic sort of sv[0, P) in shared memory by nth threads (P a power of two).
+__device__ void block_sort_desc(uint64_t* sv, int P, int nth) {
   for (int size = 2; size <= P; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      __syncthreads();
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+      bsync(nth);
+      for (int i = threadIdx.x; i < P; i += nth) {
         const int j = i ^ stride;
         if (j > i) {
           const uint64_t a = sv[i], b = sv[j];
@@ -116,30 +195,31 @@ __device__ void block_sort_desc(uint64_t* sv, int P) {
       }
     }
   }
-  __syncthreads();
+  bsync(nth);
 }
 
-// The k best keys of L descending lists of k keys (list j at lists[j * lstride], empty slots
-// 0) -> out[0, k) descending (0-padded), by the whole block.  Every key of the top k is
-// >= T = max_j lists[j][k-1] (k keys of one list are >= T), so only those survive to a sort.
-__device__ void topk_of_lists(const uint64_t* lists, int L, int64_t lstride, int k,
-                              uint64_t* sv, int sv_cap, uint64_t* out, SmallSmem& sm) {
+// The k best keys of L descending lists of k keys in smem (list j at lists[j * lstride],
+// empty slots 0) -> out[0, k) descending (0-padded), by the first nth threads.  Every key of
+// the top k is >= T = max_j lists[j][k-1] (k keys of one list are >= T), so only those
+// survive to a sort.
+__device__ void topk_of_lists(const uint64_t* lists, int L, int lstride, int k, uint64_t* sv,
+                              int sv_cap, uint64_t* out, SmallSmem& sm, int nth) {
   uint64_t t = 0ull;
-  for (int j = threadIdx.x; j < L; j += blockDim.x) {
-    const uint64_t x = lists[(int64_t)j * lstride + k - 1];
+  for (int j = threadIdx.x; j < L; j += nth) {
+    const uint64_t x = lists[j * lstride + k - 1];
     t = x > t ? x : t;
   }
-  const uint64_t T = block_max(t, sm);
+  const uint64_t T = block_max(t, sm, nth);
   if (threadIdx.x == 0) sm.s_int[0] = 0;
-  __syncthreads();
-  for (int e = threadIdx.x; e < L * k; e += blockDim.x) {
-    const uint64_t x = lists[(int64_t)(e / k) * lstride + e % k];
+  bsync(nth);
+  for (int e = threadIdx.x; e < L * k; e += nth) {
+    const uint64_t x = lists[(e / k) * lstride + e % k];
     if (x != 0ull && x >= T) {
       const int pos = atomicAdd(&sm.s_int[0], 1);
       if (pos < sv_cap) sv[pos] = x;
     }
   }
-  __syncthreads();
+  bsync(nth);
   const int m = min(sm.s_int[0], sv_cap);
   if (m <= 64) {
     if (threadIdx.x < 32) {
@@ -152,79 +232,203 @@ __device__ void topk_of_lists(const uint64_t* lists, int L, int64_t lstride, int
   } else {
     int P = 1;
     while (P < m) P <<= 1;
-    for (int i = m + threadIdx.x; i < P; i += blockDim.x) sv[i] = 0ull;
-    block_sort_desc(sv, P);
-    for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = sv[i];
+    for (int i = m + threadIdx.x; i < P; i += nth) sv[i] = 0ull;
+    block_sort_desc(sv, P, nth);
+    for (int i = threadIdx.x; i < k; i += nth) out[i] = sv[i];
   }
-  __syncthreads();
+  bsync(nth);
+}
+
+// The nprobe-th largest of the n distinct keys kb[0, n) (n >= nprobe), MSB-first radix
+// select over the 64 key bits, by the whole CTA.
+__device__ uint64_t radix_kth(const uint64_t* kb, int n, int nprobe, SmallSmem& sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t prefix = 0ull, mask = 0ull;
+  int remaining = nprobe;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += kThreads) sm.hist[i] = 0u;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kThreads) {
+      const uint64_t v = kb[i];
+      if ((v & mask) == prefix) atomicAdd(&sm.hist[(v >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // buckets from the top, 8 per lane: the first bucket where the count reaches
+      // `remaining` holds the k-th key
+      uint32_t cnt[8], sum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        cnt[i] = sm.hist[255 - (lane * 8 + i)];
+        sum += cnt[i];
+      }
+      const uint32_t incl = warp_incl_scan(sum);
+      const unsigned hit = __ballot_sync(0xffffffffu, incl >= (uint32_t)remaining);
+      const int owner = hit ? __ffs(hit) - 1 : 31;
+      if (lane == owner) {
+        uint32_t acc = incl - sum;
+        int bk = 255 - lane * 8;
+        for (int i = 0; i < 8; ++i, --bk) {
+          if (bk == 0 || acc + cnt[i] >= (uint32_t)remaining) break;
+          acc += cnt[i];
+        }
+        sm.s_int[1] = bk;
+        sm.s_int[2] = (int)acc;
+      }
+    }
+    __syncthreads();
+    remaining -= sm.s_int[2];
+    prefix |= (uint64_t)(uint32_t)sm.s_int[1] << shift;
+    mask |= 255ull << shift;
+    __syncthreads();
+  }
+  return prefix;
+}
+
+// ring keys the fast probe path needs: published [nq][G][mp], first-m [nq][G*m], candidates
+__host__ __device__ inline int64_t fast_keys(int nq, int m, int G) {
+  return (int64_t)nq * G * (m + IVSM_EXTRA) + (int64_t)nq * G * m + (int64_t)nq * kFastCap;
 }
 
 }  // namespace
 
-// survivors capacity of the merges: a power of two >= max(grid * k, warps * IVSM_MAX_K)
-__host__ __device__ inline int sv_capacity(int grid, int k) {
-  int p = 1;
-  while (p < grid * k || p < kWarps * IVSM_MAX_K) p <<= 1;
-  return p;
+bool ivf_small_fits(int nq, int nprobe, int nlist, int grid) {
+  const int m = ivf_small_m(nprobe, grid);
+  return nlist <= IVSM_MAX_NLIST && nlist <= (int64_t)IVSM_MAX_LOCAL * grid &&
+         fast_keys(nq, m, grid) <= kRingKeys;
 }
 
 template <int NQ>
 __global__ void __launch_bounds__(kThreads, 1) ivf_small_kernel(const IvfSmallArgs a) {
-  // dynamic smem: SmallSmem, then a region shared by phase B (nlist ordered scores) and the
-  // merges of phases C / D (survivors + the k results)
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  SmallSmem& sm = *reinterpret_cast<SmallSmem*>(smem_raw);
-  uint8_t* dyn = smem_raw + (sizeof(SmallSmem) + 15) / 16 * 16;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* ring64 = reinterpret_cast<uint64_t*>(ring);
+  SmallSmem& sm = *reinterpret_cast<SmallSmem*>(ring + kRingBytes);
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x, b = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nch = a.d_pad / 8;   // 16-byte chunks per row
-  const int k = a.k;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool copier = warp == kCWarps;
+  const int nq = a.nq, k = a.k, nprobe = a.nprobe, d_pad = a.d_pad;
+  const int nch = d_pad / 8;                    // 16-byte chunks per row
+  const uint32_t row_bytes = (uint32_t)d_pad * 2;
+  const int c0 = (int)((int64_t)b * a.nlist / G), c1 = (int)((int64_t)(b + 1) * a.nlist / G);
+  const int nloc = c1 - c0;
+  const int nA = (nloc + kPiece - 1) / kPiece;
+  const uint32_t full0 = ptx::smem_u32(&sm.full[0]), empty0 = ptx::smem_u32(&sm.empty[0]);
+  const uint32_t ring0 = ptx::smem_u32(ring);
+  if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 0] = globaltimer();
 
-  // queries -> smem, RNE-rounded to bf16 (R3) then widened exactly; padding is zero
-  for (int i = threadIdx.x; i < NQ * a.d_pad; i += kThreads) {
-    const int qi = i / a.d_pad, c = i % a.d_pad;
-    float v = 0.f;
-    if (qi < a.nq && c < a.d) {
-      v = a.q_f32 ? __bfloat162float(__float2bfloat16_rn(
-                        static_cast<const float*>(a.Q)[(int64_t)qi * a.d + c]))
-                  : __bfloat162float(static_cast<const __nv_bfloat16*>(a.Q)[(int64_t)qi * a.d + c]);
+  // the copy warp's lane 0 owns the ring: it initialises the barriers and starts the first
+  // centroid copies at once (the scoring warps wait on them only after the CTA barrier below)
+  if (copier && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(full0 + s * 8, 1);
+      ptx::mbar_init(empty0 + s * 8, kCWarps);
     }
-    sm.q[qi][c] = v;
+    ptx::fence_mbar_init();
+    for (int i = 0; i < min(kStages, nA); ++i) {
+      const uint32_t bytes = (uint32_t)min(kPiece, nloc - i * kPiece) * row_bytes;
+      ptx::mbar_arrive_expect_tx(full0 + i * 8, bytes);
+      bulk_g2s(ring0 + i * kStageBytes, a.C + (int64_t)(c0 + i * kPiece) * d_pad, bytes,
+               full0 + i * 8, 0ull, false);
+    }
   }
+  // Pinned host queries: CTA 0 reads them over the host link (once) and stages them in device
+  // memory; the other CTAs wait for its release flag and read them from L2.
+  const bool host_q = a.Q_host != nullptr;
+  if (host_q) {
+    const int32_t expect = *a.seq + 1;   // *seq changes only at the end of the launch
+    if (b == 0) {
+      const int n = nq * a.d;
+      if (a.q_f32) {
+        const uint32_t* src = static_cast<const uint32_t*>(a.Q_host);
+        uint32_t* dst = static_cast<uint32_t*>(const_cast<void*>(a.Q));
+        for (int i = tid; i < n; i += kThreads) dst[i] = src[i];
+      } else {
+        const unsigned short* src = static_cast<const unsigned short*>(a.Q_host);
+        unsigned short* dst = static_cast<unsigned short*>(const_cast<void*>(a.Q));
+        for (int i = tid; i < n; i += kThreads) dst[i] = src[i];
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) ptx::st_release_gpu(a.q_ready, expect);
+    } else {
+      if (tid == 0)
+        while (ptx::ld_acquire_gpu(a.q_ready) != expect) __nanosleep(32);
+      __syncthreads();
+    }
+  }
+  // queries -> smem, RNE-rounded to bf16 (R3) then widened exactly; padding is zero
+  for (int i = tid; i < NQ * kMaxDPad; i += kThreads) {   // every slot: zero past d
+    const int qi = i / kMaxDPad, c = i % kMaxDPad;
+    float v = 0.f;
+    if (qi < nq && c < a.d) {
+      const int64_t o = (int64_t)qi * a.d + c;
+      if (a.q_f32) {
+        const float* Qf = static_cast<const float*>(a.Q);
+        v = __bfloat162float(__float2bfloat16_rn(host_q ? __ldcg(Qf + o) : Qf[o]));
+      } else {
+        const unsigned short* Qh = static_cast<const unsigned short*>(a.Q);
+        v = __uint_as_float((uint32_t)(host_q ? __ldcg(Qh + o) : Qh[o]) << 16);
+      }
+    }
+    const int ch = c >> 3, u = ch >> 5, ln = ch & 31, h = (c >> 2) & 1;
+    reinterpret_cast<float*>(&sm.qp[qi][u][h][ln])[c & 3] = v;
+  }
+  if (b == 0)   // ordered before every use by the grid barriers below
+    for (int i = tid; i <= nq; i += kThreads) a.counters[i] = 0;
   __syncthreads();
 
-  // ---- A: centroid scores of this CTA's share of the lists
-  {
-    const int c0 = (int)((int64_t)b * a.nlist / G), c1 = (int)((int64_t)(b + 1) * a.nlist / G);
-    const uint4* C4 = reinterpret_cast<const uint4*>(a.C);
-    for (int c = c0 + warp * 2; c < c1; c += kWarps * 2) {
+  // Ring position p (phase A: p = i; phase C: p = nA + j) uses stage p % kStages; its full
+  // barrier completes phase p / kStages, its empty barrier (16 warp arrivals) likewise.
+  // ---- A: this CTA's centroid keys
+  if (copier) {
+    if (lane == 0)
+      for (int i = kStages; i < nA; ++i) {
+        const int s = i % kStages;
+        ptx::mbar_wait(empty0 + s * 8, (uint32_t)((i / kStages - 1) & 1));
+        const uint32_t bytes = (uint32_t)min(kPiece, nloc - i * kPiece) * row_bytes;
+        ptx::mbar_arrive_expect_tx(full0 + s * 8, bytes);
+        bulk_g2s(ring0 + s * kStageBytes, a.C + (int64_t)(c0 + i * kPiece) * d_pad, bytes,
+                 full0 + s * 8, 0ull, false);
+      }
+    __syncwarp();
+  } else {
+    for (int i = 0; i < nA; ++i) {
+      const int s = i % kStages;
+      ptx::mbar_wait(full0 + s * 8, (uint32_t)((i / kStages) & 1));
+      const uint8_t* st = ring + s * kStageBytes;
+      const int r0 = i * kPiece, rows = min(kPiece, nloc - r0);
       uint4 v[2][3];
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
+      for (int h = 0; h < 2; ++h) {
+        const uint4* row = reinterpret_cast<const uint4*>(st + (warp + h * kCWarps) * row_bytes);
 #pragma unroll
         for (int u = 0; u < 3; ++u) {
           const int ch = lane + 32 * u;
-          v[r][u] = (c + r < c1 && ch < nch) ? __ldg(C4 + (int64_t)(c + r) * nch + ch)
-                                             : make_uint4(0, 0, 0, 0);
+          v[h][u] = (warp + h * kCWarps < rows && ch < nch) ? row[ch] : make_uint4(0, 0, 0, 0);
         }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(empty0 + s * 8);   // this warp is done with the stage
+      // both rows against each query chunk: one pair of conflict-free LDS.128 per (chunk, query)
       float acc[2][NQ];
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int qi = 0; qi < NQ; ++qi) acc[r][qi] = 0.f;
+        for (int qi = 0; qi < NQ; ++qi) acc[h][qi] = 0.f;
 #pragma unroll
       for (int u = 0; u < 3; ++u) {
-        const int ch = lane + 32 * u;
-        if (ch >= nch) break;
+        if (lane + 32 * u >= nch) break;
 #pragma unroll
         for (int qi = 0; qi < NQ; ++qi) {
-          const float4 qa = *reinterpret_cast<const float4*>(&sm.q[qi][ch * 8]);
-          const float4 qb = *reinterpret_cast<const float4*>(&sm.q[qi][ch * 8 + 4]);
+          const float4 qa = sm.qp[qi][u][0][lane];
+          const float4 qb = sm.qp[qi][u][1][lane];
 #pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const uint4 w = v[r][u];
-            float x = acc[r][qi];
+          for (int h = 0; h < 2; ++h) {
+            const uint4 w = v[h][u];
+            float x = acc[h][qi];
             x = fmaf(__uint_as_float(w.x << 16), qa.x, x);
             x = fmaf(__uint_as_float(w.x & 0xFFFF0000u), qa.y, x);
             x = fmaf(__uint_as_float(w.y << 16), qa.z, x);
@@ -233,242 +437,349 @@ __global__ void __launch_bounds__(kThreads, 1) ivf_small_kernel(const IvfSmallAr
             x = fmaf(__uint_as_float(w.z & 0xFFFF0000u), qb.y, x);
             x = fmaf(__uint_as_float(w.w << 16), qb.z, x);
             x = fmaf(__uint_as_float(w.w & 0xFFFF0000u), qb.w, x);
-            acc[r][qi] = x;
+            acc[h][qi] = x;
           }
         }
       }
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
+      for (int h = 0; h < 2; ++h) {
+        const int r = warp + h * kCWarps;
+        if (r >= rows) break;
 #pragma unroll
         for (int qi = 0; qi < NQ; ++qi) {
-          float s = acc[r][qi];
+          float s2 = acc[h][qi];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          if (lane == 0 && qi < a.nq && c + r < c1) a.psc[(int64_t)qi * a.nlist + c + r] = s;
+          for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+          if (lane == 0 && qi < nq) sm.lk[qi][r0 + r] = make_key(s2, (uint32_t)(c0 + r0 + r));
         }
+      }
+      if (a.debug_ns && i == 0 && tid == 0) a.debug_ns[b * 8 + 6] = globaltimer();
     }
   }
-  grid.sync();
-
-  // ---- B: query b's probe set = its nprobe best lists (ties -> lowest list id)
-  if (b < a.nq) {
-    uint32_t* key = reinterpret_cast<uint32_t*>(dyn);
-    const float* ps = a.psc + (int64_t)b * a.nlist;
-    for (int c = threadIdx.x; c < a.nlist; c += kThreads) key[c] = ordered_from_float(ps[c]);
-    uint32_t prefix = 0u, mask = 0u;
-    int remaining = a.nprobe;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = threadIdx.x; i < 256; i += kThreads) sm.hist[i] = 0u;
-      __syncthreads();
-      for (int c = threadIdx.x; c < a.nlist; c += kThreads) {
-        const uint32_t v = key[c];
-        if ((v & mask) == prefix) atomicAdd(&sm.hist[(v >> shift) & 255u], 1u);
-      }
-      __syncthreads();
-      if (warp == 0) {
-        // buckets from the top, 8 per lane: the first bucket where the count reaches
-        // `remaining` holds the threshold
-        uint32_t cnt[8], sum = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          cnt[i] = sm.hist[255 - (lane * 8 + i)];
-          sum += cnt[i];
-        }
-        const uint32_t incl = warp_incl_scan(sum);
-        const unsigned hit = __ballot_sync(0xffffffffu, incl >= (uint32_t)remaining);
-        const int owner = hit ? __ffs(hit) - 1 : 31;
-        if (lane == owner) {
-          uint32_t acc = incl - sum;
-          int bk = 255 - lane * 8;
-          for (int i = 0; i < 8; ++i, --bk) {
-            if (bk == 0 || acc + cnt[i] >= (uint32_t)remaining) break;
-            acc += cnt[i];
-          }
-          sm.s_int[1] = bk;
-          sm.s_int[2] = (int)acc;
-        }
-      }
-      __syncthreads();
-      remaining -= sm.s_int[2];
-      prefix |= (uint32_t)sm.s_int[1] << shift;
-      mask |= 255u << shift;
-      __syncthreads();
-    }
-    // prefix = the nprobe-th largest value T; take every list above T, then the first
-    // `remaining` lists equal to T in ascending id order
-    int32_t* out = a.probes + (int64_t)b * a.nprobe;
-    if (threadIdx.x == 0) sm.s_int[0] = 0;
-    __syncthreads();
-    for (int c = threadIdx.x; c < a.nlist; c += kThreads)
-      if (key[c] > prefix) out[atomicAdd(&sm.s_int[0], 1)] = c;
-    __syncthreads();
-    const int above = sm.s_int[0];
-    int taken = 0;
-    for (int c0 = 0; c0 < a.nlist && taken < remaining; c0 += kThreads) {
-      const int c = c0 + threadIdx.x;
-      const bool eq = c < a.nlist && key[c] == prefix;
-      const unsigned bal = __ballot_sync(0xffffffffu, eq);
-      if (lane == 0) sm.red[warp] = __popc(bal);
-      __syncthreads();
-      int before = 0, tot = 0;
-      for (int w = 0; w < kWarps; ++w) {
-        const int n = (int)sm.red[w];
-        if (w < warp) before += n;
-        tot += n;
-      }
-      const int pos = taken + before + __popc(bal & ((1u << lane) - 1u));
-      if (eq && pos < remaining) out[above + pos] = c;
-      taken += tot;
-      __syncthreads();
-    }
-  }
-  grid.sync();
-
-  // ---- C: scan the probed lists in 64-row chunks, an equal share of chunks per CTA
-  const int np = a.nq * a.nprobe;
-  for (int e = threadIdx.x; e < np; e += kThreads) sm.lst[e] = a.probes[e];
   __syncthreads();
-  {
-    // exclusive prefix of chunk counts (np <= 2048: 4 entries per thread)
-    int loc[4], s = 0;
+  // this CTA's mp = m + IVSM_EXTRA best keys per query, descending (0 where it holds fewer)
+  const int m = ivf_small_m(nprobe, G);
+  const int mp = m + IVSM_EXTRA;
+  if (warp < nq) {
+    uint64_t x[IVSM_MAX_LOCAL / 32];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int e = threadIdx.x * 4 + i;
-      int c = 0;
-      if (e < np) {
-        const int l = sm.lst[e];
-        c = (int)((a.list_off[l + 1] - a.list_off[l] + kChunk - 1) / kChunk);
+    for (int j = 0; j < IVSM_MAX_LOCAL / 32; ++j) {
+      const int c = lane + 32 * j;
+      x[j] = c < nloc ? sm.lk[warp][c] : 0ull;
+    }
+    for (int r = 0; r < mp; ++r) {
+      uint64_t mx = 0ull;
+#pragma unroll
+      for (int j = 0; j < IVSM_MAX_LOCAL / 32; ++j) mx = x[j] > mx ? x[j] : mx;
+      mx = warp_max_u64(mx);
+#pragma unroll
+      for (int j = 0; j < IVSM_MAX_LOCAL / 32; ++j)
+        if (x[j] == mx) x[j] = 0ull;     // keys are distinct: one owner (or mx == 0)
+      if (lane == 0) a.top[((int64_t)warp * G + b) * mp + r] = mx;
+    }
+  }
+  if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 1] = globaltimer();
+  grid.sync();
+
+  // ---- B: the probe sets (every CTA, every query)
+  // probe entry e -> its list's stored rows [probe[e], lend[e]) (n_local < 2^31); the loads
+  // overlap the ranking
+  auto set_probe = [&](int e, uint32_t l) __attribute__((always_inline)) {
+    sm.probe[e] = (int32_t)a.list_off[l];
+    sm.lend[e] = (int32_t)a.list_off[l + 1];
+  };
+  {
+    const int Gm = G * m, Gmp = G * mp;
+    uint64_t* tk = ring64;                   // [nq][G][mp] published keys
+    uint64_t* tm = tk + nq * Gmp;            // [nq][G * m] the CTAs' first m keys
+    uint64_t* cs = tm + nq * Gm;             // [nq][kFastCap] published keys >= T'
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.top);
+    for (int i = tid; i < nq * Gmp; i += kThreads) {
+      const uint64_t x = __ldcg(src + i);
+      tk[i] = x;
+      const int qi = i / Gmp, r = i - qi * Gmp, bb = r / mp, jj = r - bb * mp;
+      if (jj < m) tm[qi * Gm + bb * m + jj] = x;
+    }
+    if (tid < nq) {
+      sm.ccnt[tid] = 0;
+      sm.unpub[tid] = 0;
+    }
+    __syncthreads();
+    for (int p = tid; p < nq * Gm; p += kThreads) {
+      const uint64_t x = tm[p];
+      if (x == 0ull) continue;
+      const uint64_t* L = tm + (p / Gm) * Gm;
+      int rank = 0;
+      for (int i = 0; i < Gm; ++i) rank += L[i] > x;
+      if (rank == nprobe - 1) sm.thr[p / Gm] = x;   // keys distinct, >= nprobe nonzero ones
+    }
+    __syncthreads();
+    for (int p = tid; p < nq * Gmp; p += kThreads) {
+      const int qi = p / Gmp;
+      const uint64_t x = tk[p];
+      if (x != 0ull && x >= sm.thr[qi]) {
+        if ((p - qi * Gmp) % mp == mp - 1) sm.unpub[qi] = 1;   // keys >= T' may be unpublished
+        const int pos = atomicAdd(&sm.ccnt[qi], 1);
+        if (pos < kFastCap) cs[qi * kFastCap + pos] = x;
       }
-      loc[i] = s;
-      s += c;
+    }
+    __syncthreads();
+    bool fast = true;
+    for (int qi = 0; qi < nq; ++qi) fast = fast && !sm.unpub[qi] && sm.ccnt[qi] <= kFastCap;
+    if (fast) {   // grid-uniform: every CTA read the same published keys
+      for (int p = tid; p < nq * kFastCap; p += kThreads) {
+        const int qi = p / kFastCap, j = p - qi * kFastCap, n = sm.ccnt[qi];
+        if (j >= n) continue;
+        const uint64_t* C = cs + qi * kFastCap;
+        const uint64_t x = C[j];
+        int rank = 0;
+        for (int i = 0; i < n; ++i) rank += C[i] > x;
+        if (rank < nprobe) set_probe(qi * nprobe + rank, key_id(x));
+      }
+      __syncthreads();
+    }
+    if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 2] = globaltimer();
+    if (!fast) {
+      // every key >= T' of this CTA -> the query's candidates; rank them after a grid barrier
+      for (int p = tid; p < nq * nloc; p += kThreads) {
+        const int qi = p / nloc;
+        const uint64_t x = sm.lk[qi][p - qi * nloc];
+        if (x >= sm.thr[qi]) {
+          const int pos = atomicAdd(&a.counters[qi], 1);
+          a.pcand[(int64_t)qi * a.nlist + pos] = x;
+        }
+      }
+      grid.sync();
+      for (int qi = 0; qi < nq; ++qi) {
+        uint64_t* kb = ring64;
+        const int cq = __ldcg(a.counters + qi);
+        for (int i = tid; i < cq; i += kThreads)
+          kb[i] = __ldcg(reinterpret_cast<const unsigned long long*>(a.pcand) +
+                         (int64_t)qi * a.nlist + i);
+        __syncthreads();
+        int n = cq;
+        if (cq > kRankMax) {
+          // many candidates: keep the keys >= the nprobe-th largest, then rank those
+          const uint64_t kth = radix_kth(kb, cq, nprobe, sm);
+          uint64_t* sel = kb + cq;
+          if (tid == 0) sm.s_int[0] = 0;
+          __syncthreads();
+          for (int i = tid; i < cq; i += kThreads)
+            if (kb[i] >= kth) sel[atomicAdd(&sm.s_int[0], 1)] = kb[i];
+          __syncthreads();
+          kb = sel;
+          n = nprobe;
+        }
+        for (int j = tid; j < n; j += kThreads) {
+          const uint64_t x = kb[j];
+          int rank = 0;
+          for (int i = 0; i < n; ++i) rank += kb[i] > x;
+          if (rank < nprobe) set_probe(qi * nprobe + rank, key_id(x));
+        }
+        __syncthreads();
+      }
+    }
+  }
+  if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 3] = globaltimer();
+
+  // ---- C: scan the probed lists in 32-row pieces, an equal share of pieces per CTA
+  const int np = nq * nprobe;
+  {
+    // exclusive prefix of piece counts over the scoring threads (np <= 2048: 4 per thread)
+    int loc[4], s = 0;
+    if (!copier) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = tid * 4 + i;
+        int c = 0;
+        if (e < np) c = (sm.lend[e] - sm.probe[e] + kPiece - 1) / kPiece;
+        loc[i] = s;
+        s += c;
+      }
     }
     const uint32_t incl = warp_incl_scan((uint32_t)s);
     if (lane == 31) sm.red[warp] = incl;
     __syncthreads();
-    int base = 0;
-    for (int w = 0; w < warp; ++w) base += (int)sm.red[w];
-    base += (int)incl - s;
+    if (!copier) {
+      int base = 0;
+      for (int w = 0; w < warp; ++w) base += (int)sm.red[w];
+      base += (int)incl - s;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int e = threadIdx.x * 4 + i;
-      if (e < np) sm.pre[e] = base + loc[i];
+      for (int i = 0; i < 4; ++i) {
+        const int e = tid * 4 + i;
+        if (e < np) sm.pre[e] = base + loc[i];
+      }
+      if (tid == kCThreads - 1) sm.pre[np] = base + s;
     }
-    if (threadIdx.x == kThreads - 1) sm.pre[np] = base + s;
-    for (int i = threadIdx.x; i < kWarps * IVSM_MAX_NQ * IVSM_MAX_K; i += kThreads)
-      (&sm.wl[0][0][0])[i] = 0ull;
+    for (int i = tid; i < nq * k; i += kThreads) a.cand[(int64_t)b * nq * k + i] = 0ull;
+    ptx::fence_proxy_async_smem();   // the ring's generic-proxy use above precedes the copies
     __syncthreads();
   }
   const int total = sm.pre[np];
-  const int cb = (int)((int64_t)b * total / G), ce = (int)((int64_t)(b + 1) * total / G);
-  const uint4* X4 = reinterpret_cast<const uint4*>(a.X);
-  int e = 0;
-  for (int ch = cb; ch < ce; ++ch) {
-    // probe entry of chunk ch: the last e with pre[e] <= ch (entries with no rows are skipped)
-    int lo = e, hi = np - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (sm.pre[mid] <= ch) lo = mid;
-      else hi = mid - 1;
-    }
-    e = lo;
-    const int qi = e / a.nprobe;
-    const int l = sm.lst[e];
-    const int64_t lend = a.list_off[l + 1];
-    const int64_t r0 = a.list_off[l] + (int64_t)(ch - sm.pre[e]) * kChunk + warp * kRowsPerWarp;
-    uint4 v[kRowsPerWarp][3];
-#pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r)
-#pragma unroll
-      for (int u = 0; u < 3; ++u) {
-        const int cc = lane + 32 * u;
-        v[r][u] = (r0 + r < lend && cc < nch) ? __ldg(X4 + (r0 + r) * nch + cc)
-                                              : make_uint4(0, 0, 0, 0);
-      }
-    float acc[kRowsPerWarp];
-#pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) acc[r] = 0.f;
-    const float* qv = sm.q[qi];
-#pragma unroll
-    for (int u = 0; u < 3; ++u) {
-      const int cc = lane + 32 * u;
-      if (cc >= nch) break;
-      const float4 qa = *reinterpret_cast<const float4*>(qv + cc * 8);
-      const float4 qb = *reinterpret_cast<const float4*>(qv + cc * 8 + 4);
-#pragma unroll
-      for (int r = 0; r < kRowsPerWarp; ++r) {
-        const uint4 w = v[r][u];
-        acc[r] = fmaf(__uint_as_float(w.x << 16), qa.x, acc[r]);
-        acc[r] = fmaf(__uint_as_float(w.x & 0xFFFF0000u), qa.y, acc[r]);
-        acc[r] = fmaf(__uint_as_float(w.y << 16), qa.z, acc[r]);
-        acc[r] = fmaf(__uint_as_float(w.y & 0xFFFF0000u), qa.w, acc[r]);
-        acc[r] = fmaf(__uint_as_float(w.z << 16), qb.x, acc[r]);
-        acc[r] = fmaf(__uint_as_float(w.z & 0xFFFF0000u), qb.y, acc[r]);
-        acc[r] = fmaf(__uint_as_float(w.w << 16), qb.z, acc[r]);
-        acc[r] = fmaf(__uint_as_float(w.w & 0xFFFF0000u), qb.w, acc[r]);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+  const int pb = (int)((int64_t)b * total / G), pe = (int)((int64_t)(b + 1) * total / G);
+  const int nP = pe - pb;
+  if (copier) {
     if (lane == 0) {
-      uint64_t* wl = sm.wl[warp][qi];
+      const uint64_t pol = policy_evict_first();
+      for (int j = 0; j < nP; ++j) {
+        const int p = pb + j, pos = nA + j, s = pos % kStages;
+        int lo = 0, hi = np - 1;   // the last entry e with pre[e] <= p (it has pieces)
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sm.pre[mid] <= p) lo = mid;
+          else hi = mid - 1;
+        }
+        const int32_t lend = sm.lend[lo];
+        PieceInfo pi;
+        pi.row0 = sm.probe[lo] + (int64_t)(p - sm.pre[lo]) * kPiece;
+        pi.rows = (int32_t)(lend - pi.row0 < kPiece ? lend - pi.row0 : kPiece);
+        pi.qi = lo / nprobe;
+        // the piece's ids: the 16-byte aligned range around them (row_ids is padded)
+        const int64_t i0 = pi.row0 & ~int64_t(3), i1 = (pi.row0 + pi.rows + 3) & ~int64_t(3);
+        if (pos >= kStages) ptx::mbar_wait(empty0 + s * 8, (uint32_t)((pos / kStages - 1) & 1));
+        sm.info[s] = pi;
+        const uint32_t rb = (uint32_t)pi.rows * row_bytes, ib = (uint32_t)(i1 - i0) * 4;
+        ptx::mbar_arrive_expect_tx(full0 + s * 8, rb + ib);
+        bulk_g2s(ring0 + s * kStageBytes, a.X + pi.row0 * d_pad, rb, full0 + s * 8, pol, true);
+        bulk_g2s(ring0 + s * kStageBytes + kRowsBytes, a.row_ids + i0, ib, full0 + s * 8, pol,
+                 true);
+      }
+    }
+    __syncwarp();
+  } else {
+    // this warp's sorted top-k of the current query: lane j holds the j-th best (0 = empty)
+    uint64_t L = 0ull, lthr = 0ull;
+    int qcur = -1;
+    float qr[3][8];
+    auto flush = [&](int qi) __attribute__((always_inline)) {
+      if (lane < k) sm.wl[warp][lane] = L;
+      bsync(kCThreads);
+      topk_of_lists(&sm.wl[0][0], kCWarps, IVSM_MAX_K, k, sm.sv, kSvCap,
+                    a.cand + ((int64_t)b * nq + qi) * k, sm, kCThreads);
+    };
+    for (int j = 0; j < nP; ++j) {
+      const int pos = nA + j, s = pos % kStages;
+      ptx::mbar_wait(full0 + s * 8, (uint32_t)((pos / kStages) & 1));
+      const PieceInfo pi = sm.info[s];
+      if (pi.qi != qcur) {   // uniform over the scoring warps (each takes every piece)
+        if (qcur >= 0) flush(qcur);
+        qcur = pi.qi;
 #pragma unroll
-      for (int r = 0; r < kRowsPerWarp; ++r) {
-        if (r0 + r >= lend) break;
-        uint64_t key = make_key(acc[r], (uint32_t)a.row_ids[r0 + r]);
-        if (key <= wl[k - 1]) continue;
-        for (int j = 0; j < k; ++j) {      // insert into the descending list
-          const uint64_t x = wl[j];
-          if (key > x) {
-            wl[j] = key;
-            key = x;
-          }
+        for (int u = 0; u < 3; ++u) {   // zero past d_pad
+          const float4 qa = sm.qp[qcur][u][0][lane], qb = sm.qp[qcur][u][1][lane];
+          qr[u][0] = qa.x; qr[u][1] = qa.y; qr[u][2] = qa.z; qr[u][3] = qa.w;
+          qr[u][4] = qb.x; qr[u][5] = qb.y; qr[u][6] = qb.z; qr[u][7] = qb.w;
+        }
+        L = 0ull;
+        lthr = 0ull;
+      }
+      if (a.debug_ns && j == 0 && tid == 0) a.debug_ns[b * 8 + 7] = globaltimer();
+      const uint8_t* st = ring + s * kStageBytes;
+      const int32_t* ids = reinterpret_cast<const int32_t*>(st + kRowsBytes) + (pi.row0 & 3);
+      uint4 v[2][3];
+      int32_t id[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = warp + h * kCWarps;
+        const uint4* row = reinterpret_cast<const uint4*>(st + r * row_bytes);
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int ch = lane + 32 * u;
+          v[h][u] = (r < pi.rows && ch < nch) ? row[ch] : make_uint4(0, 0, 0, 0);
+        }
+        id[h] = r < pi.rows ? ids[r] : 0;
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(empty0 + s * 8);   // this warp is done with the stage
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (warp + h * kCWarps >= pi.rows) break;
+        float acc = 0.f;
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const uint4 w = v[h][u];   // zero past d_pad
+          acc = fmaf(__uint_as_float(w.x << 16), qr[u][0], acc);
+          acc = fmaf(__uint_as_float(w.x & 0xFFFF0000u), qr[u][1], acc);
+          acc = fmaf(__uint_as_float(w.y << 16), qr[u][2], acc);
+          acc = fmaf(__uint_as_float(w.y & 0xFFFF0000u), qr[u][3], acc);
+          acc = fmaf(__uint_as_float(w.z << 16), qr[u][4], acc);
+          acc = fmaf(__uint_as_float(w.z & 0xFFFF0000u), qr[u][5], acc);
+          acc = fmaf(__uint_as_float(w.w << 16), qr[u][6], acc);
+          acc = fmaf(__uint_as_float(w.w & 0xFFFF0000u), qr[u][7], acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const uint64_t key = make_key(acc, (uint32_t)id[h]);
+        if (key > lthr) {   // warp-uniform: insert into the sorted register list
+          uint64_t prev = __shfl_up_sync(0xffffffffu, L, 1);
+          if (lane == 0) prev = ~0ull;
+          const uint64_t nl = key > L ? (key > prev ? prev : key) : L;
+          L = lane < k ? nl : 0ull;
+          lthr = __shfl_sync(0xffffffffu, L, k - 1);
         }
       }
     }
+    if (qcur >= 0) flush(qcur);
   }
-  __syncthreads();
-  // this CTA's k best per query (the 16 warp lists merged) -> cand[b][q]
-  {
-    uint64_t* sv = reinterpret_cast<uint64_t*>(dyn);
-    for (int qi = 0; qi < a.nq; ++qi)
-      topk_of_lists(&sm.wl[0][qi][0], kWarps, (int64_t)IVSM_MAX_NQ * IVSM_MAX_K, k, sv,
-                    sv_capacity(G, k), a.cand + ((int64_t)b * a.nq + qi) * k, sm);
-  }
-  grid.sync();
+  if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 4] = globaltimer();
 
-  // ---- D: query b's k best over the G per-CTA lists -> output
-  if (b < a.nq) {
-    uint64_t* sv = reinterpret_cast<uint64_t*>(dyn);
-    const int cap = sv_capacity(G, k);
-    uint64_t* best = sv + cap;   // the k sorted keys, after the survivors
-    topk_of_lists(a.cand + (int64_t)b * k, G, (int64_t)a.nq * k, k, sv, cap, best, sm);
-    for (int j = threadIdx.x; j < k; j += kThreads) {
-      const uint64_t key = best[j];
-      const int64_t o = (int64_t)b * k + j;
-      if (a.out_keys) {
-        a.out_keys[o] = key;
-      } else {
-        a.out_ids[o] = key == 0ull ? -1 : (int64_t)key_id(key);
-        a.out_scores[o] = key == 0ull ? -__int_as_float(0x7f800000) : key_score(key);
+  // ---- D: the last CTA to finish merges the G per-CTA lists of every query
+  // (CTA barrier, then a gpu-scope acq_rel increment by one thread: releases this CTA's
+  // lists, and the last CTA acquires everyone's)
+  __syncthreads();
+  if (tid == 0) sm.s_int[3] = ptx::atom_add_acq_rel_gpu(&a.counters[nq], 1);
+  __syncthreads();
+  if (sm.s_int[3] != G - 1) return;
+  // per-CTA lists of as many queries as fit the ring, loaded in one pass (one L2 round trip)
+  const int gk = G * k;
+  int cap = 1;
+  while (cap < gk) cap <<= 1;
+  const int fit = max(1, (kRingKeys - cap - IVSM_MAX_K) / gk);
+  uint64_t* lists = ring64;
+  for (int q0 = 0; q0 < nq; q0 += fit) {
+    const int nf = min(fit, nq - q0);
+    uint64_t* sv = lists + nf * gk;
+    uint64_t* best = sv + cap;
+    for (int i = tid; i < nf * gk; i += kThreads) {   // lists[qj][bb][j] <- cand[bb][q0 + qj][j]
+      const int qj = i / gk, bb = (i - qj * gk) / k, j = i - qj * gk - bb * k;
+      lists[i] = __ldcg(reinterpret_cast<const unsigned long long*>(a.cand) +
+                        ((int64_t)bb * nq + q0 + qj) * k + j);
+    }
+    __syncthreads();
+    for (int qj = 0; qj < nf; ++qj) {
+      topk_of_lists(lists + qj * gk, G, k, k, sv, cap, best, sm, kThreads);
+      for (int j = tid; j < k; j += kThreads) {
+        const uint64_t key = best[j];
+        const int64_t o = (int64_t)(q0 + qj) * k + j;
+        if (a.out_keys) {
+          a.out_keys[o] = key;
+        } else {
+          a.out_ids[o] = key == 0ull ? -1 : (int64_t)key_id(key);
+          a.out_scores[o] = key == 0ull ? -__int_as_float(0x7f800000) : key_score(key);
+        }
       }
+      if (a.done_host) __threadfence_system();   // results visible before the signal
+      __syncthreads();
     }
   }
+  if (a.done_host && tid == 0) {
+    const int32_t v = *a.seq + 1;
+    *a.seq = v;
+    __threadfence_system();
+    *reinterpret_cast<volatile int32_t*>(a.done_host) = v;
+  }
+  if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 5] = globaltimer();
 }
 
-size_t ivf_small_smem_bytes(int nlist, int grid, int k) {
-  // phase B: nlist ordered scores; phases C / D: survivors + the k results
-  const size_t cd = ((size_t)sv_capacity(grid, k) + IVSM_MAX_K) * sizeof(uint64_t);
-  const size_t bsel = (size_t)nlist * sizeof(uint32_t);
-  return (sizeof(SmallSmem) + 15) / 16 * 16 + (bsel > cd ? bsel : cd);
-}
+size_t ivf_small_smem_bytes() { return 128 + (size_t)kRingBytes + sizeof(SmallSmem); }
 
 cudaError_t launch_ivf_small(const IvfSmallArgs& a, int grid, cudaStream_t s) {
   if (a.nq < 1 || a.nq > IVSM_MAX_NQ || a.k < 1 || a.k > IVSM_MAX_K || a.nprobe < 1 ||
-      a.nprobe > IVSM_MAX_NPROBE || a.d_pad > kMaxDPad || grid < a.nq)
+      a.nprobe > IVSM_MAX_NPROBE || a.nprobe > a.nlist || a.d_pad > kMaxDPad || a.d_pad % 64 ||
+      grid < a.nq || !ivf_small_fits(a.nq, a.nprobe, a.nlist, grid) ||
+      (int64_t)grid * a.k * 2 + IVSM_MAX_K > kRingKeys)
     return cudaErrorInvalidValue;
-  const size_t smem = ivf_small_smem_bytes(a.nlist, grid, a.k);
+  const size_t smem = ivf_small_smem_bytes();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kThreads);

@@ -10,7 +10,10 @@ namespace sa {
 constexpr int IVSM_MAX_NQ = 8;     // queries per launch (agent-step batches)
 constexpr int IVSM_MAX_K = 32;
 constexpr int IVSM_MAX_NPROBE = 256;
-constexpr int IVSM_THREADS = 512;
+constexpr int IVSM_THREADS = 544;  // 16 scoring warps + 1 copy-issuing warp
+constexpr int IVSM_MAX_LOCAL = 256;  // centroids per CTA: nlist <= 256 * grid
+constexpr int IVSM_MAX_NLIST = 18176;  // probe candidates + selection in the smem ring
+constexpr int IVSM_EXTRA = 7;      // keys published per CTA beyond the m of the probe threshold
 
 struct IvfSmallArgs {
   const void* Q;              // queries [nq, d] row-major, bf16 or fp32 (q_f32)
@@ -18,22 +21,35 @@ struct IvfSmallArgs {
   int32_t nq;                 // 1..IVSM_MAX_NQ
   int32_t d, d_pad;           // d_pad multiple of 64, <= 768
   const __nv_bfloat16* C;     // bf16 centroids [nlist, d_pad]
-  int32_t nlist;
+  int32_t nlist;              // <= min(IVSM_MAX_NLIST, IVSM_MAX_LOCAL * grid)
   int32_t nprobe;             // 1..min(nlist, IVSM_MAX_NPROBE)
   const __nv_bfloat16* X;     // list-major rows [n_local, d_pad]
   const int64_t* list_off;    // [nlist + 1]
   const int32_t* row_ids;     // stored row -> global id
   int32_t k;                  // 1..IVSM_MAX_K
-  float* psc;                 // scratch [nq, nlist]
-  int32_t* probes;            // scratch [nq, nprobe] (the probe set, unordered)
-  uint64_t* cand;             // scratch [grid, nq, k] per-CTA top-k lists
+  // scratch (no initialisation needed: the kernel zeroes what it counts with)
+  uint64_t* top;              // [nq, grid, m + IVSM_EXTRA] per-CTA best centroid keys
+  uint64_t* pcand;            // [nq, nlist] probe candidates
+  int32_t* counters;          // [nq + 1]: candidates per query, CTAs done
+  uint64_t* cand;             // [grid, nq, k] per-CTA top-k lists
+  int64_t* debug_ns;          // optional [grid, 8] %globaltimer at the phase ends (tests)
+  const void* Q_host;         // optional pinned host queries (layout of Q): CTA 0 reads them
+  int32_t* q_ready;           // and stores them to Q (device), then *q_ready = *seq + 1
+  int32_t* seq;               // optional completion signal: the last CTA increments *seq
+  int32_t* done_host;         // (device memory) and stores it to *done_host (pinned host)
+                              // after the results, so a host thread can spin on it
+                              // (seq and q_ready live in persistent, zeroed scratch)
   uint64_t* out_keys;         // [nq, k] sorted packed keys, or
   int64_t* out_ids;           // [nq, k] ids (-1 padded) +
   float* out_scores;          // [nq, k] scores (-inf padded)
 };
 
+// Per-CTA best centroid keys that set the probe threshold: m * grid >= nprobe.
+__host__ __device__ inline int ivf_small_m(int nprobe, int grid) { return (nprobe + grid - 1) / grid; }
+// Whether the kernel's smem ring holds the probe step's working set for this shape.
+bool ivf_small_fits(int nq, int nprobe, int nlist, int grid);
 // Dynamic shared memory of one CTA.
-size_t ivf_small_smem_bytes(int nlist, int grid, int k);
+size_t ivf_small_smem_bytes();
 // Cooperative launch, grid = one CTA per SM.
 cudaError_t launch_ivf_small(const IvfSmallArgs& a, int grid, cudaStream_t s);
 

@@ -624,6 +624,8 @@ static void free_graph_entry(sa_graph_entry& g) {
   cudaFree(g.d_q);
   cudaFree(g.d_ids);
   cudaFree(g.d_sc);
+  cudaFree(g.small_scratch);
+  cudaFreeHost(g.h_done);
   g = sa_graph_entry{};
 }
 
@@ -637,6 +639,11 @@ static sa_status capture_search(const sa_index* idx, sa_graph_entry& g) {
   if (st == SA_OK) st = cuda_status(cudaMalloc(&g.d_q, qbytes), "graph buffers");
   if (st == SA_OK) st = cuda_status(cudaMalloc(&g.d_ids, nk * 8), "graph buffers");
   if (st == SA_OK) st = cuda_status(cudaMalloc(&g.d_sc, nk * 4), "graph buffers");
+  if (st == SA_OK && g.nprobe > 0 && ivf_small_applies(idx, g.nq, g.k, g.nprobe)) {
+    st = ivf_small_scratch_alloc(idx, g.nq, g.k, g.nprobe, &g.small_scratch);
+    if (st == SA_OK) st = cuda_status(cudaMallocHost(&g.h_done, sizeof(int32_t)), "pinned flag");
+    if (st == SA_OK) *g.h_done = 0;
+  }
   if (st != SA_OK) return st;
   cudaStream_t cs;
   st = cuda_status(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "capture stream");
@@ -645,17 +652,34 @@ static sa_status capture_search(const sa_index* idx, sa_graph_entry& g) {
   st = cuda_status(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "begin capture");
   if (st == SA_OK) {
     set_capturing(true);
-    sa_status s1 = cuda_status(cudaMemcpyAsync(g.d_q, g.h_q, qbytes, cudaMemcpyHostToDevice, cs),
-                               "H2D");
+    const bool small = g.nprobe > 0 && ivf_small_applies(idx, g.nq, g.k, g.nprobe);
+    // agent-step batch: no copy node -- one CTA of the kernel reads the pinned queries over
+    // the host link and hands them to the others through device memory
+    sa_status s1 = small ? SA_OK
+                         : cuda_status(cudaMemcpyAsync(g.d_q, g.h_q, qbytes,
+                                                       cudaMemcpyHostToDevice, cs), "H2D");
     SearchOut out;
     out.ids = g.d_ids;
     out.scores = g.d_sc;
-    if (s1 == SA_OK)
-      s1 = search_local(idx, g.d_q, (sa_dtype)g.qdtype, g.nq, g.k, g.nprobe, out, cs);
-    if (s1 == SA_OK)
-      s1 = cuda_status(cudaMemcpyAsync(g.h_ids, g.d_ids, nk * 8, cudaMemcpyDeviceToHost, cs), "D2H");
-    if (s1 == SA_OK)
-      s1 = cuda_status(cudaMemcpyAsync(g.h_sc, g.d_sc, nk * 4, cudaMemcpyDeviceToHost, cs), "D2H");
+    if (small) {
+      // agent-step batch: one kernel on persistent scratch whose final merge writes the
+      // results straight into the pinned host buffers (zero-copy: the D2H transfer of
+      // nq * k * 12 bytes is the kernel's own stores over the host link)
+      out.ids = g.h_ids;
+      out.scores = g.h_sc;
+      if (s1 == SA_OK)
+        s1 = ivf_small_search(idx, g.d_q, g.qdtype == SA_F32, g.nq, g.k, g.nprobe, out, cs,
+                              nullptr, g.small_scratch, g.h_done, g.h_q);
+    } else {
+      if (s1 == SA_OK)
+        s1 = search_local(idx, g.d_q, (sa_dtype)g.qdtype, g.nq, g.k, g.nprobe, out, cs);
+      if (s1 == SA_OK)
+        s1 = cuda_status(cudaMemcpyAsync(g.h_ids, g.d_ids, nk * 8, cudaMemcpyDeviceToHost, cs),
+                         "D2H");
+      if (s1 == SA_OK)
+        s1 = cuda_status(cudaMemcpyAsync(g.h_sc, g.d_sc, nk * 4, cudaMemcpyDeviceToHost, cs),
+                         "D2H");
+    }
     capture_tally(g.launches);
     set_capturing(false);
     cudaError_t e = cudaStreamEndCapture(cs, &graph);
@@ -718,7 +742,25 @@ sa_status sa_search_host(const sa_index* idx, const void* queries_host, sa_dtype
     g->last_use = ++mi->use_clock;
     std::memcpy(g->h_q, queries_host, qbytes);
     st = cuda_status(cudaGraphLaunch(g->exec, s), "graph launch");
-    if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "search sync");
+    if (st == SA_OK && g->h_done) {
+      // the agent-step kernel signals completion through pinned memory after writing the
+      // results there: spin on the flag (no stream-synchronisation wake-up on the critical
+      // path); a stream error or a completed stream without the flag is reported
+      const int32_t want = ++g->seq;
+      for (uint64_t it = 1;; ++it) {
+        if (*reinterpret_cast<volatile int32_t*>(g->h_done) == want) break;
+        if ((it & 255) == 0) {
+          const cudaError_t e = cudaStreamQuery(s);
+          if (e == cudaErrorNotReady) continue;
+          if (e != cudaSuccess) return cuda_status(e, "search");
+          if (*reinterpret_cast<volatile int32_t*>(g->h_done) != want)
+            return set_error(SA_ERR_CUDA, "agent-step search finished without its signal");
+          break;
+        }
+      }
+    } else if (st == SA_OK) {
+      st = cuda_status(cudaStreamSynchronize(s), "search sync");
+    }
     if (st != SA_OK) return st;
     std::memcpy(out_ids_host, g->h_ids, (size_t)nq * k * 8);
     std::memcpy(out_scores_host, g->h_sc, (size_t)nq * k * 4);
@@ -816,6 +858,32 @@ sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, 
                                      cudaMemcpyDeviceToDevice, s), "copy scores");
   if (Qs) cudaFreeAsync(Qs, s);
   if (dbg) cudaFreeAsync(dbg, s);
+  return st;
+}
+
+sa_status sa_debug_small_phases(const sa_index* idx, const void* queries, int64_t nq, int32_t k,
+                                int32_t nprobe, int64_t* out_ids, float* out_scores,
+                                int64_t* host_ns, int32_t* host_grid, void* stream) {
+  if (!idx || !queries || !out_ids || !out_scores || !host_ns || !host_grid)
+    return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  if (!ivf_small_applies(idx, nq, k, nprobe) || idx->num_sms > 1024)
+    return set_error(SA_ERR_UNSUPPORTED, "the one-launch path does not apply");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = idx->num_sms;
+  int64_t* dns = nullptr;
+  sa_status st = dalloc(&dns, (size_t)grid * 8, s, "alloc debug timestamps");
+  if (st != SA_OK) return st;
+  st = cuda_status(cudaMemsetAsync(dns, 0, (size_t)grid * 8 * sizeof(int64_t), s), "memset");
+  SearchOut out{};
+  out.ids = out_ids;
+  out.scores = out_scores;
+  if (st == SA_OK) st = ivf_small_search(idx, queries, false, nq, k, nprobe, out, s, dns);
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(host_ns, dns, (size_t)grid * 8 * sizeof(int64_t),
+                                     cudaMemcpyDeviceToHost, s), "copy timestamps");
+  if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "sync");
+  cudaFreeAsync(dns, s);
+  *host_grid = grid;
   return st;
 }
 

@@ -63,19 +63,19 @@ def test_p10_all_lists_is_exact(sa, setup, batch):
     assert rep["ok"], rep
 
 
-@pytest.mark.parametrize("nprobe,k", [(1, 10), (5, 1), (8, 32), (16, 5), (48, 10)])
-def test_p11_exact_over_oracle_probe_set(sa, setup, nprobe, k):
-    idx, Xb, Qb, lists, Cb = setup
-    gi, gs = small_search(idx, Qb, k, nprobe, 8)
+def p11_check(gi, gs, Xb, Qb, lists, Cb, nprobe, k):
+    """P11 for every query whose probe boundary is wider than the fp32 error bound; returns the
+    number of queries skipped at a probe near-tie."""
+    nlist = len(lists)
     C = oracle.bf16_to_f64(Cb)
     Q = oracle.bf16_to_f64(Qb)
     pc = Q @ C.T
     eb = 2 * (Q.shape[1] - 1) * 2.0 ** -24 * (np.abs(Q) @ np.abs(C).T)
     skipped = 0
     for qi in range(len(Qb)):
-        order = np.lexsort((np.arange(64), -pc[qi]))
+        order = np.lexsort((np.arange(nlist), -pc[qi]))
         P = order[:nprobe]
-        if nprobe < 64:
+        if nprobe < nlist:
             a, b = order[nprobe - 1], order[nprobe]
             if pc[qi, a] - pc[qi, b] <= eb[qi, a] + eb[qi, b]:
                 skipped += 1       # probe boundary inside the fp32 error: either set is right
@@ -88,8 +88,44 @@ def test_p11_exact_over_oracle_probe_set(sa, setup, nprobe, k):
                                                       np.zeros(len(ids_), int), ids_),
                   k, n_avail=min(k, len(rows)))
         assert r["ok"], (nprobe, k, qi, r)
+    return skipped
+
+
+@pytest.mark.parametrize("nprobe,k", [(1, 10), (5, 1), (8, 32), (16, 5), (48, 10)])
+def test_p11_exact_over_oracle_probe_set(sa, setup, nprobe, k):
+    idx, Xb, Qb, lists, Cb = setup
+    gi, gs = small_search(idx, Qb, k, nprobe, 8)
+    skipped = p11_check(gi, gs, Xb, Qb, lists, Cb, nprobe, k)
     assert skipped <= 2, skipped
     print(f"P11 small path nprobe={nprobe} k={k}: {skipped} probe near-ties skipped")
+
+
+@pytest.mark.parametrize("nprobe", [16, 48, 256])
+def test_p11_many_centroids_per_cta_correlated_slices(sa, nprobe):
+    """nlist = 6000 > 32 x grid: every CTA scores several 32-row centroid pieces.  The centroids
+    are ordered by descending score against query 0, so each CTA's slice is a contiguous score
+    band: the probe threshold T' taken from the per-CTA best keys lies far below the nprobe-th
+    key and the candidate set is large -- counted ranks at nprobe = 16 (~600 candidates), the
+    radix-select branch at 48 and 256 (> 1024 candidates).  P11 against the oracle's probe set."""
+    mix = make_mixture(d=128, C=16, r=16, s_n=0.7)
+    Xb = to_bf16_bits(draw_rows(mix, 60_000, row_seed=41))
+    Qb = to_bf16_bits(draw_rows(mix, 4, row_seed=42))
+    rng = np.random.default_rng(43)
+    C = rng.standard_normal((6000, 128)).astype(np.float32)
+    C /= np.linalg.norm(C, axis=1, keepdims=True)
+    s0 = oracle.bf16_to_f64(bits(C)) @ oracle.bf16_to_f64(Qb[0])
+    C = np.ascontiguousarray(C[np.lexsort((np.arange(6000), -s0))])
+    idx = sa.Index.build(t16(Xb).cuda(), 6000, centroids=torch.from_numpy(C).cuda())
+    off, gid = idx.export_lists()
+    lists = [gid[off[j]:off[j + 1]] for j in range(6000)]
+    Cb = bits(idx.export_centroids())
+    gi, gs = small_search(idx, Qb, 10, nprobe, 4)
+    skipped = p11_check(gi, gs, Xb, Qb, lists, Cb, nprobe, 10)
+    assert skipped <= 1, skipped
+    # a query alone == inside the batch
+    si, ss = small_search(idx, Qb, 10, nprobe, 1)
+    assert np.array_equal(si, gi) and np.array_equal(ss, gs)
+    idx.free()
 
 
 def test_batch_invariance_and_input_dtype(sa, setup):
