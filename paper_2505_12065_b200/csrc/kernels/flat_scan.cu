@@ -358,9 +358,9 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       const int H = a.q_max_stride;
       int cur = -1, next_at = 0;
       while (true) {
-        const int qkey = *reinterpret_cast<volatile int32_t*>(&tail->bw_qkey);
+        const int qkey = atomicAdd(&tail->bw_qkey, 0);   // shared flags: atomics (no data race)
         if (qkey == -2) break;
-        const int done = *reinterpret_cast<volatile int32_t*>(&tail->tiles_done);
+        const int done = atomicAdd(&tail->tiles_done, 0);
         if (qkey != cur) {
           cur = qkey;
           next_at = done + 1;
@@ -404,9 +404,9 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
               }
             }
             if (kth != 0u)
-              *reinterpret_cast<volatile uint64_t*>(&tail->bound[i]) =
-                  ((uint64_t)(uint32_t)qkey << 32) | kth;
-            if (*reinterpret_cast<volatile int32_t*>(&tail->bw_qkey) != qkey) break;
+              atomicExch(reinterpret_cast<unsigned long long*>(&tail->bound[i]),
+                         ((unsigned long long)(uint32_t)qkey << 32) | kth);
+            if (atomicAdd(&tail->bw_qkey, 0) != qkey) break;
           }
         }
         __nanosleep(500);
@@ -445,7 +445,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     // arrive on a_full.  Callers guarantee every MMA that read the previous block has
     // completed (they consumed that block's last tmem_full).
     auto stage_a = [&](int qkey) __attribute__((always_inline)) {
-      if (ew == 0 && lane == 0) *reinterpret_cast<volatile int32_t*>(&tail->bw_qkey) = qkey;
+      if (ew == 0 && lane == 0) atomicExch(&tail->bw_qkey, qkey);
       const int64_t q_row = ((int64_t)qkey * CG + rank) * kBM + rib;
       const bool q_ok = q_row < a.nq;
       const bool tma_thread = ew == 0 && lane == 0 && kb_s > 0;
@@ -518,7 +518,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       for (int32_t t = wi.t0; t < wi.t1; ++t) {
         if (valid && ((t - wi.t0) & 3) == 3) {
           if (a.q_hint && h_next != 0u) hint = fmaxf(hint, float_from_ordered(h_next));
-          const uint64_t b = *reinterpret_cast<volatile uint64_t*>(&tail->bound[rib]);
+          const uint64_t b = atomicAdd(reinterpret_cast<unsigned long long*>(&tail->bound[rib]), 0ull);
           if ((uint32_t)(b >> 32) == (uint32_t)wi.qkey && (uint32_t)b != 0u)
             hint = fmaxf(hint, float_from_ordered((uint32_t)b));
           thr = fmaxf(thr, hint);
@@ -541,8 +541,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         }
         if (++acc == nacc) { acc = 0; acc_phase ^= 1; }
         if (ew == 0 && lane == 0) {
-          const int32_t td = *reinterpret_cast<volatile int32_t*>(&tail->tiles_done);
-          *reinterpret_cast<volatile int32_t*>(&tail->tiles_done) = td + 1;
+          atomicAdd(&tail->tiles_done, 1);
         }
         // The last accumulator of this item is in registers, so every MMA that read this
         // item's A operand has completed: stage the next item's queries now, before the
@@ -644,7 +643,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         thr = heap_threshold(0ull);
       }
     }
-    if (ew == 0 && lane == 0) *reinterpret_cast<volatile int32_t*>(&tail->bw_qkey) = -2;
+    if (ew == 0 && lane == 0) atomicExch(&tail->bw_qkey, -2);
   }
 
   ptx::tc_fence_before();
