@@ -53,16 +53,50 @@ def workload_name(cfg, name, nprobe):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING a timed region: NVML polled every 5 ms from
+    a thread (a 40 ms region still yields several samples); nvidia-smi -lms 100 if NVML is
+    missing."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event-reason bits (nvml.h): sw power cap, hw slowdown, sw / hw thermal
+    NVML_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+                 "hw_thermal_slowdown": 0x40}
 
     def __init__(self, device_index):
         self.dev = device_index
         self.proc = None
         self.lines = []
+        self.stop = threading.Event()
+        self.nvml = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nvml = (pynvml, h, mx)
+
+            def poll():
+                while True:
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    except Exception:
+                        break
+                    names = [n for n, bit in self.NVML_BITS.items() if rs & bit]
+                    self.lines.append(", ".join([str(sm), str(mx)] + [
+                        "Active" if n in names else "Not Active"
+                        for n in ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                  "sw_power_cap")]))
+                    if self.stop.wait(0.005):
+                        break
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
@@ -82,6 +116,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml:
+            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -1044,10 +1081,11 @@ def run_maturity(args, sa, idx, batches, k, nq, d, nlist, n, rank):
 
 
 def run_simulated(args, cfg, sa):
-    """Per-rank work of a W-GPU row-sharded run, measured on one GPU (no NCCL): rank 0's
-    shard of n/W rows, exact and IVF (nprobe = --nprobe or 48, centroids trained on the full
-    corpus as the sharded build would).  The all-gather of [nq, k] keys (40 KB/rank) and the
-    final merge are not included."""
+    """Per-rank work of a W-GPU sharded run, measured on one GPU (no NCCL): rank 0's shard,
+    exact and IVF (nprobe = --nprobe or 48, centroids trained on the full corpus as the sharded
+    build would) on the contiguous row shard (n/W rows), and IVF on the list-sharded layout
+    (rank 0 stores the whole lists l % W == 0).  The all-gather of [nq, k] keys (40 KB/rank)
+    and the final merge are not included."""
     W = args.simulate_world
     n, d, nq, k = cfg["n"], cfg["d"], cfg["nq"], cfg["k"]
     nprobe = args.nprobe or 48
@@ -1056,13 +1094,23 @@ def run_simulated(args, cfg, sa):
     draw_rows_into(mix, X, CORPUS_SEED, 0)
     full = sa.Index.build(X, args.nlist)
     C = torch.from_numpy(full.export_centroids()).cuda()
+    full_lists = full.export_lists()
     full.free()
+    # list-sharded layout: rank r stores the rows of the lists l with
+    # l % W == r (whole lists), under the same global centroids -- the rank-0 subset
+    lo_, gid_ = full_lists
+    own = np.concatenate([gid_[lo_[l]:lo_[l + 1]] for l in range(0, args.nlist, W)])
+    own.sort()
+    Xl = X[torch.from_numpy(own).cuda()].contiguous()
     off, ln = sa.shard_range(n, 0, W)
     Xs = X[off:off + ln].contiguous()
     del X
     torch.cuda.empty_cache()
     idx = sa.Index.build(Xs, args.nlist, row_offset=off, n_total=n, centroids=C)
     del Xs
+    idx_l = sa.Index.build(Xl, args.nlist, centroids=C)
+    n_l = Xl.shape[0]
+    del Xl
     nb = args.warmup + args.steps
     Q = torch.empty(nb * nq, d, dtype=torch.bfloat16, device="cuda")
     draw_rows_into(mix, Q, QUERY_SEED, 0)
@@ -1071,25 +1119,28 @@ def run_simulated(args, cfg, sa):
     res = {"simulated_world": W, "rank_rows": ln, "n": n, "nq": nq, "k": k, "nlist": args.nlist,
            "note": "rank 0's shard timed alone on one B200; excludes the NCCL all-gather "
                    "(nq*k*8 B per rank) and the final merge"}
-    for p in (0, nprobe):
+    for p, ix in ((0, idx), (nprobe, idx), (-nprobe, idx_l)):
+        name = "exact" if p == 0 else (f"ivf_nprobe{p}" if p > 0 else f"ivf_list_sharded_nprobe{-p}")
+        p = abs(p)
         for i in range(args.warmup):
-            idx.search(batches[i], k, p)
+            ix.search(batches[i], k, p)
         torch.cuda.synchronize()
         sa.profile_enable(True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for i in range(args.warmup, nb):
-            idx.search(batches[i], k, p)
+            ix.search(batches[i], k, p)
         e1.record(stream)
         torch.cuda.synchronize()
         kern = {kind: round(sa.profile_read(kind)[0] / args.steps, 4) for kind in sa.KERNEL_KINDS}
         sa.profile_enable(False)
         ms = e0.elapsed_time(e1) / args.steps
-        res["exact" if p == 0 else f"ivf_nprobe{p}"] = {"ms_per_batch_per_rank": ms,
-                                                       "projected_job_qps": nq / (ms / 1e3),
-                                                       "kernel_ms_per_batch": kern}
+        res[name] = {"ms_per_batch_per_rank": ms, "projected_job_qps": nq / (ms / 1e3),
+                     "kernel_ms_per_batch": kern}
+    res["list_sharded_rank_rows"] = n_l
     print(json.dumps(res))
     idx.free()
+    idx_l.free()
     return 0
 
 

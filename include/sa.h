@@ -192,8 +192,10 @@ const char* sa_last_error(void);
  *   - after every check_every lists the device reads *engine_ready; the query stops there
  *     if EMA_t >= tau and the flag is nonzero, else it goes on, up to nprobe_max lists;
  *   - the result is R after the last scanned list (score desc, id asc; padded -1/-INF).
- * The device makes every decision (one captured graph with a conditional WHILE node per
- * shape); no host round trip sits between stages. */
+ * The device makes every decision; no host round trip sits between stages.  Agent-step
+ * batches (nq * min(check_every, nprobe_max) <= 64, k <= 32) run as ONE cooperative kernel
+ * whose stages are closed on the device; larger ones as one captured graph with a conditional
+ * WHILE node per shape. */
 typedef struct {
   double tau;              /* EMA threshold (the paper's HNSW value is 0.9) */
   int32_t window;          /* EMA window in lists, >= 1 (the paper's is 500 candidates) */
@@ -403,6 +405,14 @@ sa_status sa_search_probes(const sa_index* idx, const void* queries, int64_t nq,
  * [nq, n_local], columns in stored-row order (tests of the tensor-core path only). */
 sa_status sa_debug_scores(const sa_index* idx, const void* queries, int64_t nq, float* out_scores,
                           void* stream);
+/* Debug: sa_search_mature on the one-launch path with per-stage timestamps: host_ns HOST
+ * int64 [64 * 4] receives %globaltimer (ns) per stage: CTA 0 stage start, CTA 0 scan done,
+ * last CTA arrival, stage release.  Synchronous.  SA_ERR_UNSUPPORTED when the one-launch path
+ * does not apply. */
+sa_status sa_debug_mature_stages(const sa_index* idx, const void* queries, int64_t nq, int32_t k,
+                                 int32_t nprobe_max, const sa_maturity_opts* opts,
+                                 int64_t* out_ids, float* out_scores, int32_t* out_lists_scanned,
+                                 int64_t* host_ns, void* stream);
 /* Debug: the one-launch agent-step IVF search (nq <= 8; DESIGN.md §4.2 "small batches") with
  * per-CTA phase timestamps.  queries DEVICE bf16 [nq, d]; out_ids / out_scores DEVICE as in
  * sa_search; host_ns HOST int64 [grid * 8] receives %globaltimer (ns) per CTA at: 0 start,

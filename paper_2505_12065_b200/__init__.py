@@ -136,6 +136,8 @@ def lib() -> ctypes.CDLL:
                                   P, P, P, P, P, P]),
         "sa_debug_scores": (st, [P, P, i64, P, P]),
         "sa_debug_small_phases": (st, [P, P, i64, i32, i32, P, P, P, P, P]),
+        "sa_debug_mature_stages": (st, [P, P, i64, i32, i32, ctypes.POINTER(_MaturityOpts), P, P,
+                                        P, P, P]),
         "sa_profile_enable": (st, [i32]),
         "sa_profile_read": (st, [i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]),
     }
@@ -536,6 +538,21 @@ class Index:
                                            _ptr(sc), ns.ctypes.data_as(ctypes.c_void_p),
                                            ctypes.byref(grid), _stream_ptr(stream)))
         return ids, sc, ns[:grid.value * 8].reshape(grid.value, 8)
+
+    def debug_mature_stages(self, queries: torch.Tensor, k: int, nprobe_max: int, *, tau: float,
+                            window: int, check_every: int = 1, stream=None):
+        """One-launch maturity search with per-stage timestamps (ns, [64, 4])."""
+        nq = queries.shape[0]
+        ids = torch.empty(nq, k, dtype=torch.int64, device=queries.device)
+        sc = torch.empty(nq, k, dtype=torch.float32, device=queries.device)
+        t = torch.empty(nq, dtype=torch.int32, device=queries.device)
+        ns = np.zeros(64 * 4, dtype=np.int64)
+        o = _maturity_opts(tau, window, check_every, None)
+        _check(lib().sa_debug_mature_stages(self.handle, _ptr(queries), nq, k, nprobe_max,
+                                            ctypes.byref(o), _ptr(ids), _ptr(sc), _ptr(t),
+                                            ns.ctypes.data_as(ctypes.c_void_p),
+                                            _stream_ptr(stream)))
+        return ids, sc, t, ns.reshape(64, 4)
 
     def debug_scores(self, queries: torch.Tensor, stream=None) -> torch.Tensor:
         n = self.info()["n_local"]

@@ -65,7 +65,8 @@ static_assert((IVSM_MAX_NLIST + IVSM_MAX_NPROBE) <= kRingKeys, "probe candidates
 
 struct PieceInfo {
   int64_t row0;
-  int32_t rows, qi;
+  int32_t rows, qi, o;   // stored rows [row0, +rows), query, output list
+  int32_t pad;
 };
 
 struct __align__(16) SmallSmem {
@@ -81,6 +82,7 @@ struct __align__(16) SmallSmem {
   int32_t probe[kMaxNp];                      // probe entries (query-major, by descending
                                               // key): the list's first stored row
   int32_t lend[kMaxNp];                       // each probe entry's list end
+  int32_t seb[IVSM_MAX_STAGE], see[IVSM_MAX_STAGE];   // a maturity stage's entries
   int32_t pre[kMaxNp + 1];                    // exclusive prefix of pieces per probe entry
   uint32_t hist[256];
   uint64_t red[kWarps];
@@ -109,6 +111,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         " [%0], [%1], %2, [%3];" ::"r"(dst),
         "l"(src), "r"(bytes), "r"(bar)
         : "memory");
+}
+
+__device__ __forceinline__ int32_t read_ready(const int32_t* p) {
+  if (p == nullptr) return 1;
+  int32_t v;
+  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ int64_t globaltimer() {
@@ -239,6 +248,30 @@ __device__ void topk_of_lists(const uint64_t* lists, int L, int lstride, int k, 
   bsync(nth);
 }
 
+// The k best keys of L descending lists of k keys in smem (list j at lists[j * k], empty slots
+// 0) -> out[0, k) descending (0-padded), by ONE warp: k rounds of "largest key below the
+// previous one" (keys are distinct), each round skipping lists whose best key is already
+// taken.  No CTA barrier, so the warps of a CTA merge different outputs concurrently.
+__device__ void warp_topk_of_lists(const uint64_t* lists, int L, int k, uint64_t* out) {
+  const int lane = threadIdx.x & 31;
+  uint64_t prev = ~0ull;
+  for (int r = 0; r < k; ++r) {
+    uint64_t m = 0ull;
+    for (int e = lane; e < L * k; e += 32) {
+      const uint64_t x = lists[e];
+      if (x < prev && x > m) m = x;
+    }
+    m = warp_max_u64(m);
+    if (lane == 0) out[r] = m;
+    prev = m;
+    if (m == 0ull) {
+      for (int r2 = r + 1 + lane; r2 < k; r2 += 32) out[r2] = 0ull;
+      break;
+    }
+  }
+  __syncwarp();
+}
+
 // The nprobe-th largest of the n distinct keys kb[0, n) (n >= nprobe), MSB-first radix
 // select over the 64 key bits, by the whole CTA.
 __device__ uint64_t radix_kth(const uint64_t* kb, int n, int nprobe, SmallSmem& sm) {
@@ -298,8 +331,9 @@ bool ivf_small_fits(int nq, int nprobe, int nlist, int grid) {
          fast_keys(nq, m, grid) <= kRingKeys;
 }
 
-template <int NQ>
-__global__ void __launch_bounds__(kThreads, 1) ivf_small_kernel(const IvfSmallArgs a) {
+template <int NQ, bool MATURE>
+__global__ void __launch_bounds__(kThreads, 1)
+ivf_small_kernel(const IvfSmallArgs a, const SmallMatureArgs mo) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -376,8 +410,22 @@ __global__ void __launch_bounds__(kThreads, 1) ivf_small_kernel(const IvfSmallAr
     const int ch = c >> 3, u = ch >> 5, ln = ch & 31, h = (c >> 2) & 1;
     reinterpret_cast<float*>(&sm.qp[qi][u][h][ln])[c & 3] = v;
   }
-  if (b == 0)   // ordered before every use by the grid barriers below
-    for (int i = tid; i <= nq; i += kThreads) a.counters[i] = 0;
+  if (b == 0) {   // ordered before every use by the grid barriers below
+    for (int i = tid; i <= nq + (MATURE ? 2 : 0); i += kThreads) a.counters[i] = 0;
+    if constexpr (MATURE) {
+      for (int i = tid; i < nq * k; i += kThreads) mo.R[i] = 0ull;
+      for (int qi = tid; qi < nq; qi += kThreads) {
+        mo.ema[qi] = 0.0;
+        mo.active[qi] = 1;
+        mo.t_done[qi] = 0;
+      }
+      if (mo.trace_rq)
+        for (int i = tid; i < nq * nprobe; i += kThreads) {
+          mo.trace_rq[i] = __longlong_as_double(0x7ff8000000000000ll);
+          mo.trace_ema[i] = __longlong_as_double(0x7ff8000000000000ll);
+        }
+    }
+  }
   __syncthreads();
 
   // Ring position p (phase A: p = i; phase C: p = nA + j) uses stage p % kStages; its full
@@ -494,11 +542,21 @@ __global__ void __launch_bounds__(kThreads, 1) ivf_small_kernel(const IvfSmallAr
     uint64_t* tm = tk + nq * Gmp;            // [nq][G * m] the CTAs' first m keys
     uint64_t* cs = tm + nq * Gm;             // [nq][kFastCap] published keys >= T'
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(a.top);
-    for (int i = tid; i < nq * Gmp; i += kThreads) {
-      const uint64_t x = __ldcg(src + i);
-      tk[i] = x;
-      const int qi = i / Gmp, r = i - qi * Gmp, bb = r / mp, jj = r - bb * mp;
-      if (jj < m) tm[qi * Gm + bb * m + jj] = x;
+    for (int i0 = tid; i0 < nq * Gmp; i0 += 8 * kThreads) {   // 8 loads in flight per thread
+      uint64_t x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kThreads;
+        x[u] = i < nq * Gmp ? __ldcg(src + i) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * kThreads;
+        if (i >= nq * Gmp) break;
+        tk[i] = x[u];
+        const int qi = i / Gmp, r = i - qi * Gmp, bb = r / mp, jj = r - bb * mp;
+        if (jj < m) tm[qi * Gm + bb * m + jj] = x[u];
+      }
     }
     if (tid < nq) {
       sm.ccnt[tid] = 0;
@@ -582,202 +640,395 @@ __global__ void __launch_bounds__(kThreads, 1) ivf_small_kernel(const IvfSmallAr
   }
   if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 3] = globaltimer();
 
-  // ---- C: scan the probed lists in 32-row pieces, an equal share of pieces per CTA
-  const int np = nq * nprobe;
-  {
-    // exclusive prefix of piece counts over the scoring threads (np <= 2048: 4 per thread)
-    int loc[4], s = 0;
-    if (!copier) {
+  // ---- C: scan entries [0, E) -- stored rows [sm.probe[e], sm.lend[e]) of `ebeg`/`eend` --
+  // in 32-row pieces, an equal share of pieces per CTA, continuing the ring at position pos.
+  // Entry e belongs to query e / eq_div and to output list eo(e) = e / eo_div; each CTA
+  // writes its top-k of every output list to cand[(b * nout + o) * k] (0-padded, zeros for
+  // lists it did not touch).  Returns the next ring position.
+  auto scan_entries = [&](const int32_t* ebeg, const int32_t* eend, int E, int eq_div,
+                          int eo_div, int nout, uint64_t* cand, int pos, int gscan) -> int {
+    {
+      // exclusive prefix of piece counts over the scoring threads (E <= 2048: 4 per thread)
+      int loc[4], s = 0;
+      if (!copier) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int e = tid * 4 + i;
-        int c = 0;
-        if (e < np) c = (sm.lend[e] - sm.probe[e] + kPiece - 1) / kPiece;
-        loc[i] = s;
-        s += c;
-      }
-    }
-    const uint32_t incl = warp_incl_scan((uint32_t)s);
-    if (lane == 31) sm.red[warp] = incl;
-    __syncthreads();
-    if (!copier) {
-      int base = 0;
-      for (int w = 0; w < warp; ++w) base += (int)sm.red[w];
-      base += (int)incl - s;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int e = tid * 4 + i;
-        if (e < np) sm.pre[e] = base + loc[i];
-      }
-      if (tid == kCThreads - 1) sm.pre[np] = base + s;
-    }
-    for (int i = tid; i < nq * k; i += kThreads) a.cand[(int64_t)b * nq * k + i] = 0ull;
-    ptx::fence_proxy_async_smem();   // the ring's generic-proxy use above precedes the copies
-    __syncthreads();
-  }
-  const int total = sm.pre[np];
-  const int pb = (int)((int64_t)b * total / G), pe = (int)((int64_t)(b + 1) * total / G);
-  const int nP = pe - pb;
-  if (copier) {
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      for (int j = 0; j < nP; ++j) {
-        const int p = pb + j, pos = nA + j, s = pos % kStages;
-        int lo = 0, hi = np - 1;   // the last entry e with pre[e] <= p (it has pieces)
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (sm.pre[mid] <= p) lo = mid;
-          else hi = mid - 1;
-        }
-        const int32_t lend = sm.lend[lo];
-        PieceInfo pi;
-        pi.row0 = sm.probe[lo] + (int64_t)(p - sm.pre[lo]) * kPiece;
-        pi.rows = (int32_t)(lend - pi.row0 < kPiece ? lend - pi.row0 : kPiece);
-        pi.qi = lo / nprobe;
-        // the piece's ids: the 16-byte aligned range around them (row_ids is padded)
-        const int64_t i0 = pi.row0 & ~int64_t(3), i1 = (pi.row0 + pi.rows + 3) & ~int64_t(3);
-        if (pos >= kStages) ptx::mbar_wait(empty0 + s * 8, (uint32_t)((pos / kStages - 1) & 1));
-        sm.info[s] = pi;
-        const uint32_t rb = (uint32_t)pi.rows * row_bytes, ib = (uint32_t)(i1 - i0) * 4;
-        ptx::mbar_arrive_expect_tx(full0 + s * 8, rb + ib);
-        bulk_g2s(ring0 + s * kStageBytes, a.X + pi.row0 * d_pad, rb, full0 + s * 8, pol, true);
-        bulk_g2s(ring0 + s * kStageBytes + kRowsBytes, a.row_ids + i0, ib, full0 + s * 8, pol,
-                 true);
-      }
-    }
-    __syncwarp();
-  } else {
-    // this warp's sorted top-k of the current query: lane j holds the j-th best (0 = empty)
-    uint64_t L = 0ull, lthr = 0ull;
-    int qcur = -1;
-    float qr[3][8];
-    auto flush = [&](int qi) __attribute__((always_inline)) {
-      if (lane < k) sm.wl[warp][lane] = L;
-      bsync(kCThreads);
-      topk_of_lists(&sm.wl[0][0], kCWarps, IVSM_MAX_K, k, sm.sv, kSvCap,
-                    a.cand + ((int64_t)b * nq + qi) * k, sm, kCThreads);
-    };
-    for (int j = 0; j < nP; ++j) {
-      const int pos = nA + j, s = pos % kStages;
-      ptx::mbar_wait(full0 + s * 8, (uint32_t)((pos / kStages) & 1));
-      const PieceInfo pi = sm.info[s];
-      if (pi.qi != qcur) {   // uniform over the scoring warps (each takes every piece)
-        if (qcur >= 0) flush(qcur);
-        qcur = pi.qi;
-#pragma unroll
-        for (int u = 0; u < 3; ++u) {   // zero past d_pad
-          const float4 qa = sm.qp[qcur][u][0][lane], qb = sm.qp[qcur][u][1][lane];
-          qr[u][0] = qa.x; qr[u][1] = qa.y; qr[u][2] = qa.z; qr[u][3] = qa.w;
-          qr[u][4] = qb.x; qr[u][5] = qb.y; qr[u][6] = qb.z; qr[u][7] = qb.w;
-        }
-        L = 0ull;
-        lthr = 0ull;
-      }
-      if (a.debug_ns && j == 0 && tid == 0) a.debug_ns[b * 8 + 7] = globaltimer();
-      const uint8_t* st = ring + s * kStageBytes;
-      const int32_t* ids = reinterpret_cast<const int32_t*>(st + kRowsBytes) + (pi.row0 & 3);
-      uint4 v[2][3];
-      int32_t id[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = warp + h * kCWarps;
-        const uint4* row = reinterpret_cast<const uint4*>(st + r * row_bytes);
-#pragma unroll
-        for (int u = 0; u < 3; ++u) {
-          const int ch = lane + 32 * u;
-          v[h][u] = (r < pi.rows && ch < nch) ? row[ch] : make_uint4(0, 0, 0, 0);
-        }
-        id[h] = r < pi.rows ? ids[r] : 0;
-      }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(empty0 + s * 8);   // this warp is done with the stage
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (warp + h * kCWarps >= pi.rows) break;
-        float acc = 0.f;
-#pragma unroll
-        for (int u = 0; u < 3; ++u) {
-          const uint4 w = v[h][u];   // zero past d_pad
-          acc = fmaf(__uint_as_float(w.x << 16), qr[u][0], acc);
-          acc = fmaf(__uint_as_float(w.x & 0xFFFF0000u), qr[u][1], acc);
-          acc = fmaf(__uint_as_float(w.y << 16), qr[u][2], acc);
-          acc = fmaf(__uint_as_float(w.y & 0xFFFF0000u), qr[u][3], acc);
-          acc = fmaf(__uint_as_float(w.z << 16), qr[u][4], acc);
-          acc = fmaf(__uint_as_float(w.z & 0xFFFF0000u), qr[u][5], acc);
-          acc = fmaf(__uint_as_float(w.w << 16), qr[u][6], acc);
-          acc = fmaf(__uint_as_float(w.w & 0xFFFF0000u), qr[u][7], acc);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        const uint64_t key = make_key(acc, (uint32_t)id[h]);
-        if (key > lthr) {   // warp-uniform: insert into the sorted register list
-          uint64_t prev = __shfl_up_sync(0xffffffffu, L, 1);
-          if (lane == 0) prev = ~0ull;
-          const uint64_t nl = key > L ? (key > prev ? prev : key) : L;
-          L = lane < k ? nl : 0ull;
-          lthr = __shfl_sync(0xffffffffu, L, k - 1);
+        for (int i = 0; i < 4; ++i) {
+          const int e = tid * 4 + i;
+          const int c = e < E ? (eend[e] - ebeg[e] + kPiece - 1) / kPiece : 0;
+          loc[i] = s;
+          s += c;
         }
       }
-    }
-    if (qcur >= 0) flush(qcur);
-  }
-  if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 4] = globaltimer();
-
-  // ---- D: the last CTA to finish merges the G per-CTA lists of every query
-  // (CTA barrier, then a gpu-scope acq_rel increment by one thread: releases this CTA's
-  // lists, and the last CTA acquires everyone's)
-  __syncthreads();
-  if (tid == 0) sm.s_int[3] = ptx::atom_add_acq_rel_gpu(&a.counters[nq], 1);
-  __syncthreads();
-  if (sm.s_int[3] != G - 1) return;
-  // per-CTA lists of as many queries as fit the ring, loaded in one pass (one L2 round trip)
-  const int gk = G * k;
-  int cap = 1;
-  while (cap < gk) cap <<= 1;
-  const int fit = max(1, (kRingKeys - cap - IVSM_MAX_K) / gk);
-  uint64_t* lists = ring64;
-  for (int q0 = 0; q0 < nq; q0 += fit) {
-    const int nf = min(fit, nq - q0);
-    uint64_t* sv = lists + nf * gk;
-    uint64_t* best = sv + cap;
-    for (int i = tid; i < nf * gk; i += kThreads) {   // lists[qj][bb][j] <- cand[bb][q0 + qj][j]
-      const int qj = i / gk, bb = (i - qj * gk) / k, j = i - qj * gk - bb * k;
-      lists[i] = __ldcg(reinterpret_cast<const unsigned long long*>(a.cand) +
-                        ((int64_t)bb * nq + q0 + qj) * k + j);
-    }
-    __syncthreads();
-    for (int qj = 0; qj < nf; ++qj) {
-      topk_of_lists(lists + qj * gk, G, k, k, sv, cap, best, sm, kThreads);
-      for (int j = tid; j < k; j += kThreads) {
-        const uint64_t key = best[j];
-        const int64_t o = (int64_t)(q0 + qj) * k + j;
-        if (a.out_keys) {
-          a.out_keys[o] = key;
-        } else {
-          a.out_ids[o] = key == 0ull ? -1 : (int64_t)key_id(key);
-          a.out_scores[o] = key == 0ull ? -__int_as_float(0x7f800000) : key_score(key);
+      const uint32_t incl = warp_incl_scan((uint32_t)s);
+      if (lane == 31) sm.red[warp] = incl;
+      __syncthreads();
+      if (!copier) {
+        int base = 0;
+        for (int w = 0; w < warp; ++w) base += (int)sm.red[w];
+        base += (int)incl - s;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = tid * 4 + i;
+          if (e < E) sm.pre[e] = base + loc[i];
         }
+        if (tid == kCThreads - 1) sm.pre[E] = base + s;
       }
-      if (a.done_host) __threadfence_system();   // results visible before the signal
+      for (int i = tid; i < nout * k; i += kThreads) cand[(int64_t)b * nout * k + i] = 0ull;
+      ptx::fence_proxy_async_smem();   // the ring's generic-proxy use above precedes the copies
       __syncthreads();
     }
+    const int total = sm.pre[E];
+    // pieces of CTA b among the gscan scanning CTAs
+    const int pb = (int)((int64_t)b * total / gscan), pe = (int)((int64_t)(b + 1) * total / gscan);
+    const int nP = pe - pb;
+    if (copier) {
+      if (lane == 0) {
+        const uint64_t pol = policy_evict_first();
+        for (int j = 0; j < nP; ++j) {
+          const int p = pb + j, ps = pos + j, s = ps % kStages;
+          int lo = 0, hi = E - 1;   // the last entry e with pre[e] <= p (it has pieces)
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sm.pre[mid] <= p) lo = mid;
+            else hi = mid - 1;
+          }
+          const int32_t lend = eend[lo];
+          PieceInfo pi;
+          pi.row0 = ebeg[lo] + (int64_t)(p - sm.pre[lo]) * kPiece;
+          pi.rows = (int32_t)(lend - pi.row0 < kPiece ? lend - pi.row0 : kPiece);
+          pi.qi = lo / eq_div;
+          pi.o = lo / eo_div;
+          // the piece's ids: the 16-byte aligned range around them (row_ids is padded)
+          const int64_t i0 = pi.row0 & ~int64_t(3), i1 = (pi.row0 + pi.rows + 3) & ~int64_t(3);
+          if (ps >= kStages) ptx::mbar_wait(empty0 + s * 8, (uint32_t)((ps / kStages - 1) & 1));
+          sm.info[s] = pi;
+          const uint32_t rb = (uint32_t)pi.rows * row_bytes, ib = (uint32_t)(i1 - i0) * 4;
+          ptx::mbar_arrive_expect_tx(full0 + s * 8, rb + ib);
+          bulk_g2s(ring0 + s * kStageBytes, a.X + pi.row0 * d_pad, rb, full0 + s * 8, pol, true);
+          bulk_g2s(ring0 + s * kStageBytes + kRowsBytes, a.row_ids + i0, ib, full0 + s * 8, pol,
+                   true);
+        }
+      }
+      __syncwarp();
+    } else {
+      // this warp's sorted top-k of the current output list: lane j holds the j-th best
+      uint64_t L = 0ull, lthr = 0ull;
+      int qcur = -1, ocur = -1;
+      float qr[3][8];
+      // the 16 warp lists -> this CTA's list of output o, merged by warp 0 alone (the first
+      // barrier keeps the next flush from overwriting lists warp 0 may still be reading)
+      uint64_t* wl = &sm.wl[0][0];   // [kCWarps][k], contiguous
+      auto flush = [&](int o) __attribute__((always_inline)) {
+        bsync(kCThreads);
+        if (lane < k) wl[warp * k + lane] = L;
+        bsync(kCThreads);
+        if (warp == 0) warp_topk_of_lists(wl, kCWarps, k, cand + ((int64_t)b * nout + o) * k);
+      };
+      for (int j = 0; j < nP; ++j) {
+        const int ps = pos + j, s = ps % kStages;
+        ptx::mbar_wait(full0 + s * 8, (uint32_t)((ps / kStages) & 1));
+        const PieceInfo pi = sm.info[s];
+        if (pi.o != ocur) {   // uniform over the scoring warps (each takes every piece)
+          if (ocur >= 0) flush(ocur);
+          ocur = pi.o;
+          L = 0ull;
+          lthr = 0ull;
+        }
+        if (pi.qi != qcur) {
+          qcur = pi.qi;
+#pragma unroll
+          for (int u = 0; u < 3; ++u) {   // zero past d_pad
+            const float4 qa = sm.qp[qcur][u][0][lane], qb = sm.qp[qcur][u][1][lane];
+            qr[u][0] = qa.x; qr[u][1] = qa.y; qr[u][2] = qa.z; qr[u][3] = qa.w;
+            qr[u][4] = qb.x; qr[u][5] = qb.y; qr[u][6] = qb.z; qr[u][7] = qb.w;
+          }
+        }
+        if (a.debug_ns && j == 0 && tid == 0) a.debug_ns[b * 8 + 7] = globaltimer();
+        const uint8_t* st = ring + s * kStageBytes;
+        const int32_t* ids = reinterpret_cast<const int32_t*>(st + kRowsBytes) + (pi.row0 & 3);
+        uint4 v[2][3];
+        int32_t id[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = warp + h * kCWarps;
+          const uint4* row = reinterpret_cast<const uint4*>(st + r * row_bytes);
+#pragma unroll
+          for (int u = 0; u < 3; ++u) {
+            const int ch = lane + 32 * u;
+            v[h][u] = (r < pi.rows && ch < nch) ? row[ch] : make_uint4(0, 0, 0, 0);
+          }
+          id[h] = r < pi.rows ? ids[r] : 0;
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(empty0 + s * 8);   // this warp is done with the stage
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (warp + h * kCWarps >= pi.rows) break;
+          float acc = 0.f;
+#pragma unroll
+          for (int u = 0; u < 3; ++u) {
+            const uint4 w = v[h][u];   // zero past d_pad
+            acc = fmaf(__uint_as_float(w.x << 16), qr[u][0], acc);
+            acc = fmaf(__uint_as_float(w.x & 0xFFFF0000u), qr[u][1], acc);
+            acc = fmaf(__uint_as_float(w.y << 16), qr[u][2], acc);
+            acc = fmaf(__uint_as_float(w.y & 0xFFFF0000u), qr[u][3], acc);
+            acc = fmaf(__uint_as_float(w.z << 16), qr[u][4], acc);
+            acc = fmaf(__uint_as_float(w.z & 0xFFFF0000u), qr[u][5], acc);
+            acc = fmaf(__uint_as_float(w.w << 16), qr[u][6], acc);
+            acc = fmaf(__uint_as_float(w.w & 0xFFFF0000u), qr[u][7], acc);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          const uint64_t key = make_key(acc, (uint32_t)id[h]);
+          if (key > lthr) {   // warp-uniform: insert into the sorted register list
+            uint64_t prev = __shfl_up_sync(0xffffffffu, L, 1);
+            if (lane == 0) prev = ~0ull;
+            const uint64_t nl = key > L ? (key > prev ? prev : key) : L;
+            L = lane < k ? nl : 0ull;
+            lthr = __shfl_sync(0xffffffffu, L, k - 1);
+          }
+        }
+      }
+      if (ocur >= 0) flush(ocur);
+    }
+    return pos + nP;
+  };
+
+  // The k best keys of each of the nl lists cand[(bb * nout + o0 + o) * k], bb < G, o < nl ->
+  // dst + o * k, by the whole CTA (lists of as many outputs as fit the ring loaded in one
+  // pass, one L2 round trip).  cand was written by other CTAs: read through L2.
+  // `reserve` keys at the end of the ring are not touched (dst may live there).
+  auto merge_outputs = [&](const uint64_t* cand, int nout, int o0, int nl, uint64_t* dst,
+                           int reserve) {
+    const int gk = G * k;
+    const int fit = max(1, (kRingKeys - reserve) / gk);
+    uint64_t* lists = ring64;
+    for (int f0 = 0; f0 < nl; f0 += fit) {
+      const int nf = min(fit, nl - f0);
+      for (int i0 = tid; i0 < nf * gk; i0 += 8 * kThreads) {   // lists[of][bb][j], 8 in flight
+        uint64_t x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u * kThreads;
+          const int of = i / gk, bb = (i - of * gk) / k, j = i - of * gk - bb * k;
+          x[u] = i < nf * gk ? __ldcg(reinterpret_cast<const unsigned long long*>(cand) +
+                                      ((int64_t)bb * nout + o0 + f0 + of) * k + j)
+                             : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + u * kThreads < nf * gk) lists[i0 + u * kThreads] = x[u];
+      }
+      __syncthreads();
+      for (int of = warp; of < nf; of += kWarps)   // one output per warp
+        warp_topk_of_lists(lists + of * gk, G, k, dst + (int64_t)(f0 + of) * k);
+      __syncthreads();
+    }
+  };
+  auto write_result = [&](int qi, int j, uint64_t key) {
+    const int64_t o = (int64_t)qi * k + j;
+    if (a.out_keys) {
+      a.out_keys[o] = key;
+    } else {
+      a.out_ids[o] = key == 0ull ? -1 : (int64_t)key_id(key);
+      a.out_scores[o] = key == 0ull ? -__int_as_float(0x7f800000) : key_score(key);
+    }
+  };
+
+  if constexpr (!MATURE) {
+    const int np = nq * nprobe;
+    const int pos = scan_entries(sm.probe, sm.lend, np, nprobe, nprobe, nq, a.cand, nA, G);
+    (void)pos;
+    if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 4] = globaltimer();
+
+    // ---- D: the last CTA to finish merges the G per-CTA lists of every query
+    // (CTA barrier, then a gpu-scope acq_rel increment by one thread: releases this CTA's
+    // lists, and the last CTA acquires everyone's)
+    __syncthreads();
+    if (tid == 0) sm.s_int[3] = ptx::atom_add_acq_rel_gpu(&a.counters[nq], 1);
+    __syncthreads();
+    if (sm.s_int[3] != G - 1) return;
+    uint64_t* best = ring64 + kRingKeys - nq * k;   // past every merge's working set
+    merge_outputs(a.cand, nq, 0, nq, best, nq * k);
+    for (int i = tid; i < nq * k; i += kThreads) write_result(i / k, i % k, best[i]);
+    if (a.done_host) __threadfence_system();   // results visible before the signal
+    __syncthreads();
+    if (a.done_host && tid == 0) {
+      const int32_t v = *a.seq + 1;
+      *a.seq = v;
+      __threadfence_system();
+      *reinterpret_cast<volatile int32_t*>(a.done_host) = v;
+    }
+    if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 5] = globaltimer();
+  } else {
+    // ---- maturity exit (§3.3; R14-R19): stage s scans lists
+    // [s*g, (s+1)*g) of every active query; the last CTA to finish a stage merges each list's
+    // per-CTA lists, inserts the lists into the running top-k R in probe-rank order, updates
+    // RQ / EMA per list and takes the exit decision at the checkpoint, then releases the
+    // next stage.  One launch; the engine-ready flag is read on the device.
+    const int P = nprobe, g = mo.g;
+    // CTAs 0..G-2 scan, CTA G-1 closes the stages.  Stage st's scan overlaps stage st-1's
+    // closure: the entries of stage st are those of the queries still active after closure
+    // st-2 (a superset of the true set -- a query that exits at closure st-1 just has its
+    // stage-st lists ignored), and the per-CTA lists are double-buffered by stage parity.
+    // The closer waits for every scanner's arrival at stage st, merges each list's per-CTA
+    // lists, inserts the lists into the running top-k R in probe-rank order, updates RQ / EMA
+    // per list, takes the exit decisions and releases the stage with the new active mask.
+    const int Gs = G - 1;
+    int32_t* arr = a.counters + nq;        // [2] scanners done with a stage, per parity
+    int32_t* rel = a.counters + nq + 2;    // release word: closed stages | active mask << 16
+    const int64_t cand_stage = (int64_t)G * nq * g * k;
+    // tid 0: wait until stages [0, upto) are closed, or the search has ended (mask 0)
+    auto wait_release = [&](int upto) -> uint32_t {
+      int32_t v;
+      while (true) {
+        v = ptx::ld_acquire_gpu(rel);
+        if ((v & 0xFFFF) >= upto || ((v & 0xFFFF) > 0 && ((uint32_t)v >> 16) == 0u)) break;
+        __nanosleep(32);
+      }
+      return (uint32_t)v >> 16;
+    };
+    const uint32_t full_mask = (1u << nq) - 1u;
+    if (b == G - 1) {
+      // ---- the closer
+      for (int i = tid; i < 2 * nq * g * k; i += kThreads)   // its own (empty) lists
+        a.cand[(i / (nq * g * k)) * cand_stage + (int64_t)b * nq * g * k + i % (nq * g * k)] = 0ull;
+      uint32_t cmask = full_mask;   // active after the previous closure
+      for (int st = 0;; ++st) {
+        const bool stamp = mo.stage_ns && st < 64 && tid == 0;
+        if (tid == 0) {
+          while (ptx::ld_acquire_gpu(arr + (st & 1)) < Gs) __nanosleep(32);
+          if (stamp) mo.stage_ns[st * 4 + 2] = globaltimer();
+        }
+        __syncthreads();
+        // the engine flag, read once per stage (its latency overlaps the merges)
+        const int32_t ready = tid == 0 ? read_ready(mo.ready) : 0;
+        const uint64_t* cand = a.cand + (st & 1) * cand_stage;
+        // the stage's lists (exact top-k per list: its best key is element 0)
+        uint64_t* lt = ring64 + kRingKeys - nq * g * k;
+        merge_outputs(cand, nq * g, 0, nq * g, lt, nq * g * k);
+        if (tid == 0) {
+          sm.s_int[1] = ready;
+          sm.s_int[2] = (int32_t)cmask;
+        }
+        __syncthreads();
+        if (warp < nq && ((cmask >> warp) & 1u)) {
+          const int qi = warp;
+          uint64_t R = lane < k ? __ldcg(reinterpret_cast<const unsigned long long*>(mo.R) +
+                                         (int64_t)qi * k + lane)
+                                : 0ull;
+          double ema = __ldcg(mo.ema + qi);
+          // the g insertions in probe-rank order (shuffles only); lane j keeps step j's
+          // (s_best, s_worst, s_t) keys, so the fp64 divisions below run side by side
+          uint64_t kb = 0ull, kw = 0ull, ks = 0ull;
+          const int ng = min(g, P - st * g);
+          for (int j = 0; j < ng; ++j) {
+            const uint64_t* lj = lt + (qi * g + j) * k;
+            // R <- top-k(R u list): both descending, the list reversed across lanes makes the
+            // 64 keys bitonic; one max/min step keeps the best 32 (bitonic), 5 more sort them
+            const uint64_t lv = lane < k ? lj[lane] : 0ull;
+            const uint64_t lrev = __shfl_sync(0xffffffffu, lv, 31 - lane);
+            uint64_t x = R > lrev ? R : lrev;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const uint64_t y = __shfl_xor_sync(0xffffffffu, x, o);
+              x = (lane & o) ? (x < y ? x : y) : (x > y ? x : y);
+            }
+            R = lane < k ? x : 0ull;
+            const uint64_t best = __shfl_sync(0xffffffffu, R, 0);
+            const unsigned nz = __ballot_sync(0xffffffffu, R != 0ull);
+            const uint64_t worst = nz ? __shfl_sync(0xffffffffu, R, 31 - __clz(nz)) : 0ull;
+            if (lane == j) {
+              kb = best;
+              kw = worst;
+              ks = lj[0];
+            }
+          }
+          // signal (R15-R17) in fp64 from the fp32 scores, the oracle's two roundings
+          double rq = 1.0;
+          if (lane < ng && ks != 0ull && kb != 0ull) {
+            const double sb = (double)key_score(kb), sw = (double)key_score(kw);
+            const double s_t = (double)key_score(ks);
+            if (sb != sw) rq = __ddiv_rn(__dsub_rn(sb, s_t), __dsub_rn(sb, sw));
+          }
+          for (int j = 0; j < ng; ++j) {   // the EMA recurrence, identical in every lane
+            const double rj = __shfl_sync(0xffffffffu, rq, j);
+            const int r = st * g + j;
+            ema = r == 0 ? rj : __dadd_rn(__dmul_rn(mo.alpha, rj), __dmul_rn(1.0 - mo.alpha, ema));
+            if (lane == j && mo.trace_rq) {
+              mo.trace_rq[(int64_t)qi * P + r] = rj;
+              mo.trace_ema[(int64_t)qi * P + r] = ema;
+            }
+          }
+          if (lane < k) reinterpret_cast<unsigned long long*>(mo.R)[(int64_t)qi * k + lane] = R;
+          if (lane == 0) {
+            mo.ema[qi] = ema;
+            // checkpoint after the stage (R18): t = lists scanned so far
+            const int t = min((st + 1) * g, P);
+            const bool exit_now = (t % g) == 0 && ema >= mo.tau && sm.s_int[1] != 0;
+            if (exit_now || t >= P) {
+              mo.t_done[qi] = t;
+              atomicAnd(reinterpret_cast<unsigned*>(&sm.s_int[2]), ~(1u << qi));
+            }
+          }
+        }
+        __syncthreads();
+        cmask = (uint32_t)sm.s_int[2];
+        if (cmask == 0u) {   // the last queries finished: R -> the output
+          for (int i = tid; i < nq * k; i += kThreads)
+            write_result(i / k, i % k,
+                         __ldcg(reinterpret_cast<const unsigned long long*>(mo.R) + i));
+          for (int qi = tid; qi < nq; qi += kThreads)
+            if (mo.out_t) mo.out_t[qi] = __ldcg(mo.t_done + qi);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          arr[st & 1] = 0;
+          if (stamp) mo.stage_ns[st * 4 + 3] = globaltimer();
+          ptx::st_release_gpu(rel, (int32_t)((cmask << 16) | (uint32_t)(st + 1)));
+        }
+        if (cmask == 0u) break;
+      }
+    } else {
+      // ---- the scanners
+      int pos = nA;
+      for (int st = 0;; ++st) {
+        const bool stamp = mo.stage_ns && st < 64 && tid == 0 && b == 0;
+        if (tid == 0) sm.s_int[2] = (int32_t)(st >= 2 ? wait_release(st - 1) : full_mask);
+        __syncthreads();
+        const uint32_t amask = (uint32_t)sm.s_int[2];
+        __syncthreads();
+        if (amask == 0u) break;
+        if (stamp) mo.stage_ns[st * 4 + 0] = globaltimer();
+        // this stage's entries: e = qi * g + j -> probe rank st * g + j of query qi
+        for (int e = tid; e < nq * g; e += kThreads) {
+          const int qi = e / g, r = st * g + e % g;
+          const bool on = r < P && ((amask >> qi) & 1u);
+          sm.seb[e] = on ? sm.probe[qi * P + r] : 0;
+          sm.see[e] = on ? sm.lend[qi * P + r] : 0;
+        }
+        __syncthreads();
+        pos = scan_entries(sm.seb, sm.see, nq * g, g, 1, nq * g, a.cand + (st & 1) * cand_stage,
+                           pos, Gs);
+        __syncthreads();
+        if (stamp) mo.stage_ns[st * 4 + 1] = globaltimer();
+        if (tid == 0) ptx::atom_add_acq_rel_gpu(arr + (st & 1), 1);   // releases the lists
+      }
+    }
   }
-  if (a.done_host && tid == 0) {
-    const int32_t v = *a.seq + 1;
-    *a.seq = v;
-    __threadfence_system();
-    *reinterpret_cast<volatile int32_t*>(a.done_host) = v;
-  }
-  if (a.debug_ns && tid == 0) a.debug_ns[b * 8 + 5] = globaltimer();
 }
 
 size_t ivf_small_smem_bytes() { return 128 + (size_t)kRingBytes + sizeof(SmallSmem); }
 
-cudaError_t launch_ivf_small(const IvfSmallArgs& a, int grid, cudaStream_t s) {
+static cudaError_t launch_small(const IvfSmallArgs& a, const SmallMatureArgs& mo, bool mature,
+                                int grid, cudaStream_t s) {
   if (a.nq < 1 || a.nq > IVSM_MAX_NQ || a.k < 1 || a.k > IVSM_MAX_K || a.nprobe < 1 ||
       a.nprobe > IVSM_MAX_NPROBE || a.nprobe > a.nlist || a.d_pad > kMaxDPad || a.d_pad % 64 ||
       grid < a.nq || !ivf_small_fits(a.nq, a.nprobe, a.nlist, grid) ||
-      (int64_t)grid * a.k * 2 + IVSM_MAX_K > kRingKeys)
+      (int64_t)grid * a.k * 2 + (int64_t)a.nq * a.k > kRingKeys)
+    return cudaErrorInvalidValue;
+  if (mature && (mo.g < 1 || mo.g > IVSM_MAX_G || a.nq * mo.g > IVSM_MAX_STAGE || grid < 2 ||
+                 (int64_t)grid * a.k * 2 + (int64_t)a.nq * mo.g * a.k > kRingKeys))
     return cudaErrorInvalidValue;
   const size_t smem = ivf_small_smem_bytes();
   cudaLaunchConfig_t cfg{};
@@ -793,14 +1044,29 @@ cudaError_t launch_ivf_small(const IvfSmallArgs& a, int grid, cudaStream_t s) {
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = ensure_max_smem(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
-    e = cudaLaunchKernelEx(&cfg, kern, a);
+    e = cudaLaunchKernelEx(&cfg, kern, a, mo);
     note_launch();
     return e;
   };
-  if (a.nq <= 1) return go(ivf_small_kernel<1>);
-  if (a.nq <= 2) return go(ivf_small_kernel<2>);
-  if (a.nq <= 4) return go(ivf_small_kernel<4>);
-  return go(ivf_small_kernel<8>);
+  if (mature) {
+    if (a.nq <= 1) return go(ivf_small_kernel<1, true>);
+    if (a.nq <= 2) return go(ivf_small_kernel<2, true>);
+    if (a.nq <= 4) return go(ivf_small_kernel<4, true>);
+    return go(ivf_small_kernel<8, true>);
+  }
+  if (a.nq <= 1) return go(ivf_small_kernel<1, false>);
+  if (a.nq <= 2) return go(ivf_small_kernel<2, false>);
+  if (a.nq <= 4) return go(ivf_small_kernel<4, false>);
+  return go(ivf_small_kernel<8, false>);
+}
+
+cudaError_t launch_ivf_small(const IvfSmallArgs& a, int grid, cudaStream_t s) {
+  return launch_small(a, SmallMatureArgs{}, false, grid, s);
+}
+
+cudaError_t launch_ivf_small_mature(const IvfSmallArgs& a, const SmallMatureArgs& mo, int grid,
+                                    cudaStream_t s) {
+  return launch_small(a, mo, true, grid, s);
 }
 
 }  // namespace sa

@@ -14,6 +14,8 @@ constexpr int IVSM_THREADS = 544;  // 16 scoring warps + 1 copy-issuing warp
 constexpr int IVSM_MAX_LOCAL = 256;  // centroids per CTA: nlist <= 256 * grid
 constexpr int IVSM_MAX_NLIST = 18176;  // probe candidates + selection in the smem ring
 constexpr int IVSM_EXTRA = 7;      // keys published per CTA beyond the m of the probe threshold
+constexpr int IVSM_MAX_STAGE = 64; // maturity path: nq * check_every entries per stage
+constexpr int IVSM_MAX_G = 32;     // maturity path: check_every (one lane per list of a stage)
 
 struct IvfSmallArgs {
   const void* Q;              // queries [nq, d] row-major, bf16 or fp32 (q_f32)
@@ -44,6 +46,23 @@ struct IvfSmallArgs {
   float* out_scores;          // [nq, k] scores (-inf padded)
 };
 
+// Non-stall maturity exit in the same launch (§3.3; R14-R19): stages of g
+// lists per active query; state in device memory, initialised by the kernel.
+struct SmallMatureArgs {
+  int32_t g = 0;              // lists per stage (exit test after each stage), nq * g <= 64
+  double tau = 0, alpha = 0;  // EMA threshold, EMA weight 2 / (W + 1)
+  const int32_t* ready = nullptr;   // engine-ready flag (host pinned or device), null = ready
+  uint64_t* R = nullptr;      // [nq, k] running top-k keys
+  double* ema = nullptr;      // [nq]
+  int32_t* active = nullptr;  // [nq]
+  int32_t* t_done = nullptr;  // [nq] lists scanned at the exit
+  double* trace_rq = nullptr; // optional [nq, nprobe] (NaN past the exit)
+  double* trace_ema = nullptr;
+  int32_t* out_t = nullptr;   // optional [nq]: lists scanned, written at the end
+  int64_t* stage_ns = nullptr;   // optional debug [64][4] %globaltimer per stage: CTA 0 start,
+                                 // CTA 0 scan done, last CTA arrival, release
+};
+
 // Per-CTA best centroid keys that set the probe threshold: m * grid >= nprobe.
 __host__ __device__ inline int ivf_small_m(int nprobe, int grid) { return (nprobe + grid - 1) / grid; }
 // Whether the kernel's smem ring holds the probe step's working set for this shape.
@@ -52,5 +71,9 @@ bool ivf_small_fits(int nq, int nprobe, int nlist, int grid);
 size_t ivf_small_smem_bytes();
 // Cooperative launch, grid = one CTA per SM.
 cudaError_t launch_ivf_small(const IvfSmallArgs& a, int grid, cudaStream_t s);
+// The same search with the maturity exit: nprobe = nprobe_max; a.cand holds
+// [2][grid, nq * g, k] (stage parity); a.counters [nq + 3].
+cudaError_t launch_ivf_small_mature(const IvfSmallArgs& a, const SmallMatureArgs& mo, int grid,
+                                    cudaStream_t s);
 
 }  // namespace sa

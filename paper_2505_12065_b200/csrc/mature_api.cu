@@ -20,6 +20,7 @@
 #include "internal.h"
 #include "kernels/ivf_kernels.cuh"
 #include "kernels/ivf_scan.cuh"
+#include "kernels/ivf_small.cuh"
 #include "kernels/mature.cuh"
 #include "kernels/merge.cuh"
 
@@ -262,6 +263,51 @@ sa_status make_plan(const sa_index* idx, MaturePlan& p) {
   return SA_OK;
 }
 
+// Agent-step batches (nq * g <= 64, k <= 32): the whole progressive search in ONE cooperative
+// launch (ivf_small.cu) -- probe, then stages of g lists per active query, each closed by the
+// last CTA to finish it (in-order merge, RQ / EMA, exit test on the engine flag), no graph.
+sa_status mature_small(const sa_index* idx, const void* queries, bool q_f32, int64_t nq,
+                       int32_t k, int32_t P, int32_t g, const sa_maturity_opts& o,
+                       int64_t* out_ids, float* out_scores, int32_t* out_t, double* out_rq,
+                       double* out_ema, cudaStream_t s, int64_t* stage_ns = nullptr) {
+  const int grid = idx->num_sms;
+  StreamFreer f{s};
+  IvfSmallArgs a{};
+  SmallMatureArgs m{};
+  SA_TRY(f.alloc(&a.top, (size_t)nq * grid * (ivf_small_m(P, grid) + IVSM_EXTRA), "mature scratch"));
+  SA_TRY(f.alloc(&a.pcand, (size_t)nq * idx->nlist, "mature scratch"));
+  SA_TRY(f.alloc(&a.counters, (size_t)nq + 3, "mature scratch"));
+  SA_TRY(f.alloc(&a.cand, (size_t)2 * grid * nq * g * k, "mature scratch"));
+  SA_TRY(f.alloc(&m.R, (size_t)nq * k, "mature scratch"));
+  SA_TRY(f.alloc(&m.ema, (size_t)nq, "mature scratch"));
+  SA_TRY(f.alloc(&m.active, (size_t)nq, "mature scratch"));
+  SA_TRY(f.alloc(&m.t_done, (size_t)nq, "mature scratch"));
+  a.Q = queries;
+  a.q_f32 = q_f32 ? 1 : 0;
+  a.nq = (int32_t)nq;
+  a.d = idx->d;
+  a.d_pad = idx->d_pad;
+  a.C = idx->centroids_bf16;
+  a.nlist = idx->nlist;
+  a.nprobe = P;
+  a.X = idx->X;
+  a.list_off = idx->list_off;
+  a.row_ids = idx->row_ids;
+  a.k = k;
+  a.out_ids = out_ids;
+  a.out_scores = out_scores;
+  m.g = g;
+  m.tau = o.tau;
+  m.alpha = 2.0 / (o.window + 1.0);
+  m.ready = o.engine_ready;
+  m.trace_rq = out_rq;
+  m.trace_ema = out_ema;
+  m.out_t = out_t;
+  m.stage_ns = stage_ns;
+  ProfRegion prof_region(SA_KERNEL_IVF_SCAN, s);
+  return cuda_status(launch_ivf_small_mature(a, m, grid, s), "maturity search (one launch)");
+}
+
 }  // namespace
 }  // namespace sa
 
@@ -291,6 +337,10 @@ extern "C" sa_status sa_search_mature(const sa_index* idx, const void* queries, 
   if (idx->comm && idx->comm->world > 1)
     return set_error(SA_ERR_UNSUPPORTED, "maturity exit on a sharded index");
   cudaStream_t s = (cudaStream_t)stream;
+  if (nq * g <= IVSM_MAX_STAGE && g <= IVSM_MAX_G && k <= IVSM_MAX_K &&
+      ivf_small_applies(idx, nq, k, nprobe_max))
+    return mature_small(idx, queries, qdtype == SA_F32, nq, k, nprobe_max, g, *opts, out_ids,
+                        out_scores, out_lists_scanned, out_rq, out_ema, s);
   sa_index* mi = const_cast<sa_index*>(idx);
   std::lock_guard<std::mutex> lock(mi->graph_mu);
   MaturePlan* p = nullptr;
@@ -350,5 +400,32 @@ extern "C" sa_status sa_search_mature(const sa_index* idx, const void* queries, 
                        "trace out");
   }
   if (st == SA_OK) prof_add_launches(p->launches);
+  return st;
+}
+
+extern "C" sa_status sa_debug_mature_stages(const sa_index* idx, const void* queries, int64_t nq,
+                                            int32_t k, int32_t nprobe_max,
+                                            const sa_maturity_opts* opts, int64_t* out_ids,
+                                            float* out_scores, int32_t* out_lists_scanned,
+                                            int64_t* host_ns, void* stream) {
+  if (!idx || !queries || !opts || !out_ids || !out_scores || !host_ns)
+    return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  const int32_t g = std::min(opts->check_every, nprobe_max);
+  if (g < 1 || nq * g > IVSM_MAX_STAGE || g > IVSM_MAX_G || k > IVSM_MAX_K ||
+      !ivf_small_applies(idx, nq, k, nprobe_max))
+    return set_error(SA_ERR_UNSUPPORTED, "the one-launch maturity path does not apply");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t* dns = nullptr;
+  sa_status st = dalloc(&dns, 64 * 4, s, "alloc debug timestamps");
+  if (st != SA_OK) return st;
+  st = cuda_status(cudaMemsetAsync(dns, 0, 64 * 4 * sizeof(int64_t), s), "memset");
+  if (st == SA_OK)
+    st = mature_small(idx, queries, false, nq, k, nprobe_max, g, *opts, out_ids, out_scores,
+                      out_lists_scanned, nullptr, nullptr, s, dns);
+  if (st == SA_OK)
+    st = cuda_status(cudaMemcpyAsync(host_ns, dns, 64 * 4 * sizeof(int64_t),
+                                     cudaMemcpyDeviceToHost, s), "copy timestamps");
+  if (st == SA_OK) st = cuda_status(cudaStreamSynchronize(s), "sync");
+  cudaFreeAsync(dns, s);
   return st;
 }

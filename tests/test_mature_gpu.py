@@ -107,9 +107,19 @@ def check_prefix_result(gi, gs, Xb, Qb, qi, rows, k):
     (50, 16, 1.5, 8, 4),
     (10, 20, math.inf, 8, 5),
 ])
-def test_matches_oracle_on_mixture(sa, mix, k, P, tau, window, g):
+@pytest.mark.parametrize("nq", [24, 8])
+def test_matches_oracle_on_mixture(sa, mix, k, P, tau, window, g, nq):
+    """nq = 24: the captured-graph stage loop; nq = 8 (and k <= 32, 8 g <= 64): the one-launch
+    kernel whose stages are closed on the device (ivf_small.cu).  The oracle walks the probe
+    order of the batch probe; a query whose first P + 1 probe ranks hold an fp32 near-tie may
+    be ordered differently by the one-launch path's CUDA-core probe and is skipped."""
     idx, Xb, Qb, lists = mix
+    Qb = Qb[:nq]
     Qd = bits_to_tensor(Qb).cuda()
+    C = oracle.bf16_to_f64(oracle.bf16_round(np.asarray(idx.export_centroids(), np.float32)))
+    Q64 = oracle.bf16_to_f64(Qb)
+    pc = Q64 @ C.T
+    eb = 2 * (Q64.shape[1] - 1) * 2.0 ** -24 * (np.abs(Q64) @ np.abs(C).T)
     probes = idx.probes(Qd, P).cpu().numpy()
     gi, gs, gt, grq, gema = idx.search_mature(Qd, k, P, tau=tau, window=window, check_every=g,
                                               trace=True)
@@ -118,7 +128,15 @@ def test_matches_oracle_on_mixture(sa, mix, k, P, tau, window, g):
     grq, gema = grq.cpu().numpy(), gema.cpu().numpy()
     delta = 1e-5
     exits = []
+    skipped = 0
     for qi in range(len(Qb)):
+        ranked = probes[qi][:P].tolist() + [int(j) for j in np.argsort(-pc[qi]) if j not in
+                                            set(probes[qi][:P].tolist())][:1]
+        gaps = [pc[qi, ranked[i]] - pc[qi, ranked[i + 1]] - eb[qi, ranked[i]] - eb[qi, ranked[i + 1]]
+                for i in range(len(ranked) - 1)]
+        if min(gaps) <= 0:
+            skipped += 1
+            continue
         o = maturity.search_query(Xb, lists, probes[qi], Qb[qi], k, tau=math.inf, window=window)
         brq, bema = ema_error_bound(o, window, delta, k)
         t = int(gt[qi])
@@ -139,6 +157,7 @@ def test_matches_oracle_on_mixture(sa, mix, k, P, tau, window, g):
         rows = np.sort(np.concatenate([lists[j] for j in probes[qi][:t]]))
         check_prefix_result(gi, gs, Xb, Qb, qi, rows, k)
         exits.append(t)
+    assert skipped <= max(2, len(Qb) // 6), skipped
     if tau == math.inf:
         assert all(t == P for t in exits)
 
