@@ -226,6 +226,14 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
       a.out_scores = out_scores + q0 * k;
       a.out_expanded = out_expanded ? out_expanded + q0 : nullptr;
       a.nq = (int32_t)nq;   // row stride of out_expanded
+      // bits: 1 row prefetch (0.85x), 2 list prefetch (1.00x), 4 rows evict-first, 8 ids
+      // evict-last (4+8: 1.00-1.03x; meant to keep the 84 MB of row ids in L2 across the row
+      // stream)
+      a.prefetch = 12;
+      if (const char* e = tuning_env("SA_GRAPH_PF")) a.prefetch = atoi(e);
+      if (R % 4 != 0) a.prefetch &= ~2;   // bulk prefetch needs 16-byte aligned list rows
+      if (const char* e = tuning_env("SA_GRAPH_DBG"))   // device pointer, [nq, 8] u64
+        a.dbg = reinterpret_cast<unsigned long long*>(strtoull(e, nullptr, 0)) + q0 * 8;
       GraphMatureArgs m{};
       if (mo) {
         m.tau = mo->tau;

@@ -251,6 +251,40 @@ __device__ __forceinline__ int32_t read_ready(const int32_t* p) {
   return v;
 }
 
+// one bulk L2 prefetch of [p, p + bytes) (16-byte aligned, bytes a multiple of 16)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// L2 eviction-priority policies (createpolicy) and loads that carry them
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ldg_policy(const uint4* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int32_t ldg_policy(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ bool visit(uint32_t* hash, int32_t pos) {
   const uint32_t v = (uint32_t)pos + 1u;
   uint32_t h = ((uint32_t)pos * 2654435761u) >> (32 - GR_HASH_LOG);
@@ -297,6 +331,10 @@ __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, in
   constexpr int kSWarps = kSThreads / 32;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint4* X4 = reinterpret_cast<const uint4*>(a.X);
+  // rows are read once per query (evict first); row ids are 4 bytes per 1.5 KB row, 84 MB at
+  // C3, and fit the L2 when the row stream does not evict them (evict last)
+  const uint64_t pol_stream = (a.prefetch & 4) ? policy_evict_first() : policy_evict_normal();
+  const uint64_t pol_keep = (a.prefetch & 8) ? policy_evict_last() : policy_evict_normal();
   for (int j0 = warp * kRowsPerWarp; j0 < cnt; j0 += kSWarps * kRowsPerWarp) {
     uint4 v[kRowsPerWarp][3];
     int32_t p[kRowsPerWarp];
@@ -305,12 +343,14 @@ __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, in
     for (int u = 0; u < kRowsPerWarp; ++u) {
       p[u] = j0 + u < cnt ? sm.npos[j0 + u] : -1;
       // the row's global id, loaded with its data (not after the dot product)
-      gid[u] = (lane == 0 && p[u] >= 0) ? (uint32_t)__ldg(a.row_ids + p[u]) : 0u;
+      gid[u] = (lane == 0 && p[u] >= 0)
+                   ? (uint32_t)ldg_policy(a.row_ids + p[u], pol_keep) : 0u;
 #pragma unroll
       for (int rd = 0; rd < 3; ++rd) {
         const int c = rd * 32 + lane;
-        v[u][rd] = (p[u] >= 0 && c < nchunk) ? __ldg(X4 + (int64_t)p[u] * nchunk + c)
-                                             : make_uint4(0, 0, 0, 0);
+        v[u][rd] = (p[u] >= 0 && c < nchunk)
+                       ? ldg_policy(X4 + (int64_t)p[u] * nchunk + c, pol_stream)
+                       : make_uint4(0, 0, 0, 0);
       }
     }
     // the query chunk is loaded from smem once per rd and reused by every row in flight
@@ -339,6 +379,7 @@ __device__ void score_rows(const GraphSearchArgs& a, SearchSmem& sm, int cnt, in
           const int t = atomicAdd(&sm.n_ins, 1);
           sm.nkey[t] = key;
           sm.ipos[t] = p[u];
+          if (a.prefetch & 2) prefetch_l2(a.nbr + (int64_t)p[u] * a.R, (uint32_t)a.R * 4u);
         }
       }
     }
@@ -432,6 +473,7 @@ __device__ void score_rows_f8(const GraphSearchArgs& a, SearchSmem& sm, int cnt,
           const int t = atomicAdd(&sm.n_ins, 1);
           sm.nkey[t] = key;
           sm.ipos[t] = p[u];
+          if (a.prefetch & 2) prefetch_l2(a.nbr + (int64_t)p[u] * a.R, (uint32_t)a.R * 4u);
         }
       }
     }
@@ -458,6 +500,25 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
   const int q = blockIdx.x;
   const int lane = threadIdx.x % 32;
   const int nchunk = a.d_pad / 8;
+#ifdef SA_TUNING_BUILD
+  const bool dbg = a.dbg != nullptr && threadIdx.x == 0;
+#else
+  constexpr bool dbg = false;   // the product library never times phases
+#endif
+  unsigned long long dcy[4] = {0, 0, 0, 0};
+  long long dt = 0;
+  auto dmark = [&](int ph) {
+    if (dbg) {
+      const long long c = clock64();
+      dcy[ph] += (unsigned long long)(c - dt);
+      dt = c;
+    }
+  };
+  if (dbg) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    a.dbg[(int64_t)q * 8] = g;
+  }
   for (int i = threadIdx.x; i < GR_HASH; i += kSThreads) sm.hash[i] = 0u;
   if constexpr (kF8) {
     for (int i = threadIdx.x; i < a.d8_pad; i += kSThreads)
@@ -495,8 +556,11 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
   int visited = n_new;   // entries in the visited table
   double ema = 0.0;  // thread 0 (maturity exit)
   int steps = 0;     // iterations run (maturity exit)
+  int iters = 0;
+  if (dbg) dt = clock64();
   for (int it = 0;; ++it) {
     if (kMature) steps = it;
+    iters = it;
     // ---- merge the surviving new rows into the sorted list (top-L); keys are distinct, so an
     // entry's new position = its rank in the old list + the number of new keys above it (v.v.)
     const int n_ins = sm.n_ins;
@@ -526,6 +590,7 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
       cur = nxt;
       __syncthreads();
     }
+    dmark(0);
     // ---- maturity signal of step it (R28-R29): s_t = best key scored in the step, RQ_t over
     // the list's first / last entries after the merge, EMA in fp64 with the oracle's roundings
     bool stop = false;
@@ -573,6 +638,7 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
       }
     }
     __syncthreads();
+    dmark(1);
     const int nc = sm.n_chosen;
     if (nc == 0) break;
     expanded += nc;
@@ -591,9 +657,16 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
     // ---- neighbours not yet visited
     for (int t = threadIdx.x; t < nc * a.R; t += kSThreads) {
       const int32_t c = a.nbr[(int64_t)sm.chosen[t / a.R] * a.R + (t % a.R)];
-      if (c >= 0 && visit(sm.hash, c)) sm.npos[atomicAdd(&sm.n_new, 1)] = c;
+      if (c >= 0 && visit(sm.hash, c)) {
+        sm.npos[atomicAdd(&sm.n_new, 1)] = c;
+        if (a.prefetch & 1) {
+          if constexpr (kF8) prefetch_l2(a.X8 + (int64_t)c * a.d8_pad, (uint32_t)a.d8_pad);
+          else prefetch_l2(a.X + (int64_t)c * a.d_pad, (uint32_t)a.d_pad * 2u);
+        }
+      }
     }
     __syncthreads();
+    dmark(2);
     n_new = sm.n_new;
     scored += n_new;
     visited += n_new;
@@ -604,6 +677,14 @@ __global__ void __launch_bounds__(kSThreads, 1024 / kSThreads)
       score_rows<kSThreads, kRowsPerWarp, kMature>(a, sm, n_new, nchunk,
                                                    cnt == a.L ? sm.key[cur][a.L - 1] : 0ull);
     __syncthreads();
+    dmark(3);
+  }
+  if (dbg) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    a.dbg[(int64_t)q * 8 + 1] = g;
+    for (int i = 0; i < 4; ++i) a.dbg[(int64_t)q * 8 + 2 + i] = dcy[i];
+    a.dbg[(int64_t)q * 8 + 6] = (unsigned long long)iters;
   }
   if constexpr (kF8) {
     // the whole list, re-keyed with stored positions, for the bf16 re-rank

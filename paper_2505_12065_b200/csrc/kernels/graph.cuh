@@ -54,6 +54,14 @@ struct GraphSearchArgs {
   const uint8_t* Q8;
   int32_t d8_pad;
   uint64_t* out_keys;
+  // L2 prefetch (bit 0: a row's bytes when it is first discovered, so the warps' register
+  // gathers hit L2; bit 1: the neighbour list of a row scored above the list's floor, read
+  // when it is expanded)
+  int32_t prefetch;
+  // tuning builds only (SA_GRAPH_DBG): per query [8] u64 -- globaltimer at start / end, clock64
+  // cycles thread 0 spent in merge, pick, expand, score (each up to its closing barrier),
+  // iterations, 0
+  unsigned long long* dbg;
 };
 // non-stall maturity exit on the beam search (§3.3; readings R28-R29): a step is one
 // iteration; RQ_t / EMA_t in fp64; after every g-th step the query stops if EMA_t >= tau and

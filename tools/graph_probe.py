@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--entries", default="8")
     ap.add_argument("--latency", action="store_true", help="also time agent-step batches")
     ap.add_argument("--fp8", default="0", help="comma list of 0/1: bf16 and/or fp8 navigation")
+    ap.add_argument("--pf", default="", help="comma list of SA_GRAPH_PF values (tuning library)")
     args = ap.parse_args()
     cfg = dict(CONFIGS["c3"])
     n, d = args.n, cfg["d"]
@@ -61,18 +62,23 @@ def main():
            "nprobe_build": args.nprobe_build, "ivf_build_s": ivf_s, "graph_build_s": graph_s,
            "nq": args.nq, "rows": []}
     stream = torch.cuda.current_stream()
-    for f8, E, w, L in [(f8, E, w, L) for f8 in fp8s
+    for pf, f8, E, w, L in [(pf, f8, E, w, L) for pf in (args.pf.split(",") if args.pf else [None])
+                        for f8 in fp8s
                         for E in [int(x) for x in args.entries.split(",")]
                         for w in [int(x) for x in args.widths.split(",")]
                         for L in [int(x) for x in args.ranges.split(",")]]:
+        if pf is not None:
+            os.environ["SA_GRAPH_PF"] = pf
         if True:
-            rec, exp = [], []
+            rec, exp, scd = [], [], []
             for q, t in zip(qs, gt):
                 gi, _, ex, sc_rows = idx.search_graph(q, 10, L, search_width=w, n_entries=E,
                                                       expanded=True, fp8=bool(f8))
                 gi = gi.cpu().numpy()
                 rec.append(np.mean([len(set(gi[i]) & set(t[i])) / 10 for i in range(len(t))]))
                 exp.append(ex.float().mean().item())
+                scd.append(sc_rows.float().cpu().numpy())
+            scd = np.concatenate(scd)
             torch.cuda.synchronize()
             reps = []
             for rep in range(5):
@@ -90,8 +96,12 @@ def main():
             torch.cuda.synchronize()
             kern = {kd: round(sa.profile_read(kd)[0] / 8, 4) for kd in sa.KERNEL_KINDS}
             sa.profile_enable(False)
-            out["rows"].append({"fp8": f8, "L": L, "w": w, "E": E, "recall": float(np.mean(rec)),
+            out["rows"].append({"pf": pf, "fp8": f8, "L": L, "w": w, "E": E, "recall": float(np.mean(rec)),
                                 "expanded": float(np.mean(exp)), "ms_per_batch": ms,
+                                "scored_mean": float(scd.mean()),
+                                "scored_p90_p99_max": [float(np.percentile(scd, 90)),
+                                                       float(np.percentile(scd, 99)),
+                                                       float(scd.max())],
                                 "qps": args.nq / (ms / 1e3), "kernel_ms": kern})
             print(json.dumps(out["rows"][-1]), file=sys.stderr, flush=True)
     if args.latency:

@@ -2,7 +2,7 @@
 # compute-sanitizer over tools/sanitize_cases.py; logs in gpurun_out/sanitize_<tool>.txt
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-CASES="${CASES:-flat1 flat2 flatk merge ivf ivfsmall mature graph graph_mature fp8}"
+CASES="${CASES:-flat1 flat2 flatk merge ivf ivfsmall mature graph graph_mature fp8 host}"
 for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
   echo "== $tool" > gpurun_out/sanitize_$tool.txt
   for c in $CASES; do

@@ -4,7 +4,8 @@ synccheck / initcheck).  Usage:
   compute-sanitizer --tool racecheck python tools/sanitize_cases.py [case ...]
 
 Cases: flat1 (cta_group 1, C1 shape), flat2 (cta_group 2, nq 300), flatk (k = 100, global
-heaps), ivf, ivfsmall (agent-step batch), mature, graph, graph_mature, fp8, merge.
+heaps), ivf, ivfsmall (agent-step batch), mature, graph, graph_mature, fp8, merge, host
+(agent-step host-buffer calls: one-launch IVF search, persistent scratch, pinned results).
 Every case checks its result against the exact mode so a sanitizer-perturbed run that
 returns garbage fails loudly too.
 """
@@ -41,7 +42,7 @@ def main(cases):
             out[c] = recall(flat.search(Q, 10)[0], gt10)
         elif c == "flatk":
             out[c] = recall(flat.search(Q[:64].contiguous(), 100)[0][:, :10], gt10[:64])
-        elif c in ("ivf", "ivfsmall", "mature", "graph", "graph_mature", "fp8"):
+        elif c in ("ivf", "ivfsmall", "mature", "graph", "graph_mature", "fp8", "host"):
             if ivf is None:
                 ivf = sa.Index.build(X, 64, kmeans_iters=3)
             if c == "ivf":
@@ -60,6 +61,11 @@ def main(cases):
                 ids = ivf.search_graph_mature(Q[:16].contiguous(), 10, 128, tau=1e9, window=4,
                                               search_width=2, n_entries=8)[0]
                 out[c] = recall(ids, gt10[:16])
+            elif c == "host":
+                qh = Q[:8].float().cpu().contiguous()
+                got = torch.cat([ivf.search_host(qh[i:i + 1].contiguous(), 10, 64)[0]
+                                 for i in range(8)] + [ivf.search_host(qh, 10, 64)[0]])
+                out[c] = recall(got, torch.cat([gt10[:8].cpu(), gt10[:8].cpu()]))
             elif c == "fp8":
                 ivf.build_fp8()
                 out[c] = recall(ivf.search_fp8(Q[:128].contiguous(), 10, 64)[0], gt10[:128])
@@ -82,4 +88,4 @@ def main(cases):
 
 if __name__ == "__main__":
     main(sys.argv[1:] or ["flat1", "flat2", "flatk", "merge", "ivf", "ivfsmall", "mature",
-                          "graph", "graph_mature", "fp8"])
+                          "graph", "graph_mature", "fp8", "host"])
