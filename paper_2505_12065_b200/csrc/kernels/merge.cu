@@ -349,6 +349,171 @@ select_dense_kernel(const MergeArgs a) {
   for (int i = tid; i < k; i += kThreads) write_out(a, q, i, sel[i]);
 }
 
+// Top-k (k <= 64) of a dense score row without caching the row in shared memory, so 6-8 CTAs
+// fit an SM and a 512-query probe runs in one wave (select_dense_kernel's 64 KB row cache
+// allows 2 per SM).  Two streaming passes over the row (L2-resident right after the score
+// dump): (1) each thread keeps its two largest values; each warp sorts its 64 and T_w = their
+// k-th largest is a lower bound of the row's k-th largest value (k distinct elements are
+// >= T_w), T0 = max_w T_w;
+// (2) the values >= T0 (usually ~100) are appended to smem as (value, index) keys and each
+// key's rank among them (keys are distinct) is its output position.  More than kStreamCap
+// survivors (heavy ties): the exact radix select of select_dense_kernel, reading the row from
+// global memory.  Same keys and ties as select_dense_kernel (value desc, index asc).
+constexpr int kStreamCap = 1024;
+constexpr int kStreamMaxK = 64;
+
+__global__ void __launch_bounds__(kThreads)
+select_dense_stream_kernel(const MergeArgs a) {
+  __shared__ uint64_t cand[kStreamCap];
+  __shared__ uint32_t wT[kThreads / 32];
+  __shared__ uint32_t hist[256];
+  __shared__ uint64_t sel[kStreamMaxK];
+  __shared__ int s_pos, s_bucket, s_above;
+  __shared__ int wsum[kThreads / 32];
+  const int64_t q = blockIdx.x;
+  const int k = a.k;
+  const int M = (int)a.m_flat;
+  const float* row = a.cand_scores + (size_t)q * a.qstride;
+  const float4* r4 = reinterpret_cast<const float4*>(row);
+  const int M4 = M >> 2;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_pos = 0;
+  // pass 1: per-thread two largest values, 4 float4 loads in flight
+  uint32_t m1 = 0u, m2 = 0u;
+  for (int i0 = tid; i0 < M4; i0 += 4 * kThreads) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = i0 + u * kThreads < M4 ? __ldcg(r4 + i0 + u * kThreads)
+                                    : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t o = ordered_from_float(f[c]);
+        m2 = max(m2, min(m1, o));
+        m1 = max(m1, o);
+      }
+    }
+  }
+  // bitonic sort of the warp's 64 values {m1, m2} (element e = j * 32 + lane of register j),
+  // descending; element k-1 is the k-th largest
+  uint32_t x[2] = {m1, m2};
+#pragma unroll
+  for (int sz = 2; sz <= 64; sz <<= 1)
+#pragma unroll
+    for (int st = sz >> 1; st > 0; st >>= 1) {
+      if (st == 32) {   // sz == 64: partners are the lane's two registers, all descending
+        const uint32_t hi = max(x[0], x[1]), lo = min(x[0], x[1]);
+        x[0] = hi;
+        x[1] = lo;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int e = j * 32 + lane;
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, x[j], st);
+          const bool desc = (e & sz) == 0 || sz == 64;
+          const bool lower = (e & st) == 0;
+          x[j] = (lower == desc) ? max(x[j], y) : min(x[j], y);
+        }
+      }
+    }
+  const uint32_t tw = __shfl_sync(0xffffffffu, (k - 1) < 32 ? x[0] : x[1], (k - 1) & 31);
+  if (lane == 0) wT[wid] = tw;
+  __syncthreads();
+  uint32_t T0 = 0u;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) T0 = max(T0, wT[w]);
+  // pass 2: the values >= T0 as keys
+  for (int i0 = tid; i0 < M4; i0 += 4 * kThreads) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = i0 + u * kThreads < M4 ? __ldcg(r4 + i0 + u * kThreads)
+                                    : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t o = ordered_from_float(f[c]);
+        if (o >= T0 && i0 + u * kThreads < M4) {
+          const int p = atomicAdd(&s_pos, 1);
+          const uint32_t idx = (uint32_t)(4 * (i0 + u * kThreads) + c);
+          if (p < kStreamCap) cand[p] = ((uint64_t)o << 32) | (0xFFFFFFFFu - idx);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int nc = s_pos;
+  if (nc <= kStreamCap) {
+    // rank of each key among the survivors = its output position
+    for (int i = tid; i < nc; i += kThreads) {
+      const uint64_t key = cand[i];
+      int r = 0;
+      for (int j = 0; j < nc; ++j) r += cand[j] > key;
+      if (r < k) write_out(a, q, r, key);
+    }
+    for (int i = nc + tid; i < k; i += kThreads) write_out(a, q, i, 0ull);
+    return;
+  }
+  // heavy ties: exact radix select over the row (global reads), as select_dense_kernel
+  auto val = [&](int i) { return ordered_from_float(__ldcg(row + i)); };
+  uint32_t prefix = 0, pmask = 0;
+  int kr = k;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int i = tid; i < 256; i += kThreads) hist[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < M; i += kThreads) {
+      const uint32_t v = val(i);
+      if ((v & pmask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) pick_bucket(hist, kr, &s_bucket, &s_above);
+    __syncthreads();
+    prefix |= (uint32_t)s_bucket << shift;
+    pmask |= 255u << shift;
+    kr -= s_above;
+  }
+  const uint32_t T = prefix;            // k-th largest value; k - kr values are larger
+  const int size = pow2_at_least(k);
+  if (tid == 0) s_pos = 0;
+  for (int i = tid; i < size; i += kThreads) sel[i] = 0ull;
+  __syncthreads();
+  for (int i = tid; i < M; i += kThreads) {
+    const uint32_t v = val(i);
+    if (v > T) sel[atomicAdd(&s_pos, 1)] = ((uint64_t)v << 32) | (0xFFFFFFFFu - (uint32_t)i);
+  }
+  // values == T: the kr smallest indices -- contiguous chunks, block prefix count
+  const int chunk = (M + kThreads - 1) / kThreads;
+  const int lo = tid * chunk, hi = min(M, lo + chunk);
+  int my = 0;
+  for (int i = lo; i < hi; ++i) my += val(i) == T;
+  int incl = my;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  int wbase = 0;
+  for (int w = 0; w < wid; ++w) wbase += wsum[w];
+  int r = wbase + incl - my;
+  const int first = k - kr;
+  for (int i = lo; i < hi && r < kr; ++i)
+    if (val(i) == T) {
+      sel[first + r] = ((uint64_t)T << 32) | (0xFFFFFFFFu - (uint32_t)i);
+      ++r;
+    }
+  __syncthreads();
+  sort_desc(sel, size);
+  for (int i = tid; i < k; i += kThreads) write_out(a, q, i, sel[i]);
+}
+
 // k = 1 with few grouped candidates (k-means / full assignment: millions of queries):
 // one thread per query, max over its candidate keys.
 __global__ void merge_top1_kernel(const MergeArgs a, int64_t nq) {
@@ -365,6 +530,12 @@ __global__ void merge_top1_kernel(const MergeArgs a, int64_t nq) {
 
 cudaError_t launch_merge(const MergeArgs& a, int64_t nq, cudaStream_t stream) {
   if (nq <= 0) return cudaSuccess;
+  if (a.cand_scores && a.k <= kStreamMaxK && (a.m_flat & 3) == 0 && (a.qstride & 3) == 0 &&
+      (reinterpret_cast<uintptr_t>(a.cand_scores) & 15) == 0 && a.m_flat >= kThreads) {
+    select_dense_stream_kernel<<<(unsigned)nq, kThreads, 0, stream>>>(a);
+    note_launch();
+    return cudaGetLastError();
+  }
   if (a.cand_scores) {
     const size_t smem = (size_t)a.m_flat * sizeof(uint32_t);
     cudaError_t e = ensure_max_smem(reinterpret_cast<const void*>(select_dense_kernel), smem);
