@@ -367,6 +367,9 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
         }
         if (qkey >= 0 && done >= next_at) {
           next_at = done + (done > 1 ? done : 1);
+#ifdef SA_TUNING_BUILD
+          if (a.counters && lane == 0) atomicAdd(a.counters + 2, 1ull);
+#endif
           for (int i = lane; i < FS_BM; i += 32) {
             const int64_t q = ((int64_t)qkey * CG + rank) * kBM + i;
             if (q >= a.nq) break;
@@ -434,6 +437,12 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
     if constexpr (!DUMP)
       for (int i = 0; i < k; ++i) heap[(size_t)i * kEpiT] = 0ull;
     float thr = heap_threshold(0ull);
+#ifdef SA_TUNING_BUILD
+    uint32_t c_pass = 0, c_ins = 0;
+#define SA_FS_COUNT(x) ++x
+#else
+#define SA_FS_COUNT(x) (void)0
+#endif
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t a_tma_phase = 0;
@@ -563,6 +572,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
 #pragma unroll
             for (int j = 0; j < 32; ++j) tb[lane * 32 + (j ^ lane)] = __uint_as_float(r0[j]);
             __syncwarp();
+#pragma unroll 4
             for (int rr = 0; rr < 32; ++rr)
               if (qbase + rr < a.nq && row0 + lane < a.n_rows)
                 a.dbg[(qbase + rr) * a.n_rows + row0 + lane] = tb[rr * 32 + (lane ^ rr)];
@@ -570,6 +580,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
 #pragma unroll
             for (int j = 0; j < 32; ++j) tb[lane * 32 + (j ^ lane)] = __uint_as_float(r1[j]);
             __syncwarp();
+#pragma unroll 4
             for (int rr = 0; rr < 32; ++rr)
               if (qbase + rr < a.nq && row0 + 32 + lane < a.n_rows)
                 a.dbg[(qbase + rr) * a.n_rows + row0 + 32 + lane] = tb[rr * 32 + (lane ^ rr)];
@@ -598,6 +609,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
           continue;
         }
         if (mt >= thr) {
+          SA_FS_COUNT(c_pass);
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             if (gm[g] < thr) continue;
@@ -611,6 +623,7 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
                   const uint32_t id =
                       a.id_base + (a.row_ids ? (uint32_t)a.row_ids[row] : (uint32_t)row);
                   const uint64_t key = make_key(s, id);
+                  SA_FS_COUNT(c_ins);
                   thr = fmaxf(heap_offer(heap, k, key), hint);
                   const uint32_t o = (uint32_t)(key >> 32);
                   if (my_max && o > best_o) {
@@ -644,6 +657,12 @@ flat_scan_topk_kernel(const __grid_constant__ CUtensorMap tmap_x,
       }
     }
     if (ew == 0 && lane == 0) atomicExch(&tail->bw_qkey, -2);
+#ifdef SA_TUNING_BUILD
+    if (a.counters) {
+      atomicAdd(a.counters + 0, (unsigned long long)c_pass);
+      atomicAdd(a.counters + 1, (unsigned long long)c_ins);
+    }
+#endif
   }
 
   ptx::tc_fence_before();

@@ -61,6 +61,8 @@ struct FlatScanArgs {
                            // processing, 2 = also skip the TMEM loads, 3 = the 64-way max
                            // only (no insertion).  0 in production.
   int32_t lockstep_lag;    // tiles a unit may run ahead of the units sharing its slice (0 = 4)
+  unsigned long long* counters;  // tuning builds only (SA_FS_COUNT): [0] passing (thread, tile)
+                           // pairs, [1] heap insertions, [2] bound-warp rounds
   int32_t fp8;             // 1: Q and the corpus are e4m3 bytes (kind::f8f6f4 MMAs), passed
                            // as 16-bit pairs -- d_pad counts PAIRS of e4m3 values (bytes / 2),
                            // so TMA boxes, swizzle, descriptors and TMEM columns are the bf16

@@ -361,6 +361,7 @@ select_dense_kernel(const MergeArgs a) {
 // global memory.  Same keys and ties as select_dense_kernel (value desc, index asc).
 constexpr int kStreamCap = 1024;
 constexpr int kStreamMaxK = 64;
+constexpr int kStreamLoads = 8;   // float4 loads in flight per thread and pass
 
 __global__ void __launch_bounds__(kThreads)
 select_dense_stream_kernel(const MergeArgs a) {
@@ -378,16 +379,16 @@ select_dense_stream_kernel(const MergeArgs a) {
   const int M4 = M >> 2;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) s_pos = 0;
-  // pass 1: per-thread two largest values, 4 float4 loads in flight
+  // pass 1: per-thread two largest values, kStreamLoads float4 loads in flight
   uint32_t m1 = 0u, m2 = 0u;
-  for (int i0 = tid; i0 < M4; i0 += 4 * kThreads) {
-    float4 v[4];
+  for (int i0 = tid; i0 < M4; i0 += kStreamLoads * kThreads) {
+    float4 v[kStreamLoads];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < kStreamLoads; ++u)
       v[u] = i0 + u * kThreads < M4 ? __ldcg(r4 + i0 + u * kThreads)
                                     : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kStreamLoads; ++u) {
       const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -426,14 +427,14 @@ select_dense_stream_kernel(const MergeArgs a) {
 #pragma unroll
   for (int w = 0; w < kThreads / 32; ++w) T0 = max(T0, wT[w]);
   // pass 2: the values >= T0 as keys
-  for (int i0 = tid; i0 < M4; i0 += 4 * kThreads) {
-    float4 v[4];
+  for (int i0 = tid; i0 < M4; i0 += kStreamLoads * kThreads) {
+    float4 v[kStreamLoads];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < kStreamLoads; ++u)
       v[u] = i0 + u * kThreads < M4 ? __ldcg(r4 + i0 + u * kThreads)
                                     : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kStreamLoads; ++u) {
       const float f[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {

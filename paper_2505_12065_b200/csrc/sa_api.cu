@@ -14,6 +14,7 @@
 #include "internal.h"
 #include "kernels/flat_scan.cuh"
 #include "kernels/merge.cuh"
+#include "kernels/score_gemm.cuh"
 
 // ====================================================================== errors
 static thread_local std::string g_last_error;
@@ -230,7 +231,11 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   if (p.S > 1) {
     SA_TRY(f.alloc(&hint, (size_t)nq, "alloc hints"));
     SA_CUDA(cudaMemsetAsync(hint, 0, nq * sizeof(uint32_t), s), "memset");
-    if (k <= 16 && p.S * FS_LISTS_PER_ITEM >= k) {
+    static const bool no_bound = [] {   // SA_NO_BOUND=1: tuning experiments only
+      const char* e = tuning_env("SA_NO_BOUND");
+      return e && e[0] == '1';
+    }();
+    if (k <= 16 && p.S * FS_LISTS_PER_ITEM >= k && !no_bound) {
       SA_TRY(f.alloc(&qmax, (size_t)nq * H, "alloc heap maxima"));
       SA_CUDA(cudaMemsetAsync(qmax, 0, (size_t)nq * H * sizeof(uint32_t), s), "memset");
     }
@@ -281,6 +286,8 @@ sa_status flat_search_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
     SA_CUDA(cudaMemsetAsync(progress, 0, units * sizeof(int32_t), s), "memset");
   }
   FlatScanArgs a{};
+  if (const char* e = tuning_env("SA_FS_COUNT"))   // device pointer, [4] u64 (tuning only)
+    a.counters = reinterpret_cast<unsigned long long*>(strtoull(e, nullptr, 0));
   a.progress = progress;
   a.q_hint = hint;
   a.q_max = qmax;
@@ -351,6 +358,17 @@ sa_status flat_scores_view(const CorpusView& cv, int num_sms, const __nv_bfloat1
   CUtensorMap tmap_q;
   sa_status st = make_tmap_bf16(&tmap_q, Qs, nq, cv.d_pad, FS_BM);
   if (st != SA_OK) return st;
+  if (!cv.fp8 && score_gemm_applies(cv.d_pad)) {
+    // a plain streaming GEMM (both operands through one TMA ring): the flat scan's per-unit
+    // query staging does not pay off over the few tiles a probe gives each unit
+    ScoreGemmArgs g{};
+    g.nq = nq;
+    g.n_rows = cv.n_rows;
+    g.d_pad = cv.d_pad;
+    g.out = out;
+    g.ldo = cv.n_rows;
+    return cuda_status(launch_score_gemm(tmap_q, *cv.tmap1, g, num_sms, s), "score gemm");
+  }
   const CUtensorMap& tm = p.cg == 2 ? *cv.tmap2 : *cv.tmap1;
   cudaError_t e = launch_flat_scan(tm, tmap_q, a, p.cg, p.grid, s);
   return cuda_status(e, "score scan");

@@ -50,8 +50,12 @@ def main():
     Q = torch.empty(args.nq, d, dtype=torch.bfloat16, device="cuda")
     draw_rows_into(mix, Q, QUERY_SEED, 0)
     out = {"nq": args.nq, "E": args.E, "nlist": C.shape[0]}
+    torch.cuda.nvtx.range_push("probe")
     out["probe_dump_select_ms"] = timeit(lambda: idx.probes(Q, args.E))
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.nvtx.range_push("flat")
     out["flat_topk_ms"] = timeit(lambda: cflat.search(Q, args.E))
+    torch.cuda.nvtx.range_pop()
     sa.profile_enable(True)
     for _ in range(10):
         idx.probes(Q, args.E)

@@ -50,6 +50,14 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     prof = {k: sa.profile_read(k) for k in sa.KERNEL_KINDS}
+    counts = None
+    if sa.TUNING and os.environ.get("COUNT"):
+        cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+        os.environ["SA_FS_COUNT"] = str(cnt.data_ptr())
+        run()
+        torch.cuda.synchronize()
+        del os.environ["SA_FS_COUNT"]
+        counts = cnt.tolist()
     sa.profile_enable(False)
     ms = e0.elapsed_time(e1) / a.reps
     fs_ms, fs_n = prof["flat_scan"]
@@ -60,6 +68,7 @@ def main():
                                                          "SA_SEED_ROWS", "SA_NO_SEED")
                               if v in os.environ},
                       "ms_per_search": ms, "flat_kernel_ms": kms,
+                      "counts_pass_ins_boundrounds": counts,
                       "other_ms": prof["other"][0] / a.reps,
                       "tflops_kernel": flop / (kms / 1e3) / 1e12,
                       "tflops_search": flop / (ms / 1e3) / 1e12}))

@@ -1,0 +1,4 @@
+set -x
+for n in 1000000:256 2626916:512 21015324:512; do
+  COUNT=1 SA_LIBRARY=tuning timeout 300 python tools/flat_probe.py --n ${n%%:*} --nq ${n##*:} --reps 5
+done
