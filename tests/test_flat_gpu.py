@@ -25,7 +25,8 @@ def _search(sa, X, Q, k, qdtype=torch.bfloat16):
 
 
 # ------------------------------------------------------------ tensor-core layout
-@pytest.mark.parametrize("n,d,nq", [(200, 64, 5), (1000, 128, 130), (777, 768, 129), (333, 100, 3)])
+@pytest.mark.parametrize("n,d,nq", [(200, 64, 5), (1000, 128, 130), (777, 768, 129), (333, 100, 3),
+                                    (5003, 256, 515)])   # > 148 tiles: several per CTA
 def test_debug_scores_match_oracle(sa, n, d, nq):
     g = torch.Generator().manual_seed(n + d)
     X = torch.randn(n, d, generator=g)
