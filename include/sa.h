@@ -172,6 +172,16 @@ sa_status sa_comm_init_local(sa_comm_group* g, int32_t rank, int32_t cuda_device
  * All ranks must set the same value.
  */
 sa_status sa_comm_set_checks(sa_comm* c, int32_t on);
+/*
+ * Sharded code path at world 1 (tests and one-GPU validation).  When on, an
+ * index built with this communicator takes the sharded path even if world == 1: the sharded
+ * IVF build assembles its training sample with the communicator's broadcasts, and every search
+ * runs rank-local keys -> all-gather -> k-way merge (and the argument check when enabled) --
+ * with an NCCL communicator of one rank these are real NCCL calls, so a one-GPU job executes
+ * exactly the collective code a multi-GPU job does (the results equal the unsharded search).
+ * Set before building the index; off by default.  c NULL -> SA_ERR_INVALID_ARG.
+ */
+sa_status sa_comm_set_collectives(sa_comm* c, int32_t on);
 /* rank / world of this communicator; nccl_nranks = ncclCommCount for an NCCL communicator
  * (world for the in-process transport).  Any output pointer may be NULL. */
 sa_status sa_comm_info(const sa_comm* c, int32_t* rank, int32_t* world, int32_t* nccl_nranks);

@@ -102,6 +102,7 @@ def lib() -> ctypes.CDLL:
         "sa_comm_group_free": (st, [P]),
         "sa_comm_init_local": (st, [P, i32, i32, ctypes.POINTER(P)]),
         "sa_comm_set_checks": (st, [P, i32]),
+        "sa_comm_set_collectives": (st, [P, i32]),
         "sa_comm_info": (st, [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]),
         "sa_status_string": (ctypes.c_char_p, [ctypes.c_int]),
         "sa_last_error": (ctypes.c_char_p, []),
@@ -217,6 +218,22 @@ class Comm:
         """sa_comm_set_checks: cross-rank argument check before every sharded search."""
         _check(lib().sa_comm_set_checks(self.handle, 1 if on else 0))
         return self
+
+    def set_collectives(self, on: bool = True):
+        """sa_comm_set_collectives: the sharded path (broadcasts, all-gather + merge) even at
+        world 1 -- one NCCL rank executes the real collective calls."""
+        _check(lib().sa_comm_set_collectives(self.handle, 1 if on else 0))
+        return self
+
+    @classmethod
+    def nccl_single(cls, device: int | None = None):
+        """An NCCL communicator of one rank (sa_comm_unique_id + sa_comm_init, world 1)."""
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib().sa_comm_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+        h = ctypes.c_void_p()
+        dev = torch.cuda.current_device() if device is None else device
+        _check(lib().sa_comm_init(ctypes.cast(buf, ctypes.c_void_p), 0, 1, dev, ctypes.byref(h)))
+        return cls(h, 0, 1)
 
     def info(self):
         r, w, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()

@@ -175,7 +175,7 @@ sa_status comm_allgather_bytes(const sa_comm* c, const void* send, void* recv, s
 // `local` itself on the rank that failed).  A no-op when checks are off.
 sa_status comm_check_args(const sa_comm* c, const int64_t (&args)[kCommArgs], sa_status local,
                           cudaStream_t s) {
-  if (!c || c->world <= 1 || !c->check_args) return local;
+  if (!comm_sharded(c) || !c->check_args) return local;
   int64_t hdr[kCommArgs + 1];
   std::memcpy(hdr, args, sizeof(args));
   hdr[kCommArgs] = (int64_t)local;
@@ -286,6 +286,12 @@ sa_status sa_comm_init_local(sa_comm_group* g, int32_t rank, int32_t device, sa_
 sa_status sa_comm_set_checks(sa_comm* c, int32_t on) {
   if (!c) return set_error(SA_ERR_INVALID_ARG, "null pointer");
   c->check_args = on != 0;
+  return SA_OK;
+}
+
+sa_status sa_comm_set_collectives(sa_comm* c, int32_t on) {
+  if (!c) return set_error(SA_ERR_INVALID_ARG, "null pointer");
+  c->collectives_at_one = on != 0;
   return SA_OK;
 }
 

@@ -93,7 +93,7 @@ sa_status sa_index_build_fp8(sa_index* idx, void* stream) {
   if (st == SA_OK) st = cuda_status(cudaMemsetAsync(amax, 0, 64 * sizeof(uint32_t), s), "memset");
   if (st == SA_OK)
     st = cuda_status(launch_absmax_bf16(idx->X, n, idx->d_pad, amax, idx->num_sms, s), "absmax");
-  if (st == SA_OK && idx->comm && idx->comm->world > 1) {
+  if (st == SA_OK && comm_sharded(idx->comm)) {
     // R30: one scale for the whole (sharded) corpus -> max over the ranks' maxima
     const int w = idx->comm->world;
     uint32_t* all = nullptr;
@@ -160,7 +160,7 @@ sa_status sa_search_fp8(const sa_index* idx, const void* queries, sa_dtype qdtyp
     st = set_error(nprobe > 0 && idx->nlist == 0 ? SA_ERR_STATE : SA_ERR_INVALID_ARG,
                    "need 0 <= nprobe <= nlist");
   cudaStream_t s = (cudaStream_t)stream;
-  const bool sharded = idx->comm && idx->comm->world > 1;
+  const bool sharded = comm_sharded(idx->comm);
   if (sharded) {
     const int64_t args[kCommArgs] = {0x5a58, nq, k, nprobe, (int64_t)qdtype, n_cand};
     st = comm_check_args(idx->comm, args, st, s);

@@ -45,7 +45,7 @@ sa_status sa_index_build_graph(sa_index* idx, int32_t knn_k, int32_t degree, int
                                int32_t flags, void* stream) {
   if (!idx) return set_error(SA_ERR_INVALID_ARG, "null index");
   if (idx->nlist == 0) return set_error(SA_ERR_STATE, "the graph is built on an IVF index");
-  if (idx->comm && idx->comm->world > 1)
+  if (comm_sharded(idx->comm))
     return set_error(SA_ERR_UNSUPPORTED, "graph index on a sharded index");
   const int64_t n = idx->n_local;
   if (degree < 1 || degree > GR_MAX_R || knn_k < degree || knn_k > GR_MAX_K || knn_k >= n)

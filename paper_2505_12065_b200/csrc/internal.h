@@ -18,7 +18,12 @@ struct sa_comm {
   sa_comm_group* group = nullptr;  // in-process transport (sa_comm_init_local)
   int32_t rank = 0, world = 1, device = 0;
   bool check_args = false;         // sa_comm_set_checks: cross-rank argument check
+  bool collectives_at_one = false; // sa_comm_set_collectives: sharded path even at world 1
 };
+// the sharded code path (collectives + merge) applies to indexes built with this communicator
+inline bool comm_sharded(const sa_comm* c) {
+  return c != nullptr && (c->world > 1 || c->collectives_at_one);
+}
 
 // One captured search (sa_search_host fast path): H2D from a pinned staging buffer, the whole
 // search, D2H into pinned staging -- replayed with a single cudaGraphLaunch.

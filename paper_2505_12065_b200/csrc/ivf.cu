@@ -72,7 +72,7 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   const int64_t n = idx->n_local;
   if (nlist > 65536) return set_error(SA_ERR_UNSUPPORTED, "nlist > 65536");
   const int64_t n_total = idx->n_total;
-  const sa_comm* comm = (idx->comm && idx->comm->world > 1) ? idx->comm : nullptr;
+  const sa_comm* comm = comm_sharded(idx->comm) ? idx->comm : nullptr;
   const int64_t n_train = std::min<int64_t>(n_total, (int64_t)o.train_per_list * nlist);
   StreamFreer f{s};
 

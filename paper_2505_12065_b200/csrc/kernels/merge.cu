@@ -531,7 +531,10 @@ __global__ void merge_top1_kernel(const MergeArgs a, int64_t nq) {
 
 cudaError_t launch_merge(const MergeArgs& a, int64_t nq, cudaStream_t stream) {
   if (nq <= 0) return cudaSuccess;
-  if (a.cand_scores && a.k <= kStreamMaxK && (a.m_flat & 3) == 0 && (a.qstride & 3) == 0 &&
+  // k <= 32: for larger k the per-warp bound (the k-th of 64 lane values) is weaker, more values
+  // survive and the quadratic ranking loses to the cached radix select (measured at k = 48,
+  // M = 16384: 42 vs 27 us)
+  if (a.cand_scores && a.k <= 32 && (a.m_flat & 3) == 0 && (a.qstride & 3) == 0 &&
       (reinterpret_cast<uintptr_t>(a.cand_scores) & 15) == 0 && a.m_flat >= kThreads) {
     select_dense_stream_kernel<<<(unsigned)nq, kThreads, 0, stream>>>(a);
     note_launch();

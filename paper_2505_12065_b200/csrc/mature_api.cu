@@ -334,7 +334,7 @@ extern "C" sa_status sa_search_mature(const sa_index* idx, const void* queries, 
   const int32_t g = std::min(opts->check_every, nprobe_max);
   if (nq * (int64_t)g > kInvertSmallMax)
     return set_error(SA_ERR_UNSUPPORTED, "nq * check_every > 4096 (agent-step batches)");
-  if (idx->comm && idx->comm->world > 1)
+  if (comm_sharded(idx->comm))
     return set_error(SA_ERR_UNSUPPORTED, "maturity exit on a sharded index");
   cudaStream_t s = (cudaStream_t)stream;
   if (nq * g <= IVSM_MAX_STAGE && g <= IVSM_MAX_G && k <= IVSM_MAX_K &&

@@ -461,7 +461,7 @@ sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nl
   if (d_pad > FS_MAX_DPAD) return set_error(SA_ERR_UNSUPPORTED, "d > 768 not supported");
   if (n >= (1ll << 31)) return set_error(SA_ERR_UNSUPPORTED, "n_local >= 2^31");
   if (n_total >= (1ll << 32) - 1) return set_error(SA_ERR_UNSUPPORTED, "n_total >= 2^32");
-  if (opts->comm && opts->comm->world > 1 && nlist > 0 && opts->n_total <= 0)
+  if (comm_sharded(opts->comm) && nlist > 0 && opts->n_total <= 0)
     return set_error(SA_ERR_INVALID_ARG, "sharded IVF build needs n_total");
   int dev = 0, sms = 0;
   sa_status st = check_device(&dev, &sms);
@@ -568,7 +568,7 @@ sa_status sa_search_ex(const sa_index* idx, const void* queries, sa_dtype qdtype
   if (st == SA_OK && qdtype != SA_BF16 && qdtype != SA_F32)
     st = set_error(SA_ERR_INVALID_ARG, "bad qdtype");
   cudaStream_t s = (cudaStream_t)stream;
-  const bool sharded = idx && idx->comm && idx->comm->world > 1;
+  const bool sharded = idx && comm_sharded(idx->comm);
   if (sharded) {
     const int64_t args[kCommArgs] = {0x5a5e, nq, k, nprobe, (int64_t)qdtype, 0};
     st = comm_check_args(idx->comm, args, st, s);
@@ -725,7 +725,7 @@ sa_status sa_search_host(const sa_index* idx, const void* queries_host, sa_dtype
   if (qdtype != SA_BF16 && qdtype != SA_F32) return set_error(SA_ERR_INVALID_ARG, "bad qdtype");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t qbytes = (size_t)nq * idx->d * (qdtype == SA_F32 ? 4 : 2);
-  const bool sharded = idx->comm && idx->comm->world > 1;
+  const bool sharded = comm_sharded(idx->comm);
   if (!sharded && nq <= 1024 && graphs_enabled()) {
     // Small batches (agent-step retrieval) are launch-bound: replay a captured graph.
     sa_index* mi = const_cast<sa_index*>(idx);
