@@ -167,7 +167,8 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
   for (int64_t q0 = 0; st == SA_OK && q0 < nq; q0 += C) {
     const int64_t nc = std::min(C, nq - q0);
     const int64_t nq_pad = padded_nq(nc);
-    __nv_bfloat16* Qs = nullptr;
+    __nv_bfloat16* Qbuf = nullptr;   // staged copy (fp32 input, padding or fp8 navigation)
+    const __nv_bfloat16* Qs = nullptr;
     float* psc = nullptr;
     uint64_t* pkeys = nullptr;
     uint8_t* Q8 = nullptr;
@@ -176,17 +177,22 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
       st = dalloc(&Q8, (size_t)nq_pad * idx->d8_pad, s, "graph search");
       if (st == SA_OK) st = dalloc(&cand, (size_t)nc * L, s, "graph search");
     }
-    if (st == SA_OK) st = dalloc(&Qs, (size_t)nq_pad * idx->d_pad, s, "graph search");
+    // bf16 queries whose rows need no padding are read in place (every reader stays below row
+    // nc: the probe GEMM's tensor map covers nc rows, the search reads rows < nc)
+    const uint8_t* qsrc = static_cast<const uint8_t*>(queries) + q0 * qsize;
+    const bool in_place = !fp8 && qdtype == SA_BF16 && idx->d == idx->d_pad &&
+                          (reinterpret_cast<uintptr_t>(qsrc) & 15) == 0;
+    if (st == SA_OK && !in_place) st = dalloc(&Qbuf, (size_t)nq_pad * idx->d_pad, s, "graph search");
+    Qs = in_place ? reinterpret_cast<const __nv_bfloat16*>(qsrc) : Qbuf;
     if (st == SA_OK) st = dalloc(&psc, (size_t)nc * idx->nlist, s, "graph search");
     if (st == SA_OK) st = dalloc(&pkeys, (size_t)nc * E, s, "graph search");
-    if (st == SA_OK) {
+    if (st == SA_OK && !in_place) {
       ProfRegion prof_region(SA_KERNEL_STAGE, s);
-      st = cuda_status(launch_cast_pad(static_cast<const uint8_t*>(queries) + q0 * qsize,
-                                       qdtype == SA_F32, nc, idx->d, Qs, nq_pad, idx->d_pad,
-                                       idx->num_sms, s),
+      st = cuda_status(launch_cast_pad(qsrc, qdtype == SA_F32, nc, idx->d, Qbuf, nq_pad,
+                                       idx->d_pad, idx->num_sms, s),
                        "stage queries");
       if (st == SA_OK && fp8)
-        st = cuda_status(launch_quant_e4m3(Qs, nq_pad, idx->d_pad, nullptr, Q8, idx->d8_pad,
+        st = cuda_status(launch_quant_e4m3(Qbuf, nq_pad, idx->d_pad, nullptr, Q8, idx->d8_pad,
                                            nullptr, idx->num_sms, s),
                          "stage fp8 queries");
     }
@@ -270,7 +276,7 @@ sa_status graph_search(const sa_index* idx, const void* queries, sa_dtype qdtype
       ProfRegion prof_region(SA_KERNEL_MERGE, s);
       st = cuda_status(launch_rerank(r, nc, s), "graph re-rank");
     }
-    if (Qs) cudaFreeAsync(Qs, s);
+    if (Qbuf) cudaFreeAsync(Qbuf, s);
     if (psc) cudaFreeAsync(psc, s);
     if (pkeys) cudaFreeAsync(pkeys, s);
     if (Q8) cudaFreeAsync(Q8, s);
