@@ -484,7 +484,7 @@ def main():
     # ---- pick nprobe: smallest on the ladder with recall@k >= target on the first batch
     sweep = []
     nprobe = 0
-    if mode == "auto":
+    if mode == "auto" or (mode == "ivf" and not args.nprobe):   # --mode ivf without --nprobe
         calib = list(range(args.warmup, min(nb, args.warmup + 2)))   # first two timed batches
         for p in NPROBE_LADDER:
             if p > nlist:
