@@ -1083,8 +1083,8 @@ def run_maturity(args, sa, idx, batches, k, nq, d, nlist, n, rank):
 def run_simulated(args, cfg, sa):
     """Per-rank work of a W-GPU sharded run, measured on one GPU (no NCCL): rank 0's shard,
     exact and IVF (nprobe = --nprobe or 48, centroids trained on the full corpus as the sharded
-    build would) on the contiguous row shard (n/W rows), and IVF on the list-sharded layout
-    (rank 0 stores the whole lists l % W == 0).  The all-gather of [nq, k] keys (40 KB/rank)
+    build would) on the contiguous row shard (n/W rows), and IVF on the library's list-sharded
+    layout (sa_build_opts.list_shard_*: rank 0 keeps the whole lists l % W == 0).  The all-gather of [nq, k] keys (40 KB/rank)
     and the final merge are not included."""
     W = args.simulate_world
     n, d, nq, k = cfg["n"], cfg["d"], cfg["nq"], cfg["k"]
@@ -1094,23 +1094,17 @@ def run_simulated(args, cfg, sa):
     draw_rows_into(mix, X, CORPUS_SEED, 0)
     full = sa.Index.build(X, args.nlist)
     C = torch.from_numpy(full.export_centroids()).cuda()
-    full_lists = full.export_lists()
     full.free()
-    # list-sharded layout: rank r stores the rows of the lists l with
-    # l % W == r (whole lists), under the same global centroids -- the rank-0 subset
-    lo_, gid_ = full_lists
-    own = np.concatenate([gid_[lo_[l]:lo_[l + 1]] for l in range(0, args.nlist, W)])
-    own.sort()
-    Xl = X[torch.from_numpy(own).cuda()].contiguous()
+    # list-sharded layout (sa_build_opts.list_shard_*): rank r keeps the whole
+    # lists l % W == r of the full corpus, under the same global centroids -- rank 0's index
+    idx_l = sa.Index.build(X, args.nlist, centroids=C, list_shard=(0, W))
+    n_l = idx_l.info()["n_local"]
     off, ln = sa.shard_range(n, 0, W)
     Xs = X[off:off + ln].contiguous()
     del X
     torch.cuda.empty_cache()
     idx = sa.Index.build(Xs, args.nlist, row_offset=off, n_total=n, centroids=C)
     del Xs
-    idx_l = sa.Index.build(Xl, args.nlist, centroids=C)
-    n_l = Xl.shape[0]
-    del Xl
     nb = args.warmup + args.steps
     Q = torch.empty(nb * nq, d, dtype=torch.bfloat16, device="cuda")
     draw_rows_into(mix, Q, QUERY_SEED, 0)

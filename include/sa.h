@@ -72,6 +72,16 @@ typedef struct {
   void* stream;            /* stream used for the build (default NULL) */
   const float* centroids;  /* optional DEVICE fp32 [nlist, d]: use these IVF centroids instead
                               of training (e.g. a quantiser trained once for all shards) */
+  int32_t list_shard_world; /* 0 (default): row sharding as above.  >= 1: LIST sharding --
+                              `corpus` is the FULL corpus on every rank (row_offset 0, n_total
+                              n or 0), the quantiser is trained identically on every rank from
+                              it (no training collective), and this index keeps the whole IVF
+                              lists l with l % list_shard_world == list_shard_rank (global ids).
+                              A rank's search work then depends only on its lists; a sharded
+                              search (comm of the same world and rank) all-gathers and merges
+                              exactly as for row shards.  Needs nlist >= 1; SA_ERR_UNSUPPORTED
+                              if the rank owns no rows. */
+  int32_t list_shard_rank;
 } sa_build_opts;
 
 /* Fill *o with the defaults listed above. */

@@ -46,6 +46,8 @@ class _BuildOpts(ctypes.Structure):
         ("comm", ctypes.c_void_p),
         ("stream", ctypes.c_void_p),
         ("centroids", ctypes.c_void_p),
+        ("list_shard_world", ctypes.c_int32),
+        ("list_shard_rank", ctypes.c_int32),
     ]
 
 
@@ -304,7 +306,7 @@ class Index:
     def build(cls, corpus: torch.Tensor, nlist: int = 0, *, kmeans_iters: int = 20,
               train_per_list: int = 256, seed: int = 0x5A2505, row_offset: int = 0,
               n_total: int | None = None, comm: Comm | None = None, centroids=None,
-              stream=None) -> "Index":
+              list_shard: tuple[int, int] | None = None, stream=None) -> "Index":
         if not corpus.is_cuda or corpus.dim() != 2 or not corpus.is_contiguous():
             raise ValueError("corpus must be a contiguous 2-D CUDA tensor")
         o = _BuildOpts()
@@ -316,6 +318,8 @@ class Index:
         o.row_offset = row_offset
         o.n_total = n_total if n_total is not None else 0
         o.comm = comm.handle if comm is not None else None
+        if list_shard is not None:        # (rank, world): keep lists l % world == rank
+            o.list_shard_rank, o.list_shard_world = int(list_shard[0]), int(list_shard[1])
         o.stream = _stream_ptr(stream)
         if centroids is not None:
             if not centroids.is_cuda or centroids.dtype != torch.float32 or \

@@ -59,6 +59,7 @@ struct sa_index {
   int32_t d = 0, d_pad = 0;
   int32_t nlist = 0;
   int64_t row_offset = 0, n_total = 0;
+  int32_t list_world = 0, list_rank = 0;   // list sharding (sa_build_opts.list_shard_*)
   __nv_bfloat16* X = nullptr;  // [n_local, d_pad] (list-major when nlist > 0)
   CUtensorMap tmap_x;   // box 128 rows (cta_group 1)
   CUtensorMap tmap_x2;  // box 64 rows (cta_group 2: each CTA of a pair stages half a tile)

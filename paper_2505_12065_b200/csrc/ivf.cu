@@ -19,6 +19,7 @@
 #include "kernels/ivf_kernels.cuh"
 #include "kernels/ivf_scan.cuh"
 #include "kernels/ivf_small.cuh"
+#include "kernels/launch.cuh"
 #include "kernels/merge.cuh"
 
 namespace sa {
@@ -65,6 +66,15 @@ sa_status sort_by_list(const int64_t* ids, int64_t n, int nlist, int num_sms, in
 
 }  // namespace
 
+// list sharding: dst[d0 + i] = src[s0 + i] for every kept list's segment (s0, d0, len)
+static __global__ void copy_segments_kernel(const int32_t* __restrict__ src, const int64_t* __restrict__ seg,
+                                     int nseg, int32_t* __restrict__ dst) {
+  for (int g = blockIdx.x; g < nseg; g += gridDim.x) {
+    const int64_t s0 = seg[3 * g], d0 = seg[3 * g + 1], len = seg[3 * g + 2];
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) dst[d0 + i] = src[s0 + i];
+  }
+}
+
 sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   const int nlist = idx->nlist;
   const int dp = idx->d_pad;
@@ -72,7 +82,8 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   const int64_t n = idx->n_local;
   if (nlist > 65536) return set_error(SA_ERR_UNSUPPORTED, "nlist > 65536");
   const int64_t n_total = idx->n_total;
-  const sa_comm* comm = comm_sharded(idx->comm) ? idx->comm : nullptr;
+  // list sharding trains on the full corpus every rank holds: no training collective
+  const sa_comm* comm = comm_sharded(idx->comm) && idx->list_world == 0 ? idx->comm : nullptr;
   const int64_t n_train = std::min<int64_t>(n_total, (int64_t)o.train_per_list * nlist);
   StreamFreer f{s};
 
@@ -203,13 +214,45 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   }
   SA_CUDA(cudaMalloc(&idx->list_off, (nlist + 1) * sizeof(int64_t)), "alloc list offsets");
   SA_TRY(sort_by_list(ids_all, n, nlist, sms, perm_all, idx->list_off, s));
+  int64_t n_keep = n;
+  if (idx->list_world > 0) {
+    // list sharding: keep the whole lists l % W == R (list-major order, so each is one
+    // contiguous segment of the sorted permutation); the other lists become empty
+    std::vector<int64_t> off(nlist + 1), noff(nlist + 1, 0), seg;
+    SA_CUDA(cudaMemcpyAsync(off.data(), idx->list_off, (nlist + 1) * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, s), "list offsets D2H");
+    SA_CUDA(cudaStreamSynchronize(s), "list offsets");
+    for (int l = 0; l < nlist; ++l) {
+      const int64_t len = l % idx->list_world == idx->list_rank ? off[l + 1] - off[l] : 0;
+      noff[l + 1] = noff[l] + len;
+      if (len > 0) seg.insert(seg.end(), {off[l], noff[l], len});
+    }
+    n_keep = noff[nlist];
+    if (n_keep == 0) return set_error(SA_ERR_UNSUPPORTED, "this list shard owns no rows");
+    int64_t* dseg;
+    int32_t* perm_keep;
+    SA_TRY(dalloc(&dseg, seg.size(), s, "alloc segments"));
+    f.add(dseg);
+    SA_TRY(dalloc(&perm_keep, (size_t)n_keep, s, "alloc kept permutation"));
+    f.add(perm_keep);
+    SA_CUDA(cudaMemcpyAsync(dseg, seg.data(), seg.size() * sizeof(int64_t), cudaMemcpyHostToDevice,
+                            s), "segments H2D");
+    SA_CUDA(cudaMemcpyAsync(idx->list_off, noff.data(), (nlist + 1) * sizeof(int64_t),
+                            cudaMemcpyHostToDevice, s), "list offsets H2D");
+    const int nseg = (int)(seg.size() / 3);
+    copy_segments_kernel<<<std::min(nseg, sms * 8), 256, 0, s>>>(perm_all, dseg, nseg, perm_keep);
+    note_launch();
+    SA_CUDA(cudaGetLastError(), "copy segments");
+    SA_CUDA(cudaStreamSynchronize(s), "list shard");   // seg / noff (host) outlive the copies
+    perm_all = perm_keep;
+  }
   __nv_bfloat16* Xp = nullptr;
-  SA_CUDA(cudaMalloc(&Xp, (size_t)n * dp * sizeof(__nv_bfloat16)), "alloc list-major corpus");
-  cudaError_t e = launch_gather_rows(idx->X, dp, perm_all, 0, 0, 0, 1, n, Xp, sms, s);
+  SA_CUDA(cudaMalloc(&Xp, (size_t)n_keep * dp * sizeof(__nv_bfloat16)), "alloc list-major corpus");
+  cudaError_t e = launch_gather_rows(idx->X, dp, perm_all, 0, 0, 0, 1, n_keep, Xp, sms, s);
   // +4 entries: the agent-step kernel bulk-copies 16-byte-aligned id ranges (ivf_small.cu)
-  if (e == cudaSuccess) e = cudaMalloc(&idx->row_ids, ((size_t)n + 4) * sizeof(int32_t));
-  if (e == cudaSuccess) e = launch_perm_ids(perm_all, n, idx->row_offset, idx->row_ids, sms, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(idx->row_ids + n, 0xff, 4 * sizeof(int32_t), s);
+  if (e == cudaSuccess) e = cudaMalloc(&idx->row_ids, ((size_t)n_keep + 4) * sizeof(int32_t));
+  if (e == cudaSuccess) e = launch_perm_ids(perm_all, n_keep, idx->row_offset, idx->row_ids, sms, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(idx->row_ids + n_keep, 0xff, 4 * sizeof(int32_t), s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
     cudaFree(Xp);
@@ -217,9 +260,10 @@ sa_status ivf_build(sa_index* idx, const sa_build_opts& o, cudaStream_t s) {
   }
   cudaFree(idx->X);
   idx->X = Xp;
-  SA_TRY(make_tmap_bf16(&idx->tmap_x, idx->X, n, dp, FS_BN));
-  SA_TRY(make_tmap_bf16(&idx->tmap_x2, idx->X, n, dp, FS_BN / 2));
-  SA_TRY(make_tmap_bf16(&idx->tmap_xt, idx->X, n, dp, FS_TAIL_ROWS));
+  idx->n_local = n_keep;
+  SA_TRY(make_tmap_bf16(&idx->tmap_x, idx->X, n_keep, dp, FS_BN));
+  SA_TRY(make_tmap_bf16(&idx->tmap_x2, idx->X, n_keep, dp, FS_BN / 2));
+  SA_TRY(make_tmap_bf16(&idx->tmap_xt, idx->X, n_keep, dp, FS_TAIL_ROWS));
   idx->h_list_off.resize(nlist + 1);
   SA_CUDA(cudaMemcpy(idx->h_list_off.data(), idx->list_off, (nlist + 1) * sizeof(int64_t),
                      cudaMemcpyDeviceToHost),

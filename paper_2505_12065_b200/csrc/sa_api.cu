@@ -461,8 +461,19 @@ sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nl
   if (d_pad > FS_MAX_DPAD) return set_error(SA_ERR_UNSUPPORTED, "d > 768 not supported");
   if (n >= (1ll << 31)) return set_error(SA_ERR_UNSUPPORTED, "n_local >= 2^31");
   if (n_total >= (1ll << 32) - 1) return set_error(SA_ERR_UNSUPPORTED, "n_total >= 2^32");
-  if (comm_sharded(opts->comm) && nlist > 0 && opts->n_total <= 0)
+  const bool list_sharded = opts->list_shard_world > 0;
+  if (list_sharded) {
+    if (nlist < 1) return set_error(SA_ERR_INVALID_ARG, "list sharding needs nlist >= 1");
+    if (opts->list_shard_rank < 0 || opts->list_shard_rank >= opts->list_shard_world)
+      return set_error(SA_ERR_INVALID_ARG, "list_shard_rank must be in [0, list_shard_world)");
+    if (opts->row_offset != 0 || n_total != n)
+      return set_error(SA_ERR_INVALID_ARG, "list sharding takes the full corpus (row_offset 0)");
+    if (opts->comm && (opts->comm->world != opts->list_shard_world ||
+                       opts->comm->rank != opts->list_shard_rank))
+      return set_error(SA_ERR_INVALID_ARG, "list shard (rank, world) differs from the comm's");
+  } else if (comm_sharded(opts->comm) && nlist > 0 && opts->n_total <= 0) {
     return set_error(SA_ERR_INVALID_ARG, "sharded IVF build needs n_total");
+  }
   int dev = 0, sms = 0;
   sa_status st = check_device(&dev, &sms);
   if (st != SA_OK) return st;
@@ -488,6 +499,8 @@ sa_status sa_index_build_ex(const void* corpus, int64_t n, int32_t d, int32_t nl
   idx->row_offset = opts->row_offset;
   idx->n_total = n_total;
   idx->comm = opts->comm;
+  idx->list_world = opts->list_shard_world;
+  idx->list_rank = opts->list_shard_rank;
   st = cuda_status(cudaMalloc(&idx->X, (size_t)n * d_pad * sizeof(__nv_bfloat16)), "alloc corpus");
   if (st == SA_OK) {
     ProfRegion region(SA_KERNEL_STAGE, s);
