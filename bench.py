@@ -385,6 +385,14 @@ def main():
     torch.cuda.empty_cache()
     graph_build_s = None
     gidx = None
+    lidx = None    # list-sharded IVF index (N > 1): the IVF leg's scaling layout
+    if use_ivf and nlist > 0 and (world > 1 or os.environ.get("SA_BENCH_LIST_SHARD")) and \
+            not (use_graph and nlist > 0 and world > 1):
+        Xf = torch.empty(n, d, dtype=torch.bfloat16, device="cuda")
+        draw_rows_into(mix, Xf, CORPUS_SEED, 0)
+        lidx = build_list_shard(sa, Xf, nlist, comm, rank, world)
+        del Xf
+        torch.cuda.empty_cache()
     if use_graph and nlist > 0:
         t0 = time.perf_counter()
         if world == 1:
@@ -393,6 +401,7 @@ def main():
             Xf = torch.empty(n, d, dtype=torch.bfloat16, device="cuda")
             draw_rows_into(mix, Xf, CORPUS_SEED, 0)
             gidx = sa.Index.build(Xf, nlist)
+            lidx = build_list_shard(sa, Xf, nlist, comm, rank, world)
             del Xf
             torch.cuda.empty_cache()
         gidx.build_graph(knn_k=args.graph_knn, degree=args.graph_degree,
@@ -401,6 +410,7 @@ def main():
         graph_build_s = time.perf_counter() - t0
     else:
         use_graph = False
+    iidx = lidx if lidx is not None else idx   # the IVF legs' index
 
     nb = args.warmup + args.steps
     Qall = torch.empty(nb * nq, d, dtype=torch.bfloat16, device="cuda")
@@ -441,7 +451,7 @@ def main():
         if isinstance(nprobe, tuple):          # ("graph", L)
             return gidx.search_graph(gbatches[i], k, nprobe[1], search_width=GRAPH_W,
                                      n_entries=GRAPH_E)
-        return idx.search(batches[i], k, nprobe, out=(ids, scores))
+        return (iidx if nprobe else idx).search(batches[i], k, nprobe, out=(ids, scores))
 
     def timed(nprobe):
         """W warm-up + K timed search steps; returns (ms, per-kind kernel (ms, launches), clocks)."""
@@ -489,7 +499,7 @@ def main():
         for p in NPROBE_LADDER:
             if p > nlist:
                 break
-            r = float(np.mean([recall_at_k(idx.search(batches[i], k, p)[0], gt[i]) for i in calib]))
+            r = float(np.mean([recall_at_k(iidx.search(batches[i], k, p)[0], gt[i]) for i in calib]))
             sweep.append({"nprobe": p, "recall": r})
             if r >= RECALL_TARGET + CALIBRATION_MARGIN:
                 nprobe = p
@@ -558,14 +568,14 @@ def main():
         ms_i, kern_i, clk_i = timed(nprobe)
         rec = []
         for i in range(args.warmup, nb):
-            gi, _ = idx.search(batches[i], k, nprobe)
+            gi, _ = iidx.search(batches[i], k, nprobe)
             rec.append(recall_at_k(gi, gt[i]))
         # algorithmic bytes per batch: rows of the distinct probed lists (+ the centroids)
-        loff, _ = idx.export_lists()
+        loff, _ = iidx.export_lists()
         sizes = np.diff(loff)
         byts = []
         for i in range(args.warmup, nb):
-            P = idx.probes(batches[i], nprobe).cpu().numpy()
+            P = iidx.probes(batches[i], nprobe).cpu().numpy()
             u = np.unique(P)
             byts.append(float(sizes[u].sum()) * d * 2)
         alg_bytes = float(np.mean(byts)) + nlist * d * 2
@@ -671,6 +681,8 @@ def main():
                          "traffic": traffic_from_profiles("graph_search", args.config, nq, world, f"L{L}")},
         }
 
+    if result_ivf is not None and lidx is not None:
+        result_ivf["parallelism"] = f"list-shard x{world}"
     for r in (result_exact, result_fp8, result_ivf, result_ivf_fp8):
         if r is not None:
             r.setdefault("parallelism", f"row-shard x{world}")
@@ -693,7 +705,7 @@ def main():
             gidx.search_graph_host(qhost, k, head["search_range"], search_width=GRAPH_W,
                                    n_entries=GRAPH_E, out=(ids_h, sc_h))
         else:
-            idx.search_host(qhost, k, head_nprobe, out=(ids_h, sc_h))
+            (iidx if head_nprobe else idx).search_host(qhost, k, head_nprobe, out=(ids_h, sc_h))
 
     for i in range(args.warmup):
         host_search(qh[i])
@@ -1078,6 +1090,19 @@ def run_maturity(args, sa, idx, batches, k, nq, d, nlist, n, rank):
         print(json.dumps(out))
     idx.free()
     return 0
+
+
+def build_list_shard(sa, Xf, nlist, comm, rank, world):
+    """The IVF legs' list-sharded index (sa_build_opts.list_shard_*): this rank keeps the whole
+    lists l % world == rank of the full corpus Xf; None (row shards stay in use) if the library
+    refuses, with the reason on stderr."""
+    try:
+        return sa.Index.build(Xf, nlist, comm=comm if world > 1 else None,
+                              list_shard=(rank, world))
+    except sa.SAError as e:
+        print(f"list-sharded IVF index not built ({e}); the IVF leg stays row-sharded",
+              file=sys.stderr, flush=True)
+        return None
 
 
 def run_simulated(args, cfg, sa):
